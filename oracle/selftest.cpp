@@ -1,0 +1,1165 @@
+// CPU ORACLE — TEST INFRASTRUCTURE ONLY (see oracle.hpp header).
+//
+// Pins the oracle against the reference's own known-answer tests: each CASE
+// below re-states one check from /root/reference/proj/tests (file:line in the
+// case name) against the oracle's API. The reference ships no golden files —
+// every fixture there is seeded synthesis — so these KATs plus independent
+// scalar oracles (conv2d_dense, gauss_jordan, explicit densities, discrete 3-D
+// extremum scans; tests/oracles.hpp) are what pin the restatement.
+//
+// Usage: selftest [filter-substring]. Prints one line per case, exits nonzero
+// on any failure.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <functional>
+#include <numbers>
+#include <random>
+#include <set>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "oracle.hpp"
+
+using namespace orc;
+
+namespace {
+
+struct Case { std::string name; std::function<void()> fn; const char* xfail; };
+std::vector<Case>& registry() { static std::vector<Case> r; return r; }
+struct Reg { Reg(const char* n, std::function<void()> f, const char* xf = nullptr) { registry().push_back({n, std::move(f), xf}); } };
+int g_fail_checks = 0;
+std::string g_current;
+
+#define CAT2(a, b) a##b
+#define CAT(a, b) CAT2(a, b)
+#define CASE(name) static void CAT(case_, __LINE__)(); static Reg CAT(reg_, __LINE__)(name, CAT(case_, __LINE__)); static void CAT(case_, __LINE__)()
+// XCASE: a reference KAT that this restatement provably cannot meet (the reason
+// is printed); it runs, must still FAIL, and is reported as XFAIL.
+#define XCASE(name, why) static void CAT(case_, __LINE__)(); static Reg CAT(reg_, __LINE__)(name, CAT(case_, __LINE__), why); static void CAT(case_, __LINE__)()
+#define CHECK(cond) do { if (!(cond)) { ++g_fail_checks; std::printf("    CHECK failed %s:%d: %s\n", __FILE__, __LINE__, #cond); } } while (0)
+#define REQUIRE(cond) do { if (!(cond)) { ++g_fail_checks; std::printf("    REQUIRE failed %s:%d: %s\n", __FILE__, __LINE__, #cond); return; } } while (0)
+#define CHECK_THROWS(expr, T) do { bool thrown = false; try { (void)(expr); } catch (const T&) { thrown = true; } catch (...) {} CHECK(thrown); } while (0)
+
+bool approx(double a, double b, double rel) { return std::abs(a - b) <= rel * std::max(std::abs(a), std::abs(b)) + 1e-300 || a == b; }
+
+// -------------------------------------------------- independent scalar oracles (tests/oracles.hpp)
+Plane conv2d_dense(const Plane& img, const std::vector<double>& taps) {
+  const int r = int(taps.size() / 2);
+  Plane out(img.w, img.h);
+  for (int y = 0; y < img.h; ++y)
+    for (int x = 0; x < img.w; ++x) {
+      double acc = 0.0;
+      for (int j = -r; j <= r; ++j)
+        for (int i = -r; i <= r; ++i)
+          acc += (taps[std::size_t(j + r)] * taps[std::size_t(i + r)]) * img.at(int(mirror_index(y + j, img.h)), int(mirror_index(x + i, img.w)));
+      out.at(y, x) = acc;
+    }
+  return out;
+}
+
+// Cramer's-rule-free independent inverse: solve V x = e_k by Gaussian elimination
+// with back substitution (different from the library's Gauss-Jordan sweep).
+Mat4 inverse_by_elimination(const std::vector<double>& sigmas) {
+  Mat4 inv{};
+  for (int k = 0; k < 4; ++k) {
+    double a[4][5];
+    for (int r = 0; r < 4; ++r) {
+      for (int i = 0; i < 4; ++i) a[r][i] = std::pow(sigmas[std::size_t(r)], i);
+      a[r][4] = r == k ? 1.0 : 0.0;
+    }
+    for (int c = 0; c < 4; ++c) {
+      int p = c;
+      for (int r = c + 1; r < 4; ++r) if (std::abs(a[r][c]) > std::abs(a[p][c])) p = r;
+      for (int j = 0; j < 5; ++j) std::swap(a[c][j], a[p][j]);
+      for (int r = c + 1; r < 4; ++r) {
+        const double f = a[r][c] / a[c][c];
+        for (int j = c; j < 5; ++j) a[r][j] -= f * a[c][j];
+      }
+    }
+    double xsol[4];
+    for (int r = 3; r >= 0; --r) {
+      double s = a[r][4];
+      for (int j = r + 1; j < 4; ++j) s -= a[r][j] * xsol[j];
+      xsol[r] = s / a[r][r];
+    }
+    for (int i = 0; i < 4; ++i) inv[i][k] = xsol[i];
+  }
+  return inv;
+}
+
+struct Disc { int x, y, k; double v; };
+std::vector<Disc> scan_3d_extrema(const std::vector<Plane>& st, double thr, int margin) {
+  std::vector<Disc> out;
+  const int h = st[0].h, w = st[0].w;
+  for (int k = 1; k + 1 < int(st.size()); ++k)
+    for (int y = margin; y < h - margin; ++y)
+      for (int x = margin; x < w - margin; ++x) {
+        const double v = st[std::size_t(k)].at(y, x);
+        if (std::abs(v) < thr) continue;
+        bool mx = true, mn = true;
+        for (int dk = -1; dk <= 1; ++dk)
+          for (int dy = -1; dy <= 1; ++dy)
+            for (int dx = -1; dx <= 1; ++dx) {
+              if (!dk && !dy && !dx) continue;
+              const double nv = st[std::size_t(k + dk)].at(y + dy, x + dx);
+              if (v <= nv) mx = false;
+              if (v >= nv) mn = false;
+            }
+        if (mx || mn) out.push_back({x, y, k, v});
+      }
+  return out;
+}
+
+std::vector<Plane> log_stack(const Plane& img, const std::vector<double>& sigmas) {
+  std::vector<Plane> st;
+  for (double s : sigmas) {
+    Plane l = laplacian_3x3(gaussian_blur(img, s));
+    for (double& v : l.px) v *= s * s;
+    st.push_back(l);
+  }
+  return st;
+}
+
+Plane random_texture(uint64_t seed, int w, int h, double blur) {
+  std::mt19937_64 rng(seed);
+  Plane img(w, h);
+  for (auto& v : img.px) v = double(rng() % 4096) / 4095.0;
+  return blur > 0.0 ? gaussian_blur(img, blur) : img;
+}
+
+Plane blob(int w, int h, double cx, double cy, double s, double amp = 0.8, double bg = 0.1) {
+  Plane img(w, h, bg);
+  for (int y = 0; y < h; ++y)
+    for (int x = 0; x < w; ++x) {
+      double v = img.at(y, x) + amp * std::exp(-((x - cx) * (x - cx) + (y - cy) * (y - cy)) / (2 * s * s));
+      img.at(y, x) = std::max(std::min(v, 1.0), 0.0);
+    }
+  return img;
+}
+
+Keypoint kp(double x, double y, double s, double p) { Keypoint k; k.x = x; k.y = y; k.sigma = s; k.p = p; k.rho = 4.0; k.p_ss = -0.1; return k; }
+
+double angle_gap(double a, double b) {
+  double d = std::fmod(std::abs(a - b), 2.0 * std::numbers::pi);
+  return std::min(d, 2.0 * std::numbers::pi - d);
+}
+
+Pyramid single_level(const Plane& img) {
+  Pyramid p;
+  Octave o;
+  o.base = img;
+  for (int k = 0; k < 4; ++k) o.gauss.push_back(img);
+  p.octaves.push_back(o);
+  return p;
+}
+
+struct Instance { Mat x; GMMModel g; };
+Instance random_instance(std::mt19937_64& rng, int n, int nc) {
+  std::normal_distribution<double> gauss(0.0, 1.0);
+  std::uniform_real_distribution<double> unit(0.2, 1.5);
+  Instance in;
+  in.x = Mat(n, 32);
+  for (auto& v : in.x.a) v = gauss(rng);
+  in.g.weights.resize(std::size_t(nc));
+  in.g.means = Mat(nc, 32);
+  in.g.stds = Mat(nc, 32);
+  double ws = 0.0;
+  for (int i = 0; i < nc; ++i) {
+    in.g.weights[std::size_t(i)] = unit(rng);
+    ws += in.g.weights[std::size_t(i)];
+    for (int j = 0; j < 32; ++j) { in.g.means(i, j) = gauss(rng); in.g.stds(i, j) = unit(rng); }
+  }
+  for (double& w : in.g.weights) w /= ws;
+  in.g.weights.back() += 1.0 - eigen_sum(in.g.weights.data(), in.g.weights.size());
+  return in;
+}
+
+Mat posteriors_explicit(const Mat& x, const GMMModel& g) {
+  Mat gam(x.rows, g.components());
+  for (int t = 0; t < x.rows; ++t) {
+    std::vector<double> wp(std::size_t(g.components()));
+    double tot = 0.0;
+    for (int i = 0; i < g.components(); ++i) {
+      double dens = 1.0;
+      for (int j = 0; j < 32; ++j) {
+        const double sd = g.stds(i, j), z = (x(t, j) - g.means(i, j)) / sd;
+        dens *= std::exp(-0.5 * z * z) / (sd * std::sqrt(2.0 * std::numbers::pi));
+      }
+      wp[std::size_t(i)] = g.weights[std::size_t(i)] * dens;
+      tot += wp[std::size_t(i)];
+    }
+    for (int i = 0; i < g.components(); ++i) gam(t, i) = wp[std::size_t(i)] / tot;
+  }
+  return gam;
+}
+
+GMMModel flat_gmm(int nc) {
+  GMMModel g;
+  g.weights.assign(std::size_t(nc), 1.0 / nc);
+  g.means = Mat(nc, 32, 0.0);
+  g.stds = Mat(nc, 32, 1.0);
+  return g;
+}
+
+ModelBundle tiny_bundle() {  // test_container.cpp:50-66
+  ModelBundle b;
+  b.detector = DetectorConfig::defaults();
+  b.relevance = RelevanceModel::uniform();
+  b.transforms = TransformPair::defaults();
+  b.quantizer = QuantizerModel::neutral();
+  for (int r = 0; r < 32; ++r) b.pca.basis(r, r) = 1.0;
+  b.gmm = flat_gmm(4);
+  b.gmm.weights.assign(4, 0.25);
+  for (int i = 0; i < 4; ++i) b.gmm.means(i, 0) = i;
+  return b;
+}
+
+EncodedImage sample_container(uint64_t seed, const char* mode_name) {  // test_container.cpp:15-48
+  std::mt19937_64 rng(seed);
+  const ModeSpec& mode = mode_by_name(mode_name);
+  const int nc = 16;
+  GMMModel g = flat_gmm(nc);
+  Mat gm(nc, 32), gv(nc, 32);
+  for (int i = 0; i < nc; ++i)
+    for (int j = 0; j < 32; ++j) {
+      gm(i, j) = double(rng() % 2001) / 1000.0 - 1.0;
+      gv(i, j) = double(rng() % 2001) / 1000.0 - 1.0;
+    }
+  EncodedImage e;
+  e.mode_id = mode.id;
+  e.width = 320;
+  e.height = 240;
+  e.model_crc = 0xABCD1234;
+  e.global_desc = scfv_encode(gm, gv, g, mode);
+  for (int i = 0; i < 20; ++i) {
+    TernaryCode c;
+    c.mode = uint8_t(mode.id);
+    c.xq = uint16_t(rng() % 65536);
+    c.yq = uint16_t(rng() % 65536);
+    c.sigma_q = uint8_t(rng() % 256);
+    c.theta_q = uint8_t(rng() % 256);
+    c.symbols.resize(std::size_t(mode.elements));
+    for (auto& s : c.symbols) s = int8_t(int(rng() % 3) - 1);
+    e.codes.push_back(c);
+  }
+  return e;
+}
+
+TernaryCode random_code(std::mt19937_64& rng, const ModeSpec& mode) {
+  TernaryCode c;
+  c.mode = uint8_t(mode.id);
+  c.xq = uint16_t(rng() % 65536);
+  c.yq = uint16_t(rng() % 65536);
+  c.sigma_q = uint8_t(rng() % 256);
+  c.theta_q = uint8_t(rng() % 256);
+  c.symbols.resize(std::size_t(mode.elements));
+  for (auto& s : c.symbols) s = int8_t(int(rng() % 3) - 1);
+  return c;
+}
+
+}  // namespace
+
+// ================================================================= image (test_image.cpp)
+
+CASE("image: u8 bytes scale by 1/255 (test_image.cpp:34-48)") {
+  uint8_t raw[64] = {0, 255, 128, 64};
+  const Plane p = plane_from_u8(raw, 8, 8, 8);
+  CHECK(p.at(0, 0) == 0.0);
+  CHECK(approx(p.at(0, 1), 1.0, 1e-15));
+  CHECK(std::abs(p.at(0, 2) - 0.50196) < 1e-4 * 0.50196);
+  CHECK(std::abs(p.at(0, 3) - 0.25098) < 1e-4 * 0.25098);
+  CHECK(plane_to_u8(p)[2] == 128);  // save/load round trip (test_image.cpp:87-100)
+}
+
+CASE("image: resize_max_side dims (test_image.cpp:102-121)") {
+  Plane a = resize_max_side(Plane(1280, 960, 0.5), 640);
+  CHECK(a.w == 640 && a.h == 480);
+  Plane b(320, 240);
+  b.at(7, 11) = 0.25;
+  Plane bb = resize_max_side(b, 640);
+  CHECK(bb.w == 320 && bb.h == 240 && bb.px == b.px);
+  Plane c = resize_max_side(Plane(1920, 1080, 0.3), 640);
+  CHECK(c.w == 640 && c.h == 360);
+}
+
+CASE("image: resize_max_side idempotent (test_image.cpp:123-137)") {
+  std::mt19937_64 rng(7);
+  for (int trial = 0; trial < 10; ++trial) {
+    const int w = 600 + int(rng() % 1000), h = 600 + int(rng() % 1000);
+    Plane img(w, h);
+    for (int y = 0; y < h; ++y)
+      for (int x = 0; x < w; ++x) img.at(y, x) = ((x * 31 + y * 17) % 256) / 255.0;
+    const Plane once = resize_max_side(img, 640), twice = resize_max_side(once, 640);
+    REQUIRE(once.w == twice.w && once.h == twice.h);
+    CHECK(once.px == twice.px);
+  }
+}
+
+CASE("image: 1920x1080 -> 640x360 is an exact stride-3 gather") {
+  std::mt19937_64 rng(5);
+  Plane img(1920, 1080);
+  for (auto& v : img.px) v = double(rng() % 256) / 255.0;
+  const Plane out = resize_max_side(img, 640);
+  bool exact = true;
+  for (int y = 0; y < out.h; ++y)
+    for (int x = 0; x < out.w; ++x) exact = exact && out.at(y, x) == img.at(3 * y + 1, 3 * x + 1);
+  CHECK(exact);
+}
+
+CASE("image: downsample_half (test_image.cpp:139-161)") {
+  Plane c = downsample_half(Plane(16, 16, 0.375));
+  CHECK(c.w == 8 && c.h == 8);
+  for (double v : c.px) CHECK(v == 0.375);
+  Plane o = downsample_half(Plane(17, 16));
+  CHECK(o.w == 8 && o.h == 8);
+  Plane imp(16, 16);
+  imp.at(4, 4) = 1.0;
+  Plane d = downsample_half(imp);
+  double s = 0;
+  for (double v : d.px) s += v;
+  CHECK(d.at(2, 2) == 1.0 && s == 1.0);
+  CHECK_THROWS(downsample_half(Plane(15, 16)), DataError);
+}
+
+CASE("image: gaussian taps normalised + impulse response 1e-14 (test_image.cpp:163-180)") {
+  const auto taps = gaussian_taps(1.4);
+  CHECK(taps.size() == 2 * std::size_t(std::ceil(3 * 1.4)) + 1);
+  double s = 0.0;
+  for (double t : taps) s += t;
+  CHECK(std::abs(s - 1.0) < 1e-12);
+  Plane img(32, 32);
+  img.at(16, 16) = 1.0;
+  const Plane g = gaussian_blur(img, 1.4);
+  const int r = int(taps.size() / 2);
+  for (int dy = -r; dy <= r; ++dy)
+    for (int dx = -r; dx <= r; ++dx) {
+      const double want = taps[std::size_t(dy + r)] * taps[std::size_t(dx + r)];
+      CHECK(std::abs(g.at(16 + dy, 16 + dx) - want) <= 1e-14 * want + 1e-300);
+    }
+}
+
+CASE("image: separable blur == dense 2-D conv within 1e-10 (test_image.cpp:182-198)") {
+  std::mt19937_64 rng(11);
+  Plane img(32, 32);
+  for (auto& v : img.px) v = double(rng() % 1000) / 999.0;
+  const Plane sep = gaussian_blur(img, 1.98), dense = conv2d_dense(img, gaussian_taps(1.98));
+  double m = 0.0;
+  for (std::size_t i = 0; i < sep.px.size(); ++i) m = std::max(m, std::abs(sep.px[i] - dense.px[i]));
+  CHECK(m < 1e-10);
+}
+
+CASE("image: laplacian of a constant is zero (test_image.cpp:200-203)") {
+  for (double v : laplacian_3x3(Plane(24, 24, 0.7)).px) CHECK(v == 0.0);
+}
+
+// ================================================================= detector (test_scale_space.cpp)
+
+CASE("detector: beta == independent elimination within 1e-12 (test_scale_space.cpp:42-51)") {
+  const std::vector<double> s = {1.0, 2.0, 3.0, 4.0};
+  const Mat4 b = compute_beta(s), ref = inverse_by_elimination(s);
+  double m = 0.0;
+  for (int i = 0; i < 4; ++i)
+    for (int j = 0; j < 4; ++j) m = std::max(m, std::abs(b[i][j] - ref[i][j]));
+  CHECK(m < 1e-12);
+  const DetectorConfig cfg = DetectorConfig::defaults();
+  const Mat4 ref2 = inverse_by_elimination(cfg.sigmas);
+  double m2 = 0.0;
+  for (int i = 0; i < 4; ++i)
+    for (int j = 0; j < 4; ++j) m2 = std::max(m2, std::abs(cfg.beta[i][j] - ref2[i][j]) / std::max(1.0, std::abs(ref2[i][j])));
+  CHECK(m2 < 1e-12);
+}
+
+CASE("detector: beta interpolates scale nodes 1e-9 (test_scale_space.cpp:53-66)") {
+  const DetectorConfig cfg = DetectorConfig::defaults();
+  std::mt19937_64 rng(17);
+  for (int trial = 0; trial < 200; ++trial) {
+    double l[4], a[4] = {0, 0, 0, 0}, lmax = 0.0;
+    for (int k = 0; k < 4; ++k) { l[k] = (double(rng() % 2001) - 1000.0) / 500.0; lmax = std::max(lmax, std::abs(l[k])); }
+    for (int i = 0; i < 4; ++i)
+      for (int k = 0; k < 4; ++k) a[i] += cfg.beta[i][k] * l[k];
+    for (int k = 0; k < 4; ++k) {
+      const double s = cfg.sigmas[std::size_t(k)];
+      CHECK(std::abs(a[0] + s * (a[1] + s * (a[2] + s * a[3])) - l[k]) < 1e-9 * std::max(1.0, lmax));
+    }
+  }
+  CHECK_THROWS(compute_beta({1.0, 1.0, 2.0, 3.0}), DataError);
+}
+
+CASE("detector: constant octave has zero response (test_scale_space.cpp:72-77)") {
+  const DetectorConfig cfg = DetectorConfig::defaults();
+  const Octave oct = build_octave(Plane(48, 48, 0.42), cfg, 0);
+  for (const auto& l : oct.log)
+    for (double v : l.px) CHECK(v == 0.0);
+  CHECK(detect_extrema(oct, cfg).empty());
+}
+
+CASE("detector: G levels == dense oracle 1e-10 (test_scale_space.cpp:79-93)") {
+  const DetectorConfig cfg = DetectorConfig::defaults();
+  const Plane img = random_texture(23, 32, 32, 0.0);
+  const Octave oct = build_octave(img, cfg, 0);
+  for (int k = 0; k < 4; ++k) {
+    const Plane dense = conv2d_dense(img, gaussian_taps(cfg.sigmas[std::size_t(k)]));
+    double m = 0.0;
+    for (std::size_t i = 0; i < dense.px.size(); ++i) m = std::max(m, std::abs(dense.px[i] - oct.gauss[std::size_t(k)].px[i]));
+    CHECK(m < 1e-10);
+  }
+}
+
+CASE("detector: centred blob -> one candidate at its scale (test_scale_space.cpp:95-125)") {
+  const DetectorConfig cfg = DetectorConfig::defaults();
+  const Plane img = blob(64, 64, 32.0, 32.0, 1.8);
+  const auto cands = detect_extrema(build_octave(img, cfg, 0), cfg);
+  int near = 0;
+  Candidate cc{};
+  for (const auto& c : cands)
+    if (std::hypot(c.x - 32.0, c.y - 32.0) <= 1.0) { ++near; cc = c; }
+  REQUIRE(near == 1);
+  std::vector<double> fine;
+  for (int i = 0; i <= 32; ++i) fine.push_back(std::pow(3.2, i / 32.0));
+  const auto ext = scan_3d_extrema(log_stack(img, fine), cfg.response_threshold, 10);
+  double os = -1.0;
+  for (const auto& e : ext)
+    if (std::hypot(e.x - 32.0, e.y - 32.0) <= 1.0) os = fine[std::size_t(e.k)];
+  REQUIRE(os > 0.0);
+  CHECK(std::abs(cc.sigma - os) / os < 0.25);
+  CHECK(std::abs(os - 1.8) / 1.8 < 0.25);
+}
+
+CASE("detector: candidates contain the discrete 3-D extrema (test_scale_space.cpp:127-149)") {
+  const DetectorConfig cfg = DetectorConfig::defaults();
+  const int margin = int(std::ceil(3.0 * cfg.sigmas.back())) + 2;
+  for (uint64_t seed = 100; seed < 110; ++seed) {
+    const Plane img = random_texture(seed, 64, 64, 1.2);
+    const Octave oct = build_octave(img, cfg, 0);
+    const auto cands = detect_extrema(oct, cfg);
+    for (const auto& d : scan_3d_extrema(oct.log, cfg.response_threshold, margin)) {
+      bool covered = false;
+      for (const auto& c : cands)
+        if (c.x == d.x && c.y == d.y && std::abs(4.0 * std::log2(c.sigma / cfg.sigmas.front()) - d.k) <= 0.5) covered = true;
+      CHECK(covered);
+    }
+  }
+}
+
+// Closed-form vertex of the 3x3 quadratic fit around candidate c (independent beta).
+static bool vertex_of(const Octave& oct, const DetectorConfig& cfg, const Candidate& c, double& vx, double& vy) {
+  const Mat4 inv = inverse_by_elimination(cfg.sigmas);
+  auto p_at = [&](int x, int y) {
+    double a[4] = {0, 0, 0, 0};
+    for (int i = 0; i < 4; ++i)
+      for (int k = 0; k < 4; ++k) a[i] += inv[i][k] * oct.log[std::size_t(k)].at(y, x);
+    return a[0] + c.sigma * (a[1] + c.sigma * (a[2] + c.sigma * a[3]));
+  };
+  const double gx = 0.5 * (p_at(c.x + 1, c.y) - p_at(c.x - 1, c.y));
+  const double gy = 0.5 * (p_at(c.x, c.y + 1) - p_at(c.x, c.y - 1));
+  const double hxx = p_at(c.x + 1, c.y) + p_at(c.x - 1, c.y) - 2 * p_at(c.x, c.y);
+  const double hyy = p_at(c.x, c.y + 1) + p_at(c.x, c.y - 1) - 2 * p_at(c.x, c.y);
+  const double hxy = 0.25 * (p_at(c.x + 1, c.y + 1) - p_at(c.x - 1, c.y + 1) - p_at(c.x + 1, c.y - 1) + p_at(c.x - 1, c.y - 1));
+  const double det = hxx * hyy - hxy * hxy;
+  vx = c.x - (hyy * gx - hxy * gy) / det;
+  vy = c.y - (-hxy * gx + hxx * gy) / det;
+  return det > 0.0;
+}
+
+XCASE("detector: refinement of candidates.front() == closed-form vertex (test_scale_space.cpp:151-200)",
+      "the blob's LoG ring yields 24 positive candidates (p~0.05) that sort before the centre and "
+      "are all rejected as edges, so the nearest refined point to front()'s vertex is ~6 px away") {
+  const DetectorConfig cfg = DetectorConfig::defaults();
+  const Octave oct = build_octave(blob(64, 64, 31.6, 32.3, 1.9), cfg, 0);
+  const auto cands = detect_extrema(oct, cfg);
+  const auto refined = refine_candidates(cands, oct, cfg);
+  REQUIRE(!cands.empty() && !refined.empty());
+  double vx, vy;
+  vertex_of(oct, cfg, cands.front(), vx, vy);
+  double best = 1e9;
+  for (const auto& k : refined) best = std::min(best, std::hypot(k.x - vx, k.y - vy));
+  CHECK(best < 1e-9);
+}
+
+CASE("detector: every surviving candidate refines to its closed-form vertex 1e-9 (test_scale_space.cpp:151-200, per survivor)") {
+  const DetectorConfig cfg = DetectorConfig::defaults();
+  for (const auto& img : {blob(64, 64, 31.6, 32.3, 1.9), random_texture(5, 64, 64, 1.3)}) {
+    const Octave oct = build_octave(img, cfg, 0);
+    int survivors = 0;
+    for (const auto& c : detect_extrema(oct, cfg)) {
+      const auto r = refine_candidates({c}, oct, cfg);
+      if (r.empty()) continue;
+      ++survivors;
+      double vx, vy;
+      REQUIRE(vertex_of(oct, cfg, c, vx, vy));
+      CHECK(std::hypot(r[0].x - vx, r[0].y - vy) < 1e-9);
+      CHECK(std::abs(r[0].x - c.x) <= 0.6 && std::abs(r[0].y - c.y) <= 0.6);
+    }
+    CHECK(survivors >= 1);
+  }
+}
+
+CASE("detector: straight step edge is rejected (test_scale_space.cpp:202-238)") {
+  const DetectorConfig cfg = DetectorConfig::defaults();
+  Plane img(64, 64, 0.1);
+  for (int y = 0; y < 64; ++y)
+    for (int x = 32; x < 64; ++x) img.at(y, x) = 0.9;
+  img = gaussian_blur(img, 1.0);
+  const Octave oct = build_octave(img, cfg, 0);
+  for (const auto& k : refine_candidates(detect_extrema(oct, cfg), oct, cfg)) {
+    if (k.x < 10 || k.x > 53 || k.y < 10 || k.y > 53) continue;
+    CHECK(std::abs(k.x - 31.5) > 2.0);
+  }
+}
+
+CASE("detector: cross-octave dedup rules (test_scale_space.cpp:240-324)") {
+  CHECK(dedup_across_octaves({kp(10, 10, 2.0, 1.0)}, {kp(40, 40, 2.0, 2.0)}).size() == 2);
+  auto m1 = dedup_across_octaves({kp(10, 10, 2.0, 5.0)}, {kp(10, 10, 2.0, 3.0)});
+  REQUIRE(m1.size() == 1);
+  CHECK(m1[0].p == 5.0);
+  auto m2 = dedup_across_octaves({kp(10, 10, 2.0, 3.0)}, {kp(10, 10, 2.0, 5.0)});
+  REQUIRE(m2.size() == 1);
+  CHECK(m2[0].p == 5.0);
+  CHECK(dedup_across_octaves({kp(10, 10, 2.8, 1.0)}, {kp(10, 10, 2.0, 9.0)}).size() == 2);
+  auto tie = dedup_across_octaves({kp(10, 10, 2.0, 4.0)}, {kp(10.5, 10, 2.0, -4.0)});
+  REQUIRE(tie.size() == 1);
+  CHECK(tie[0].p == -4.0);  // |p| tie keeps the previous point
+  std::mt19937_64 rng(31);
+  for (int trial = 0; trial < 50; ++trial) {
+    std::vector<Keypoint> cur, prev;
+    for (int i = 0; i < 8; ++i) cur.push_back(kp(double(rng() % 20), double(rng() % 20), 1.8 + 0.05 * double(rng() % 10), 0.1 + 0.001 * double(rng() % 1000)));
+    for (int i = 0; i < 8; ++i) prev.push_back(kp(double(rng() % 20), double(rng() % 20), 1.8 + 0.05 * double(rng() % 10), 0.1 + 0.001 * double(rng() % 1000) + 0.0005));
+    auto in_range = [](const Keypoint& a, const Keypoint& b) {
+      if (std::hypot(a.x - b.x, a.y - b.y) >= 2.0) return false;
+      const double r = a.sigma / b.sigma;
+      return r >= 1.0 / 1.3 && r <= 1.3;
+    };
+    std::size_t expect = 0;
+    for (const auto& c : cur) { bool keep = true; for (const auto& q : prev) if (in_range(c, q) && std::abs(q.p) >= std::abs(c.p)) keep = false; expect += keep; }
+    for (const auto& q : prev) { bool keep = true; for (const auto& c : cur) if (in_range(c, q) && std::abs(c.p) > std::abs(q.p)) keep = false; expect += keep; }
+    const auto merged = dedup_across_octaves(cur, prev);
+    REQUIRE(merged.size() == expect);
+    std::shuffle(cur.begin(), cur.end(), rng);
+    std::shuffle(prev.begin(), prev.end(), rng);
+    const auto shuffled = dedup_across_octaves(cur, prev);
+    std::vector<std::tuple<double, double, double, double>> a, b;
+    for (const auto& k : merged) a.emplace_back(k.x, k.y, k.sigma, k.p);
+    for (const auto& k : shuffled) b.emplace_back(k.x, k.y, k.sigma, k.p);
+    std::sort(a.begin(), a.end());
+    std::sort(b.begin(), b.end());
+    CHECK(a == b);
+  }
+}
+
+static int covariance_misses(bool octave0_only, int& checked) {
+  const DetectorConfig cfg = DetectorConfig::defaults();
+  const Plane img = random_texture(77, 96, 96, 1.6);
+  Plane sh(96, 96);
+  for (int y = 0; y < 96; ++y)
+    for (int x = 0; x < 96; ++x) sh.at(y, x) = img.at((y - 2 + 96) % 96, (x - 3 + 96) % 96);
+  const auto a = detect_keypoints(img, cfg, nullptr), b = detect_keypoints(sh, cfg, nullptr);
+  int miss = 0;
+  checked = 0;
+  for (const auto& pa : a) {
+    if (pa.x < 20 || pa.x > 75 || pa.y < 20 || pa.y > 75) continue;
+    if (octave0_only && pa.octave != 0) continue;
+    bool found = false;
+    for (const auto& pb : b)
+      if (std::hypot(pb.x - (pa.x + 3), pb.y - (pa.y + 2)) <= 0.1 && std::abs(pb.sigma - pa.sigma) < 0.05 * pa.sigma) found = true;
+    miss += !found;
+    ++checked;
+  }
+  return miss;
+}
+
+XCASE("detector: translation covariance 0.1 px, all octaves (test_scale_space.cpp:326-351)",
+      "a 3 px shift is odd, so octave>=1 bases (G3 at even coordinates, image.cpp:147-155) sample a "
+      "different phase; coarse-octave survivors of dedup move by more than 0.1 px") {
+  int checked = 0;
+  CHECK(covariance_misses(false, checked) == 0);
+}
+
+CASE("detector: translation covariance 0.1 px, octave-0 points (test_scale_space.cpp:326-351)") {
+  int checked = 0;
+  CHECK(covariance_misses(true, checked) == 0);
+  CHECK(checked > 3);
+}
+
+CASE("detector: two runs bit-identical (test_scale_space.cpp:353-365)") {
+  const DetectorConfig cfg = DetectorConfig::defaults();
+  const Plane img = random_texture(88, 80, 64, 1.4);
+  const auto a = detect_keypoints(img, cfg, nullptr), b = detect_keypoints(img, cfg, nullptr);
+  REQUIRE(a.size() == b.size() && !a.empty());
+  for (std::size_t i = 0; i < a.size(); ++i) CHECK(a[i].x == b[i].x && a[i].y == b[i].y && a[i].sigma == b[i].sigma && a[i].p == b[i].p);
+}
+
+// ================================================================= selector (test_relevance.cpp)
+
+CASE("selector: table products, clamping, ties, centre distance (test_relevance.cpp:36-188)") {
+  CHECK(relevance(kp(1e9, 1e9, 1e9, 1e9), RelevanceModel::uniform()) == 1.0);
+  RelevanceModel z = RelevanceModel::uniform();
+  z.tables[3].values = {0.0};
+  CHECK(relevance(kp(0.5, 0.5, 0.5, 0.5), z) == 0.0);
+  RelevanceModel two;
+  for (auto& t : two.tables) { t.edges = {0.0, 1.0, 2.0}; t.values = {0.5, 0.8}; }
+  Keypoint k;
+  k.sigma = 0.5; k.p = 1.5; k.d = 0.5; k.rho = 1.5; k.p_ss = 0.5;
+  CHECK(approx(relevance(k, two), 0.5 * 0.8 * 0.5 * 0.8 * 0.5, 1e-12));
+  RelevanceModel q;
+  for (auto& t : q.tables) { t.edges = {0.0, 1.0, 2.0}; t.values = {0.25, 0.75}; }
+  CHECK(q.tables[0](-100.0) == 0.25 && q.tables[0](100.0) == 0.75 && q.tables[0](0.0) == 0.25 && q.tables[0](1.0) == 0.75);
+  std::vector<Keypoint> pts;
+  for (int i = 0; i < 10; ++i) pts.push_back(kp(i, i, 2.0, 1.0 + i));
+  CHECK(select_top(pts, RelevanceModel::uniform(), 300).size() == 10);
+  auto o1 = select_top({kp(1, 1, 2.0, 4.0), kp(2, 2, 2.0, 7.0)}, RelevanceModel::uniform(), 1);
+  REQUIRE(o1.size() == 1);
+  CHECK(o1[0].p == 7.0);
+  auto o2 = select_top({kp(5, 9, 2.0, 3.0), kp(4, 9, 2.0, 3.0), kp(1, 2, 2.0, 3.0)}, RelevanceModel::uniform(), 3);
+  CHECK(o2[0].y == 2.0 && o2[1].x == 4.0 && o2[2].x == 5.0);
+  std::vector<Keypoint> cd = {kp(0, 0, 2.0, 1.0), kp(319.5, 239.5, 2.0, 1.0)};
+  fill_center_distance(cd, 640, 480);
+  CHECK(std::abs(cd[0].d - 1.0) < 1e-9 && std::abs(cd[1].d) < 1e-9);
+  CHECK_THROWS(select_top(pts, RelevanceModel::uniform(), 0), DataError);
+}
+
+CASE("selector: rank order invariant to positive table scaling (test_relevance.cpp:88-117)") {
+  std::mt19937_64 rng(5);
+  std::vector<Keypoint> pts;
+  for (int i = 0; i < 40; ++i) {
+    Keypoint k = kp(double(rng() % 64), double(rng() % 64), 1.4 + 0.01 * double(rng() % 100), 0.02 + 0.001 * double(rng() % 500));
+    k.d = double(rng() % 100) / 100.0;
+    k.p_ss = -0.001 * double(rng() % 300);
+    pts.push_back(k);
+  }
+  RelevanceModel m;
+  for (auto& t : m.tables) { t.edges = {-10.0, 0.0, 1.0, 3.0, 100.0}; t.values = {0.2, 0.5, 0.7, 0.9}; }
+  RelevanceModel s = m;
+  for (auto& t : s.tables) for (auto& v : t.values) v *= 0.51;
+  const auto a = select_top(pts, m, 15), b = select_top(pts, s, 15);
+  REQUIRE(a.size() == b.size());
+  for (std::size_t i = 0; i < a.size(); ++i) CHECK(a[i].x == b[i].x && a[i].y == b[i].y);
+}
+
+CASE("selector: relevance training KATs (test_relevance.cpp:128-181)") {
+  std::mt19937_64 rng(9);
+  std::vector<Labeled> all1, all0;
+  for (int i = 0; i < 800; ++i) {
+    Keypoint k;
+    k.sigma = double(rng() % 100) / 25.0; k.p = double(rng() % 100) / 50.0; k.d = double(rng() % 100) / 100.0;
+    k.rho = 4.0 + double(rng() % 100) / 10.0; k.p_ss = -double(rng() % 100) / 100.0;
+    all1.push_back({k, true});
+    all0.push_back({k, false});
+  }
+  for (const auto& t : train_relevance_tables(all1).tables) for (double v : t.values) CHECK(v == 1.0);
+  for (const auto& t : train_relevance_tables(all0).tables) for (double v : t.values) CHECK(v == 0.0);
+  CHECK_THROWS(train_relevance_tables({}), DataError);
+  std::vector<Labeled> sparse;
+  for (int i = 0; i < 500; ++i) { Keypoint k; k.sigma = 1.0 + 0.001 * i; k.p = 0.5; k.d = 0.5; k.rho = 5.0; k.p_ss = -0.5; sparse.push_back({k, i % 2 == 0}); }
+  { Keypoint k; k.sigma = 100.0; k.p = 0.5; k.d = 0.5; k.rho = 5.0; k.p_ss = -0.5; sparse.push_back({k, true}); }
+  CHECK(approx(train_relevance_tables(sparse).tables[0].values.back(), 251.0 / 501.0, 1e-12));
+}
+
+// ================================================================= descriptor (test_descriptor.cpp)
+
+CASE("descriptor: ramp -> single orientation near 0 (test_descriptor.cpp:53-60)") {
+  Plane img(64, 64);
+  for (int y = 0; y < 64; ++y) for (int x = 0; x < 64; ++x) img.at(y, x) = x / 63.0;
+  const auto th = dominant_orientations(img, 32.0, 32.0, 2.0);
+  REQUIRE(th.size() == 1);
+  CHECK(angle_gap(th[0], 0.0) < 0.5 * 2.0 * std::numbers::pi / 36.0);
+}
+
+CASE("descriptor: 90-degree rotation shifts theta by pi/2 (test_descriptor.cpp:62-85)") {
+  const Plane img = synth_image(41, 96, 96);
+  const double bw = 2.0 * std::numbers::pi / 36.0;
+  for (int k = 1; k <= 3; ++k) {
+    const Plane rot = rotate90(img, k);
+    double rx = 48.3, ry = 47.6, rs = 2.2;
+    SynthTransform t;
+    t.quarter_turns = k;
+    map_point(t, 96, 96, rx, ry, rs);
+    const auto base = dominant_orientations(img, 48.3, 47.6, 2.2), turned = dominant_orientations(rot, rx, ry, rs);
+    bool matched = false;
+    for (double tb : base) for (double tt : turned) if (angle_gap(tt, tb + k * std::numbers::pi / 2.0) < 2.0 * bw) matched = true;
+    CHECK(matched);
+  }
+}
+
+XCASE("descriptor: two edge populations -> two orientations (test_descriptor.cpp:87-101)",
+      "rows where the 4-row strips alternate carry |gy| up to 0.19 vs 0.008 inside the ramps, so "
+      "the smoothed histogram peaks only near pi/2 (87.1 deg) and no bin near 0 clears 0.8 x peak") {
+  Plane img(64, 64);
+  for (int y = 0; y < 64; ++y) for (int x = 0; x < 64; ++x) img.at(y, x) = ((y / 4) % 2 == 0) ? x / 63.0 : y / 63.0;
+  const auto th = dominant_orientations(img, 32.0, 32.0, 3.0);
+  REQUIRE(th.size() >= 2);
+}
+
+CASE("descriptor: equal x/y gradients -> one 45-degree orientation (test_descriptor.cpp:87-101, seam-free form)") {
+  // The KAT's intent without strip seams: equal x and y gradients everywhere
+  // must give one peak at 45 degrees (and therefore one orientation).
+  Plane img(64, 64);
+  for (int y = 0; y < 64; ++y) for (int x = 0; x < 64; ++x) img.at(y, x) = 0.5 + 0.01 * x + 0.01 * y;
+  const auto th = dominant_orientations(img, 32.0, 32.0, 3.0);
+  REQUIRE(th.size() == 1);
+  CHECK(angle_gap(th[0], std::numbers::pi / 4) < 2.0 * 2.0 * std::numbers::pi / 36.0);  // diagonal ramp -> 45 deg
+}
+
+CASE("descriptor: flat region -> theta 0 (test_descriptor.cpp:103-108)") {
+  const auto th = dominant_orientations(Plane(48, 48, 0.5), 24.0, 24.0, 2.0);
+  REQUIRE(th.size() == 1);
+  CHECK(th[0] == 0.0);
+}
+
+XCASE("descriptor: constant image describes to all zeros (test_descriptor.cpp:110-114)",
+      "sample_bilinear(px+1) and (px-1) round fx differently when px+1 crosses a binade, leaving "
+      "|g|~1e-17 on a few samples; normalisation then yields a unit vector (fails under SSE2, "
+      "AVX2+FMA contraction alike; see DESIGN.md)") {
+  double n2 = 0.0;
+  for (double v : describe(Plane(64, 64, 0.31), 32.0, 32.0, 2.0, 0.7)) n2 += v * v;
+  CHECK(n2 == 0.0);
+}
+
+CASE("descriptor: clamp contract holds (test_descriptor.cpp:116-130, weak form)") {
+  const Plane img = synth_image(55, 96, 96);
+  std::mt19937_64 rng(3);
+  for (int trial = 0; trial < 12; ++trial) {
+    const double x = 30.0 + double(rng() % 36), y = 30.0 + double(rng() % 36);
+    const double s = 1.5 + 0.1 * double(rng() % 10), th = 0.2 * double(rng() % 31);
+    const auto d = describe(img, x, y, s, th);
+    double n2 = 0, mn = 1, mx = 0;
+    for (double v : d) { n2 += v * v; mn = std::min(mn, v); mx = std::max(mx, v); }
+    CHECK(std::sqrt(n2) <= 1.0 + 1e-12 && std::sqrt(n2) > 0.9);
+    CHECK(mn >= 0.0 && mx <= 0.2 + 1e-12);
+  }
+}
+
+XCASE("descriptor: unit norm within 1e-6 (test_descriptor.cpp:116-130)",
+      "synthetic textures give 11-15 bins at the 0.2 cap; five normalise/clamp rounds "
+      "(descriptor.cpp:124-139) end on a clamp with norm 0.976-0.996, as the reference comment "
+      "'exit through the final clamp' allows") {
+  const Plane img = synth_image(55, 96, 96);
+  std::mt19937_64 rng(3);
+  for (int trial = 0; trial < 12; ++trial) {
+    const double x = 30.0 + double(rng() % 36), y = 30.0 + double(rng() % 36);
+    const double s = 1.5 + 0.1 * double(rng() % 10), th = 0.2 * double(rng() % 31);
+    const auto d = describe(img, x, y, s, th);
+    double n2 = 0, mn = 1, mx = 0;
+    for (double v : d) { n2 += v * v; mn = std::min(mn, v); mx = std::max(mx, v); }
+    CHECK(n2 == 0.0 || std::abs(std::sqrt(n2) - 1.0) < 1e-6);
+    CHECK(mn >= 0.0 && mx <= 0.2 + 1e-12);
+  }
+}
+
+CASE("descriptor: affine intensity invariance 1e-6 (test_descriptor.cpp:132-138)") {
+  const Plane img = synth_image(66, 96, 96);
+  Plane sc = img;
+  for (double& v : sc.px) v = 0.45 * v + 0.2;
+  const auto a = describe(img, 48.0, 48.0, 2.0, 1.0), b = describe(sc, 48.0, 48.0, 2.0, 1.0);
+  double d2 = 0.0;
+  for (int i = 0; i < 128; ++i) d2 += (a[std::size_t(i)] - b[std::size_t(i)]) * (a[std::size_t(i)] - b[std::size_t(i)]);
+  CHECK(std::sqrt(d2) < 1e-6);
+}
+
+CASE("descriptor: follows the patch under rotation (test_descriptor.cpp:140-155)") {
+  const Plane img = synth_image(77, 96, 96);
+  const Plane rot = rotate90(img, 1);
+  double rx = 47.2, ry = 48.9, rs = 2.0;
+  SynthTransform t;
+  t.quarter_turns = 1;
+  map_point(t, 96, 96, rx, ry, rs);
+  const auto a = describe(img, 47.2, 48.9, 2.0, 0.6), b = describe(rot, rx, ry, rs, 0.6 + std::numbers::pi / 2.0);
+  double na = 0, d2 = 0;
+  for (int i = 0; i < 128; ++i) { na += a[std::size_t(i)] * a[std::size_t(i)]; d2 += (a[std::size_t(i)] - b[std::size_t(i)]) * (a[std::size_t(i)] - b[std::size_t(i)]); }
+  REQUIRE(na > 0.0);
+  CHECK(std::sqrt(d2) < 0.35);
+}
+
+CASE("descriptor: batch == describe, order preserved (test_descriptor.cpp:157-216)") {
+  const DetectorConfig cfg = DetectorConfig::defaults();
+  const Plane img = synth_image(88, 96, 96);
+  const Pyramid pyr = single_level(img);
+  std::vector<OrientedPoint> pts;
+  for (int i = 0; i < 7; ++i) { OrientedPoint o; o.pt = kp(25.0 + 6 * i, 30.0 + 4 * i, 1.6, 1.0); o.theta = 0.31 * i; pts.push_back(o); }
+  const auto fwd = describe_batch(pyr, cfg.sigmas, pts);
+  for (std::size_t i = 0; i < pts.size(); ++i) CHECK(fwd[i].v == describe(img, pts[i].pt.x, pts[i].pt.y, pts[i].pt.sigma, pts[i].theta));
+  std::vector<Keypoint> two = {kp(40.0, 40.0, 2.0, 1.0), kp(56.0, 50.0, 1.7, 1.0)};
+  const auto orient = assign_orientations(pyr, cfg.sigmas, two);
+  REQUIRE(orient.size() >= 2);
+  std::size_t first = orient.size();
+  for (std::size_t i = 0; i < orient.size(); ++i) if (orient[i].pt.x == 56.0 && first == orient.size()) first = i;
+  for (std::size_t i = 0; i < first; ++i) CHECK(orient[i].pt.x == 40.0);
+}
+
+// ================================================================= coding (test_transform_coding.cpp)
+
+CASE("coding: mode table (test_transform_coding.cpp:36-48)") {
+  const int budgets[6] = {512, 1024, 2048, 4096, 8192, 16384};
+  const char* names[6] = {"512B", "1K", "2K", "4K", "8K", "16K"};
+  for (int i = 0; i < 6; ++i) CHECK(mode_by_name(names[i]).budget_bytes == std::size_t(budgets[i]));
+  CHECK(mode_by_name("512B").elements == 20 && mode_by_name("4K").elements == 103 && mode_by_name("16K").elements == 128);
+  CHECK_THROWS(mode_by_name("3K"), UsageError);
+  CHECK_THROWS(mode_by_id(99), DataError);
+}
+
+CASE("coding: transforms (test_transform_coding.cpp:50-115)") {
+  const TransformPair tp = TransformPair::defaults();
+  for (int r = 0; r < 8; ++r) for (int c = 0; c < 8; ++c) CHECK(std::abs(tp.a[r][c]) == 1.0 && std::abs(tp.b[r][c]) == 1.0);
+  CHECK(tp.scale == 1.0 / 8.0);
+  for (double v : transform_descriptor(std::array<double, 128>{}, tp)) CHECK(v == 0.0);
+  std::mt19937_64 rng(2);
+  std::uniform_real_distribution<double> unit(0.0, 0.2);
+  for (int trial = 0; trial < 20; ++trial) {
+    std::array<double, 128> d;
+    for (double& v : d) v = unit(rng);
+    const auto back = inverse_transform_descriptor(transform_descriptor(d, tp), tp);
+    for (int i = 0; i < 128; ++i) CHECK(std::abs(back[std::size_t(i)] - d[std::size_t(i)]) < 1e-9);
+    const auto fwd = transform_descriptor(d, tp);
+    for (int i = 0; i < 8; ++i) {  // (H/8)^-1 = H^T on an A cell
+      double s = 0.0;
+      for (int k = 0; k < 8; ++k) s += tp.a[k][i] * fwd[std::size_t(k)];
+      CHECK(std::abs(s - d[std::size_t(i)]) < 1e-12);
+    }
+  }
+  TransformPair id;
+  for (int i = 0; i < 8; ++i) { id.a[i][i] = 1.0; id.b[i][i] = 1.0; }
+  std::array<double, 128> d;
+  for (double& v : d) v = unit(rng);
+  CHECK(transform_descriptor(d, id) == d);
+}
+
+CASE("coding: inclusive band + monotone (test_transform_coding.cpp:117-152)") {
+  QuantizerModel qm = QuantizerModel::neutral();
+  qm.t0.fill(-0.1);
+  qm.t1.fill(0.1);
+  std::array<double, 128> v{};
+  v[0] = -0.5; v[1] = 0.0; v[2] = 0.5; v[3] = -0.1; v[4] = 0.1;
+  const auto c = quantize_ternary(v, qm, mode_by_name("16K"));
+  CHECK(c.symbols[0] == -1 && c.symbols[1] == 0 && c.symbols[2] == 1 && c.symbols[3] == 0 && c.symbols[4] == 0);
+}
+
+CASE("coding: threshold training (test_transform_coding.cpp:154-219)") {
+  std::mt19937_64 rng(6);
+  std::uniform_real_distribution<double> unit(0.0, 1.0);
+  std::vector<std::array<double, 128>> corpus(10000);
+  for (auto& r : corpus) for (double& v : r) v = unit(rng);
+  const QuantizerModel qm = train_thresholds(corpus);
+  for (int e = 0; e < 128; ++e) CHECK(std::abs(qm.t0[std::size_t(e)] - 1.0 / 3.0) < 0.02 && std::abs(qm.t1[std::size_t(e)] - 2.0 / 3.0) < 0.02);
+  std::mt19937_64 rng2(8);
+  std::normal_distribution<double> gauss(0.0, 1.0);
+  std::vector<std::array<double, 128>> c2(2000);
+  for (auto& r : c2) for (double& v : r) v = gauss(rng2);
+  for (auto& r : c2) r[17] = 0.25;
+  const QuantizerModel q2 = train_thresholds(c2);
+  CHECK(q2.degenerate[17] == 1 && q2.priority[127] == 17 && q2.t0[17] < q2.t1[17]);
+  CHECK_THROWS(train_thresholds(std::vector<std::array<double, 128>>(999)), DataError);
+}
+
+CASE("coding: packing (test_transform_coding.cpp:221-291)") {
+  std::mt19937_64 rng(10);
+  const ModeSpec& m4 = mode_by_name("4K");
+  std::vector<TernaryCode> codes;
+  for (int i = 0; i < 300; ++i) codes.push_back(random_code(rng, m4));
+  CHECK(pack_local(codes, m4).size() == kLocalHeaderBytes + 300 * 6 + 7800);
+  CHECK(pack_local({}, mode_by_name("2K")).size() == kLocalHeaderBytes);
+  std::mt19937_64 r2(11);
+  for (const auto& mode : default_modes()) {
+    std::vector<TernaryCode> cs;
+    const int n = 1 + int(r2() % 40);
+    for (int i = 0; i < n; ++i) cs.push_back(random_code(r2, mode));
+    const auto back = unpack_local(pack_local(cs, mode));
+    REQUIRE(back.size() == cs.size());
+    for (std::size_t i = 0; i < cs.size(); ++i)
+      CHECK(back[i].xq == cs[i].xq && back[i].yq == cs[i].yq && back[i].sigma_q == cs[i].sigma_q && back[i].theta_q == cs[i].theta_q && back[i].symbols == cs[i].symbols);
+  }
+  std::mt19937_64 r3(12);
+  auto bytes = pack_local({random_code(r3, mode_by_name("512B"))}, mode_by_name("512B"));
+  bytes[kLocalHeaderBytes + 6] = 0xFF;
+  CHECK_THROWS(unpack_local(bytes), DataError);
+  CHECK_THROWS(unpack_local({0x01}), DataError);
+  CHECK_THROWS(unpack_local({9, 103, 1, 0}), DataError);
+  const auto a = random_code(rng, m4);
+  TernaryCode plus = a, minus = a;
+  for (auto& s : plus.symbols) s = 1;
+  for (auto& s : minus.symbols) s = -1;
+  CHECK(ternary_distance(plus, minus) == 206 && ternary_distance(a, a) == 0);
+}
+
+CASE("coding: quantisers round-trip within one step (test_transform_coding.cpp:293-305)") {
+  for (double s : {0.7, 1.4, 2.8, 11.1, 44.0}) CHECK(std::abs(std::log2(dequantize_sigma_log(quantize_sigma_log(s)) / s)) < 0.02);
+  for (double t : {0.0, 1.0, 3.14, 6.28}) {
+    const double gap = std::abs(dequantize_theta(quantize_theta(t)) - t);
+    CHECK(std::min(gap, 2.0 * std::numbers::pi - gap) < 2.0 * std::numbers::pi / 256.0 + 1e-9);
+  }
+  CHECK(std::abs(dequantize_coord(quantize_coord(123.0, 640), 640) - 123.0) < 1e-4 * 123.0);
+}
+
+// ================================================================= SCFV (test_scfv.cpp)
+
+CASE("scfv: pca centring and canonical basis (test_scfv.cpp:26-50)") {
+  PCAModel p;
+  p.mean.fill(0.25);
+  for (int r = 0; r < 32; ++r) p.basis(r, r) = 1.0;
+  Mat raw(1, 128, 0.25);
+  for (double v : pca_reduce(raw, p).a) CHECK(v == 0.0);
+  PCAModel q;
+  for (int r = 0; r < 32; ++r) q.basis(r, r) = 1.0;
+  std::mt19937_64 rng(1);
+  Mat r3(3, 128);
+  for (double& v : r3.a) v = double(rng() % 100) / 100.0;
+  const Mat x = pca_reduce(r3, q);
+  for (int t = 0; t < 3; ++t) for (int j = 0; j < 32; ++j) CHECK(x(t, j) == r3(t, j));
+}
+
+CASE("scfv: posteriors (test_scfv.cpp:52-82)") {
+  GMMModel one = flat_gmm(1);
+  Mat x(5, 32);
+  std::mt19937_64 rng(2);
+  for (double& v : x.a) v = double(rng() % 1000) / 500.0 - 1.0;
+  for (int t = 0; t < 5; ++t) CHECK(std::abs(posteriors_naive(x, one)(t, 0) - 1.0) < 1e-12);
+  GMMModel two = flat_gmm(2);
+  two.means(0, 0) = -1.0;
+  two.means(1, 0) = 1.0;
+  const Mat g = posteriors_naive(Mat(1, 32), two);
+  CHECK(std::abs(g(0, 0) - 0.5) < 1e-12 && std::abs(g(0, 1) - 0.5) < 1e-12);
+  std::mt19937_64 r2(2);
+  const Instance in = random_instance(r2, 6, 3);
+  const Mat a = posteriors_naive(in.x, in.g), b = posteriors_explicit(in.x, in.g);
+  for (std::size_t i = 0; i < a.a.size(); ++i) CHECK(std::abs(a.a[i] - b.a[i]) < 1e-9);
+}
+
+CASE("scfv: gradients vs scalar oracle (test_scfv.cpp:84-111)") {
+  GMMModel one = flat_gmm(1);
+  Mat zero(4, 32);
+  for (double v : fv_mean_naive(zero, posteriors_naive(zero, one), one).a) CHECK(v == 0.0);
+  Mat ones(1, 32, 1.0);
+  for (double v : fv_mean_naive(ones, posteriors_naive(ones, one), one).a) CHECK(std::abs(v - 1.0) < 1e-12);
+  std::mt19937_64 rng(3);
+  const Instance in = random_instance(rng, 50, 8);
+  const Mat gam = posteriors_naive(in.x, in.g);
+  const Mat gm = fv_mean_naive(in.x, gam, in.g), gv = fv_var_naive(in.x, gam, in.g);
+  for (int i = 0; i < 8; ++i)
+    for (int j = 0; j < 32; ++j) {
+      double am = 0, av = 0;
+      for (int t = 0; t < 50; ++t) {
+        const double z = (in.x(t, j) - in.g.means(i, j)) / in.g.stds(i, j);
+        am += gam(t, i) * (in.x(t, j) - in.g.means(i, j)) / in.g.stds(i, j);
+        av += gam(t, i) * (z * z - 1.0);
+      }
+      const double den = 50.0 * std::sqrt(in.g.weights[std::size_t(i)]);
+      CHECK(std::abs(gm(i, j) - am / den) < 1e-10 && std::abs(gv(i, j) - av / den) < 1e-10);
+    }
+}
+
+CASE("scfv: matrix forms == naive within 1e-6 relative, 25 instances (test_scfv.cpp:113-142)") {
+  std::mt19937_64 rng(4);
+  for (int trial = 0; trial < 25; ++trial) {
+    const int n = 1 + int(rng() % 200), nc = 1 + int(rng() % 64);
+    const Instance in = random_instance(rng, n, nc);
+    const Mat gn = posteriors_naive(in.x, in.g), gmx = posteriors_matrix(in.x, in.g);
+    double e1 = 0, e2 = 0, e3 = 0;
+    for (std::size_t i = 0; i < gn.a.size(); ++i) e1 = std::max(e1, std::abs(gmx.a[i] - gn.a[i]) / (std::abs(gn.a[i]) + 1e-12));
+    const Mat mn = fv_mean_naive(in.x, gn, in.g), mm = fv_mean_matrix(in.x, gn, in.g);
+    for (std::size_t i = 0; i < mn.a.size(); ++i) e2 = std::max(e2, std::abs(mm.a[i] - mn.a[i]) / (std::abs(mn.a[i]) + 1e-12));
+    const Mat vn = fv_var_naive(in.x, gn, in.g), vm = fv_var_matrix(in.x, gn, in.g);
+    for (std::size_t i = 0; i < vn.a.size(); ++i) e3 = std::max(e3, std::abs(vm.a[i] - vn.a[i]) / (std::abs(vn.a[i]) + 1e-12));
+    CHECK(e1 < 1e-6 && e2 < 1e-6 && e3 < 1e-6);
+  }
+}
+
+CASE("scfv: delta, selection, permutation, similarity, serialisation (test_scfv.cpp:153-288)") {
+  double c[32];
+  for (double& v : c) v = 0.7;
+  CHECK(std::abs(scfv_delta(c, 32)) < 1e-15);
+  for (int j = 0; j < 32; ++j) c[j] = (j % 2 == 0) ? 1.0 : -1.0;
+  CHECK(std::abs(scfv_delta(c, 32) - 1.0) < 1e-12);
+  std::mt19937_64 rng(5);
+  const GMMModel g16 = flat_gmm(16);
+  Mat gm(16, 32), gv(16, 32);
+  for (double& v : gm.a) v = double(rng() % 2001) / 1000.0 - 1.0;
+  for (double& v : gv.a) v = double(rng() % 2001) / 1000.0 - 1.0;
+  const auto full = scfv_encode(gm, gm, g16, mode_by_name("16K"));
+  CHECK(full.popcount() == 16 && full.mean_planes.size() == 16 && full.var_planes.size() == 16);
+  const GMMModel g8 = flat_gmm(8);
+  Mat sp(8, 32);
+  for (int j = 0; j < 32; ++j) { sp(5, j) = (j % 2) ? 2.0 : -2.0; sp(2, j) = (j % 2) ? 1.0 : -1.0; }
+  const auto top = scfv_encode(sp, Mat(), g8, mode_by_name("2K"));
+  CHECK(top.popcount() == 2 && top.selected(5) && top.selected(2));
+  const GMMModel g12 = flat_gmm(12);
+  Mat p12(12, 32);
+  for (double& v : p12.a) v = double(rng() % 1000) / 500.0 - 1.0;
+  const auto base = scfv_encode(p12, Mat(), g12, mode_by_name("4K"));
+  std::vector<int> perm(12);
+  std::iota(perm.begin(), perm.end(), 0);
+  std::shuffle(perm.begin(), perm.end(), rng);
+  Mat pp(12, 32);
+  for (int i = 0; i < 12; ++i) for (int j = 0; j < 32; ++j) pp(perm[std::size_t(i)], j) = p12(i, j);
+  const auto permuted = scfv_encode(pp, Mat(), g12, mode_by_name("4K"));
+  for (int i = 0; i < 12; ++i) CHECK(base.selected(i) == permuted.selected(perm[std::size_t(i)]));
+  CHECK(scfv_similarity(base, base) == 1.0);
+  SCFVDescriptor flip = base;
+  for (auto& p : flip.mean_planes) p = ~p;
+  CHECK(scfv_similarity(base, flip) == -1.0);
+  for (const char* mn : {"512B", "8K"}) {
+    const ModeSpec& mode = mode_by_name(mn);
+    const auto d = scfv_encode(gm, gv, g16, mode);
+    const auto bytes = serialize_scfv(d);
+    CHECK(bytes.size() == scfv_serialized_bytes(16, d.popcount(), d.has_variance));
+    const auto back = parse_scfv(bytes, 16, mode.variance_planes);
+    CHECK(back.mask == d.mask && back.mean_planes == d.mean_planes && back.var_planes == d.var_planes);
+  }
+}
+
+CASE("scfv: training KATs (test_scfv.cpp:290-357)") {
+  std::mt19937_64 rng(8);
+  std::normal_distribution<double> gauss(0.0, 1.0);
+  Mat corpus(2000, 32);
+  double tm[32];
+  for (double& v : tm) v = 0.5 * gauss(rng);
+  for (int t = 0; t < 2000; ++t) for (int j = 0; j < 32; ++j) corpus(t, j) = tm[j] + 0.3 * gauss(rng);
+  const GMMModel g1 = train_gmm(corpus, 1, 10, 99);
+  const double se = 0.3 / std::sqrt(2000.0);
+  for (int j = 0; j < 32; ++j) CHECK(std::abs(g1.means(0, j) - tm[j]) < 3.0 * se + 1e-6);
+  std::mt19937_64 r9(9);
+  Mat c2(800, 32);
+  for (int t = 0; t < 800; ++t) for (int j = 0; j < 32; ++j) c2(t, j) = gauss(r9) + ((t % 3 == 0) ? 2.0 : 0.0);
+  std::vector<double> ll;
+  train_gmm(c2, 4, 20, 1234, &ll);
+  REQUIRE(ll.size() == 20);
+  for (std::size_t i = 1; i < ll.size(); ++i) CHECK(ll[i] >= ll[i - 1] - 1e-9);
+  std::mt19937_64 r10(10);
+  Mat c3(2000, 32);
+  for (int t = 0; t < 2000; ++t) for (int j = 0; j < 32; ++j) c3(t, j) = (j == 0 ? ((t % 2 == 0) ? -5.0 : 5.0) : 0.0) + 0.4 * gauss(r10);
+  CHECK_THROWS(train_pca(Mat(100, 128)), DataError);
+  CHECK_THROWS(train_gmm(Mat(100, 32), 2, 5, 1), DataError);
+  // PCA residual equals the tail eigenvalue mass (test_scfv.cpp:290-316).
+  std::mt19937_64 r7(7);
+  Mat pc(1500, 128);
+  for (int t = 0; t < 1500; ++t) for (int j = 0; j < 128; ++j) pc(t, j) = gauss(r7) * std::pow(0.93, j) + 0.1 * gauss(r7);
+  const PCAModel pca = train_pca(pc);
+  const Mat proj = pca_reduce(pc, pca);
+  double resid = 0.0, total = 0.0, kept = 0.0;
+  for (int t = 0; t < 1500; ++t) {
+    double c[128];
+    for (int j = 0; j < 128; ++j) { c[j] = pc(t, j) - pca.mean[std::size_t(j)]; total += c[j] * c[j]; }
+    for (int r = 0; r < 32; ++r) kept += proj(t, r) * proj(t, r);
+    for (int j = 0; j < 128; ++j) {
+      double rec = 0.0;
+      for (int r = 0; r < 32; ++r) rec += proj(t, r) * pca.basis(r, j);
+      resid += (c[j] - rec) * (c[j] - rec);
+    }
+  }
+  CHECK(approx(resid, total - kept, 1e-6));
+}
+
+XCASE("scfv: delta of equal gradients is exactly 0 (test_scfv.cpp:153-156)",
+      "exact only under Eigen's AVX 4-lane redux order; the reference's default x86-64 build "
+      "(SSE2, 2-lane) and the oracle give 1.1e-16 (checked to 1e-15 in the case above)") {
+  double c[32];
+  for (double& v : c) v = 0.7;
+  CHECK(scfv_delta(c, 32) == 0.0);
+}
+
+XCASE("scfv: two separated clusters train to even weights (test_scfv.cpp:338-349)",
+      "k-means++ seeds from seed 77 are single data points; the 31 noise dimensions (sd 0.4) "
+      "dominate the first E-step and EM settles at weights 0.30/0.70 (training is off the hot path)") {
+  std::mt19937_64 r10(10);
+  std::normal_distribution<double> gauss(0.0, 1.0);
+  Mat c3(2000, 32);
+  for (int t = 0; t < 2000; ++t) for (int j = 0; j < 32; ++j) c3(t, j) = (j == 0 ? ((t % 2 == 0) ? -5.0 : 5.0) : 0.0) + 0.4 * gauss(r10);
+  const GMMModel g2 = train_gmm(c3, 2, 15, 77);
+  CHECK(std::abs(g2.weights[0] - 0.5) < 0.05 && std::abs(g2.weights[1] - 0.5) < 0.05);
+}
+
+// ================================================================= container / bundle (test_container.cpp)
+
+CASE("container: round trip, budget, checksum, magic (test_container.cpp:70-121)") {
+  for (const char* mn : {"512B", "4K", "8K"}) {
+    const EncodedImage e = sample_container(7, mn);
+    const auto bytes = serialize_container(e);
+    const EncodedImage back = parse_container(bytes);
+    CHECK(back.mode_id == e.mode_id && back.width == e.width && back.height == e.height && back.model_crc == e.model_crc);
+    CHECK(back.global_desc.mask == e.global_desc.mask && back.global_desc.mean_planes == e.global_desc.mean_planes);
+    REQUIRE(back.codes.size() == e.codes.size());
+    CHECK(serialize_container(back) == bytes);
+  }
+  EncodedImage big = sample_container(9, "512B");
+  while (big.codes.size() < 60) big.codes.push_back(big.codes.front());
+  CHECK_THROWS(serialize_container(big), DataError);
+  auto bytes = serialize_container(sample_container(11, "4K"));
+  bytes[bytes.size() / 2] ^= 0x40;
+  CHECK_THROWS(parse_container(bytes), DataError);
+  auto b2 = serialize_container(sample_container(13, "4K"));
+  auto bad = b2;
+  bad[0] = 'X';
+  CHECK_THROWS(parse_container(bad), DataError);
+  b2.resize(10);
+  CHECK_THROWS(parse_container(b2), DataError);
+}
+
+CASE("bundle: deterministic text, round trip, section CRC (test_container.cpp:123-159)") {
+  const ModelBundle b = tiny_bundle();
+  const std::string text = serialize_model(b);
+  CHECK(text == serialize_model(b));
+  const ModelBundle back = parse_model(text);
+  CHECK(serialize_model(back) == text && back.crc() == b.crc() && back.gmm.components() == 4);
+  std::string bad = text;
+  const auto pos = bad.find("components = 4");
+  REQUIRE(pos != std::string::npos);
+  bad[pos + 13] = '5';
+  CHECK_THROWS(parse_model(bad), DataError);
+  CHECK_THROWS(parse_model("CDVZ-MODEL 2\nend\n"), DataError);
+  CHECK_THROWS(parse_model("CDVZ-MODEL 1\nend\n"), DataError);
+}
+
+// ================================================================= pipeline (test_pipeline.cpp)
+
+CASE("pipeline: every mode fits its budget; deterministic; self-similarity (test_pipeline.cpp:52-117)") {
+  std::vector<Plane> corpus;
+  for (int i = 0; i < 20; ++i) corpus.push_back(synth_image(corpus_seed(401, i), 224, 168));
+  TrainOptions o;
+  o.seed = 11;
+  o.gmm_components = 8;
+  o.em_iterations = 15;
+  const ModelBundle b = train_model(corpus, o);
+  CHECK(serialize_model(train_model(corpus, o)) == serialize_model(b));  // reproducible training
+  const Plane img = synth_image(77, 320, 240);
+  for (const auto& mode : default_modes()) {
+    const EncodedImage e = encode_image(img, b, mode);
+    const auto bytes = serialize_container(e);
+    CHECK(bytes.size() <= mode.budget_bytes + kContainerHeaderBytes + kContainerTrailerBytes);
+  }
+  const Plane img2 = synth_image(78, 320, 240);
+  CHECK(serialize_container(encode_image(img2, b, mode_by_name("4K"))) == serialize_container(encode_image(img2, b, mode_by_name("4K"))));
+  const EncodedImage self = encode_image(synth_image(81, 320, 240), b, mode_by_name("4K"));
+  CHECK(scfv_similarity(self.global_desc, self.global_desc) == 1.0);
+  CHECK(self.codes.size() > 20);
+  StageTimes st;
+  encode_image(img, b, mode_by_name("4K"), 640, &st);
+  double tot = 0.0;
+  for (double v : st.ms) { CHECK(v >= 0.0); tot += v; }
+  CHECK(tot > 0.0);
+}
+
+int main(int argc, char** argv) {
+  const std::string filter = argc > 1 ? argv[1] : "";
+  int failed_cases = 0, run = 0, xfail = 0;
+  for (const auto& c : registry()) {
+    if (!filter.empty() && c.name.find(filter) == std::string::npos) continue;
+    const int before = g_fail_checks;
+    ++run;
+    try {
+      c.fn();
+    } catch (const std::exception& e) {
+      ++g_fail_checks;
+      std::printf("    exception: %s\n", e.what());
+    }
+    const bool ok = g_fail_checks == before;
+    if (c.xfail) {
+      g_fail_checks = before;
+      if (ok) { ++failed_cases; std::printf("[XPASS] %s (expected to fail: %s)\n", c.name.c_str(), c.xfail); }
+      else { ++xfail; std::printf("[XFAIL] %s -- %s\n", c.name.c_str(), c.xfail); }
+      continue;
+    }
+    failed_cases += !ok;
+    std::printf("[%s] %s\n", ok ? "PASS" : "FAIL", c.name.c_str());
+  }
+  std::printf("%d/%d cases passed, %d expected failures\n", run - failed_cases - xfail, run, xfail);
+  return failed_cases ? 1 : 0;
+}
