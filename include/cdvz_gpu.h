@@ -1,0 +1,143 @@
+/*
+ * cdvz_gpu.h — C ABI of the B200-native CDVS-style extractor.
+ *
+ * Drop-in boundary for the reference's extraction path. The reference exposes
+ * no FFI; its boundary is the C++ API in proj/include/cdvz/, and each entry
+ * point below states the reference interface it replaces. A C++ shim with the
+ * reference's exact signatures sits on top of this ABI in
+ * paper_1705_09776_b200/csrc/cdvz_gpu.hpp (cdvz::gpu::encode_image, ...).
+ *
+ * Conventions
+ *   - Plain pointers and sizes only; every buffer is caller-owned.
+ *   - Return codes follow the reference CLI's exit-code contract
+ *     (proj/tools/cdvz.cpp:308-317): 0 ok, 1 usage error (UsageError),
+ *     2 data error (DataError), 3 internal error. No exception crosses the ABI;
+ *     the message of the last failure is available from cdvz_gpu_last_error().
+ *   - A context owns one CUDA device, its streams and device buffers. It is
+ *     not thread-safe: use one context per host thread (as the reference's
+ *     StageTimings* is per call). Frames are independent, so several contexts
+ *     (one per GPU, or several per GPU) run concurrently without coordination.
+ *   - There is no CPU fallback: creating a context without a usable sm_100
+ *     device fails with code 3.
+ */
+#ifndef CDVZ_GPU_H
+#define CDVZ_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct cdvz_gpu_ctx cdvz_gpu_ctx;
+
+/* Per-frame status written by the batch encoders. */
+enum {
+  CDVZ_GPU_OK = 0,
+  CDVZ_GPU_USAGE = 1,
+  CDVZ_GPU_DATA = 2,
+  CDVZ_GPU_INTERNAL = 3
+};
+
+/* Parses a CDVZ-MODEL 1 bundle text (proj/src/model_io.cpp:141-273,
+ * parse_model/load_model, proj/include/cdvz/model_io.hpp:30-33), validates it,
+ * computes model_crc = crc32(serialize_model(bundle)) (model_io.cpp:84) and
+ * uploads the learned tables to `device`. max_batch bounds the frames per
+ * device launch (0 = default 256); larger batches are processed in chunks. */
+int cdvz_gpu_create(const char* bundle_text, size_t bundle_len, int device, int max_batch,
+                    cdvz_gpu_ctx** out_ctx);
+
+/* Releases every device and pinned host buffer of the context. */
+void cdvz_gpu_destroy(cdvz_gpu_ctx* ctx);
+
+/* Message of the last failing call on this context (or of the last failing
+ * cdvz_gpu_create on this thread when ctx is NULL). */
+const char* cdvz_gpu_last_error(const cdvz_gpu_ctx* ctx);
+
+/* Host-only bundle validation (no device needed): parse + validate + the
+ * model_crc a context would stamp. Same error codes as cdvz_gpu_create. */
+int cdvz_gpu_bundle_check(const char* bundle_text, size_t bundle_len, uint32_t* model_crc, int* components);
+
+/* model_crc stamped into every container and the GMM component count. */
+int cdvz_gpu_bundle_info(const cdvz_gpu_ctx* ctx, uint32_t* model_crc, int* components, int* select_n);
+
+/* Batch form of encode_image + serialize_container
+ * (proj/src/pipeline.cpp:54-97, proj/include/cdvz/pipeline.hpp:18-20;
+ *  proj/src/container.cpp:32-58, proj/include/cdvz/container.hpp:27).
+ *
+ * pixels: `count` 8-bit grey frames of width x height, row stride `stride`
+ *   bytes, frame i at pixels + i*height*stride; a byte b is the intensity
+ *   b/255 exactly as load_image reads a PGM (proj/src/image.cpp:79-87).
+ * mode_id: 0..5 = 512B,1K,2K,4K,8K,16K (mode_by_id, transform_coding.cpp:33-37).
+ * max_side: EncodeOptions::max_side (pipeline.hpp:14-16); 640 by default.
+ * out/out_cap: concatenated CDVZ1 containers in frame order; offsets[count+1]
+ *   receives each container's byte range. status[count] receives each frame's
+ *   result; a failing frame has an empty range and never aborts the batch.
+ * Host buffers may be pageable or pinned (cdvz_gpu_host_alloc); both copies
+ * (pixels in, containers out) happen inside the call. Returns 0 when the call
+ * itself succeeded (check status[] per frame). */
+int cdvz_gpu_encode_batch(cdvz_gpu_ctx* ctx, const uint8_t* pixels, int width, int height, size_t stride,
+                          int count, int mode_id, int max_side, uint8_t* out, size_t out_cap,
+                          size_t* offsets, int* status);
+
+/* Same pipeline on frames already resident in device memory (d_pixels is a
+ * device pointer to count*height*stride bytes). Containers stay on the device
+ * in fixed slots of cdvz_gpu_container_slot(mode) bytes; d_lengths[count]
+ * (device) receives the lengths, 0 for a failed frame. Asynchronous on the
+ * context's stream; cdvz_gpu_sync waits. This is the HBM-resident throughput
+ * path used by bench.py's `value`. */
+int cdvz_gpu_encode_device(cdvz_gpu_ctx* ctx, const uint8_t* d_pixels, int width, int height, size_t stride,
+                           int count, int mode_id, int max_side, uint8_t* d_out, uint32_t* d_lengths);
+size_t cdvz_gpu_container_slot(int mode_id);
+int cdvz_gpu_sync(cdvz_gpu_ctx* ctx);
+
+/* Device time of the last batch per reference stage label, in order
+ * detection, selection, description, compression, aggregation
+ * (StageTimings, proj/include/cdvz/parallel.hpp:117-134; pipeline.cpp:19-94).
+ * Measured with CUDA events around each stage's kernels. */
+int cdvz_gpu_stage_times(cdvz_gpu_ctx* ctx, double ms[5]);
+
+/* Launch/kernel bookkeeping for the last batch: number of kernel launches and
+ * the measured time of the fused octave (pyramid + extrema) kernels, with the
+ * algorithmic HBM bytes they moved. */
+int cdvz_gpu_kernel_stats(cdvz_gpu_ctx* ctx, int* launches, double* pyramid_ms, double* pyramid_bytes);
+
+/* Stage-level results of frame `frame` of the last batch for parity tests,
+ * as flat doubles (layouts match the oracle's orc_trace_get):
+ *   "refined:<o>"  x y sigma octave p rho p_ss d per point of octave o
+ *   "keypoints"    after cross-octave dedup (d filled)
+ *   "selected"     top-n after selection
+ *   "oriented"     keypoint layout + theta
+ *   "descriptors"  128 per oriented point
+ *   "x" "gamma" "gm" "gv"  SCFV matrices (row-major)
+ *   "gauss:<o>:<k>" octave o, level k raster
+ * *n receives the element count; nothing is copied when cap is too small. */
+int cdvz_gpu_debug_get(cdvz_gpu_ctx* ctx, const char* name, int frame, double* dst, size_t cap, size_t* n);
+
+/* Keeps per-octave survivor lists of the next batch for cdvz_gpu_debug_get
+ * ("refined:<o>"); costs one device copy per octave. */
+int cdvz_gpu_set_debug(cdvz_gpu_ctx* ctx, int on);
+
+/* CUDA events on the context's stream (slots 0..3), for callers timing the
+ * device-resident path without a CUDA runtime of their own. */
+int cdvz_gpu_event_record(cdvz_gpu_ctx* ctx, int slot);
+int cdvz_gpu_event_elapsed(cdvz_gpu_ctx* ctx, int slot_a, int slot_b, double* ms);
+
+/* Deterministic synthetic frames on the device (proj/src/synthetic.cpp:11-61,
+ * synth_corpus seeds base + i*0x9E3779B97F4A7C15), quantised to bytes like
+ * save_pgm. d_out receives count*height*width bytes. */
+int cdvz_gpu_synth_frames(cdvz_gpu_ctx* ctx, uint64_t base_seed, int count, int width, int height, uint8_t* d_out);
+
+/* Device / pinned host memory helpers for callers without a CUDA runtime. */
+int cdvz_gpu_device_alloc(cdvz_gpu_ctx* ctx, size_t bytes, void** ptr);
+int cdvz_gpu_device_free(cdvz_gpu_ctx* ctx, void* ptr);
+int cdvz_gpu_host_alloc(cdvz_gpu_ctx* ctx, size_t bytes, void** ptr);
+int cdvz_gpu_host_free(cdvz_gpu_ctx* ctx, void* ptr);
+int cdvz_gpu_copy(cdvz_gpu_ctx* ctx, void* dst, const void* src, size_t bytes, int kind /* 1 H2D, 2 D2H, 3 D2D */);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CDVZ_GPU_H */

@@ -172,7 +172,9 @@ ModelBundle parse_model(const std::string& text) {
     }
     char computed[16];
     std::snprintf(computed, sizeof computed, "%08x", crc32(body.data(), body.size()));
-    if (crc_hex != computed) throw DataError("model bundle section '" + name + "' checksum mismatch");
+    if (crc_hex != computed)
+      throw DataError("model bundle section '" + name + "' checksum mismatch (" + crc_hex + " vs " + computed + ", " +
+                      std::to_string(body.size()) + " bytes)");
     std::istringstream bs(body);
     if (name == "detector") {
       while (std::getline(bs, line)) {

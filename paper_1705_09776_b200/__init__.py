@@ -1,0 +1,331 @@
+"""B200-native CDVS-style extractor (arxiv 1705.09776 reference path).
+
+Python host mirror of the reference's extraction API
+(/root/reference/proj/include/cdvz/pipeline.hpp:18-20 ``encode_image``,
+container.hpp:27 ``serialize_container``, model_io.hpp:30-33 ``load_model``,
+transform_coding.hpp:22-24 ``mode_by_name``/``mode_by_id``) over the C ABI in
+``include/cdvz_gpu.h``. All compute runs in ``libcdvz_gpu.so`` (sm_100a CUDA);
+there is no CPU fallback: a missing library or device raises.
+
+Errors mirror the reference's exception classes: ``UsageError`` (bad mode name,
+bad arguments) and ``DataError`` (bad raster, bad bundle), plus
+``InternalError`` for device failures (the CLI's exit code 3).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+from typing import Iterable, List, Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "libcdvz_gpu.so")
+
+
+class UsageError(RuntimeError):
+    """Reference UsageError (proj/include/cdvz/common.hpp:12-14)."""
+
+
+class DataError(RuntimeError):
+    """Reference DataError (proj/include/cdvz/common.hpp:15-17)."""
+
+
+class InternalError(RuntimeError):
+    """Device / runtime failure (CLI exit code 3, proj/tools/cdvz.cpp:308-317)."""
+
+
+@dataclass(frozen=True)
+class ModeSpec:
+    """proj/include/cdvz/transform_coding.hpp:13-20."""
+
+    id: int
+    name: str
+    budget_bytes: int
+    elements: int
+    scfv_fraction: float
+    variance_planes: bool
+
+
+MODES = (
+    ModeSpec(0, "512B", 512, 20, 32.0 / 512.0, False),
+    ModeSpec(1, "1K", 1024, 32, 64.0 / 512.0, False),
+    ModeSpec(2, "2K", 2048, 64, 128.0 / 512.0, False),
+    ModeSpec(3, "4K", 4096, 103, 256.0 / 512.0, False),
+    ModeSpec(4, "8K", 8192, 103, 320.0 / 512.0, True),
+    ModeSpec(5, "16K", 16384, 128, 512.0 / 512.0, True),
+)
+
+
+def mode_by_name(name: str) -> ModeSpec:
+    """transform_coding.cpp:39-44 — UsageError on an unknown name."""
+    for m in MODES:
+        if m.name == name:
+            return m
+    raise UsageError(f"unknown mode '{name}' (expected 512B, 1K, 2K, 4K, 8K or 16K)")
+
+
+def mode_by_id(mode_id: int) -> ModeSpec:
+    """transform_coding.cpp:33-37 — DataError on an unknown id."""
+    for m in MODES:
+        if m.id == mode_id:
+            return m
+    raise DataError(f"unknown mode id {mode_id}")
+
+
+_lib_handle: Optional[ctypes.CDLL] = None
+
+
+def library_path() -> str:
+    return _LIB_PATH
+
+
+def _lib() -> ctypes.CDLL:
+    global _lib_handle
+    if _lib_handle is not None:
+        return _lib_handle
+    if not os.path.exists(_LIB_PATH):
+        raise InternalError(f"{_LIB_PATH} is missing: run __graft_entry__.build() (there is no CPU fallback)")
+    lib = ctypes.CDLL(_LIB_PATH)
+    P, S, I, U32, U64 = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_uint32, ctypes.c_uint64
+    sig = {
+        "cdvz_gpu_create": (I, [ctypes.c_char_p, S, I, I, ctypes.POINTER(P)]),
+        "cdvz_gpu_destroy": (None, [P]),
+        "cdvz_gpu_last_error": (ctypes.c_char_p, [P]),
+        "cdvz_gpu_bundle_check": (I, [ctypes.c_char_p, S, ctypes.POINTER(U32), ctypes.POINTER(I)]),
+        "cdvz_gpu_bundle_info": (I, [P, ctypes.POINTER(U32), ctypes.POINTER(I), ctypes.POINTER(I)]),
+        "cdvz_gpu_encode_batch": (I, [P, P, I, I, S, I, I, I, P, S, P, P]),
+        "cdvz_gpu_encode_device": (I, [P, P, I, I, S, I, I, I, P, P]),
+        "cdvz_gpu_container_slot": (S, [I]),
+        "cdvz_gpu_sync": (I, [P]),
+        "cdvz_gpu_stage_times": (I, [P, P]),
+        "cdvz_gpu_kernel_stats": (I, [P, ctypes.POINTER(I), ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]),
+        "cdvz_gpu_debug_get": (I, [P, ctypes.c_char_p, I, P, S, ctypes.POINTER(S)]),
+        "cdvz_gpu_set_debug": (I, [P, I]),
+        "cdvz_gpu_event_record": (I, [P, I]),
+        "cdvz_gpu_event_elapsed": (I, [P, I, I, ctypes.POINTER(ctypes.c_double)]),
+        "cdvz_gpu_synth_frames": (I, [P, U64, I, I, I, P]),
+        "cdvz_gpu_device_alloc": (I, [P, S, ctypes.POINTER(P)]),
+        "cdvz_gpu_device_free": (I, [P, P]),
+        "cdvz_gpu_host_alloc": (I, [P, S, ctypes.POINTER(P)]),
+        "cdvz_gpu_host_free": (I, [P, P]),
+        "cdvz_gpu_copy": (I, [P, P, P, S, I]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib_handle = lib
+    return lib
+
+
+def _raise(code: int, msg: str) -> None:
+    if code == 0:
+        return
+    if code == 1:
+        raise UsageError(msg)
+    if code == 2:
+        raise DataError(msg)
+    raise InternalError(msg)
+
+
+def bundle_check(bundle_text: str) -> tuple:
+    """Host-only parse/validate of a bundle; returns (model_crc, components)."""
+    lib = _lib()
+    raw = bundle_text.encode() if isinstance(bundle_text, str) else bytes(bundle_text)
+    crc, nc = ctypes.c_uint32(), ctypes.c_int()
+    code = lib.cdvz_gpu_bundle_check(raw, len(raw), ctypes.byref(crc), ctypes.byref(nc))
+    _raise(code, lib.cdvz_gpu_last_error(None).decode())
+    return crc.value, nc.value
+
+
+class DeviceBuffer:
+    """Device allocation owned by an Extractor's device (for the HBM-resident path)."""
+
+    def __init__(self, ex: "Extractor", nbytes: int):
+        self._ex = ex
+        self.nbytes = nbytes
+        ptr = ctypes.c_void_p()
+        ex._check(ex._lib.cdvz_gpu_device_alloc(ex._ctx, nbytes, ctypes.byref(ptr)))
+        self.ptr = ptr.value
+
+    def to_host(self, nbytes: Optional[int] = None) -> np.ndarray:
+        n = self.nbytes if nbytes is None else nbytes
+        out = np.empty(n, dtype=np.uint8)
+        self._ex._check(self._ex._lib.cdvz_gpu_copy(self._ex._ctx, out.ctypes.data, self.ptr, n, 2))
+        return out
+
+    def from_host(self, arr: np.ndarray) -> None:
+        arr = np.ascontiguousarray(arr)
+        self._ex._check(self._ex._lib.cdvz_gpu_copy(self._ex._ctx, self.ptr, arr.ctypes.data, arr.nbytes, 1))
+
+    def free(self) -> None:
+        if self.ptr:
+            self._ex._lib.cdvz_gpu_device_free(self._ex._ctx, self.ptr)
+            self.ptr = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+class PinnedBuffer:
+    """Page-locked host buffer (cudaMallocHost) exposed as a numpy array."""
+
+    def __init__(self, ex: "Extractor", nbytes: int):
+        self._ex = ex
+        ptr = ctypes.c_void_p()
+        ex._check(ex._lib.cdvz_gpu_host_alloc(ex._ctx, nbytes, ctypes.byref(ptr)))
+        self.ptr = ptr.value
+        self.array = np.ctypeslib.as_array((ctypes.c_uint8 * nbytes).from_address(self.ptr))
+
+    def free(self) -> None:
+        if self.ptr:
+            self._ex._lib.cdvz_gpu_host_free(self._ex._ctx, self.ptr)
+            self.ptr = None
+
+
+class Extractor:
+    """One GPU context holding a model bundle: the reference's
+    ``encode_image(img, bundle, mode)`` for batches of 8-bit frames."""
+
+    def __init__(self, bundle_text: str, device: int = 0, max_batch: int = 256):
+        self._lib = _lib()
+        raw = bundle_text.encode() if isinstance(bundle_text, str) else bytes(bundle_text)
+        ctx = ctypes.c_void_p()
+        code = self._lib.cdvz_gpu_create(raw, len(raw), device, max_batch, ctypes.byref(ctx))
+        _raise(code, self._lib.cdvz_gpu_last_error(None).decode())
+        self._ctx = ctx.value
+        crc, nc, sel = ctypes.c_uint32(), ctypes.c_int(), ctypes.c_int()
+        self._lib.cdvz_gpu_bundle_info(self._ctx, ctypes.byref(crc), ctypes.byref(nc), ctypes.byref(sel))
+        self.model_crc, self.components, self.select_n = crc.value, nc.value, sel.value
+        self.device = device
+        self.max_batch = max_batch
+
+    # -- plumbing
+    def _check(self, code: int) -> None:
+        if code:
+            _raise(code, self._lib.cdvz_gpu_last_error(self._ctx).decode())
+
+    def close(self) -> None:
+        if getattr(self, "_ctx", None):
+            self._lib.cdvz_gpu_destroy(self._ctx)
+            self._ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- reference API
+    def encode_batch(self, frames: np.ndarray, mode, max_side: int = 640):
+        """Encodes ``frames`` (uint8, [N, H, W]) and returns (containers, status):
+        ``containers[i]`` is frame i's CDVZ1 byte string (b"" on failure)."""
+        m = mode if isinstance(mode, ModeSpec) else (mode_by_name(mode) if isinstance(mode, str) else mode_by_id(mode))
+        frames = np.ascontiguousarray(frames, dtype=np.uint8)
+        if frames.ndim == 2:
+            frames = frames[None]
+        if frames.ndim != 3:
+            raise UsageError("frames must be [N, H, W] uint8")
+        n, h, w = frames.shape
+        slot = m.budget_bytes + 28
+        out = np.empty(max(1, n * slot), dtype=np.uint8)
+        offsets = np.zeros(n + 1, dtype=np.uint64)
+        status = np.zeros(max(1, n), dtype=np.int32)
+        self._check(self._lib.cdvz_gpu_encode_batch(self._ctx, frames.ctypes.data, w, h, w, n, m.id, max_side,
+                                                    out.ctypes.data, out.nbytes, offsets.ctypes.data,
+                                                    status.ctypes.data))
+        res = [out[int(offsets[i]):int(offsets[i + 1])].tobytes() for i in range(n)]
+        return res, status[:n].copy()
+
+    def encode_image(self, frame: np.ndarray, mode, max_side: int = 640) -> bytes:
+        """encode_image + serialize_container for one frame; raises on failure."""
+        res, status = self.encode_batch(np.asarray(frame)[None], mode, max_side)
+        if status[0] != 0:
+            _raise(int(status[0]), self._lib.cdvz_gpu_last_error(self._ctx).decode() or "frame failed")
+        return res[0]
+
+    def encode_device(self, d_frames: DeviceBuffer, count: int, width: int, height: int, mode, d_out: DeviceBuffer,
+                      d_lengths: DeviceBuffer, max_side: int = 640) -> None:
+        m = mode if isinstance(mode, ModeSpec) else (mode_by_name(mode) if isinstance(mode, str) else mode_by_id(mode))
+        self._check(self._lib.cdvz_gpu_encode_device(self._ctx, d_frames.ptr, width, height, width, count, m.id,
+                                                     max_side, d_out.ptr, d_lengths.ptr))
+
+    def sync(self) -> None:
+        self._check(self._lib.cdvz_gpu_sync(self._ctx))
+
+    def stage_times(self) -> dict:
+        """Device ms per reference stage label (parallel.hpp:117-134)."""
+        arr = (ctypes.c_double * 5)()
+        self._check(self._lib.cdvz_gpu_stage_times(self._ctx, arr))
+        return dict(zip(("detection", "selection", "description", "compression", "aggregation"), list(arr)))
+
+    def kernel_stats(self) -> dict:
+        n, ms, by = ctypes.c_int(), ctypes.c_double(), ctypes.c_double()
+        self._check(self._lib.cdvz_gpu_kernel_stats(self._ctx, ctypes.byref(n), ctypes.byref(ms), ctypes.byref(by)))
+        return {"launches": n.value, "pyramid_ms": ms.value, "pyramid_bytes": by.value}
+
+    def set_debug(self, on: bool = True) -> None:
+        self._check(self._lib.cdvz_gpu_set_debug(self._ctx, 1 if on else 0))
+
+    def debug_get(self, name: str, frame: int) -> np.ndarray:
+        n = ctypes.c_size_t()
+        self._check(self._lib.cdvz_gpu_debug_get(self._ctx, name.encode(), frame, None, 0, ctypes.byref(n)))
+        out = np.empty(n.value, dtype=np.float64)
+        self._check(self._lib.cdvz_gpu_debug_get(self._ctx, name.encode(), frame, out.ctypes.data, out.size,
+                                                 ctypes.byref(n)))
+        return out
+
+    def event_record(self, slot: int) -> None:
+        self._check(self._lib.cdvz_gpu_event_record(self._ctx, slot))
+
+    def event_elapsed(self, a: int, b: int) -> float:
+        ms = ctypes.c_double()
+        self._check(self._lib.cdvz_gpu_event_elapsed(self._ctx, a, b, ctypes.byref(ms)))
+        return ms.value
+
+    def device_buffer(self, nbytes: int) -> DeviceBuffer:
+        return DeviceBuffer(self, nbytes)
+
+    def pinned_buffer(self, nbytes: int) -> PinnedBuffer:
+        return PinnedBuffer(self, nbytes)
+
+    def synth_frames_device(self, base_seed: int, count: int, width: int, height: int) -> DeviceBuffer:
+        """synth_corpus(base_seed, count, width, height) quantised to bytes, on the device."""
+        buf = DeviceBuffer(self, max(1, count * width * height))
+        self._check(self._lib.cdvz_gpu_synth_frames(self._ctx, base_seed, count, width, height, buf.ptr))
+        return buf
+
+    def synth_frames(self, base_seed: int, count: int, width: int, height: int) -> np.ndarray:
+        buf = self.synth_frames_device(base_seed, count, width, height)
+        arr = buf.to_host(count * width * height).reshape(count, height, width)
+        buf.free()
+        return arr
+
+
+def container_slot(mode) -> int:
+    m = mode if isinstance(mode, ModeSpec) else (mode_by_name(mode) if isinstance(mode, str) else mode_by_id(mode))
+    return m.budget_bytes + 28
+
+
+def parse_container_header(data: bytes) -> dict:
+    """Header fields of a CDVZ1 container (container.cpp:60-93)."""
+    if len(data) < 28 or data[:5] != b"CDVZ1":
+        raise DataError("container magic mismatch")
+    le = int.from_bytes
+    return {
+        "mode_id": data[5], "width": le(data[6:8], "little"), "height": le(data[8:10], "little"),
+        "components": le(data[10:12], "little"), "model_crc": le(data[12:16], "little"),
+        "global_len": le(data[16:20], "little"), "local_len": le(data[20:24], "little"),
+        "crc": le(data[-4:], "little"),
+    }
+
+
+__all__ = [
+    "Extractor", "ModeSpec", "MODES", "mode_by_name", "mode_by_id", "UsageError", "DataError", "InternalError",
+    "bundle_check", "container_slot", "parse_container_header", "library_path",
+]

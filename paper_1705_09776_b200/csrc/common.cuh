@@ -1,0 +1,141 @@
+// Shared device definitions for the B200 extractor kernels.
+//
+// Arithmetic contract: every file is compiled with --fmad=false so each
+// multiply and add rounds separately, in the same order as the reference's
+// double-precision code (and the oracle that restates it). Bit-level parity
+// with the oracle follows wherever no libm call intervenes.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace cdvz_gpu {
+
+constexpr int kMaxOctaves = 8;
+constexpr int kMaxTapRadius = 16;
+
+// Keypoint record shared by every list on the device (64 bytes).
+// Mirrors InterestPoint (proj/include/cdvz/scale_space.hpp:56-64).
+struct KP {
+  double x, y, sigma, p, rho, pss, d;
+  int octave;
+  uint32_t key;  // octave-local raster key (y*w + x)*2 + root slot, order of detection
+};
+static_assert(sizeof(KP) == 64, "KP layout");
+
+struct Oriented { int sel; int pad; double theta; };
+
+// Detector constants (ScaleSpaceConfig + derived; scale_space.hpp:16-27).
+struct DetConst {
+  double taps[4][2 * kMaxTapRadius + 1];
+  int radius[4];
+  double sigmas[4];
+  double s2[4];        // sigma_k * sigma_k (scale_space.cpp:150)
+  double beta[4][4];
+  double thr, rho_limit, s_lo, s_hi;
+  int margin;
+};
+
+// Per-batch geometry and buffer map (device pointers). One instance lives in
+// global memory per batch; kernels receive it by value (fits the 4 KB limit).
+struct Batch {
+  int nframes;
+  int W, H;                       // prepared (resized) size
+  int n_oct;
+  int ow[kMaxOctaves], oh[kMaxOctaves];
+  long long plane_off[kMaxOctaves][4];  // doubles, within a frame's pyramid
+  long long frame_doubles;              // pyramid doubles per frame
+  double* pyr;                          // [frame][...]
+  // Octave-0 input: either u8 frames (pix8) or resized f64 frames (pixf).
+  const uint8_t* pix8; long long stride8; long long frame_bytes8;
+  const double* pixf;
+  // Detection lists.
+  int cap_oct;                         // survivors per (frame, octave)
+  KP* raw;                             // [frame][octave][cap_oct] unordered survivors
+  int* raw_count;                      // [frame][octave]
+  int* oct_count;                      // [frame][octave] survivors per octave (after ordering)
+  uint32_t* bitmap;                    // [frame][bitmap_words]
+  long long bm_off[kMaxOctaves];       // word offset of each octave's bitmap in a frame
+  long long bitmap_words;              // per frame
+  int cap_acc;
+  KP* acc[2];                          // [frame][cap_acc] ping-pong accumulated lists
+  int* acc_count;                      // [frame][2]
+  KP* cur;                             // [frame][cap_acc] scratch (sorted current octave)
+  int* scratch_idx;                    // [frame][cap_acc]
+  uint8_t* flags;                      // [frame][2*cap_acc]
+  double* scratch_d;                   // [frame][cap_acc]
+  int* status;                         // [frame] 0 ok, 3 internal (capacity)
+  // Selection / orientation / description.
+  int select_n;
+  KP* sel;                             // [frame][select_n]
+  int* sel_count;                      // [frame]
+  double* thetas;                      // [frame][select_n][36]
+  int* theta_count;                    // [frame][select_n]
+  int cap_or;
+  Oriented* oriented;                  // [frame][cap_or]
+  int* or_count;                       // [frame]
+  double* desc;                        // [frame][cap_or][128]
+  uint8_t* codes;                      // [frame][cap_or][code_stride]
+  int code_stride;
+  // SCFV.
+  int nc;
+  double* x;                           // [frame][cap_or][32]
+  double* gamma;                       // [frame][cap_or][nc]
+  double* gm;                          // [frame][nc][32]
+  double* gv;                          // [frame][nc][32]
+  uint8_t* mask;                       // [frame][mask_bytes] (selected components)
+  uint32_t* mean_planes;               // [frame][nc] by component index
+  uint32_t* var_planes;                // [frame][nc]
+};
+
+// Model tables in global memory.
+struct Model {
+  const double* rel_edges[5];
+  const double* rel_vals[5];
+  int rel_nb[5];
+  double tr[2][8][8];
+  double tr_scale;
+  const double* t0;
+  const double* t1;
+  const int* priority;
+  const double* pca_mean;   // 128
+  const double* pca_basis;  // 32 x 128
+  int nc;
+  const double* inv_var;    // nc x 32  1/(s*s)
+  const double* m_over_v;   // nc x 32  m/(s*s)
+  const double* m2_over_v;  // nc x 32  (m*m)/(s*s)
+  const double* log_norm;   // nc       log w - sum log s - 16 log 2pi
+  const double* means;      // nc x 32
+  const double* stds;       // nc x 32
+  const double* weights;    // nc
+};
+
+// Encoding parameters of one call.
+struct EncodeConst {
+  int mode_id, elements, variance;
+  int k_select;                 // SCFV components kept
+  int max_codes;
+  int code_bytes;
+  int mask_bytes;
+  int global_bytes;
+  int slot_bytes;               // container slot
+  uint32_t model_crc;
+  double half_diag, cx, cy;     // fill_center_distance constants
+  double log2_range;            // log2(64 / 0.5)
+};
+
+__host__ __device__ inline int mirror_index(int i, int n) {
+  if (n <= 1) return 0;
+  const int period = 2 * n;
+  int m = i % period;
+  if (m < 0) m += period;
+  return m < n ? m : period - 1 - m;
+}
+
+#define CDVZ_CUDA_CHECK(expr)                                                              \
+  do {                                                                                     \
+    cudaError_t e__ = (expr);                                                              \
+    if (e__ != cudaSuccess) throw std::runtime_error(std::string(#expr) + ": " + cudaGetErrorString(e__)); \
+  } while (0)
+
+}  // namespace cdvz_gpu

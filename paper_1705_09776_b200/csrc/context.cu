@@ -1,0 +1,721 @@
+// Host runtime behind include/cdvz_gpu.h: context (device, stream, model
+// tables), batch buffer planning, the per-batch launch sequence and the C ABI.
+//
+// One context drives one device on one stream. A batch of frames flows
+// through ~20 launches with no host round trip: K0 resize (if needed),
+// K1 fused octave + K2/K3 merge per octave, K4 selection, K5 orientation,
+// K6/K7 description + coding, K8-K11 SCFV, K12 container pack. Per-frame
+// failures (capacity overflow) are flagged on the device and surface as
+// status 3 for that frame only.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <random>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/cdvz_gpu.h"
+#include "bundle.hpp"
+#include "common.cuh"
+
+namespace cdvz_gpu {
+cudaError_t launch_octave(const Batch& bt, const DetConst& dc, int o, int src, cudaStream_t st);
+cudaError_t launch_merge(const Batch& bt, int o, cudaStream_t st);
+cudaError_t launch_select(const Batch& bt, const Model& md, const EncodeConst& ec, cudaStream_t st);
+cudaError_t launch_describe(const Batch& bt, const DetConst& dc, const Model& md, const EncodeConst& ec, cudaStream_t st);
+cudaError_t launch_scfv_pack(const Batch& bt, const Model& md, const EncodeConst& ec, uint8_t* out, uint32_t* lengths,
+                             cudaStream_t st, cudaEvent_t after_aggregation);
+cudaError_t launch_resize(const uint8_t* pix, long long stride, long long frame_bytes, int w_in, int h_in, double* out,
+                          int w_out, int h_out, int frames, cudaStream_t st);
+struct SynthParams {
+  int n_blobs;
+  double blob[14][4];
+  double wave[5][4];
+};
+cudaError_t launch_synth(const SynthParams* d_params, int frames, int w, int h, double* canvas, double* bmin,
+                         double* bmax, int nblk, uint8_t* out, cudaStream_t st);
+}  // namespace cdvz_gpu
+
+using namespace cdvz_gpu;
+
+namespace {
+
+thread_local std::string g_create_error;
+
+struct DeviceBuffer {
+  void* p = nullptr;
+  size_t bytes = 0;
+  void ensure(size_t n) {
+    if (n <= bytes) return;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    CDVZ_CUDA_CHECK(cudaMalloc(&p, n));
+    bytes = n;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  template <class T> T* as() const { return static_cast<T*>(p); }
+};
+
+// Prepared size per resize_max_side (image.cpp:131-145).
+void prepared_dims(int w, int h, int limit, int& pw, int& ph) {
+  if (limit < 8) throw DataError("max-side limit must be at least 8");
+  const int longer = std::max(w, h);
+  pw = w;
+  ph = h;
+  if (longer <= limit) return;
+  const double scale = static_cast<double>(limit) / longer;
+  if (w >= h) {
+    pw = limit;
+    ph = std::max(8, static_cast<int>(std::lround(h * scale)));
+  } else {
+    ph = limit;
+    pw = std::max(8, static_cast<int>(std::lround(w * scale)));
+  }
+}
+
+}  // namespace
+
+struct cdvz_gpu_ctx {
+  int device = 0;
+  int max_batch = 256;
+  cudaStream_t st = nullptr;
+  std::string err;
+  Bundle bundle;
+  DetConst dc{};
+  Model md{};
+  std::vector<DeviceBuffer> model_bufs;
+  bool debug = false;
+
+  // Batch geometry the buffers are sized for.
+  int geo_w = 0, geo_h = 0, geo_frames = 0;
+  Batch bt{};
+  std::vector<DeviceBuffer> batch_bufs;
+  DeviceBuffer stage_in, stage_out, stage_len, dbg_oct;
+  std::vector<uint8_t> host_out;
+  std::vector<uint32_t> host_len;
+  int last_frames = 0, last_mode = -1;
+
+  cudaEvent_t ev[6] = {};
+  cudaEvent_t user_ev[4] = {};
+  cudaEvent_t evp[2 * kMaxOctaves] = {};
+  double stage_ms[5] = {0, 0, 0, 0, 0};
+  double pyr_ms = 0.0, pyr_bytes = 0.0;
+  int launches = 0;
+
+  ~cdvz_gpu_ctx() {
+    for (auto& b : model_bufs) b.release();
+    for (auto& b : batch_bufs) b.release();
+    stage_in.release();
+    stage_out.release();
+    stage_len.release();
+    dbg_oct.release();
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+    for (auto& e : evp)
+      if (e) cudaEventDestroy(e);
+    for (auto& e : user_ev)
+      if (e) cudaEventDestroy(e);
+    if (st) cudaStreamDestroy(st);
+  }
+
+  template <class T>
+  const T* upload(const T* host, size_t n) {
+    model_bufs.emplace_back();
+    model_bufs.back().ensure(std::max<size_t>(1, n * sizeof(T)));
+    CDVZ_CUDA_CHECK(cudaMemcpy(model_bufs.back().p, host, n * sizeof(T), cudaMemcpyHostToDevice));
+    return model_bufs.back().as<T>();
+  }
+
+  void setup_model() {
+    const Bundle& b = bundle;
+    // Detector constants; taps laid out for the kernel variant that runs them
+    // (exact fit for radii 5/5/6/8, zero-padded to radius 8 otherwise).
+    const bool exact = b.radius[0] == 5 && b.radius[1] == 5 && b.radius[2] == 6 && b.radius[3] == 8;
+    for (int k = 0; k < 4; ++k) {
+      if (b.radius[k] > 8) throw UsageError("detector scales need a Gaussian radius <= 8 (sigma <= 2.66)");
+      const int R = exact ? b.radius[k] : 8;
+      for (int j = 0; j < 2 * kMaxTapRadius + 1; ++j) dc.taps[k][j] = 0.0;
+      for (int j = -b.radius[k]; j <= b.radius[k]; ++j) dc.taps[k][j + R] = b.taps[k][std::size_t(j + b.radius[k])];
+      dc.radius[k] = b.radius[k];
+      dc.sigmas[k] = b.sigmas[std::size_t(k)];
+      dc.s2[k] = b.sigmas[std::size_t(k)] * b.sigmas[std::size_t(k)];
+      for (int i = 0; i < 4; ++i) dc.beta[k][i] = b.beta[k][i];
+    }
+    dc.thr = b.response_threshold;
+    dc.rho_limit = b.rho_limit;
+    dc.s_lo = b.sigmas[0];
+    dc.s_hi = b.sigmas[3];
+    dc.margin = b.margin;
+
+    for (int c = 0; c < 5; ++c) {
+      md.rel_edges[c] = upload(b.relevance[std::size_t(c)].edges.data(), b.relevance[std::size_t(c)].edges.size());
+      md.rel_vals[c] = upload(b.relevance[std::size_t(c)].values.data(), b.relevance[std::size_t(c)].values.size());
+      md.rel_nb[c] = int(b.relevance[std::size_t(c)].values.size());
+    }
+    for (int i = 0; i < 8; ++i)
+      for (int j = 0; j < 8; ++j) {
+        md.tr[0][i][j] = b.tr_a[i][j];
+        md.tr[1][i][j] = b.tr_b[i][j];
+      }
+    md.tr_scale = b.tr_scale;
+    md.t0 = upload(b.t0, 128);
+    md.t1 = upload(b.t1, 128);
+    md.priority = upload(b.priority, 128);
+    md.pca_mean = upload(b.pca_mean, 128);
+    md.pca_basis = upload(b.pca_basis.data(), b.pca_basis.size());
+    md.nc = b.nc;
+    // posteriors_matrix's derived tables (scfv.cpp:146-160), computed once on the host.
+    std::vector<double> iv(std::size_t(b.nc) * 32), mv(iv.size()), m2(iv.size()), ln(std::size_t(b.nc));
+    for (int i = 0; i < b.nc; ++i) {
+      double s = 0.0;
+      for (int j = 0; j < 32; ++j) {
+        const double sd = b.stds[std::size_t(i) * 32 + j], mu = b.means[std::size_t(i) * 32 + j];
+        const double var = sd * sd;
+        iv[std::size_t(i) * 32 + j] = 1.0 / var;
+        mv[std::size_t(i) * 32 + j] = mu / var;
+        m2[std::size_t(i) * 32 + j] = (mu * mu) / var;
+        s += std::log(sd);
+      }
+      ln[std::size_t(i)] = std::log(b.weights[std::size_t(i)]) - s - 16.0 * 1.8378770664093453;
+    }
+    md.inv_var = upload(iv.data(), iv.size());
+    md.m_over_v = upload(mv.data(), mv.size());
+    md.m2_over_v = upload(m2.data(), m2.size());
+    md.log_norm = upload(ln.data(), ln.size());
+    md.means = upload(b.means.data(), b.means.size());
+    md.stds = upload(b.stds.data(), b.stds.size());
+    md.weights = upload(b.weights.data(), b.weights.size());
+  }
+
+  // Sizes every per-batch buffer for `frames` frames of prepared size W x H.
+  void plan(int W, int H, int frames, bool need_resize) {
+    if (W == geo_w && H == geo_h && frames <= geo_frames && (!need_resize || bt.pixf)) return;
+    for (auto& b : batch_bufs) b.release();
+    batch_bufs.clear();
+    Batch nb{};
+    nb.W = W;
+    nb.H = H;
+    int n_oct = 0, w = W, h = H;
+    long long pd = 0, bw = 0;
+    while (n_oct < bundle.num_octaves && n_oct < kMaxOctaves && w >= 16 && h >= 16) {
+      nb.ow[n_oct] = w;
+      nb.oh[n_oct] = h;
+      for (int k = 0; k < 4; ++k) nb.plane_off[n_oct][k] = pd + (long long)k * w * h;
+      pd += 4LL * w * h;
+      nb.bm_off[n_oct] = bw;
+      bw += (2LL * w * h + 31) / 32;
+      ++n_oct;
+      w /= 2;
+      h /= 2;
+    }
+    nb.n_oct = n_oct;
+    nb.frame_doubles = std::max<long long>(pd, 1);
+    nb.bitmap_words = std::max<long long>(bw, 1);
+    nb.cap_oct = 32768;
+    nb.cap_acc = 32768;
+    nb.select_n = bundle.select_n;
+    nb.cap_or = std::max(64, bundle.select_n * 4);
+    nb.code_stride = 40;
+    nb.nc = bundle.nc;
+    const long long F = frames;
+    auto alloc = [&](size_t bytes) {
+      batch_bufs.emplace_back();
+      batch_bufs.back().ensure(std::max<size_t>(bytes, 16));
+      return batch_bufs.back().p;
+    };
+    nb.pyr = static_cast<double*>(alloc(sizeof(double) * F * nb.frame_doubles));
+    nb.pixf = need_resize ? static_cast<double*>(alloc(sizeof(double) * F * W * H)) : nullptr;
+    nb.raw = static_cast<KP*>(alloc(sizeof(KP) * F * std::max(1, n_oct) * nb.cap_oct));
+    nb.raw_count = static_cast<int*>(alloc(sizeof(int) * F * std::max(1, n_oct)));
+    nb.oct_count = static_cast<int*>(alloc(sizeof(int) * F * std::max(1, n_oct)));
+    nb.bitmap = static_cast<uint32_t*>(alloc(sizeof(uint32_t) * F * nb.bitmap_words));
+    nb.acc[0] = static_cast<KP*>(alloc(sizeof(KP) * F * nb.cap_acc));
+    nb.acc[1] = static_cast<KP*>(alloc(sizeof(KP) * F * nb.cap_acc));
+    nb.acc_count = static_cast<int*>(alloc(sizeof(int) * F * 2));
+    nb.cur = static_cast<KP*>(alloc(sizeof(KP) * F * nb.cap_acc));
+    nb.scratch_idx = static_cast<int*>(alloc(sizeof(int) * F * nb.cap_acc));
+    nb.flags = static_cast<uint8_t*>(alloc(F * 2 * nb.cap_acc));
+    nb.scratch_d = static_cast<double*>(alloc(sizeof(double) * F * nb.cap_acc));
+    nb.status = static_cast<int*>(alloc(sizeof(int) * F));
+    nb.sel = static_cast<KP*>(alloc(sizeof(KP) * F * nb.select_n));
+    nb.sel_count = static_cast<int*>(alloc(sizeof(int) * F));
+    nb.thetas = static_cast<double*>(alloc(sizeof(double) * F * nb.select_n * 36));
+    nb.theta_count = static_cast<int*>(alloc(sizeof(int) * F * nb.select_n));
+    nb.oriented = static_cast<Oriented*>(alloc(sizeof(Oriented) * F * nb.cap_or));
+    nb.or_count = static_cast<int*>(alloc(sizeof(int) * F));
+    nb.desc = static_cast<double*>(alloc(sizeof(double) * F * nb.cap_or * 128));
+    nb.codes = static_cast<uint8_t*>(alloc(F * nb.cap_or * nb.code_stride));
+    nb.x = static_cast<double*>(alloc(sizeof(double) * F * nb.cap_or * 32));
+    nb.gamma = static_cast<double*>(alloc(sizeof(double) * F * nb.cap_or * nb.nc));
+    nb.gm = static_cast<double*>(alloc(sizeof(double) * F * nb.nc * 32));
+    nb.gv = static_cast<double*>(alloc(sizeof(double) * F * nb.nc * 32));
+    nb.mask = static_cast<uint8_t*>(alloc(F * ((nb.nc + 7) / 8)));
+    nb.mean_planes = static_cast<uint32_t*>(alloc(sizeof(uint32_t) * F * nb.nc));
+    nb.var_planes = static_cast<uint32_t*>(alloc(sizeof(uint32_t) * F * nb.nc));
+    CDVZ_CUDA_CHECK(cudaMemsetAsync(nb.raw_count, 0, sizeof(int) * F * std::max(1, n_oct), st));
+    CDVZ_CUDA_CHECK(cudaMemsetAsync(nb.bitmap, 0, sizeof(uint32_t) * F * nb.bitmap_words, st));
+    CDVZ_CUDA_CHECK(cudaMemsetAsync(nb.acc_count, 0, sizeof(int) * F * 2, st));
+    if (debug) dbg_oct.ensure(sizeof(KP) * F * std::max(1, n_oct) * nb.cap_acc);
+    bt = nb;
+    geo_w = W;
+    geo_h = H;
+    geo_frames = frames;
+  }
+
+  EncodeConst encode_const(int mode_id) const {
+    const Mode& m = mode_by_id(mode_id);
+    const Budget bu = budget_for(m, bundle.nc);
+    EncodeConst ec{};
+    ec.mode_id = m.id;
+    ec.elements = m.elements;
+    ec.variance = m.variance ? 1 : 0;
+    ec.k_select = bu.k;
+    ec.max_codes = int(bu.max_codes);
+    ec.code_bytes = int(bu.code_bytes);
+    ec.mask_bytes = (bundle.nc + 7) / 8;
+    ec.global_bytes = int(bu.global_bytes);
+    ec.slot_bytes = int(m.budget + 28);
+    ec.model_crc = bundle.model_crc;
+    return ec;
+  }
+
+  // Runs the whole pipeline for `frames` device-resident frames (u8) of size
+  // w x h and writes containers into fixed slots of d_out.
+  void run(const uint8_t* d_pix, int w, int h, long long stride, int frames, int mode_id, int max_side, uint8_t* d_out,
+           uint32_t* d_len) {
+    if (w < 8 || h < 8) throw DataError("image smaller than 8 px per side");
+    int W, H;
+    prepared_dims(w, h, max_side, W, H);
+    const bool resize = (W != w || H != h);
+    EncodeConst ec = encode_const(mode_id);
+    ec.cx = (W - 1) / 2.0;
+    ec.cy = (H - 1) / 2.0;
+    ec.half_diag = 0.5 * std::hypot(static_cast<double>(W - 1), static_cast<double>(H - 1));
+    ec.log2_range = std::log2(64.0 / 0.5);
+    plan(W, H, std::min(frames, max_batch), resize);
+    launches = 0;
+    pyr_ms = 0.0;
+    pyr_bytes = 0.0;
+    for (double& s : stage_ms) s = 0.0;
+    for (int base = 0; base < frames; base += max_batch) {
+      const int nf = std::min(max_batch, frames - base);
+      Batch b = bt;
+      b.nframes = nf;
+      b.pix8 = d_pix + (long long)base * h * stride;
+      b.stride8 = stride;
+      b.frame_bytes8 = (long long)h * stride;
+      CDVZ_CUDA_CHECK(cudaMemsetAsync(b.status, 0, sizeof(int) * nf, st));
+      ++launches;
+      if (resize) {
+        CDVZ_CUDA_CHECK(launch_resize(b.pix8, stride, b.frame_bytes8, w, h, const_cast<double*>(b.pixf), W, H, nf, st));
+        ++launches;
+      }
+      CDVZ_CUDA_CHECK(cudaEventRecord(ev[0], st));
+      for (int o = 0; o < b.n_oct; ++o) {
+        const int src = o == 0 ? (resize ? 1 : 0) : 2;
+        CDVZ_CUDA_CHECK(cudaEventRecord(evp[2 * o], st));
+        CDVZ_CUDA_CHECK(launch_octave(b, dc, o, src, st));
+        CDVZ_CUDA_CHECK(cudaEventRecord(evp[2 * o + 1], st));
+        CDVZ_CUDA_CHECK(launch_merge(b, o, st));
+        launches += 2;
+        if (debug) {
+          const KP* srcl = (o == 0) ? b.acc[0] : b.cur;
+          CDVZ_CUDA_CHECK(cudaMemcpyAsync(dbg_oct.as<KP>() + (long long)o * bt.cap_acc * geo_frames, srcl,
+                                          sizeof(KP) * (long long)nf * b.cap_acc, cudaMemcpyDeviceToDevice, st));
+        }
+      }
+      CDVZ_CUDA_CHECK(cudaEventRecord(ev[1], st));
+      CDVZ_CUDA_CHECK(launch_select(b, md, ec, st));
+      CDVZ_CUDA_CHECK(cudaEventRecord(ev[2], st));
+      CDVZ_CUDA_CHECK(launch_describe(b, dc, md, ec, st));
+      CDVZ_CUDA_CHECK(cudaEventRecord(ev[3], st));
+      CDVZ_CUDA_CHECK(launch_scfv_pack(b, md, ec, d_out + (long long)base * ec.slot_bytes, d_len + base, st, ev[4]));
+      CDVZ_CUDA_CHECK(cudaEventRecord(ev[5], st));
+      launches += 1 + 3 + 5;
+      // Stage times per label (sum over chunks). Reading the events waits for the chunk.
+      CDVZ_CUDA_CHECK(cudaEventSynchronize(ev[5]));
+      float t[5];
+      cudaEventElapsedTime(&t[0], ev[0], ev[1]);
+      cudaEventElapsedTime(&t[1], ev[1], ev[2]);
+      cudaEventElapsedTime(&t[2], ev[2], ev[3]);
+      cudaEventElapsedTime(&t[3], ev[4], ev[5]);
+      cudaEventElapsedTime(&t[4], ev[3], ev[4]);
+      for (int i = 0; i < 5; ++i) stage_ms[i] += t[i];
+      for (int o = 0; o < b.n_oct; ++o) {
+        float pm = 0.f;
+        cudaEventElapsedTime(&pm, evp[2 * o], evp[2 * o + 1]);
+        pyr_ms += pm;
+        // Algorithmic bytes of the fused octave kernel: base read + 4 G levels written.
+        const double px = double(b.ow[o]) * b.oh[o];
+        const double in_b = (o == 0) ? (resize ? 8.0 : 1.0) : 8.0;
+        pyr_bytes += double(nf) * px * (in_b + 32.0);
+      }
+    }
+    last_frames = std::min(frames, max_batch);
+    last_mode = mode_id;
+  }
+};
+
+namespace {
+
+template <class F>
+int guarded(cdvz_gpu_ctx* ctx, F&& f) {
+  try {
+    f();
+    if (ctx) ctx->err.clear();
+    return CDVZ_GPU_OK;
+  } catch (const UsageError& e) {
+    (ctx ? ctx->err : g_create_error) = e.what();
+    return CDVZ_GPU_USAGE;
+  } catch (const DataError& e) {
+    (ctx ? ctx->err : g_create_error) = e.what();
+    return CDVZ_GPU_DATA;
+  } catch (const std::exception& e) {
+    (ctx ? ctx->err : g_create_error) = e.what();
+    return CDVZ_GPU_INTERNAL;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int cdvz_gpu_create(const char* bundle_text, size_t bundle_len, int device, int max_batch, cdvz_gpu_ctx** out_ctx) {
+  return guarded(nullptr, [&] {
+    if (!out_ctx || !bundle_text) throw UsageError("null argument");
+    *out_ctx = nullptr;
+    parse_bundle(std::string(bundle_text, bundle_len));  // data errors before device errors
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) throw std::runtime_error("no CUDA device available (the extractor has no CPU fallback)");
+    if (device < 0 || device >= ndev) throw UsageError("device index out of range");
+    cudaDeviceProp prop{};
+    CDVZ_CUDA_CHECK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10) throw std::runtime_error(std::string("the kernels are built for sm_100a only; device is ") + prop.name);
+    Bundle parsed = parse_bundle(std::string(bundle_text, bundle_len));
+    auto ctx = std::make_unique<cdvz_gpu_ctx>();
+    ctx->device = device;
+    ctx->max_batch = max_batch > 0 ? max_batch : 256;
+    CDVZ_CUDA_CHECK(cudaSetDevice(device));
+    CDVZ_CUDA_CHECK(cudaStreamCreateWithFlags(&ctx->st, cudaStreamNonBlocking));
+    for (auto& e : ctx->ev) CDVZ_CUDA_CHECK(cudaEventCreate(&e));
+    for (auto& e : ctx->evp) CDVZ_CUDA_CHECK(cudaEventCreate(&e));
+    ctx->bundle = std::move(parsed);
+    ctx->setup_model();
+    *out_ctx = ctx.release();
+  });
+}
+
+void cdvz_gpu_destroy(cdvz_gpu_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->st);
+  delete ctx;
+}
+
+const char* cdvz_gpu_last_error(const cdvz_gpu_ctx* ctx) { return ctx ? ctx->err.c_str() : g_create_error.c_str(); }
+
+int cdvz_gpu_bundle_check(const char* bundle_text, size_t bundle_len, uint32_t* model_crc, int* components) {
+  return guarded(nullptr, [&] {
+    if (!bundle_text) throw UsageError("null argument");
+    const Bundle b = parse_bundle(std::string(bundle_text, bundle_len));
+    if (model_crc) *model_crc = b.model_crc;
+    if (components) *components = b.nc;
+  });
+}
+
+int cdvz_gpu_event_record(cdvz_gpu_ctx* ctx, int slot) {
+  return guarded(ctx, [&] {
+    if (!ctx || slot < 0 || slot >= 4) throw UsageError("event slot out of range");
+    if (!ctx->user_ev[slot]) CDVZ_CUDA_CHECK(cudaEventCreate(&ctx->user_ev[slot]));
+    CDVZ_CUDA_CHECK(cudaEventRecord(ctx->user_ev[slot], ctx->st));
+  });
+}
+
+int cdvz_gpu_event_elapsed(cdvz_gpu_ctx* ctx, int a, int b, double* ms) {
+  return guarded(ctx, [&] {
+    if (!ctx || a < 0 || a >= 4 || b < 0 || b >= 4 || !ctx->user_ev[a] || !ctx->user_ev[b]) throw UsageError("event slot not recorded");
+    CDVZ_CUDA_CHECK(cudaEventSynchronize(ctx->user_ev[b]));
+    float t = 0.f;
+    CDVZ_CUDA_CHECK(cudaEventElapsedTime(&t, ctx->user_ev[a], ctx->user_ev[b]));
+    *ms = t;
+  });
+}
+
+int cdvz_gpu_bundle_info(const cdvz_gpu_ctx* ctx, uint32_t* model_crc, int* components, int* select_n) {
+  if (!ctx) return CDVZ_GPU_USAGE;
+  if (model_crc) *model_crc = ctx->bundle.model_crc;
+  if (components) *components = ctx->bundle.nc;
+  if (select_n) *select_n = ctx->bundle.select_n;
+  return CDVZ_GPU_OK;
+}
+
+size_t cdvz_gpu_container_slot(int mode_id) {
+  try {
+    return mode_by_id(mode_id).budget + 28;
+  } catch (...) {
+    return 0;
+  }
+}
+
+int cdvz_gpu_set_debug(cdvz_gpu_ctx* ctx, int on) {
+  if (!ctx) return CDVZ_GPU_USAGE;
+  ctx->debug = on != 0;
+  ctx->geo_w = ctx->geo_h = 0;  // force a re-plan with the debug buffers
+  return CDVZ_GPU_OK;
+}
+
+int cdvz_gpu_encode_device(cdvz_gpu_ctx* ctx, const uint8_t* d_pixels, int width, int height, size_t stride, int count,
+                           int mode_id, int max_side, uint8_t* d_out, uint32_t* d_lengths) {
+  return guarded(ctx, [&] {
+    if (!ctx) throw UsageError("null context");
+    if (count < 0) throw UsageError("negative frame count");
+    if (count == 0) return;
+    mode_by_id(mode_id);
+    CDVZ_CUDA_CHECK(cudaSetDevice(ctx->device));
+    ctx->run(d_pixels, width, height, (long long)stride, count, mode_id, max_side, d_out, d_lengths);
+  });
+}
+
+int cdvz_gpu_sync(cdvz_gpu_ctx* ctx) {
+  return guarded(ctx, [&] { CDVZ_CUDA_CHECK(cudaStreamSynchronize(ctx->st)); });
+}
+
+int cdvz_gpu_encode_batch(cdvz_gpu_ctx* ctx, const uint8_t* pixels, int width, int height, size_t stride, int count,
+                          int mode_id, int max_side, uint8_t* out, size_t out_cap, size_t* offsets, int* status) {
+  return guarded(ctx, [&] {
+    if (!ctx || (!pixels && count > 0) || !offsets || !status) throw UsageError("null argument");
+    if (count < 0) throw UsageError("negative frame count");
+    offsets[0] = 0;
+    if (count == 0) return;
+    const size_t slot = mode_by_id(mode_id).budget + 28;
+    if (width < 8 || height < 8) {
+      for (int i = 0; i < count; ++i) {
+        status[i] = CDVZ_GPU_DATA;
+        offsets[i + 1] = 0;
+      }
+      throw DataError("image smaller than 8 px per side");
+    }
+    CDVZ_CUDA_CHECK(cudaSetDevice(ctx->device));
+    const int chunk = ctx->max_batch;
+    const size_t frame_bytes = size_t(width) * height;
+    ctx->stage_in.ensure(frame_bytes * std::min(count, chunk));
+    ctx->stage_out.ensure(slot * std::min(count, chunk));
+    ctx->stage_len.ensure(sizeof(uint32_t) * std::min(count, chunk));
+    ctx->host_out.resize(slot * std::min(count, chunk));
+    ctx->host_len.resize(std::min(count, chunk));
+    size_t written = 0;
+    double acc_ms[5] = {0, 0, 0, 0, 0};
+    double acc_pyr_ms = 0, acc_pyr_bytes = 0;
+    int acc_launches = 0;
+    for (int base = 0; base < count; base += chunk) {
+      const int nf = std::min(chunk, count - base);
+      CDVZ_CUDA_CHECK(cudaMemcpy2DAsync(ctx->stage_in.p, width, pixels + size_t(base) * height * stride, stride, width,
+                                        size_t(height) * nf, cudaMemcpyHostToDevice, ctx->st));
+      ctx->run(ctx->stage_in.as<uint8_t>(), width, height, width, nf, mode_id, max_side, ctx->stage_out.as<uint8_t>(),
+               ctx->stage_len.as<uint32_t>());
+      for (int i = 0; i < 5; ++i) acc_ms[i] += ctx->stage_ms[i];
+      acc_pyr_ms += ctx->pyr_ms;
+      acc_pyr_bytes += ctx->pyr_bytes;
+      acc_launches += ctx->launches;
+      CDVZ_CUDA_CHECK(cudaMemcpyAsync(ctx->host_len.data(), ctx->stage_len.p, sizeof(uint32_t) * nf, cudaMemcpyDeviceToHost, ctx->st));
+      CDVZ_CUDA_CHECK(cudaMemcpyAsync(ctx->host_out.data(), ctx->stage_out.p, slot * nf, cudaMemcpyDeviceToHost, ctx->st));
+      CDVZ_CUDA_CHECK(cudaStreamSynchronize(ctx->st));
+      for (int i = 0; i < nf; ++i) {
+        const size_t len = ctx->host_len[size_t(i)];
+        const int fi = base + i;
+        if (len == 0) {
+          status[fi] = CDVZ_GPU_INTERNAL;
+        } else if (written + len > out_cap) {
+          status[fi] = CDVZ_GPU_USAGE;
+        } else {
+          std::memcpy(out + written, ctx->host_out.data() + size_t(i) * slot, len);
+          written += len;
+          status[fi] = CDVZ_GPU_OK;
+        }
+        offsets[fi + 1] = written;
+      }
+    }
+    for (int i = 0; i < 5; ++i) ctx->stage_ms[i] = acc_ms[i];
+    ctx->pyr_ms = acc_pyr_ms;
+    ctx->pyr_bytes = acc_pyr_bytes;
+    ctx->launches = acc_launches;
+  });
+}
+
+int cdvz_gpu_stage_times(cdvz_gpu_ctx* ctx, double ms[5]) {
+  if (!ctx || !ms) return CDVZ_GPU_USAGE;
+  for (int i = 0; i < 5; ++i) ms[i] = ctx->stage_ms[i];
+  return CDVZ_GPU_OK;
+}
+
+int cdvz_gpu_kernel_stats(cdvz_gpu_ctx* ctx, int* launches, double* pyramid_ms, double* pyramid_bytes) {
+  if (!ctx) return CDVZ_GPU_USAGE;
+  if (launches) *launches = ctx->launches;
+  if (pyramid_ms) *pyramid_ms = ctx->pyr_ms;
+  if (pyramid_bytes) *pyramid_bytes = ctx->pyr_bytes;
+  return CDVZ_GPU_OK;
+}
+
+int cdvz_gpu_debug_get(cdvz_gpu_ctx* ctx, const char* name, int frame, double* dst, size_t cap, size_t* n) {
+  return guarded(ctx, [&] {
+    if (!ctx || !name || !n) throw UsageError("null argument");
+    if (frame < 0 || frame >= ctx->last_frames) throw UsageError("frame index outside the last batch");
+    CDVZ_CUDA_CHECK(cudaSetDevice(ctx->device));
+    CDVZ_CUDA_CHECK(cudaStreamSynchronize(ctx->st));
+    const Batch& b = ctx->bt;
+    const std::string s(name);
+    std::vector<double> v;
+    auto get_int = [&](const int* p) {
+      int x = 0;
+      CDVZ_CUDA_CHECK(cudaMemcpy(&x, p, sizeof(int), cudaMemcpyDeviceToHost));
+      return x;
+    };
+    auto get_kps = [&](const KP* p, int count) {
+      std::vector<KP> k(std::size_t(std::max(0, count)));
+      if (count > 0) CDVZ_CUDA_CHECK(cudaMemcpy(k.data(), p, sizeof(KP) * count, cudaMemcpyDeviceToHost));
+      return k;
+    };
+    auto put_kp = [&](const KP& k) { v.insert(v.end(), {k.x, k.y, k.sigma, double(k.octave), k.p, k.rho, k.pss, k.d}); };
+    auto get_d = [&](const double* p, long long count) {
+      std::vector<double> d(std::size_t(std::max(0LL, count)));
+      if (count > 0) CDVZ_CUDA_CHECK(cudaMemcpy(d.data(), p, sizeof(double) * count, cudaMemcpyDeviceToHost));
+      return d;
+    };
+    const int last = (b.n_oct - 1) & 1;
+    const int n_acc = b.n_oct > 0 ? get_int(b.acc_count + frame * 2 + last) : 0;
+    const int n_or = get_int(b.or_count + frame);
+    if (s.rfind("refined:", 0) == 0) {
+      if (!ctx->debug) throw UsageError("per-octave lists need cdvz_gpu_set_debug(ctx, 1) before the batch");
+      const int o = std::stoi(s.substr(8));
+      if (o < b.n_oct) {
+        const KP* base = ctx->dbg_oct.as<KP>() + (long long)o * b.cap_acc * ctx->geo_frames + (long long)frame * b.cap_acc;
+        for (const KP& k : get_kps(base, get_int(b.oct_count + frame * b.n_oct + o))) put_kp(k);
+      }
+    } else if (s == "keypoints") {
+      for (const KP& k : get_kps(b.acc[last] + (long long)frame * b.cap_acc, n_acc)) put_kp(k);
+    } else if (s == "selected") {
+      const int ns = get_int(b.sel_count + frame);
+      for (const KP& k : get_kps(b.sel + (long long)frame * b.select_n, ns)) put_kp(k);
+    } else if (s == "oriented") {
+      const int ns = get_int(b.sel_count + frame);
+      const auto sel = get_kps(b.sel + (long long)frame * b.select_n, ns);
+      std::vector<Oriented> o(static_cast<std::size_t>(n_or));
+      if (n_or > 0) CDVZ_CUDA_CHECK(cudaMemcpy(o.data(), b.oriented + (long long)frame * b.cap_or, sizeof(Oriented) * n_or, cudaMemcpyDeviceToHost));
+      for (const auto& e : o) {
+        put_kp(sel[std::size_t(e.sel)]);
+        v.push_back(e.theta);
+      }
+    } else if (s == "descriptors") {
+      v = get_d(b.desc + (long long)frame * b.cap_or * 128, (long long)n_or * 128);
+    } else if (s == "x") {
+      v = get_d(b.x + (long long)frame * b.cap_or * 32, (long long)n_or * 32);
+    } else if (s == "gamma") {
+      v = get_d(b.gamma + (long long)frame * b.cap_or * b.nc, (long long)n_or * b.nc);
+    } else if (s == "gm") {
+      v = get_d(b.gm + (long long)frame * b.nc * 32, (long long)b.nc * 32);
+    } else if (s == "gv") {
+      if (ctx->last_mode >= 0 && mode_by_id(ctx->last_mode).variance) v = get_d(b.gv + (long long)frame * b.nc * 32, (long long)b.nc * 32);
+    } else if (s.rfind("gauss:", 0) == 0) {
+      const auto c2 = s.find(':', 6);
+      const int o = std::stoi(s.substr(6, c2 - 6)), k = std::stoi(s.substr(c2 + 1));
+      if (o < b.n_oct && k >= 0 && k < 4)
+        v = get_d(b.pyr + (long long)frame * b.frame_doubles + b.plane_off[o][k], (long long)b.ow[o] * b.oh[o]);
+    } else if (s == "status") {
+      v = {double(get_int(b.status + frame))};
+    } else {
+      throw UsageError("unknown debug array '" + s + "'");
+    }
+    *n = v.size();
+    if (dst && cap >= v.size()) std::memcpy(dst, v.data(), v.size() * sizeof(double));
+  });
+}
+
+int cdvz_gpu_synth_frames(cdvz_gpu_ctx* ctx, uint64_t base_seed, int count, int width, int height, uint8_t* d_out) {
+  return guarded(ctx, [&] {
+    if (!ctx || !d_out) throw UsageError("null argument");
+    if (width < 1 || height < 1 || count < 0) throw UsageError("bad synthetic frame geometry");
+    CDVZ_CUDA_CHECK(cudaSetDevice(ctx->device));
+    const int chunk = 64;
+    const int nblk = 64;
+    DeviceBuffer canvas, params, bmin, bmax;
+    canvas.ensure(sizeof(double) * size_t(width) * height * std::min(count, chunk));
+    params.ensure(sizeof(SynthParams) * std::min(count, chunk));
+    bmin.ensure(sizeof(double) * nblk * std::min(count, chunk));
+    bmax.ensure(sizeof(double) * nblk * std::min(count, chunk));
+    std::vector<SynthParams> hp(std::size_t(std::min(count, chunk)));
+    for (int base = 0; base < count; base += chunk) {
+      const int nf = std::min(chunk, count - base);
+      for (int i = 0; i < nf; ++i) {
+        // synthetic.cpp:11-44 draws, in the reference's order.
+        std::mt19937_64 rng(base_seed + static_cast<uint64_t>(base + i) * 0x9E3779B97F4A7C15ull);
+        std::uniform_real_distribution<double> unit(0.0, 1.0);
+        SynthParams& p = hp[std::size_t(i)];
+        p.n_blobs = 8 + static_cast<int>(rng() % 7);
+        for (int bl = 0; bl < p.n_blobs; ++bl) {
+          const double cx = (0.12 + 0.76 * unit(rng)) * width;
+          const double cy = (0.12 + 0.76 * unit(rng)) * height;
+          const double s = 2.0 + 10.0 * unit(rng);
+          const double amp = (unit(rng) < 0.5 ? -1.0 : 1.0) * (0.4 + 0.6 * unit(rng));
+          p.blob[bl][0] = cx;
+          p.blob[bl][1] = cy;
+          p.blob[bl][2] = amp;
+          p.blob[bl][3] = 2.0 * s * s;
+        }
+        for (int wv = 0; wv < 5; ++wv) {
+          const double freq = 1.0 / (6.0 + 26.0 * unit(rng));
+          const double angle = unit(rng) * 3.14159265358979323846;
+          const double phase = unit(rng) * 2.0 * 3.14159265358979323846;
+          const double amp = 0.08 + 0.14 * unit(rng);
+          p.wave[wv][0] = std::cos(angle) * freq;
+          p.wave[wv][1] = std::sin(angle) * freq;
+          p.wave[wv][2] = phase;
+          p.wave[wv][3] = amp;
+        }
+      }
+      CDVZ_CUDA_CHECK(cudaMemcpyAsync(params.p, hp.data(), sizeof(SynthParams) * nf, cudaMemcpyHostToDevice, ctx->st));
+      CDVZ_CUDA_CHECK(launch_synth(params.as<SynthParams>(), nf, width, height, canvas.as<double>(), bmin.as<double>(),
+                                   bmax.as<double>(), nblk, d_out + size_t(base) * width * height, ctx->st));
+      CDVZ_CUDA_CHECK(cudaStreamSynchronize(ctx->st));
+    }
+    canvas.release();
+    params.release();
+    bmin.release();
+    bmax.release();
+  });
+}
+
+int cdvz_gpu_device_alloc(cdvz_gpu_ctx* ctx, size_t bytes, void** ptr) {
+  return guarded(ctx, [&] {
+    CDVZ_CUDA_CHECK(cudaSetDevice(ctx->device));
+    CDVZ_CUDA_CHECK(cudaMalloc(ptr, std::max<size_t>(bytes, 1)));
+  });
+}
+
+int cdvz_gpu_device_free(cdvz_gpu_ctx* ctx, void* ptr) {
+  return guarded(ctx, [&] { CDVZ_CUDA_CHECK(cudaFree(ptr)); });
+}
+
+int cdvz_gpu_host_alloc(cdvz_gpu_ctx* ctx, size_t bytes, void** ptr) {
+  return guarded(ctx, [&] { CDVZ_CUDA_CHECK(cudaMallocHost(ptr, std::max<size_t>(bytes, 1))); });
+}
+
+int cdvz_gpu_host_free(cdvz_gpu_ctx* ctx, void* ptr) {
+  return guarded(ctx, [&] { CDVZ_CUDA_CHECK(cudaFreeHost(ptr)); });
+}
+
+int cdvz_gpu_copy(cdvz_gpu_ctx* ctx, void* dst, const void* src, size_t bytes, int kind) {
+  return guarded(ctx, [&] {
+    const cudaMemcpyKind k = kind == 1 ? cudaMemcpyHostToDevice : kind == 2 ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+    CDVZ_CUDA_CHECK(cudaMemcpyAsync(dst, src, bytes, k, ctx->st));
+    CDVZ_CUDA_CHECK(cudaStreamSynchronize(ctx->st));
+  });
+}
+
+}  // extern "C"

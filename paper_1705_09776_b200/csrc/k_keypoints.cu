@@ -1,0 +1,388 @@
+// K2/K3 — per-frame keypoint list assembly and K4 — relevance selection.
+//
+// k_merge_octave (one CTA per frame) restores the reference's candidate order
+// and applies cross-octave dedup:
+//   * rank: a survivor's position in (y, x, sigma) order is the number of set
+//     bits before its key in the octave's raster bitmap (k_octave set them),
+//     which reproduces std::sort in detect_extrema (scale_space.cpp:207-213)
+//     followed by the order-preserving filter of refine_candidates (:267-269);
+//   * dedup (scale_space.cpp:272-302): previous points are bucketed in an
+//     8 px grid (the pair test needs |dx|,|dy| < 2, so the 3x3 neighbourhood
+//     of buckets holds every candidate pair), decisions are the reference's
+//     per pair and order-independent; survivors are compacted previous-first.
+// k_select (one CTA per frame) fills the centre distance, scores the five
+// lookup tables (relevance.cpp:24-30, 54-69) and takes the top select_n by
+// the reference's total order (score desc, |p| desc, y, x, index;
+// relevance.cpp:71-93) with an exact MSB-first radix select on the 5-field
+// key, then a bitonic sort of the winners.
+#include "common.cuh"
+
+namespace cdvz_gpu {
+
+namespace {
+
+constexpr int kMergeThreads = 1024;
+
+// Block-wide exclusive scan over one int per thread (1024 threads).
+__device__ int block_exclusive_scan(int v, int* warp_tot, int& total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int incl = v;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int n = __shfl_up_sync(0xffffffffu, incl, d);
+    if (lane >= d) incl += n;
+  }
+  if (lane == 31) warp_tot[wid] = incl;
+  __syncthreads();
+  if (wid == 0) {
+    const int nw = blockDim.x >> 5;
+    int x = lane < nw ? warp_tot[lane] : 0;
+    int xi = x;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int n = __shfl_up_sync(0xffffffffu, xi, d);
+      if (lane >= d) xi += n;
+    }
+    if (lane < nw) warp_tot[lane] = xi - x;
+    if (lane == nw - 1) warp_tot[32] = xi;
+  }
+  __syncthreads();
+  const int res = warp_tot[wid] + incl - v;
+  total = warp_tot[32];
+  __syncthreads();
+  return res;
+}
+
+// Order-preserving compaction of `n` flags (keep != 0) into dst positions:
+// pos[i] = number of kept before i (contiguous chunk per thread).
+template <class Keep, class Emit>
+__device__ int compact(int n, Keep keep, Emit emit, int* warp_tot) {
+  const int per = (n + blockDim.x - 1) / blockDim.x;
+  const int lo = min(n, int(threadIdx.x) * per), hi = min(n, lo + per);
+  int cnt = 0;
+  for (int i = lo; i < hi; ++i) cnt += keep(i) ? 1 : 0;
+  int total = 0;
+  int pos = block_exclusive_scan(cnt, warp_tot, total);
+  for (int i = lo; i < hi; ++i)
+    if (keep(i)) emit(i, pos++);
+  return total;
+}
+
+}  // namespace
+
+// Restores octave o's survivor order and merges it into the accumulated list.
+__global__ void __launch_bounds__(kMergeThreads) k_merge_octave(Batch bt, int o) {
+  extern __shared__ int sm[];
+  __shared__ int warp_tot[33];
+  const int f = blockIdx.x;
+  const int w = bt.ow[o], h = bt.oh[o];
+  const int nwords = (2 * w * h + 31) / 32;
+  uint32_t* bm = bt.bitmap + f * bt.bitmap_words + bt.bm_off[o];
+  int n = bt.raw_count[f * bt.n_oct + o];
+  if (n > bt.cap_oct) n = bt.cap_oct;
+  const KP* raw = bt.raw + ((long long)f * bt.n_oct + o) * bt.cap_oct;
+
+  // Exclusive popcount prefix of the bitmap, per word, in shared memory.
+  int* prefix = sm;  // nwords
+  {
+    const int per = (nwords + blockDim.x - 1) / blockDim.x;
+    const int lo = min(nwords, int(threadIdx.x) * per), hi = min(nwords, lo + per);
+    int cnt = 0;
+    for (int i = lo; i < hi; ++i) cnt += __popc(bm[i]);
+    int total = 0;
+    int run = block_exclusive_scan(cnt, warp_tot, total);
+    for (int i = lo; i < hi; ++i) {
+      prefix[i] = run;
+      run += __popc(bm[i]);
+    }
+  }
+  __syncthreads();
+
+  const int src = (o + 1) & 1, dst = o & 1;  // acc ping-pong: octave o writes acc[o & 1]
+  KP* out_sorted = (o == 0) ? bt.acc[dst] + (long long)f * bt.cap_acc : bt.cur + (long long)f * bt.cap_acc;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const KP k = raw[i];
+    const uint32_t word = k.key >> 5, bit = k.key & 31u;
+    const int rank = prefix[word] + __popc(bm[word] & ((1u << bit) - 1u));
+    out_sorted[rank] = k;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < nwords; i += blockDim.x) bm[i] = 0u;  // ready for the next batch
+  if (threadIdx.x == 0) {
+    bt.raw_count[f * bt.n_oct + o] = 0;
+    bt.oct_count[f * bt.n_oct + o] = n;
+  }
+
+  if (o == 0) {
+    if (threadIdx.x == 0) bt.acc_count[f * 2 + dst] = n;
+    return;
+  }
+
+  // ---- dedup against the accumulated list (scale_space.cpp:272-302)
+  const KP* prev = bt.acc[src] + (long long)f * bt.cap_acc;
+  const int np = bt.acc_count[f * 2 + src];
+  const KP* cur = out_sorted;
+  const int nc = n;
+  const int gw = bt.W / 8 + 3, gh = bt.H / 8 + 3;
+  int* cell_start = sm;                  // gw*gh + 1 (reuses the prefix space)
+  int* cell_fill = sm + gw * gh + 1;     // gw*gh
+  uint8_t* drop_prev = bt.flags + (long long)f * 2 * bt.cap_acc;
+  uint8_t* drop_cur = drop_prev + bt.cap_acc;
+  int* sorted_idx = bt.scratch_idx + (long long)f * bt.cap_acc;
+  auto cell_of = [&](double x, double y) {
+    int cxi = int(floor(x * 0.125)) + 1, cyi = int(floor(y * 0.125)) + 1;
+    cxi = max(0, min(gw - 1, cxi));
+    cyi = max(0, min(gh - 1, cyi));
+    return cyi * gw + cxi;
+  };
+  for (int i = threadIdx.x; i < gw * gh; i += blockDim.x) cell_fill[i] = 0;
+  for (int i = threadIdx.x; i < np; i += blockDim.x) drop_prev[i] = 0;
+  for (int i = threadIdx.x; i < nc; i += blockDim.x) drop_cur[i] = 0;
+  __syncthreads();
+  for (int j = threadIdx.x; j < np; j += blockDim.x) atomicAdd(&cell_fill[cell_of(prev[j].x, prev[j].y)], 1);
+  __syncthreads();
+  {
+    const int ncell = gw * gh;
+    const int per = (ncell + blockDim.x - 1) / blockDim.x;
+    const int lo = min(ncell, int(threadIdx.x) * per), hi = min(ncell, lo + per);
+    int cnt = 0;
+    for (int i = lo; i < hi; ++i) cnt += cell_fill[i];
+    int total = 0;
+    int run = block_exclusive_scan(cnt, warp_tot, total);
+    for (int i = lo; i < hi; ++i) {
+      cell_start[i] = run;
+      run += cell_fill[i];
+    }
+    if (threadIdx.x == 0) cell_start[ncell] = total;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < gw * gh; i += blockDim.x) cell_fill[i] = cell_start[i];
+  __syncthreads();
+  for (int j = threadIdx.x; j < np; j += blockDim.x) {
+    const int pos = atomicAdd(&cell_fill[cell_of(prev[j].x, prev[j].y)], 1);
+    sorted_idx[pos] = j;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < nc; i += blockDim.x) {
+    const KP c = cur[i];
+    const int cc = cell_of(c.x, c.y);
+    const int ccx = cc % gw, ccy = cc / gw;
+    bool dc = false;
+    for (int yy = max(0, ccy - 1); yy <= min(gh - 1, ccy + 1); ++yy)
+      for (int xx = max(0, ccx - 1); xx <= min(gw - 1, ccx + 1); ++xx) {
+        const int cell = yy * gw + xx;
+        for (int q = cell_start[cell]; q < cell_start[cell + 1]; ++q) {
+          const int j = sorted_idx[q];
+          const KP pj = prev[j];
+          const double dx = c.x - pj.x, dy = c.y - pj.y;
+          if (dx * dx + dy * dy >= 4.0) continue;
+          const double ratio = c.sigma / pj.sigma;
+          if (!(ratio >= 1.0 / 1.3 && ratio <= 1.3)) continue;
+          if (fabs(pj.p) >= fabs(c.p)) dc = true;
+          else drop_prev[j] = 1;
+        }
+      }
+    drop_cur[i] = dc ? 1 : 0;
+  }
+  __syncthreads();
+  KP* out = bt.acc[dst] + (long long)f * bt.cap_acc;
+  const int kept_prev = compact(
+      np, [&](int i) { return drop_prev[i] == 0; }, [&](int i, int pos) { out[pos] = prev[i]; }, warp_tot);
+  int kept_cur = 0;
+  {
+    const int cap = bt.cap_acc;
+    kept_cur = compact(
+        nc, [&](int i) { return drop_cur[i] == 0; },
+        [&](int i, int pos) {
+          if (kept_prev + pos < cap) out[kept_prev + pos] = cur[i];
+        },
+        warp_tot);
+  }
+  if (threadIdx.x == 0) {
+    int total = kept_prev + kept_cur;
+    if (total > bt.cap_acc) {
+      total = bt.cap_acc;
+      atomicOr(&bt.status[f], 4);
+    }
+    bt.acc_count[f * 2 + dst] = total;
+  }
+}
+
+size_t merge_smem_bytes(const Batch& bt) {
+  size_t need = 0;
+  for (int o = 0; o < bt.n_oct; ++o) {
+    const size_t words = (size_t(2) * bt.ow[o] * bt.oh[o] + 31) / 32;
+    need = need > words ? need : words;
+  }
+  const size_t cells = size_t(bt.W / 8 + 3) * (bt.H / 8 + 3);
+  const size_t grid = 2 * cells + 1;
+  return sizeof(int) * (need > grid ? need : grid);
+}
+
+cudaError_t launch_merge(const Batch& bt, int o, cudaStream_t st) {
+  const size_t smem = merge_smem_bytes(bt);
+  cudaError_t e = cudaFuncSetAttribute(k_merge_octave, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  if (e != cudaSuccess) return e;
+  k_merge_octave<<<bt.nframes, kMergeThreads, smem, st>>>(bt, o);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- selection
+
+namespace {
+
+// upper_bound over edges, clamped (relevance.cpp:24-30).
+__device__ __forceinline__ double lut(const double* edges, const double* vals, int nb, double x) {
+  int lo = 0, hi = nb + 1;  // first index with edges[idx] > x in [0, nb+1]
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (edges[mid] > x) hi = mid;
+    else lo = mid + 1;
+  }
+  int bin = lo - 1;
+  bin = bin < 0 ? 0 : (bin > nb - 1 ? nb - 1 : bin);
+  return vals[bin];
+}
+
+// The five 64-bit words of the reference's total order, ascending = better.
+struct SelKey { unsigned long long k[5]; };
+
+__device__ __forceinline__ SelKey sel_key(double score, const KP& p, int idx) {
+  SelKey s;
+  s.k[0] = ~static_cast<unsigned long long>(__double_as_longlong(score));      // score >= 0
+  s.k[1] = ~static_cast<unsigned long long>(__double_as_longlong(fabs(p.p)));  // |p| >= 0
+  // y, x >= 0 after refinement (margin >= 2), so their bit patterns order like the values.
+  s.k[2] = static_cast<unsigned long long>(__double_as_longlong(p.y));
+  s.k[3] = static_cast<unsigned long long>(__double_as_longlong(p.x));
+  s.k[4] = static_cast<unsigned long long>(idx);
+  return s;
+}
+
+__device__ __forceinline__ bool key_less(const SelKey& a, const SelKey& b) {
+#pragma unroll
+  for (int i = 0; i < 5; ++i)
+    if (a.k[i] != b.k[i]) return a.k[i] < b.k[i];
+  return false;
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(kMergeThreads) k_select(Batch bt, Model md, EncodeConst ec) {
+  extern __shared__ unsigned char ssm[];
+  __shared__ int warp_tot[33];
+  __shared__ int hist[256];
+  __shared__ int s_remaining, s_digit, s_done;
+  const int f = blockIdx.x;
+  const int last = (bt.n_oct - 1) & 1;
+  KP* acc = bt.acc[last] + (long long)f * bt.cap_acc;
+  const int n = bt.n_oct > 0 ? bt.acc_count[f * 2 + last] : 0;
+  const int want = min(n, bt.select_n);
+  double* score = bt.scratch_d + (long long)f * bt.cap_acc;
+  uint8_t* state = bt.flags + (long long)f * 2 * bt.cap_acc;  // 0 alive, 1 selected, 2 rejected
+
+  // fill_center_distance + relevance product (relevance.cpp:54-69)
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    KP k = acc[i];
+    const double dist = hypot(k.x - ec.cx, k.y - ec.cy);
+    k.d = ec.half_diag > 0.0 ? fmin(dist / ec.half_diag, 1.0) : 0.0;
+    acc[i].d = k.d;
+    double s = 1.0;
+    s *= lut(md.rel_edges[0], md.rel_vals[0], md.rel_nb[0], k.sigma);
+    s *= lut(md.rel_edges[1], md.rel_vals[1], md.rel_nb[1], k.p);
+    s *= lut(md.rel_edges[2], md.rel_vals[2], md.rel_nb[2], k.d);
+    s *= lut(md.rel_edges[3], md.rel_vals[3], md.rel_nb[3], k.rho);
+    s *= lut(md.rel_edges[4], md.rel_vals[4], md.rel_nb[4], k.pss);
+    score[i] = s;
+    state[i] = 0;
+  }
+  if (threadIdx.x == 0) {
+    s_remaining = want;
+    s_done = (want == n) ? 1 : 0;
+  }
+  __syncthreads();
+  if (n > want) {
+    // MSB-first radix select over the 320-bit key (8-bit digits).
+    for (int digit = 0; digit < 40 && !s_done; ++digit) {
+      const int word = digit >> 3, shift = 56 - 8 * (digit & 7);
+      for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
+      __syncthreads();
+      for (int i = threadIdx.x; i < n; i += blockDim.x)
+        if (state[i] == 0) {
+          const SelKey kk = sel_key(score[i], acc[i], i);
+          atomicAdd(&hist[(kk.k[word] >> shift) & 0xFF], 1);
+        }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        int run = 0, d = 0;
+        const int rem = s_remaining;
+        for (d = 0; d < 256; ++d) {
+          if (run + hist[d] >= rem) break;
+          run += hist[d];
+        }
+        s_digit = d;
+        s_remaining = rem - run;
+        if (hist[d] == rem - run) s_done = 2;  // the whole bucket fits exactly
+      }
+      __syncthreads();
+      const int dsel = s_digit;
+      const bool take_bucket = s_done == 2;
+      for (int i = threadIdx.x; i < n; i += blockDim.x)
+        if (state[i] == 0) {
+          const SelKey kk = sel_key(score[i], acc[i], i);
+          const int dv = int((kk.k[word] >> shift) & 0xFF);
+          if (dv < dsel || (dv == dsel && take_bucket)) state[i] = 1;
+          else if (dv > dsel) state[i] = 2;
+        }
+      __syncthreads();
+    }
+  } else {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) state[i] = 1;
+    __syncthreads();
+  }
+  // Gather winners (any order), then bitonic-sort them by the full key.
+  int* win = reinterpret_cast<int*>(ssm);
+  const int got = compact(
+      n, [&](int i) { return state[i] == 1; }, [&](int i, int pos) { win[pos] = i; }, warp_tot);
+  int P = 1;
+  while (P < got) P <<= 1;
+  for (int i = got + threadIdx.x; i < P; i += blockDim.x) win[i] = -1;
+  __syncthreads();
+  for (int size = 2; size <= P; size <<= 1)
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = threadIdx.x; i < P; i += blockDim.x) {
+        const int j = i ^ stride;
+        if (j > i) {
+          const int a = win[i], b = win[j];
+          bool a_after_b;
+          if (a < 0) a_after_b = b >= 0;
+          else if (b < 0) a_after_b = false;
+          else a_after_b = key_less(sel_key(score[b], acc[b], b), sel_key(score[a], acc[a], a));
+          const bool up = (i & size) == 0;
+          if (up == a_after_b) {
+            win[i] = b;
+            win[j] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  KP* sel = bt.sel + (long long)f * bt.select_n;
+  for (int r = threadIdx.x; r < got; r += blockDim.x) sel[r] = acc[win[r]];
+  if (threadIdx.x == 0) bt.sel_count[f] = got;
+}
+
+size_t select_smem_bytes(const Batch& bt) {
+  size_t p = 1;
+  while (p < size_t(bt.select_n)) p <<= 1;
+  return p * sizeof(int);
+}
+
+cudaError_t launch_select(const Batch& bt, const Model& md, const EncodeConst& ec, cudaStream_t st) {
+  const size_t smem = select_smem_bytes(bt);
+  cudaError_t e = cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  if (e != cudaSuccess) return e;
+  k_select<<<bt.nframes, kMergeThreads, smem, st>>>(bt, md, ec);
+  return cudaGetLastError();
+}
+
+}  // namespace cdvz_gpu

@@ -1,0 +1,320 @@
+// K8-K11 — SCFV global descriptor: PCA 128->32, GMM soft assignment,
+// Fisher mean/variance gradients, delta-ranked component selection and sign
+// planes; K12 — CDVZ1 container packing with the CRC-32 trailer.
+//
+// Replaces pca_reduce / posteriors_matrix / softmax_rows / fv_mean_matrix /
+// fv_var_matrix / scfv_delta / scfv_encode (proj/src/scfv.cpp:40-253) and
+// serialize_scfv / pack_local / serialize_container / crc32
+// (proj/src/scfv.cpp:285-298, proj/src/transform_coding.cpp:232-270,
+// proj/src/container.cpp:32-58, proj/src/common.cpp:11-35).
+//
+// Precision: the reference computes in IEEE double; so do these kernels, on
+// the FP64 pipe. Dense products are summed over the inner index in ascending
+// order and vector reductions follow Eigen's SSE2 packet order, both as the
+// oracle restates them, so the SCFV floats agree with the
+// oracle up to libm (exp/log) ulps and the emitted bits agree exactly.
+#include "common.cuh"
+
+namespace cdvz_gpu {
+
+namespace {
+
+// Eigen SSE2 redux order over a contiguous vector (oracle eigen_sum).
+__device__ __forceinline__ double packet_sum_seq(const double* v, int n) {
+  if (n < 2) return n ? v[0] : 0.0;
+  if (n < 4) {
+    double r = v[0] + v[1];
+    for (int i = 2; i < n; ++i) r += v[i];
+    return r;
+  }
+  const int e2 = n / 4 * 4, e1 = n / 2 * 2;
+  double a0 = v[0], a1 = v[1], b0 = v[2], b1 = v[3];
+  for (int i = 4; i < e2; i += 4) {
+    a0 += v[i];
+    a1 += v[i + 1];
+    b0 += v[i + 2];
+    b1 += v[i + 3];
+  }
+  a0 += b0;
+  a1 += b1;
+  if (e1 > e2) {
+    a0 += v[e2];
+    a1 += v[e2 + 1];
+  }
+  double r = a0 + a1;
+  for (int i = e1; i < n; ++i) r += v[i];
+  return r;
+}
+
+}  // namespace
+
+// X[t][r] = sum_j (R[t][j] - mu[j]) * B[r][j], j ascending (scfv.cpp:82-92).
+// The basis is staged transposed in shared memory; each thread carries four
+// descriptor rows so four independent sums hide the FP64 add latency.
+__global__ void __launch_bounds__(128) k_pca(Batch bt, Model md) {
+  __shared__ double bT[128][33];   // basis transposed, padded
+  __shared__ double cen[16][129];  // 16 centred rows
+  const int f = blockIdx.y;
+  const int n = bt.or_count[f];
+  const int tid = threadIdx.x, r = tid & 31, grp = tid >> 5;
+  for (int i = tid; i < 32 * 128; i += blockDim.x) bT[i & 127][i >> 7] = md.pca_basis[i];
+  for (int t0 = blockIdx.x * 16; t0 < n; t0 += gridDim.x * 16) {
+    __syncthreads();
+    for (int i = tid; i < 16 * 128; i += blockDim.x) {
+      const int tt = t0 + (i >> 7), j = i & 127;
+      cen[i >> 7][j] = tt < n ? bt.desc[((long long)f * bt.cap_or + tt) * 128 + j] - md.pca_mean[j] : 0.0;
+    }
+    __syncthreads();
+    double s[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) s[q] = cen[grp * 4 + q][0] * bT[0][r];
+    for (int j = 1; j < 128; ++j) {
+      const double b = bT[j][r];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) s[q] = s[q] + cen[grp * 4 + q][j] * b;
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int tt = t0 + grp * 4 + q;
+      if (tt < n) bt.x[((long long)f * bt.cap_or + tt) * 32 + r] = s[q];
+    }
+  }
+}
+
+// posteriors_matrix (scfv.cpp:140-164) + softmax_rows (scfv.cpp:40-48); one
+// warp per descriptor row, e[] parked in shared memory for the ordered sum.
+__global__ void __launch_bounds__(128) k_posterior(Batch bt, Model md) {
+  extern __shared__ double se[];
+  __shared__ double chain[4][4];
+  const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int f = blockIdx.y;
+  const int n = bt.or_count[f];
+  const int nc = md.nc;
+  double* e = se + wi * nc;
+  for (int t = blockIdx.x * 4 + wi; t < n; t += gridDim.x * 4) {
+    const double* x = bt.x + ((long long)f * bt.cap_or + t) * 32;
+    double peak = -INFINITY;
+    for (int i = lane; i < nc; i += 32) {
+      const double* iv = md.inv_var + i * 32;
+      const double* mv = md.m_over_v + i * 32;
+      const double* m2 = md.m2_over_v + i * 32;
+      double a = (x[0] * x[0]) * iv[0], b = x[0] * mv[0], c = 1.0 * m2[0];
+      for (int j = 1; j < 32; ++j) {
+        a = a + (x[j] * x[j]) * iv[j];
+        b = b + x[j] * mv[j];
+        c = c + 1.0 * m2[j];
+      }
+      const double p = a - 2.0 * b + c;
+      const double lp = -0.5 * p + md.log_norm[i];
+      e[i] = lp;
+      peak = fmax(peak, lp);
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) peak = fmax(peak, __shfl_xor_sync(0xffffffffu, peak, d));
+    __syncwarp();
+    for (int i = lane; i < nc; i += 32) e[i] = exp(e[i] - peak);
+    __syncwarp();
+    double total;
+    if (nc < 4) {
+      total = packet_sum_seq(e, nc);
+    } else {
+      const int e2 = nc / 4 * 4;
+      if (lane < 4) {
+        double a = e[lane];
+        for (int i = lane + 4; i < e2; i += 4) a += e[i];
+        chain[wi][lane] = a;
+      }
+      __syncwarp();
+      double a0 = chain[wi][0] + chain[wi][2], a1 = chain[wi][1] + chain[wi][3];
+      const int e1 = nc / 2 * 2;
+      if (e1 > e2) {
+        a0 += e[e2];
+        a1 += e[e2 + 1];
+      }
+      total = a0 + a1;
+      for (int i = e1; i < nc; ++i) total += e[i];
+    }
+    double* g = bt.gamma + ((long long)f * bt.cap_or + t) * nc;
+    for (int i = lane; i < nc; i += 32) g[i] = e[i] / total;
+    __syncwarp();
+  }
+}
+
+// fv_mean_matrix / fv_var_matrix (scfv.cpp:166-203), one thread per (i, j).
+__global__ void __launch_bounds__(128) k_fisher(Batch bt, Model md, int variance) {
+  const int f = blockIdx.y;
+  const int n = bt.or_count[f];
+  const int nc = md.nc;
+  const int ij = blockIdx.x * blockDim.x + threadIdx.x;
+  if (ij >= nc * 32) return;
+  const int i = ij >> 5, j = ij & 31;
+  double* gm = bt.gm + (long long)f * nc * 32;
+  double* gv = bt.gv + (long long)f * nc * 32;
+  if (n == 0) {
+    gm[ij] = 0.0;
+    gv[ij] = 0.0;
+    return;
+  }
+  const double* G = bt.gamma + (long long)f * bt.cap_or * nc;
+  const double* X = bt.x + (long long)f * bt.cap_or * 32;
+  const double scale = 1.0 / (double(n) * sqrt(md.weights[i]));
+  double qx = G[i] * X[j], qo = G[i] * 1.0, qx2 = G[i] * (X[j] * X[j]);
+  for (int t = 1; t < n; ++t) {
+    const double gti = G[(long long)t * nc + i], xtj = X[t * 32 + j];
+    qx = qx + gti * xtj;
+    qo = qo + gti * 1.0;
+    if (variance) qx2 = qx2 + gti * (xtj * xtj);
+  }
+  const double m = md.means[ij], s = md.stds[ij];
+  gm[ij] = ((qx - qo * m) / s) * scale;
+  if (variance) {
+    const double var = s * s;
+    gv[ij] = ((qx2 - qx * (2.0 * m) + qo * (m * m - var)) / var) * scale;
+  }
+}
+
+// scfv_delta / scfv_encode (scfv.cpp:205-253): one CTA per frame.
+__global__ void __launch_bounds__(256) k_scfv_encode(Batch bt, Model md, EncodeConst ec) {
+  extern __shared__ double sdelta[];
+  const int f = blockIdx.x;
+  const int nc = md.nc;
+  const double* gm = bt.gm + (long long)f * nc * 32;
+  const double* gv = bt.gv + (long long)f * nc * 32;
+  for (int i = threadIdx.x; i < nc; i += blockDim.x) {
+    const double* g = gm + i * 32;
+    const double mean = packet_sum_seq(g, 32) / 32;
+    double d[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) d[j] = (g[j] - mean) * (g[j] - mean);
+    sdelta[i] = sqrt(packet_sum_seq(d, 32) / 32.0);
+  }
+  __syncthreads();
+  uint8_t* chosen = reinterpret_cast<uint8_t*>(sdelta + nc);
+  for (int i = threadIdx.x; i < nc; i += blockDim.x) {
+    const double di = sdelta[i];
+    int rank = 0;
+    for (int j = 0; j < nc; ++j) {
+      const double dj = sdelta[j];
+      rank += (dj > di || (dj == di && j < i)) ? 1 : 0;
+    }
+    const bool sel = rank < ec.k_select;
+    uint32_t mb = 0, vb = 0;
+    for (int j = 0; j < 32; ++j) {
+      if (gm[i * 32 + j] >= 0.0) mb |= (1u << j);
+      if (ec.variance && gv[i * 32 + j] >= 0.0) vb |= (1u << j);
+    }
+    bt.mean_planes[(long long)f * nc + i] = mb;
+    bt.var_planes[(long long)f * nc + i] = vb;
+    chosen[i] = sel ? 1 : 0;
+  }
+  __syncthreads();
+  uint8_t* mask = bt.mask + (long long)f * ec.mask_bytes;
+  for (int b = threadIdx.x; b < ec.mask_bytes; b += blockDim.x) {
+    uint8_t byte = 0;
+    for (int q = 0; q < 8 && b * 8 + q < nc; ++q) byte |= uint8_t(chosen[b * 8 + q] << q);
+    mask[b] = byte;
+  }
+}
+
+// serialize_container (container.cpp:32-58) into a fixed device slot.
+__global__ void __launch_bounds__(256) k_pack(Batch bt, Model md, EncodeConst ec, uint8_t* out, uint32_t* lengths) {
+  extern __shared__ uint8_t buf[];
+  __shared__ uint32_t table[256];
+  __shared__ int s_len;
+  const int f = blockIdx.x;
+  const int nc = md.nc;
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+    uint32_t c = uint32_t(i);
+    for (int k = 0; k < 8; ++k) c = (c & 1u) ? 0xEDB88320u ^ (c >> 1) : c >> 1;
+    table[i] = c;
+  }
+  if (bt.status[f] != 0) {
+    if (threadIdx.x == 0) lengths[f] = 0;
+    return;
+  }
+  const int n_codes = min(bt.or_count[f], ec.max_codes);
+  const int local_len = 4 + n_codes * ec.code_bytes;
+  const int total = 24 + ec.global_bytes + local_len + 4;
+  const uint8_t* mask = bt.mask + (long long)f * ec.mask_bytes;
+  if (threadIdx.x == 0) {
+    uint8_t* p = buf;
+    p[0] = 'C'; p[1] = 'D'; p[2] = 'V'; p[3] = 'Z'; p[4] = '1';
+    p[5] = uint8_t(ec.mode_id);
+    p[6] = uint8_t(bt.W & 0xFF); p[7] = uint8_t(bt.W >> 8);
+    p[8] = uint8_t(bt.H & 0xFF); p[9] = uint8_t(bt.H >> 8);
+    p[10] = uint8_t(nc & 0xFF); p[11] = uint8_t(nc >> 8);
+    const uint32_t vals[3] = {ec.model_crc, uint32_t(ec.global_bytes), uint32_t(local_len)};
+    for (int q = 0; q < 3; ++q)
+      for (int b = 0; b < 4; ++b) p[12 + 4 * q + b] = uint8_t((vals[q] >> (8 * b)) & 0xFF);
+    // global block: mask, then planes of selected components in ascending order
+    int off = 24;
+    for (int b = 0; b < ec.mask_bytes; ++b) p[off++] = mask[b];
+    for (int i = 0; i < nc; ++i) {
+      if (!((mask[i / 8] >> (i % 8)) & 1)) continue;
+      const uint32_t mb = bt.mean_planes[(long long)f * nc + i];
+      for (int b = 0; b < 4; ++b) p[off++] = uint8_t((mb >> (8 * b)) & 0xFF);
+      if (ec.variance) {
+        const uint32_t vb = bt.var_planes[(long long)f * nc + i];
+        for (int b = 0; b < 4; ++b) p[off++] = uint8_t((vb >> (8 * b)) & 0xFF);
+      }
+    }
+    // local block header (transform_coding.cpp:236-240)
+    p[off++] = uint8_t(ec.mode_id);
+    p[off++] = uint8_t(ec.elements);
+    p[off++] = uint8_t(n_codes & 0xFF);
+    p[off++] = uint8_t(n_codes >> 8);
+    s_len = off;
+  }
+  __syncthreads();
+  const int code_base = s_len;
+  const uint8_t* codes = bt.codes + (long long)f * bt.cap_or * bt.code_stride;
+  for (int q = threadIdx.x; q < n_codes * ec.code_bytes; q += blockDim.x) {
+    const int c = q / ec.code_bytes, b = q % ec.code_bytes;
+    buf[code_base + q] = codes[(long long)c * bt.code_stride + b];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t c = 0xFFFFFFFFu;
+    const int body = total - 4;
+    for (int i = 0; i < body; ++i) c = table[(c ^ buf[i]) & 0xFFu] ^ (c >> 8);
+    c ^= 0xFFFFFFFFu;
+    for (int b = 0; b < 4; ++b) buf[body + b] = uint8_t((c >> (8 * b)) & 0xFF);
+    lengths[f] = uint32_t(total);
+  }
+  __syncthreads();
+  uint8_t* dst = out + (long long)f * ec.slot_bytes;
+  for (int i = threadIdx.x; i < total; i += blockDim.x) dst[i] = buf[i];
+}
+
+cudaError_t launch_scfv_pack(const Batch& bt, const Model& md, const EncodeConst& ec, uint8_t* out, uint32_t* lengths,
+                             cudaStream_t st, cudaEvent_t after_aggregation) {
+  k_pca<<<dim3(8, bt.nframes), 128, 0, st>>>(bt, md);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  const size_t psm = sizeof(double) * 4 * size_t(md.nc);
+  if (psm > 48 * 1024) {
+    e = cudaFuncSetAttribute(k_posterior, cudaFuncAttributeMaxDynamicSharedMemorySize, int(psm));
+    if (e != cudaSuccess) return e;
+  }
+  k_posterior<<<dim3(64, bt.nframes), 128, psm, st>>>(bt, md);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  k_fisher<<<dim3((md.nc * 32 + 127) / 128, bt.nframes), 128, 0, st>>>(bt, md, ec.variance);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  const size_t esm = sizeof(double) * size_t(md.nc) + size_t(md.nc);
+  if (esm > 48 * 1024) {
+    e = cudaFuncSetAttribute(k_scfv_encode, cudaFuncAttributeMaxDynamicSharedMemorySize, int(esm));
+    if (e != cudaSuccess) return e;
+  }
+  k_scfv_encode<<<bt.nframes, 256, esm, st>>>(bt, md, ec);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  if (after_aggregation) cudaEventRecord(after_aggregation, st);
+  const size_t ksm = size_t(ec.slot_bytes);
+  if (ksm > 48 * 1024) {
+    e = cudaFuncSetAttribute(k_pack, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ksm));
+    if (e != cudaSuccess) return e;
+  }
+  k_pack<<<bt.nframes, 256, ksm, st>>>(bt, md, ec, out, lengths);
+  return cudaGetLastError();
+}
+
+}  // namespace cdvz_gpu

@@ -1,0 +1,66 @@
+"""CPU: the C ABI library loads, exports every entry point include/cdvz_gpu.h
+declares, and refuses to run without a B200 (no CPU fallback)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+import paper_1705_09776_b200 as cg
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    with open(os.path.join(ROOT, "include", "cdvz_gpu.h")) as f:
+        text = f.read()
+    return sorted(set(re.findall(r"\b(cdvz_gpu_\w+)\s*\(", text)))
+
+
+def test_header_declares_the_boundary():
+    names = declared_symbols()
+    for must in ("cdvz_gpu_create", "cdvz_gpu_encode_batch", "cdvz_gpu_encode_device", "cdvz_gpu_stage_times",
+                 "cdvz_gpu_last_error", "cdvz_gpu_destroy"):
+        assert must in names
+
+
+def test_library_exports_every_declared_symbol():
+    lib = ctypes.CDLL(cg.library_path())
+    missing = [n for n in declared_symbols() if not hasattr(lib, n)]
+    assert not missing, missing
+
+
+def test_library_is_sm100a_only():
+    import subprocess
+
+    out = subprocess.run(["cuobjdump", "--list-elf", cg.library_path()], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    assert "sm_90" not in out and "sm_80" not in out
+
+
+def test_no_cpu_fallback_without_device():
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    with open(os.path.join(ROOT, "tests", "golden", "bundle_b8.txt")) as f:
+        text = f.read()
+    with pytest.raises(cg.InternalError, match="CUDA device"):
+        cg.Extractor(text)
+
+
+def test_mode_table_and_errors():
+    assert [m.budget_bytes for m in cg.MODES] == [512, 1024, 2048, 4096, 8192, 16384]
+    assert cg.mode_by_name("4K").elements == 103 and cg.mode_by_name("16K").elements == 128
+    with pytest.raises(cg.UsageError):
+        cg.mode_by_name("3K")
+    with pytest.raises(cg.DataError):
+        cg.mode_by_id(99)
+    assert cg.container_slot("4K") == 4124
+
+
+def test_container_slot_from_the_library():
+    lib = ctypes.CDLL(cg.library_path())
+    lib.cdvz_gpu_container_slot.restype = ctypes.c_size_t
+    assert [lib.cdvz_gpu_container_slot(i) for i in range(6)] == [540, 1052, 2076, 4124, 8220, 16412]
+    assert lib.cdvz_gpu_container_slot(7) == 0
