@@ -52,8 +52,8 @@ __device__ __forceinline__ double packet_sum_seq(const double* v, int n) {
 // The basis is staged transposed in shared memory; each thread carries four
 // descriptor rows so four independent sums hide the FP64 add latency.
 __global__ void __launch_bounds__(128) k_pca(Batch bt, Model md) {
-  __shared__ double bT[128][33];   // basis transposed, padded
-  __shared__ double cen[16][129];  // 16 centred rows
+  __shared__ double bT[128][32];   // basis transposed (lanes read consecutive r)
+  __shared__ double cen[16][128];  // 16 centred rows (broadcast reads)
   const int f = blockIdx.y;
   const int n = bt.or_count[f];
   const int tid = threadIdx.x, r = tid & 31, grp = tid >> 5;
