@@ -22,6 +22,7 @@
 
 namespace cdvz_gpu {
 cudaError_t launch_octave(const Batch& bt, const DetConst& dc, int o, int src, cudaStream_t st);
+cudaError_t launch_detect(const Batch& bt, const DetConst& dc, int o, cudaStream_t st);
 cudaError_t launch_merge(const Batch& bt, int o, cudaStream_t st);
 cudaError_t launch_select(const Batch& bt, const Model& md, const EncodeConst& ec, cudaStream_t st);
 cudaError_t launch_describe(const Batch& bt, const DetConst& dc, const Model& md, const EncodeConst& ec, cudaStream_t st);
@@ -322,9 +323,10 @@ struct cdvz_gpu_ctx {
         const int src = o == 0 ? (resize ? 1 : 0) : 2;
         CDVZ_CUDA_CHECK(cudaEventRecord(evp[2 * o], st));
         CDVZ_CUDA_CHECK(launch_octave(b, dc, o, src, st));
+        CDVZ_CUDA_CHECK(launch_detect(b, dc, o, st));
         CDVZ_CUDA_CHECK(cudaEventRecord(evp[2 * o + 1], st));
         CDVZ_CUDA_CHECK(launch_merge(b, o, st));
-        launches += 2;
+        launches += 3;
         if (debug) {
           const KP* srcl = (o == 0) ? b.acc[0] : b.cur;
           CDVZ_CUDA_CHECK(cudaMemcpyAsync(dbg_oct.as<KP>() + (long long)o * bt.cap_acc * geo_frames, srcl,
@@ -352,10 +354,13 @@ struct cdvz_gpu_ctx {
         float pm = 0.f;
         cudaEventElapsedTime(&pm, evp[2 * o], evp[2 * o + 1]);
         pyr_ms += pm;
-        // Algorithmic bytes of the fused octave kernel: base read + 4 G levels written.
+        // Algorithmic bytes of the split octave pair: K1a reads
+        // the base (1 B/px u8 at octave 0, 8 B/px f64 above) and writes 4 G
+        // levels (32 B/px); K1b reads the 4 G levels of its window back.
         const double px = double(b.ow[o]) * b.oh[o];
         const double in_b = (o == 0) ? (resize ? 8.0 : 1.0) : 8.0;
-        pyr_bytes += double(nf) * px * (in_b + 32.0);
+        const int ww = std::max(0, b.ow[o] - 2 * dc.margin), hh = std::max(0, b.oh[o] - 2 * dc.margin);
+        pyr_bytes += double(nf) * (px * (in_b + 32.0) + 32.0 * ww * hh);
       }
     }
     last_frames = std::min(frames, max_batch);

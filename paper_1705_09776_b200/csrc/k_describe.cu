@@ -214,19 +214,31 @@ __global__ void __launch_bounds__(1024) k_expand(Batch bt) {
   }
 }
 
-// One CTA (4 warps) per oriented point, grid-strided: description
+// One CTA per oriented point, grid-strided: description
 // (descriptor.cpp:47-145) + compression (transform_coding.cpp:81-217).
+//
+// Phase A: all samples of the patch are evaluated in parallel (bilinear
+// gradients, magnitude, Gaussian weight, orientation) and parked in shared
+// memory. Phase B: thread (sub-patch s, cell c, parity p) owns the 4
+// orientation bins of cell c with parity p for sub-patch s. A sample's cell
+// coordinates depend only on its index (cu0 = floor(u(i) / 3sigma + 1.5),
+// cv0 likewise in j), so the samples feeding cell c form a rectangle in index
+// space; the thread walks it in row-major order, which is exactly the order
+// the reference adds them, and each sample adds to exactly one of its bins.
+constexpr int kMaxSamples = 33;  // samples per axis (ceil(12 sigma) for sigma <= 2.75)
+
 __global__ void __launch_bounds__(128) k_describe(Batch bt, DetConst dc, Model md, EncodeConst ec) {
-  __shared__ double s_w[4][32], s_fu[4][32], s_fv[4][32], s_fo[4][32];
-  __shared__ int s_c[4][32];  // cu0 | cv0 << 8 | ob0 << 16 (biased), -1 = no sample
+  __shared__ double s_w[kMaxSamples * kMaxSamples];       // weight; +0 for a skipped sample
+  __shared__ double s_wo[2][kMaxSamples * kMaxSamples];   // wo for the bin of parity 0 / 1
+  __shared__ uint8_t s_slot[kMaxSamples * kMaxSamples];   // bin >> 1 for parity 0 (bits 0-1) / 1 (bits 2-3)
+  __shared__ double s_wu[2][kMaxSamples], s_wv[2][kMaxSamples];  // [du][i]: 1 - fu, fu
+  __shared__ int s_cu[kMaxSamples], s_cv[kMaxSamples];
   __shared__ double part[16][128];
-  __shared__ double vec[128], sq[128], red[4], tv[128];
+  __shared__ double sq[128], red[4], tv[128], vec[128];
   __shared__ uint8_t sym[128];
-  const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
+  const int tid = threadIdx.x;
   const int f = blockIdx.y;
   const int n_or = bt.or_count[f];
-  const int cell = lane >> 1, parity = lane & 1;
-  const int cell_x = cell & 3, cell_y = cell >> 2;
   for (int idx = blockIdx.x; idx < n_or; idx += gridDim.x) {
     const Oriented orp = bt.oriented[(long long)f * bt.cap_or + idx];
     const KP k = bt.sel[(long long)f * bt.select_n + orp.sel];
@@ -241,65 +253,97 @@ __global__ void __launch_bounds__(128) k_describe(Batch bt, DetConst dc, Model m
     const double inv_cell = 1.0 / (3.0 * fr.sigma);
     const double gauss_denom = 2.0 * half * half;
     const int n_sub = spa * spa;
-    for (int sp = wi; sp < n_sub; sp += 4) {
-      const int i_lo = (sp % spa) * 16, j_lo = (sp / spa) * 16;
-      const int ni = min(samples, i_lo + 16) - i_lo, nj = min(samples, j_lo + 16) - j_lo;
-      const int ns = ni * nj;
-      double acc[4] = {0.0, 0.0, 0.0, 0.0};
-      for (int base = 0; base < ns; base += 32) {
-        const int q = base + lane;
-        int code = -1;
-        double wgt = 0.0, fu = 0.0, fv = 0.0, fo = 0.0;
-        if (q < ns) {
-          const int j = j_lo + q / ni, i = i_lo + q % ni;
-          const double v = (j + 0.5) * step - half;
-          const double u = (i + 0.5) * step - half;
-          const double px = fr.x + u * cos_t - v * sin_t;
-          const double py = fr.y + u * sin_t + v * cos_t;
-          if (!(px < 1.0 || px > fr.w - 2.0 || py < 1.0 || py > fr.h - 2.0)) {
-            const double gx = 0.5 * (sample_bilinear(fr.lvl, fr.w, px + 1.0, py) - sample_bilinear(fr.lvl, fr.w, px - 1.0, py));
-            const double gy = 0.5 * (sample_bilinear(fr.lvl, fr.w, px, py + 1.0) - sample_bilinear(fr.lvl, fr.w, px, py - 1.0));
-            const double mag = hypot(gx, gy);
-            if (mag != 0.0) {
-              wgt = mag * exp(-(u * u + v * v) / gauss_denom);
-              const double phi = wrap_angle(atan2(gy, gx) - theta);
-              const double cu = u * inv_cell + 1.5, cv = v * inv_cell + 1.5;
-              const double ob = phi / kTwoPi * 8 - 0.5;
-              const int cu0 = static_cast<int>(floor(cu)), cv0 = static_cast<int>(floor(cv));
-              const int ob0 = static_cast<int>(floor(ob));
-              fu = cu - cu0;
-              fv = cv - cv0;
-              fo = ob - ob0;
-              code = (cu0 + 64) | ((cv0 + 64) << 8) | ((ob0 + 64) << 16);
-            }
-          }
+    if (samples > kMaxSamples) {  // outside the supported scale range: flag the frame
+      if (tid == 0) atomicOr(&bt.status[f], 8);
+      continue;
+    }
+    // Per-axis cell coordinates (descriptor.cpp:89-96): cu depends on i only.
+    for (int i = tid; i < samples; i += blockDim.x) {
+      const double u = (i + 0.5) * step - half;
+      const double cu = u * inv_cell + 1.5;
+      const int cu0 = static_cast<int>(floor(cu));
+      const double fu = cu - cu0;
+      s_cu[i] = cu0;
+      s_wu[0][i] = 1.0 - fu;
+      s_wu[1][i] = fu;
+    }
+    for (int j = tid; j < samples; j += blockDim.x) {
+      const double v = (j + 0.5) * step - half;
+      const double cv = v * inv_cell + 1.5;
+      const int cv0 = static_cast<int>(floor(cv));
+      const double fv = cv - cv0;
+      s_cv[j] = cv0;
+      s_wv[0][j] = 1.0 - fv;
+      s_wv[1][j] = fv;
+    }
+    // Phase A: every sample (descriptor.cpp:75-88).
+    const int ns = samples * samples;
+    for (int q = tid; q < ns; q += blockDim.x) {
+      const int j = q / samples, i = q - j * samples;
+      const double v = (j + 0.5) * step - half;
+      const double u = (i + 0.5) * step - half;
+      const double px = fr.x + u * cos_t - v * sin_t;
+      const double py = fr.y + u * sin_t + v * cos_t;
+      int bin0 = 0;
+      double wgt = 0.0, fo = 0.0;
+      if (!(px < 1.0 || px > fr.w - 2.0 || py < 1.0 || py > fr.h - 2.0)) {
+        const double gx = 0.5 * (sample_bilinear(fr.lvl, fr.w, px + 1.0, py) - sample_bilinear(fr.lvl, fr.w, px - 1.0, py));
+        const double gy = 0.5 * (sample_bilinear(fr.lvl, fr.w, px, py + 1.0) - sample_bilinear(fr.lvl, fr.w, px, py - 1.0));
+        const double mag = hypot(gx, gy);
+        if (mag != 0.0) {
+          wgt = mag * exp(-(u * u + v * v) / gauss_denom);
+          const double phi = wrap_angle(atan2(gy, gx) - theta);
+          const double obv = phi / kTwoPi * 8 - 0.5;
+          const int ob0 = static_cast<int>(floor(obv));
+          fo = obv - ob0;
+          bin0 = ((ob0 % 8) + 8) % 8;
         }
-        s_c[wi][lane] = code;
-        s_w[wi][lane] = wgt;
-        s_fu[wi][lane] = fu;
-        s_fv[wi][lane] = fv;
-        s_fo[wi][lane] = fo;
-        __syncwarp();
-        const int nsmp = min(32, ns - base);
-        for (int s = 0; s < nsmp; ++s) {
-          const int c = s_c[wi][s];
-          if (c < 0) continue;
-          const int cu0 = (c & 0xFF) - 64, cv0 = ((c >> 8) & 0xFF) - 64, ob0 = ((c >> 16) & 0xFF) - 64;
-          const int dv = cell_y - cv0, du = cell_x - cu0;
-          if ((dv == 0 || dv == 1) && (du == 0 || du == 1)) {
-            const int bin0 = ((ob0 % 8) + 8) % 8;
-            const int dob = ((bin0 & 1) == parity) ? 0 : 1;
-            const int bin = ((ob0 + dob) % 8 + 8) % 8;
-            const double wv = dv ? s_fv[wi][s] : 1.0 - s_fv[wi][s];
-            const double wu = du ? s_fu[wi][s] : 1.0 - s_fu[wi][s];
-            const double wo = dob ? s_fo[wi][s] : 1.0 - s_fo[wi][s];
-            acc[bin >> 1] += s_w[wi][s] * wv * wu * wo;
-          }
-        }
-        __syncwarp();
       }
-#pragma unroll
-      for (int t = 0; t < 4; ++t) part[sp][cell * 8 + parity + 2 * t] = acc[t];
+      // Of the sample's two orientation bins (bin0, bin0 + 1 mod 8), the one
+      // of parity p gets wo = 1 - fo if it is bin0, fo otherwise.
+      const int odd = bin0 & 1;
+      const int b_even = odd ? (bin0 + 1) & 7 : bin0, b_odd = odd ? bin0 : (bin0 + 1) & 7;
+      s_w[q] = wgt;
+      s_wo[0][q] = odd ? fo : 1.0 - fo;
+      s_wo[1][q] = odd ? 1.0 - fo : fo;
+      s_slot[q] = uint8_t((b_even >> 1) | ((b_odd >> 1) << 2));
+    }
+    __syncthreads();
+    // Phase B: ordered accumulation (descriptor.cpp:98-116).
+    {
+      const int sp = tid >> 5, cell = (tid >> 1) & 15, parity = tid & 1;
+      const int cx = cell & 3, cy = cell >> 2;
+      double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
+      if (sp < n_sub) {
+        const int i_lo = (sp % spa) * 16, j_lo = (sp / spa) * 16;
+        const int i_hi = min(samples, i_lo + 16), j_hi = min(samples, j_lo + 16);
+        // Samples with cu0 in {cx-1, cx} (du = 1, 0) and cv0 in {cy-1, cy}.
+        int ia = i_lo, ib = i_hi, ja = j_lo, jb = j_hi;
+        while (ia < ib && s_cu[ia] < cx - 1) ++ia;
+        while (ib > ia && s_cu[ib - 1] > cx) --ib;
+        while (ja < jb && s_cv[ja] < cy - 1) ++ja;
+        while (jb > ja && s_cv[jb - 1] > cy) --jb;
+        const double* wo_p = s_wo[parity];
+        const int shift = 2 * parity;
+        for (int j = ja; j < jb; ++j) {
+          const double wv = s_wv[cy - s_cv[j]][j];
+          const int row = j * samples;
+          for (int i = ia; i < ib; ++i) {
+            const int q = row + i;
+            // A skipped sample has weight +0: the add leaves the (non-negative) sum unchanged.
+            const double add = s_w[q] * wv * s_wu[cx - s_cu[i]][i] * wo_p[q];
+            const int slot = (s_slot[q] >> shift) & 3;
+            acc0 += slot == 0 ? add : 0.0;
+            acc1 += slot == 1 ? add : 0.0;
+            acc2 += slot == 2 ? add : 0.0;
+            acc3 += slot == 3 ? add : 0.0;
+          }
+        }
+        part[sp][cell * 8 + parity] = acc0;
+        part[sp][cell * 8 + parity + 2] = acc1;
+        part[sp][cell * 8 + parity + 4] = acc2;
+        part[sp][cell * 8 + parity + 6] = acc3;
+      }
     }
     __syncthreads();
     // merge_and_normalize (descriptor.cpp:124-145): sum partials in order,
@@ -355,10 +399,10 @@ __global__ void __launch_bounds__(128) k_describe(Batch bt, DetConst dc, Model m
     }
     if (tid == 0) {
       // quantize_coord / quantize_sigma_log / quantize_theta (transform_coding.cpp:173-200)
-      const double cx = fmin(fmax(k.x, 0.0), double(bt.W - 1));
-      const double cy = fmin(fmax(k.y, 0.0), double(bt.H - 1));
-      const unsigned xq = (unsigned)llround(cx / (bt.W - 1) * 65535.0);
-      const unsigned yq = (unsigned)llround(cy / (bt.H - 1) * 65535.0);
+      const double cxq = fmin(fmax(k.x, 0.0), double(bt.W - 1));
+      const double cyq = fmin(fmax(k.y, 0.0), double(bt.H - 1));
+      const unsigned xq = (unsigned)llround(cxq / (bt.W - 1) * 65535.0);
+      const unsigned yq = (unsigned)llround(cyq / (bt.H - 1) * 65535.0);
       const double sc = fmin(fmax(k.sigma, 0.5), 64.0);
       const double tq = log2(sc / 0.5) / ec.log2_range;
       const unsigned sq8 = (unsigned)llround(tq * 255.0);

@@ -60,6 +60,26 @@ __device__ __forceinline__ int derivative_roots(const double a[4], double r[2]) 
   return n;
 }
 
+// Mirror for indices within one period of the border (|overhang| < n):
+// -1 -> 0, n -> n-1 (common.hpp:24-30 restricted to the range the walks use).
+__device__ __forceinline__ int mirror_near(int i, int n) { return i < 0 ? -1 - i : (i >= n ? 2 * n - 1 - i : i); }
+
+template <int SRC> struct RawT { using type = double; };
+template <> struct RawT<0> { using type = uint8_t; };
+
+template <int SRC>
+__device__ __forceinline__ typename RawT<SRC>::type load_raw(const Batch& bt, int f, int o, int ry, int xx) {
+  if constexpr (SRC == 0) return bt.pix8[f * bt.frame_bytes8 + (long long)ry * bt.stride8 + xx];
+  else if constexpr (SRC == 1) return bt.pixf[(long long)f * bt.W * bt.H + (long long)ry * bt.W + xx];
+  else return bt.pyr[f * bt.frame_doubles + bt.plane_off[o - 1][3] + (long long)(2 * ry) * bt.ow[o - 1] + 2 * xx];
+}
+
+template <int SRC>
+__device__ __forceinline__ double to_base(typename RawT<SRC>::type v) {
+  if constexpr (SRC == 0) return v * (1.0 / 255.0);  // image.cpp:79-87: raw * (1.0 / 255.0)
+  else return v;
+}
+
 template <int SRC>
 __device__ __forceinline__ double load_base(const Batch& bt, int f, int o, int ry, int xx) {
   if constexpr (SRC == 0) {
@@ -75,224 +95,313 @@ __device__ __forceinline__ double load_base(const Batch& bt, int f, int o, int r
 
 }  // namespace
 
-template <int R0, int R1, int R2, int R3, int SRC>
-__global__ void __launch_bounds__(256, 1) k_octave(Batch bt, DetConst dc, int o, int S) {
-  constexpr int RM = R3;
-  constexpr int D0 = RM + R0 + 1, D1 = RM + R1 + 1, D2 = RM + R2 + 1, D3 = RM + R3 + 1;
-  extern __shared__ double smem[];
-  const int T = blockDim.x;
-  const int nbrow = S + 4 + 2 * RM;
-  double* brow = smem;
-  double* Gs = brow + nbrow;  // [3 rows][4 levels][T]
-  double* As = Gs + 12 * T;   // [3 rows][4 coefs][T]
+// Exact candidate test + refinement for one pixel whose alpha rows are in
+// shared memory (scale_space.cpp:172-205 and :221-266). Emits survivors.
+__device__ __forceinline__ void exact_detect(const Batch& bt, const DetConst& dc, int f, int o, int w, int yd, int cx,
+                                          const double* up, const double* mid, const double* dn, int T, int t,
+                                          double oct_scale) {
+  const double* arow[3] = {up, mid, dn};
+  double a[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) a[i] = mid[i * T + t];
+  double roots[2];
+  const int nr = derivative_roots(a, roots);
+  for (int ri = 0; ri < nr; ++ri) {
+    const double s = roots[ri];
+    if (s < dc.s_lo || s > dc.s_hi) continue;
+    const double p = poly_at(a, s);
+    if (fabs(p) < dc.thr) continue;
+    double p3[3][3];
+    bool ext = true;
+#pragma unroll
+    for (int dy = -1; dy <= 1; ++dy)
+#pragma unroll
+      for (int dx = -1; dx <= 1; ++dx) {
+        double an[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) an[i] = arow[dy + 1][i * T + t + dx];
+        const double pn = (dx == 0 && dy == 0) ? p : poly_at(an, s);
+        p3[dy + 1][dx + 1] = pn;
+        if (!(dx == 0 && dy == 0) && (p > 0.0 ? (p <= pn) : (p >= pn))) ext = false;
+      }
+    if (!ext) continue;
+    const double gx = 0.5 * (p3[1][2] - p3[1][0]);
+    const double gy = 0.5 * (p3[2][1] - p3[0][1]);
+    const double hxx = p3[1][2] + p3[1][0] - 2.0 * p3[1][1];
+    const double hyy = p3[2][1] + p3[0][1] - 2.0 * p3[1][1];
+    const double hxy = 0.25 * (p3[2][2] - p3[2][0] - p3[0][2] + p3[0][0]);
+    const double det = hxx * hyy - hxy * hxy;
+    if (det <= 0.0) continue;
+    const double rho = (hxx + hyy) * (hxx + hyy) / det;
+    if (rho > dc.rho_limit) continue;
+    const double ox = -(hyy * gx - hxy * gy) / det;
+    const double oy = (hxy * gx - hxx * gy) / det;
+    if (fabs(ox) > 0.6 || fabs(oy) > 0.6) continue;
+    KP k;
+    k.x = (cx + ox) * oct_scale;
+    k.y = (yd + oy) * oct_scale;
+    k.sigma = s * oct_scale;
+    k.p = p;
+    k.rho = rho;
+    k.pss = 2.0 * a[2] + 6.0 * a[3] * s;
+    k.d = 0.0;
+    k.octave = o;
+    const int slot = (nr == 2 && s > roots[1 - ri]) ? 1 : 0;  // sigma order within the pixel
+    k.key = (uint32_t(yd) * uint32_t(w) + uint32_t(cx)) * 2u + uint32_t(slot);
+    const int idx = atomicAdd(&bt.raw_count[f * bt.n_oct + o], 1);
+    if (idx < bt.cap_oct) {
+      bt.raw[((long long)f * bt.n_oct + o) * bt.cap_oct + idx] = k;
+      atomicOr(&bt.bitmap[f * bt.bitmap_words + bt.bm_off[o] + (k.key >> 5)], 1u << (k.key & 31u));
+    } else {
+      atomicOr(&bt.status[f], 4);
+    }
+  }
+}
 
-  const int f = blockIdx.y, t = threadIdx.x;
+// Conservative FP32 screen (runs on the FP32 pipe, beside the FP64 work): a
+// pixel is dropped only when no root of the derivative can lie in
+// [s_lo, s_hi] or no in-range root can reach |p| >= thr, with margins orders
+// of magnitude above the float error. Everything else gets the exact test.
+__device__ __forceinline__ bool screen_pixel(const double a[4], const DetConst& dc) {
+  const double qa = 3.0 * a[3], qb = 2.0 * a[2], qc = a[1];
+  if (qa == 0.0) return true;
+  const double disc = qb * qb - 4.0 * qa * qc;
+  if (disc < 0.0) return false;  // exactly the reference's test: no real root
+  if (!(disc > 1e-6 * (qb * qb))) return true;  // near-double root: let the exact path decide
+  const float fa = float(qa), fb = float(qb), fc = float(qc);
+  const float sq = sqrtf(float(disc));
+  const float q = -0.5f * (fb + copysignf(sq, fb));
+  if (!(fabsf(q) > 1e-30f)) return true;
+  const float r0 = q / fa, r1 = fc / q;
+  const float lo = float(dc.s_lo) - 0.05f, hi = float(dc.s_hi) + 0.05f;
+  const float a0 = float(a[0]), a1 = float(a[1]), a2 = float(a[2]), a3 = float(a[3]);
+  const float thr = float(dc.thr);
+  bool any = false;
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const float r = k ? r1 : r0;
+    if (!(r >= lo && r <= hi)) {
+      if (!isfinite(r)) any = true;
+      continue;
+    }
+    const float p = a0 + r * (a1 + r * (a2 + r * a3));
+    const float bound = fabsf(a0) + r * (fabsf(a1) + r * (fabsf(a2) + r * fabsf(a3)));
+    if (fabsf(p) + 1e-5f * bound + 1e-6f >= thr) any = true;
+  }
+  return any;
+}
+
+// ---------------------------------------------------------------- K1a: blur
+// One CTA = one Gaussian level of one strip of kBlurCols columns of one frame.
+// Each thread owns a column and walks it top to bottom RS virtual rows per
+// step: x pass of the new rows into a register ring, y pass of RS output rows
+// (image.cpp:187-210), G rows stored to HBM. Base rows are double-buffered in
+// shared memory (next step's rows are fetched into registers while the
+// current step computes), so there is one barrier per step and no halo
+// columns: the strip is exactly the output.
+constexpr int kBlurCols = 128;
+constexpr int kBlurRows = 4;
+
+template <int R, int SRC>
+__device__ __forceinline__ void blur_level(const Batch& bt, const double* __restrict__ taps, int f, int o, int lvl,
+                                           double* brow /* [2][RS][NB] */) {
+  constexpr int RS = kBlurRows, NB = kBlurCols + 2 * R, D = 2 * R + RS;
+  constexpr int PER = (RS * NB + kBlurCols - 1) / kBlurCols;  // staged elements per thread
   const int w = bt.ow[o], h = bt.oh[o];
-  const int x0 = blockIdx.x * S;
-  const int cx = x0 - 2 + t;
-  const bool active = t < S + 4;
-  double* pyr = bt.pyr + f * bt.frame_doubles;
-  double* G0 = pyr + bt.plane_off[o][0];
-  double* G1 = pyr + bt.plane_off[o][1];
-  double* G2 = pyr + bt.plane_off[o][2];
-  double* G3 = pyr + bt.plane_off[o][3];
-  const bool store_col = t >= 2 && t < S + 2 && cx < w;
-  const int m = dc.margin;
-  const bool det_col = t >= 2 && t < S + 2 && cx >= m && cx < w - m;
-  const bool lap_col = t >= 1 && t <= S + 2;
-  const double oct_scale = ldexp(1.0, o);
-
-  double r0[D0], r1[D1], r2[D2], r3[D3];
+  const int c = threadIdx.x;
+  const int x0 = blockIdx.x * kBlurCols;
+  const int cx = x0 + c;
+  const bool store = cx < w;
+  double* G = bt.pyr + f * bt.frame_doubles + bt.plane_off[o][lvl];
+  // Column mirror map for this thread's staging slots (fixed for the whole walk).
+  int scol[PER], srow[PER];
 #pragma unroll
-  for (int i = 0; i < D0; ++i) r0[i] = 0.0;
+  for (int k = 0; k < PER; ++k) {
+    const int q = c + k * kBlurCols;
+    srow[k] = q / NB;
+    scol[k] = q < RS * NB ? mirror_near(x0 - R + (q - srow[k] * NB), w) : 0;
+  }
+  double t[R + 1];  // symmetric taps: t[|j|] = taps[R + |j|]
 #pragma unroll
-  for (int i = 0; i < D1; ++i) r1[i] = 0.0;
+  for (int j = 0; j <= R; ++j) t[j] = taps[R + j];
+  double ring[D];
 #pragma unroll
-  for (int i = 0; i < D2; ++i) r2[i] = 0.0;
+  for (int i = 0; i < D; ++i) ring[i] = 0.0;
+  typename RawT<SRC>::type pre[PER];  // raw values in flight; converted when parked
+  auto fetch = [&](int v0) {
 #pragma unroll
-  for (int i = 0; i < D3; ++i) r3[i] = 0.0;
-
-  for (int v = -RM; v <= h - 1 + RM; ++v) {
-    // 1. stage base row mirror(v), columns mirror(x0-2-RM+i)
-    {
-      const int ry = mirror_index(v, h);
-      for (int i = t; i < nbrow; i += T) brow[i] = load_base<SRC>(bt, f, o, ry, mirror_index(x0 - 2 - RM + i, w));
+    for (int k = 0; k < PER; ++k) {
+      const int q = c + k * kBlurCols;
+      if (q < RS * NB) pre[k] = load_raw<SRC>(bt, f, o, mirror_near(v0 + srow[k], h), scol[k]);
     }
+  };
+  auto park = [&](double* dst) {
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      const int q = c + k * kBlurCols;
+      if (q < RS * NB) dst[q] = to_base<SRC>(pre[k]);
+    }
+  };
+  int buf = 0;
+  fetch(-R);
+  park(brow);
+  __syncthreads();
+  for (int v0 = -R; v0 <= h - 1 + R; v0 += RS) {
+    const bool more = v0 + RS <= h - 1 + R;
+    if (more) fetch(v0 + RS);
+    const double* b = brow + buf * RS * NB;
+    double acc[RS];
+#pragma unroll
+    for (int i = 0; i < RS; ++i) {
+      const double* bp = b + i * NB + c + R;
+      acc[i] = t[R] * bp[-R];
+#pragma unroll
+      for (int j = -R + 1; j <= R; ++j) acc[i] = acc[i] + t[j < 0 ? -j : j] * bp[j];
+    }
+#pragma unroll
+    for (int d = 0; d < D - RS; ++d) ring[d] = ring[d + RS];
+#pragma unroll
+    for (int i = 0; i < RS; ++i) ring[D - RS + i] = acc[i];
+    // ring[0] holds virtual row v0 - 2R; output row y_i = v0 + i - R.
+#pragma unroll
+    for (int i = 0; i < RS; ++i) {
+      const int y = v0 + i - R;
+      if (y >= 0 && y < h && store) {
+        double g = t[R] * ring[i];
+#pragma unroll
+        for (int j = 1; j <= 2 * R; ++j) g = g + t[j < R ? R - j : j - R] * ring[i + j];
+        G[(long long)y * w + cx] = g;
+      }
+    }
+    if (more) park(brow + (buf ^ 1) * RS * NB);
     __syncthreads();
+    buf ^= 1;
+  }
+}
 
-    // 2. x pass (image.cpp:187-196): acc over j = -r..r; 0.0 + x == x exactly
-    //    for the non-negative products, so the first tap seeds the sum.
-    if (active) {
-      const double* bp = brow + t + RM;
-      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-#pragma unroll
-      for (int j = -RM; j <= RM; ++j) {
-        const double val = bp[j];
-        if (j >= -R0 && j <= R0) a0 = (j == -R0) ? dc.taps[0][0] * val : a0 + dc.taps[0][j + R0] * val;
-        if (j >= -R1 && j <= R1) a1 = (j == -R1) ? dc.taps[1][0] * val : a1 + dc.taps[1][j + R1] * val;
-        if (j >= -R2 && j <= R2) a2 = (j == -R2) ? dc.taps[2][0] * val : a2 + dc.taps[2][j + R2] * val;
-        a3 = (j == -R3) ? dc.taps[3][0] * val : a3 + dc.taps[3][j + R3] * val;
-      }
-#pragma unroll
-      for (int i = 0; i < D0 - 1; ++i) r0[i] = r0[i + 1];
-#pragma unroll
-      for (int i = 0; i < D1 - 1; ++i) r1[i] = r1[i + 1];
-#pragma unroll
-      for (int i = 0; i < D2 - 1; ++i) r2[i] = r2[i + 1];
-#pragma unroll
-      for (int i = 0; i < D3 - 1; ++i) r3[i] = r3[i + 1];
-      r0[D0 - 1] = a0;
-      r1[D1 - 1] = a1;
-      r2[D2 - 1] = a2;
-      r3[D3 - 1] = a3;
-    }
+template <int R0, int R1, int R2, int R3, int SRC>
+__global__ void __launch_bounds__(kBlurCols, 4) k_blur(Batch bt, DetConst dc, int o) {
+  __shared__ double brow[2 * kBlurRows * (kBlurCols + 2 * R3)];
+  const int lvl = blockIdx.y, f = blockIdx.z;
+  switch (lvl) {
+    case 0: blur_level<R0, SRC>(bt, dc.taps[0], f, o, 0, brow); break;
+    case 1: blur_level<R1, SRC>(bt, dc.taps[1], f, o, 1, brow); break;
+    case 2: blur_level<R2, SRC>(bt, dc.taps[2], f, o, 2, brow); break;
+    default: blur_level<R3, SRC>(bt, dc.taps[3], f, o, 3, brow); break;
+  }
+}
 
-    // 3. y pass (image.cpp:201-210) for output row y = v - RM.
-    const int y = v - RM;
-    if (y >= 0 && active) {
-      double g0 = dc.taps[0][0] * r0[0], g1 = dc.taps[1][0] * r1[0], g2 = dc.taps[2][0] * r2[0], g3 = dc.taps[3][0] * r3[0];
+// ---------------------------------------------------------------- K1b: extrema
+// One CTA = a kDetW x kDetH tile of the detection window [m, w-m) x [m, h-m)
+// of one octave of one frame. G of the tile plus a 2-pixel halo is read back
+// (HBM/L2), sigma^2-Laplacians and alpha = beta * L are formed for the tile
+// plus a 1-pixel halo in shared memory, every pixel is screened (FP32) and the
+// plausible ones run the exact FP64 test + refinement from a dense queue.
+constexpr int kDetW = 64, kDetH = 16, kDetThreads = 256;
+constexpr int kGW = kDetW + 4, kGH = kDetH + 4;  // G region
+constexpr int kAW = kDetW + 2, kAH = kDetH + 2;  // alpha region
+
+__global__ void __launch_bounds__(kDetThreads, 2) k_detect(Batch bt, DetConst dc, int o) {
+  extern __shared__ double dsm[];
+  double* Gt = dsm;                      // [4][kGH][kGW]
+  double* At = Gt + 4 * kGH * kGW;       // [kAH][4][kAW]
+  __shared__ int q_count;
+  __shared__ uint16_t queue[kDetW * kDetH];
+  const int f = blockIdx.z, tid = threadIdx.x;
+  const int w = bt.ow[o], h = bt.oh[o], m = dc.margin;
+  const int tx0 = m + blockIdx.x * kDetW, ty0 = m + blockIdx.y * kDetH;
+  const double* pyr = bt.pyr + f * bt.frame_doubles;
+  if (tid == 0) q_count = 0;
+  {
+    constexpr int N = 4 * kGH * kGW, PER = (N + kDetThreads - 1) / kDetThreads;
+    double v[PER];
 #pragma unroll
-      for (int i = 1; i <= 2 * R0; ++i) g0 = g0 + dc.taps[0][i] * r0[i];
-#pragma unroll
-      for (int i = 1; i <= 2 * R1; ++i) g1 = g1 + dc.taps[1][i] * r1[i];
-#pragma unroll
-      for (int i = 1; i <= 2 * R2; ++i) g2 = g2 + dc.taps[2][i] * r2[i];
-#pragma unroll
-      for (int i = 1; i <= 2 * R3; ++i) g3 = g3 + dc.taps[3][i] * r3[i];
-      double* gs = Gs + (y % 3) * 4 * T + t;
-      gs[0] = g0;
-      gs[T] = g1;
-      gs[2 * T] = g2;
-      gs[3 * T] = g3;
-      if (store_col) {
-        const long long off = (long long)y * w + cx;
-        G0[off] = g0;
-        G1[off] = g1;
-        G2[off] = g2;
-        G3[off] = g3;
+    for (int k = 0; k < PER; ++k) {  // all loads in flight before the first store
+      const int q = tid + k * kDetThreads;
+      if (q < N) {
+        const int lv = q / (kGH * kGW), r = (q / kGW) % kGH, cc = q % kGW;
+        const int y = min(ty0 - 2 + r, h - 1), x = min(tx0 - 2 + cc, w - 1);
+        v[k] = __ldg(pyr + bt.plane_off[o][lv] + (long long)y * w + x);
       }
     }
-    __syncthreads();
-
-    // 4. Laplacian (image.cpp:220-238) times sigma^2 (scale_space.cpp:150),
-    //    then alpha = beta * L (scale_space.cpp:165-170), row yl = y - 1.
-    const int yl = y - 1;
-    if (yl >= 1 && yl <= h - 2 && lap_col) {
-      const double* up = Gs + ((yl - 1) % 3) * 4 * T + t;
-      const double* mid = Gs + (yl % 3) * 4 * T + t;
-      const double* dn = Gs + ((yl + 1) % 3) * 4 * T + t;
-      double L[4];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const double lap = up[k * T] + dn[k * T] + mid[k * T - 1] + mid[k * T + 1] - 4.0 * mid[k * T];
-        L[k] = dc.s2[k] * lap;
-      }
-      double* as = As + (yl % 3) * 4 * T + t;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        double s = dc.beta[i][0] * L[0];
-        s = s + dc.beta[i][1] * L[1];
-        s = s + dc.beta[i][2] * L[2];
-        s = s + dc.beta[i][3] * L[3];
-        as[i * T] = s;
-      }
+    for (int k = 0; k < PER; ++k) {
+      const int q = tid + k * kDetThreads;
+      if (q < N) Gt[q] = v[k];
     }
-    __syncthreads();
-
-    // 5. extrema (scale_space.cpp:172-205) + refinement (:221-266), row yd.
-    const int yd = y - 2;
-    if (det_col && yd >= m && yd < h - m) {
-      const double* arow[3] = {As + ((yd - 1) % 3) * 4 * T, As + (yd % 3) * 4 * T, As + ((yd + 1) % 3) * 4 * T};
-      double a[4];
+  }
+  __syncthreads();
+  // Laplacian x sigma^2 then alpha, for the tile + 1 halo (scale_space.cpp:148-170);
+  // a fixed, unrolled set of positions per thread so loads and the four
+  // independent alpha sums of several positions overlap.
+  {
+    constexpr int N = kAH * kAW, PER = (N + kDetThreads - 1) / kDetThreads;
 #pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = arow[1][i * T + t];
-      double roots[2];
-      const int nr = derivative_roots(a, roots);
-      for (int ri = 0; ri < nr; ++ri) {
-        const double s = roots[ri];
-        if (s < dc.s_lo || s > dc.s_hi) continue;
-        const double p = poly_at(a, s);
-        if (fabs(p) < dc.thr) continue;
-        double p3[3][3];
-        bool ext = true;
+    for (int k = 0; k < PER; ++k) {
+      const int q = tid + k * kDetThreads;
+      if (q < N) {
+        const int r = q / kAW, cc = q - r * kAW;
+        double L[4];
 #pragma unroll
-        for (int dy = -1; dy <= 1; ++dy)
+        for (int lv = 0; lv < 4; ++lv) {
+          const double* g = Gt + (lv * kGH + r + 1) * kGW + cc + 1;
+          const double lap = g[-kGW] + g[kGW] + g[-1] + g[1] - 4.0 * g[0];
+          L[lv] = dc.s2[lv] * lap;
+        }
 #pragma unroll
-          for (int dx = -1; dx <= 1; ++dx) {
-            double an[4];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) an[i] = arow[dy + 1][i * T + t + dx];
-            const double pn = (dx == 0 && dy == 0) ? p : poly_at(an, s);
-            p3[dy + 1][dx + 1] = pn;
-            if (!(dx == 0 && dy == 0) && (p > 0.0 ? (p <= pn) : (p >= pn))) ext = false;
-          }
-        if (!ext) continue;
-        // refine_candidates (scale_space.cpp:221-266)
-        const double gx = 0.5 * (p3[1][2] - p3[1][0]);
-        const double gy = 0.5 * (p3[2][1] - p3[0][1]);
-        const double hxx = p3[1][2] + p3[1][0] - 2.0 * p3[1][1];
-        const double hyy = p3[2][1] + p3[0][1] - 2.0 * p3[1][1];
-        const double hxy = 0.25 * (p3[2][2] - p3[2][0] - p3[0][2] + p3[0][0]);
-        const double det = hxx * hyy - hxy * hxy;
-        if (det <= 0.0) continue;
-        const double rho = (hxx + hyy) * (hxx + hyy) / det;
-        if (rho > dc.rho_limit) continue;
-        const double ox = -(hyy * gx - hxy * gy) / det;
-        const double oy = (hxy * gx - hxx * gy) / det;
-        if (fabs(ox) > 0.6 || fabs(oy) > 0.6) continue;
-        KP k;
-        k.x = (cx + ox) * oct_scale;
-        k.y = (yd + oy) * oct_scale;
-        k.sigma = s * oct_scale;
-        k.p = p;
-        k.rho = rho;
-        k.pss = 2.0 * a[2] + 6.0 * a[3] * s;
-        k.d = 0.0;
-        k.octave = o;
-        const int slot = (nr == 2 && s > roots[1 - ri]) ? 1 : 0;  // sigma order within the pixel
-        k.key = (uint32_t(yd) * uint32_t(w) + uint32_t(cx)) * 2u + uint32_t(slot);
-        const int idx = atomicAdd(&bt.raw_count[f * bt.n_oct + o], 1);
-        if (idx < bt.cap_oct) {
-          bt.raw[((long long)f * bt.n_oct + o) * bt.cap_oct + idx] = k;
-          atomicOr(&bt.bitmap[f * bt.bitmap_words + bt.bm_off[o] + (k.key >> 5)], 1u << (k.key & 31u));
-        } else {
-          atomicOr(&bt.status[f], 4);
+        for (int i = 0; i < 4; ++i) {
+          double sum = dc.beta[i][0] * L[0];
+          sum = sum + dc.beta[i][1] * L[1];
+          sum = sum + dc.beta[i][2] * L[2];
+          sum = sum + dc.beta[i][3] * L[3];
+          At[(r * 4 + i) * kAW + cc] = sum;
         }
       }
     }
-    // The next iteration's stage writes brow only; Gs/As rows it overwrites
-    // were last read before this iteration's second barrier.
+  }
+  __syncthreads();
+  for (int q = tid; q < kDetW * kDetH; q += kDetThreads) {
+    const int r = q / kDetW, cc = q % kDetW;
+    const int yd = ty0 + r, xd = tx0 + cc;
+    if (yd < h - m && xd < w - m) {
+      const double* a = At + ((r + 1) * 4) * kAW + cc + 1;
+      const double av[4] = {a[0], a[kAW], a[2 * kAW], a[3 * kAW]};
+      if (screen_pixel(av, dc)) queue[atomicAdd(&q_count, 1)] = uint16_t(q);
+    }
+  }
+  __syncthreads();
+  const int nq = q_count;
+  const double oct_scale = ldexp(1.0, o);
+  for (int qi = tid; qi < nq; qi += kDetThreads) {
+    const int q = queue[qi];
+    const int r = q / kDetW, cc = q % kDetW;
+    exact_detect(bt, dc, f, o, w, ty0 + r, tx0 + cc, At + (r * 4) * kAW, At + ((r + 1) * 4) * kAW,
+                 At + ((r + 2) * 4) * kAW, kAW, cc + 1, oct_scale);
   }
 }
 
-// Launch helper: picks strips so a CTA holds <= 256 threads.
-struct OctaveLaunch { int strips, S, T; size_t smem; };
-
-inline OctaveLaunch plan_octave(int w, int rm) {
-  OctaveLaunch L;
-  L.strips = (w + 251) / 252;
-  L.S = (w + L.strips - 1) / L.strips;
-  L.T = ((L.S + 4 + 31) / 32) * 32;
-  L.smem = sizeof(double) * size_t(L.S + 4 + 2 * rm + 24 * L.T);
-  return L;
-}
+constexpr size_t kDetSmem = sizeof(double) * (4 * kGH * kGW + kAH * 4 * kAW);
 
 template <int R0, int R1, int R2, int R3>
 cudaError_t launch_octave_variant(const Batch& bt, const DetConst& dc, int o, int src, cudaStream_t st) {
-  const OctaveLaunch L = plan_octave(bt.ow[o], R3);
-  dim3 grid(L.strips, bt.nframes);
-  cudaError_t e = cudaSuccess;
-  if (src == 0) {
-    e = cudaFuncSetAttribute(k_octave<R0, R1, R2, R3, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(L.smem));
-    k_octave<R0, R1, R2, R3, 0><<<grid, L.T, L.smem, st>>>(bt, dc, o, L.S);
-  } else if (src == 1) {
-    e = cudaFuncSetAttribute(k_octave<R0, R1, R2, R3, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(L.smem));
-    k_octave<R0, R1, R2, R3, 1><<<grid, L.T, L.smem, st>>>(bt, dc, o, L.S);
-  } else {
-    e = cudaFuncSetAttribute(k_octave<R0, R1, R2, R3, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(L.smem));
-    k_octave<R0, R1, R2, R3, 2><<<grid, L.T, L.smem, st>>>(bt, dc, o, L.S);
+  dim3 grid((bt.ow[o] + kBlurCols - 1) / kBlurCols, 4, bt.nframes);
+  if (src == 0) k_blur<R0, R1, R2, R3, 0><<<grid, kBlurCols, 0, st>>>(bt, dc, o);
+  else if (src == 1) k_blur<R0, R1, R2, R3, 1><<<grid, kBlurCols, 0, st>>>(bt, dc, o);
+  else k_blur<R0, R1, R2, R3, 2><<<grid, kBlurCols, 0, st>>>(bt, dc, o);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_detect(const Batch& bt, const DetConst& dc, int o, cudaStream_t st) {
+  const int ww = bt.ow[o] - 2 * dc.margin, hh = bt.oh[o] - 2 * dc.margin;
+  if (ww <= 0 || hh <= 0) return cudaSuccess;  // detect_extrema: empty window (scale_space.cpp:159)
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(k_detect, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kDetSmem));
+    if (e != cudaSuccess) return e;
+    configured = true;
   }
-  if (e != cudaSuccess) return e;
+  dim3 grid((ww + kDetW - 1) / kDetW, (hh + kDetH - 1) / kDetH, bt.nframes);
+  k_detect<<<grid, kDetThreads, kDetSmem, st>>>(bt, dc, o);
   return cudaGetLastError();
 }
 
