@@ -115,8 +115,10 @@ int cdvz_gpu_kernel_stats(cdvz_gpu_ctx* ctx, int* launches, double* pyramid_ms, 
  * *n receives the element count; nothing is copied when cap is too small. */
 int cdvz_gpu_debug_get(cdvz_gpu_ctx* ctx, const char* name, int frame, double* dst, size_t cap, size_t* n);
 
-/* Keeps per-octave survivor lists of the next batch for cdvz_gpu_debug_get
- * ("refined:<o>"); costs one device copy per octave. */
+/* Debug flags. Bit 0 keeps per-octave survivor lists of the next batch for
+ * cdvz_gpu_debug_get ("refined:<o>"; one device copy per octave). Bit 1 turns
+ * off the FP32 pre-screen of the extrema kernel so every pixel takes the
+ * exact FP64 test (used to prove the screen never drops a candidate). */
 int cdvz_gpu_set_debug(cdvz_gpu_ctx* ctx, int on);
 
 /* CUDA events on the context's stream (slots 0..3), for callers timing the

@@ -34,6 +34,7 @@ struct DetConst {
   double beta[4][4];
   double thr, rho_limit, s_lo, s_hi;
   int margin;
+  int screen;          // 1: FP32 pre-screen before the exact test; 0: exact test on every pixel
 };
 
 // Per-batch geometry and buffer map (device pointers). One instance lives in

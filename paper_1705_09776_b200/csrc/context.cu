@@ -154,6 +154,7 @@ struct cdvz_gpu_ctx {
     dc.s_lo = b.sigmas[0];
     dc.s_hi = b.sigmas[3];
     dc.margin = b.margin;
+    dc.screen = 1;
 
     for (int c = 0; c < 5; ++c) {
       md.rel_edges[c] = upload(b.relevance[std::size_t(c)].edges.data(), b.relevance[std::size_t(c)].edges.size());
@@ -471,7 +472,8 @@ size_t cdvz_gpu_container_slot(int mode_id) {
 
 int cdvz_gpu_set_debug(cdvz_gpu_ctx* ctx, int on) {
   if (!ctx) return CDVZ_GPU_USAGE;
-  ctx->debug = on != 0;
+  ctx->debug = (on & 1) != 0;
+  ctx->dc.screen = (on & 2) ? 0 : 1;
   ctx->geo_w = ctx->geo_h = 0;  // force a re-plan with the debug buffers
   return CDVZ_GPU_OK;
 }

@@ -366,7 +366,7 @@ __global__ void __launch_bounds__(kDetThreads, 2) k_detect(Batch bt, DetConst dc
     if (yd < h - m && xd < w - m) {
       const double* a = At + ((r + 1) * 4) * kAW + cc + 1;
       const double av[4] = {a[0], a[kAW], a[2 * kAW], a[3 * kAW]};
-      if (screen_pixel(av, dc)) queue[atomicAdd(&q_count, 1)] = uint16_t(q);
+      if (!dc.screen || screen_pixel(av, dc)) queue[atomicAdd(&q_count, 1)] = uint16_t(q);
     }
   }
   __syncthreads();

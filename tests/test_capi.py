@@ -64,3 +64,21 @@ def test_container_slot_from_the_library():
     lib.cdvz_gpu_container_slot.restype = ctypes.c_size_t
     assert [lib.cdvz_gpu_container_slot(i) for i in range(6)] == [540, 1052, 2076, 4124, 8220, 16412]
     assert lib.cdvz_gpu_container_slot(7) == 0
+
+
+def test_cpp_shim_compiles_and_validates_bundles(tmp_path):
+    """The reference-shaped C++ API over the ABI builds and links against the
+    library; bundle validation works host-side (no GPU)."""
+    import subprocess
+
+    exe = tmp_path / "extract"
+    lib_dir = os.path.dirname(cg.library_path())
+    subprocess.run(["g++", "-std=c++17", "-O1", os.path.join(ROOT, "examples", "extract.cpp"), f"-L{lib_dir}",
+                    "-lcdvz_gpu", f"-Wl,-rpath,{lib_dir}", "-o", str(exe)], check=True)
+    bad = tmp_path / "bad.txt"
+    bad.write_text("CDVZ-MODEL 2\nend\n")
+    p = subprocess.run([str(exe), str(bad), "4K", "x.pgm", "y.cdvz"], capture_output=True, text=True)
+    assert p.returncode == 2 and "version" in p.stderr
+    good = os.path.join(ROOT, "tests", "golden", "bundle_b8.txt")
+    p = subprocess.run([str(exe), good, "3K", "x.pgm", "y.cdvz"], capture_output=True, text=True)
+    assert p.returncode == 1 and "unknown mode" in p.stderr
