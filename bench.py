@@ -164,7 +164,7 @@ def run_reference(args, rank, world):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--batch", type=int, default=BATCH)
@@ -283,10 +283,11 @@ def main():
         "gpu_launches": launches,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": achieved / hbm if hbm else None, "traffic": traffic,
-                     "kernel": "k_octave (fused Gaussian pyramid + LoG + ALP extrema + refinement)",
+                     "kernel": "octave pair k_blur (Gaussian scale space) + k_detect (LoG + ALP extrema + refinement)",
                      "peak_source": peak_kind,
-                     "algorithmic_bytes": "per octave and frame: w*h*(b_in + 4*8); b_in = 1 (u8) at octave 0, "
-                                          "8 (f64 G3) above"},
+                     "algorithmic_bytes": "per octave and frame: w*h*(b_in + 4*8) written by k_blur (b_in = 1 B u8 "
+                                          "at octave 0, 8 B f64 G3 above) + 4*8 B per detection-window pixel read "
+                                          "back by k_detect; VGA = 26.0 MB/frame (DESIGN.md 2.2)"},
         "stage_ms_per_step": {k: v for k, v in stage.items()},
         "frames_ok": ok_frames,
         "clocks": clk.summary(),
