@@ -118,7 +118,9 @@ int cdvz_gpu_debug_get(cdvz_gpu_ctx* ctx, const char* name, int frame, double* d
 /* Debug flags. Bit 0 keeps per-octave survivor lists of the next batch for
  * cdvz_gpu_debug_get ("refined:<o>"; one device copy per octave). Bit 1 turns
  * off the FP32 pre-screen of the extrema kernel so every pixel takes the
- * exact FP64 test (used to prove the screen never drops a candidate). */
+ * exact FP64 test (used to prove the screen never drops a candidate). Bit 2
+ * runs a batch's kernels on one stream, unoverlapped, so per-kernel event
+ * times are standalone (bench.py's roofline measurement). */
 int cdvz_gpu_set_debug(cdvz_gpu_ctx* ctx, int on);
 
 /* CUDA events on the context's stream (slots 0..3), for callers timing the

@@ -269,9 +269,11 @@ class Extractor:
         self._check(self._lib.cdvz_gpu_kernel_stats(self._ctx, ctypes.byref(n), ctypes.byref(ms), ctypes.byref(by)))
         return {"launches": n.value, "pyramid_ms": ms.value, "pyramid_bytes": by.value}
 
-    def set_debug(self, on: bool = True, exact_only: bool = False) -> None:
-        """on: keep per-octave lists; exact_only: bypass the FP32 extrema screen."""
-        self._check(self._lib.cdvz_gpu_set_debug(self._ctx, (1 if on else 0) | (2 if exact_only else 0)))
+    def set_debug(self, on: bool = True, exact_only: bool = False, serial: bool = False) -> None:
+        """on: keep per-octave lists; exact_only: bypass the FP32 extrema screen;
+        serial: no kernel overlap (standalone per-kernel timing)."""
+        flags = (1 if on else 0) | (2 if exact_only else 0) | (4 if serial else 0)
+        self._check(self._lib.cdvz_gpu_set_debug(self._ctx, flags))
 
     def debug_get(self, name: str, frame: int) -> np.ndarray:
         n = ctypes.c_size_t()

@@ -83,6 +83,51 @@ void prepared_dims(int w, int h, int limit, int& pw, int& ph) {
 
 }  // namespace
 
+// One in-flight batch: its device buffers, two streams (A: the Gaussian
+// blurs, which chain octave to octave; B: extrema, merge, selection,
+// description, SCFV, pack) and the events that order and time them. Two
+// lanes alternate over a call's chunks, so chunk c's description/SCFV runs
+// beside chunk c+1's pyramid.
+struct Lane {
+  Batch bt{};
+  std::vector<DeviceBuffer> bufs;
+  DeviceBuffer dbg_oct;
+  int geo_w = 0, geo_h = 0, geo_frames = 0;
+  bool geo_resize = false, geo_debug = false;
+  cudaStream_t sA = nullptr, sB = nullptr;
+  cudaEvent_t start = nullptr, done = nullptr;
+  cudaEvent_t stage[6] = {};
+  cudaEvent_t blur[2 * kMaxOctaves] = {}, det[2 * kMaxOctaves] = {};
+  bool pending = false;   // events of an enqueued chunk not yet folded into the stats
+  int pending_oct = 0;
+  double pending_bytes = 0.0;
+
+  void init() {
+    CDVZ_CUDA_CHECK(cudaStreamCreateWithFlags(&sA, cudaStreamNonBlocking));
+    CDVZ_CUDA_CHECK(cudaStreamCreateWithFlags(&sB, cudaStreamNonBlocking));
+    CDVZ_CUDA_CHECK(cudaEventCreate(&start));
+    CDVZ_CUDA_CHECK(cudaEventCreate(&done));
+    for (auto& e : stage) CDVZ_CUDA_CHECK(cudaEventCreate(&e));
+    for (auto& e : blur) CDVZ_CUDA_CHECK(cudaEventCreate(&e));
+    for (auto& e : det) CDVZ_CUDA_CHECK(cudaEventCreate(&e));
+  }
+  void release() {
+    for (auto& b : bufs) b.release();
+    bufs.clear();
+    dbg_oct.release();
+    geo_w = geo_h = geo_frames = 0;
+  }
+  void destroy() {
+    release();
+    for (auto* e : {&start, &done}) if (*e) cudaEventDestroy(*e);
+    for (auto& e : stage) if (e) cudaEventDestroy(e);
+    for (auto& e : blur) if (e) cudaEventDestroy(e);
+    for (auto& e : det) if (e) cudaEventDestroy(e);
+    if (sA) cudaStreamDestroy(sA);
+    if (sB) cudaStreamDestroy(sB);
+  }
+};
+
 struct cdvz_gpu_ctx {
   int device = 0;
   int max_batch = 256;
@@ -93,12 +138,11 @@ struct cdvz_gpu_ctx {
   Model md{};
   std::vector<DeviceBuffer> model_bufs;
   bool debug = false;
+  bool serial = false;
 
-  // Batch geometry the buffers are sized for.
-  int geo_w = 0, geo_h = 0, geo_frames = 0;
-  Batch bt{};
-  std::vector<DeviceBuffer> batch_bufs;
-  DeviceBuffer stage_in, stage_out, stage_len, dbg_oct;
+  Lane lanes[2];
+  int last_lane = 0;
+  DeviceBuffer stage_in, stage_out, stage_len;
   std::vector<uint8_t> host_out;
   std::vector<uint32_t> host_len;
   int last_frames = 0, last_mode = -1;
@@ -112,11 +156,10 @@ struct cdvz_gpu_ctx {
 
   ~cdvz_gpu_ctx() {
     for (auto& b : model_bufs) b.release();
-    for (auto& b : batch_bufs) b.release();
+    for (auto& l : lanes) l.destroy();
     stage_in.release();
     stage_out.release();
     stage_len.release();
-    dbg_oct.release();
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
     for (auto& e : evp)
@@ -197,10 +240,12 @@ struct cdvz_gpu_ctx {
   }
 
   // Sizes every per-batch buffer for `frames` frames of prepared size W x H.
-  void plan(int W, int H, int frames, bool need_resize) {
-    if (W == geo_w && H == geo_h && frames <= geo_frames && (!need_resize || bt.pixf)) return;
-    for (auto& b : batch_bufs) b.release();
-    batch_bufs.clear();
+  void plan(Lane& L, int W, int H, int frames, bool need_resize) {
+    if (W == L.geo_w && H == L.geo_h && frames <= L.geo_frames && (!need_resize || L.geo_resize) && L.geo_debug == debug)
+      return;
+    CDVZ_CUDA_CHECK(cudaStreamSynchronize(L.sA));
+    CDVZ_CUDA_CHECK(cudaStreamSynchronize(L.sB));
+    L.release();
     Batch nb{};
     nb.W = W;
     nb.H = H;
@@ -228,9 +273,9 @@ struct cdvz_gpu_ctx {
     nb.nc = bundle.nc;
     const long long F = frames;
     auto alloc = [&](size_t bytes) {
-      batch_bufs.emplace_back();
-      batch_bufs.back().ensure(std::max<size_t>(bytes, 16));
-      return batch_bufs.back().p;
+      L.bufs.emplace_back();
+      L.bufs.back().ensure(std::max<size_t>(bytes, 16));
+      return L.bufs.back().p;
     };
     nb.pyr = static_cast<double*>(alloc(sizeof(double) * F * nb.frame_doubles));
     nb.pixf = need_resize ? static_cast<double*>(alloc(sizeof(double) * F * W * H)) : nullptr;
@@ -261,14 +306,16 @@ struct cdvz_gpu_ctx {
     nb.mask = static_cast<uint8_t*>(alloc(F * ((nb.nc + 7) / 8)));
     nb.mean_planes = static_cast<uint32_t*>(alloc(sizeof(uint32_t) * F * nb.nc));
     nb.var_planes = static_cast<uint32_t*>(alloc(sizeof(uint32_t) * F * nb.nc));
-    CDVZ_CUDA_CHECK(cudaMemsetAsync(nb.raw_count, 0, sizeof(int) * F * std::max(1, n_oct), st));
-    CDVZ_CUDA_CHECK(cudaMemsetAsync(nb.bitmap, 0, sizeof(uint32_t) * F * nb.bitmap_words, st));
-    CDVZ_CUDA_CHECK(cudaMemsetAsync(nb.acc_count, 0, sizeof(int) * F * 2, st));
-    if (debug) dbg_oct.ensure(sizeof(KP) * F * std::max(1, n_oct) * nb.cap_acc);
-    bt = nb;
-    geo_w = W;
-    geo_h = H;
-    geo_frames = frames;
+    CDVZ_CUDA_CHECK(cudaMemset(nb.raw_count, 0, sizeof(int) * F * std::max(1, n_oct)));
+    CDVZ_CUDA_CHECK(cudaMemset(nb.bitmap, 0, sizeof(uint32_t) * F * nb.bitmap_words));
+    CDVZ_CUDA_CHECK(cudaMemset(nb.acc_count, 0, sizeof(int) * F * 2));
+    if (debug) L.dbg_oct.ensure(sizeof(KP) * F * std::max(1, n_oct) * nb.cap_acc);
+    L.bt = nb;
+    L.geo_w = W;
+    L.geo_h = H;
+    L.geo_frames = frames;
+    L.geo_resize = need_resize;
+    L.geo_debug = debug;
   }
 
   EncodeConst encode_const(int mode_id) const {
@@ -288,8 +335,31 @@ struct cdvz_gpu_ctx {
     return ec;
   }
 
+  // Folds a finished chunk's events into the stage / kernel statistics.
+  void collect(Lane& L) {
+    if (!L.pending) return;
+    CDVZ_CUDA_CHECK(cudaEventSynchronize(L.done));
+    float t[5];
+    cudaEventElapsedTime(&t[0], L.start, L.stage[1]);
+    cudaEventElapsedTime(&t[1], L.stage[1], L.stage[2]);
+    cudaEventElapsedTime(&t[2], L.stage[2], L.stage[3]);
+    cudaEventElapsedTime(&t[3], L.stage[4], L.stage[5]);
+    cudaEventElapsedTime(&t[4], L.stage[3], L.stage[4]);
+    for (int i = 0; i < 5; ++i) stage_ms[i] += t[i];
+    for (int o = 0; o < L.pending_oct; ++o) {
+      float a = 0.f, b = 0.f;
+      cudaEventElapsedTime(&a, L.blur[2 * o], L.blur[2 * o + 1]);
+      cudaEventElapsedTime(&b, L.det[2 * o], L.det[2 * o + 1]);
+      pyr_ms += a + b;  // kernel time of the pair (they may overlap: conservative)
+    }
+    pyr_bytes += L.pending_bytes;
+    L.pending = false;
+  }
+
   // Runs the whole pipeline for `frames` device-resident frames (u8) of size
-  // w x h and writes containers into fixed slots of d_out.
+  // w x h and writes containers into fixed slots of d_out. Ordered after
+  // everything already enqueued on the context stream; the context stream
+  // waits for the result.
   void run(const uint8_t* d_pix, int w, int h, long long stride, int frames, int mode_id, int max_side, uint8_t* d_out,
            uint32_t* d_len) {
     if (w < 8 || h < 8) throw DataError("image smaller than 8 px per side");
@@ -301,70 +371,89 @@ struct cdvz_gpu_ctx {
     ec.cy = (H - 1) / 2.0;
     ec.half_diag = 0.5 * std::hypot(static_cast<double>(W - 1), static_cast<double>(H - 1));
     ec.log2_range = std::log2(64.0 / 0.5);
-    plan(W, H, std::min(frames, max_batch), resize);
+    const int per = std::min(frames, max_batch);
+    const int chunks = (frames + per - 1) / per;
+    const int n_lanes = serial ? 1 : 2;
+    for (int l = 0; l < std::min(chunks, n_lanes); ++l) {
+      if (!lanes[l].sA) lanes[l].init();
+      plan(lanes[l], W, H, per, resize);
+    }
     launches = 0;
     pyr_ms = 0.0;
     pyr_bytes = 0.0;
-    for (double& s : stage_ms) s = 0.0;
-    for (int base = 0; base < frames; base += max_batch) {
-      const int nf = std::min(max_batch, frames - base);
-      Batch b = bt;
+    for (double& x : stage_ms) x = 0.0;
+    CDVZ_CUDA_CHECK(cudaEventRecord(ev[0], st));  // everything before this call
+    for (int c = 0; c < chunks; ++c) {
+      const int base = c * per;
+      const int nf = std::min(per, frames - base);
+      Lane& L = lanes[serial ? 0 : (c & 1)];
+      collect(L);
+      // Serial mode (debug bit 2): one stream per lane, so kernels never
+      // overlap and their event times are standalone (bench roofline).
+      const cudaStream_t sB = serial ? L.sA : L.sB;  // the lane's previous chunk (c - 2) must be done before its buffers are reused
+      Batch b = L.bt;
       b.nframes = nf;
       b.pix8 = d_pix + (long long)base * h * stride;
       b.stride8 = stride;
       b.frame_bytes8 = (long long)h * stride;
-      CDVZ_CUDA_CHECK(cudaMemsetAsync(b.status, 0, sizeof(int) * nf, st));
+      CDVZ_CUDA_CHECK(cudaStreamWaitEvent(L.sA, ev[0], 0));
+      CDVZ_CUDA_CHECK(cudaStreamWaitEvent(sB, ev[0], 0));
+      CDVZ_CUDA_CHECK(cudaEventRecord(L.start, L.sA));
+      CDVZ_CUDA_CHECK(cudaMemsetAsync(b.status, 0, sizeof(int) * nf, L.sA));
       ++launches;
       if (resize) {
-        CDVZ_CUDA_CHECK(launch_resize(b.pix8, stride, b.frame_bytes8, w, h, const_cast<double*>(b.pixf), W, H, nf, st));
+        CDVZ_CUDA_CHECK(launch_resize(b.pix8, stride, b.frame_bytes8, w, h, const_cast<double*>(b.pixf), W, H, nf, L.sA));
         ++launches;
       }
-      CDVZ_CUDA_CHECK(cudaEventRecord(ev[0], st));
+      double bytes = 0.0;
       for (int o = 0; o < b.n_oct; ++o) {
         const int src = o == 0 ? (resize ? 1 : 0) : 2;
-        CDVZ_CUDA_CHECK(cudaEventRecord(evp[2 * o], st));
-        CDVZ_CUDA_CHECK(launch_octave(b, dc, o, src, st));
-        CDVZ_CUDA_CHECK(launch_detect(b, dc, o, st));
-        CDVZ_CUDA_CHECK(cudaEventRecord(evp[2 * o + 1], st));
-        CDVZ_CUDA_CHECK(launch_merge(b, o, st));
+        CDVZ_CUDA_CHECK(cudaEventRecord(L.blur[2 * o], L.sA));
+        CDVZ_CUDA_CHECK(launch_octave(b, dc, o, src, L.sA));
+        CDVZ_CUDA_CHECK(cudaEventRecord(L.blur[2 * o + 1], L.sA));
+        CDVZ_CUDA_CHECK(cudaStreamWaitEvent(sB, L.blur[2 * o + 1], 0));
+        CDVZ_CUDA_CHECK(cudaEventRecord(L.det[2 * o], sB));
+        CDVZ_CUDA_CHECK(launch_detect(b, dc, o, sB));
+        CDVZ_CUDA_CHECK(cudaEventRecord(L.det[2 * o + 1], sB));
+        CDVZ_CUDA_CHECK(launch_merge(b, o, sB));
         launches += 3;
         if (debug) {
           const KP* srcl = (o == 0) ? b.acc[0] : b.cur;
-          CDVZ_CUDA_CHECK(cudaMemcpyAsync(dbg_oct.as<KP>() + (long long)o * bt.cap_acc * geo_frames, srcl,
-                                          sizeof(KP) * (long long)nf * b.cap_acc, cudaMemcpyDeviceToDevice, st));
+          CDVZ_CUDA_CHECK(cudaMemcpyAsync(L.dbg_oct.as<KP>() + (long long)o * b.cap_acc * L.geo_frames, srcl,
+                                          sizeof(KP) * (long long)nf * b.cap_acc, cudaMemcpyDeviceToDevice, sB));
         }
-      }
-      CDVZ_CUDA_CHECK(cudaEventRecord(ev[1], st));
-      CDVZ_CUDA_CHECK(launch_select(b, md, ec, st));
-      CDVZ_CUDA_CHECK(cudaEventRecord(ev[2], st));
-      CDVZ_CUDA_CHECK(launch_describe(b, dc, md, ec, st));
-      CDVZ_CUDA_CHECK(cudaEventRecord(ev[3], st));
-      CDVZ_CUDA_CHECK(launch_scfv_pack(b, md, ec, d_out + (long long)base * ec.slot_bytes, d_len + base, st, ev[4]));
-      CDVZ_CUDA_CHECK(cudaEventRecord(ev[5], st));
-      launches += 1 + 3 + 5;
-      // Stage times per label (sum over chunks). Reading the events waits for the chunk.
-      CDVZ_CUDA_CHECK(cudaEventSynchronize(ev[5]));
-      float t[5];
-      cudaEventElapsedTime(&t[0], ev[0], ev[1]);
-      cudaEventElapsedTime(&t[1], ev[1], ev[2]);
-      cudaEventElapsedTime(&t[2], ev[2], ev[3]);
-      cudaEventElapsedTime(&t[3], ev[4], ev[5]);
-      cudaEventElapsedTime(&t[4], ev[3], ev[4]);
-      for (int i = 0; i < 5; ++i) stage_ms[i] += t[i];
-      for (int o = 0; o < b.n_oct; ++o) {
-        float pm = 0.f;
-        cudaEventElapsedTime(&pm, evp[2 * o], evp[2 * o + 1]);
-        pyr_ms += pm;
         // Algorithmic bytes of the split octave pair: K1a reads
         // the base (1 B/px u8 at octave 0, 8 B/px f64 above) and writes 4 G
         // levels (32 B/px); K1b reads the 4 G levels of its window back.
         const double px = double(b.ow[o]) * b.oh[o];
         const double in_b = (o == 0) ? (resize ? 8.0 : 1.0) : 8.0;
         const int ww = std::max(0, b.ow[o] - 2 * dc.margin), hh = std::max(0, b.oh[o] - 2 * dc.margin);
-        pyr_bytes += double(nf) * (px * (in_b + 32.0) + 32.0 * ww * hh);
+        bytes += double(nf) * (px * (in_b + 32.0) + 32.0 * ww * hh);
       }
+      // Stream B also waits for the last blur (octaves whose window is empty
+      // launch no extrema kernel) before describing from the pyramid.
+      CDVZ_CUDA_CHECK(cudaStreamWaitEvent(sB, b.n_oct ? L.blur[2 * b.n_oct - 1] : L.start, 0));
+      CDVZ_CUDA_CHECK(cudaEventRecord(L.stage[1], sB));
+      CDVZ_CUDA_CHECK(launch_select(b, md, ec, sB));
+      CDVZ_CUDA_CHECK(cudaEventRecord(L.stage[2], sB));
+      CDVZ_CUDA_CHECK(launch_describe(b, dc, md, ec, sB));
+      CDVZ_CUDA_CHECK(cudaEventRecord(L.stage[3], sB));
+      CDVZ_CUDA_CHECK(launch_scfv_pack(b, md, ec, d_out + (long long)base * ec.slot_bytes, d_len + base, sB, L.stage[4]));
+      CDVZ_CUDA_CHECK(cudaEventRecord(L.stage[5], sB));
+      CDVZ_CUDA_CHECK(cudaEventRecord(L.done, sB));
+      // The next chunk on this lane's stream A must not overwrite the pyramid
+      // before stream B is done with it.
+      CDVZ_CUDA_CHECK(cudaStreamWaitEvent(L.sA, L.done, 0));
+      launches += 1 + 3 + 5;
+      L.pending = true;
+      L.pending_oct = b.n_oct;
+      L.pending_bytes = bytes;
+      last_lane = serial ? 0 : (c & 1);
     }
-    last_frames = std::min(frames, max_batch);
+    for (int l = 0; l < 2; ++l)
+      if (lanes[l].pending) CDVZ_CUDA_CHECK(cudaStreamWaitEvent(st, lanes[l].done, 0));
+    for (int l = 0; l < 2; ++l) collect(lanes[l]);
+    last_frames = std::min(per, frames - (chunks - 1) * per);
     last_mode = mode_id;
   }
 };
@@ -474,7 +563,7 @@ int cdvz_gpu_set_debug(cdvz_gpu_ctx* ctx, int on) {
   if (!ctx) return CDVZ_GPU_USAGE;
   ctx->debug = (on & 1) != 0;
   ctx->dc.screen = (on & 2) ? 0 : 1;
-  ctx->geo_w = ctx->geo_h = 0;  // force a re-plan with the debug buffers
+  ctx->serial = (on & 4) != 0;
   return CDVZ_GPU_OK;
 }
 
@@ -576,7 +665,8 @@ int cdvz_gpu_debug_get(cdvz_gpu_ctx* ctx, const char* name, int frame, double* d
     if (frame < 0 || frame >= ctx->last_frames) throw UsageError("frame index outside the last batch");
     CDVZ_CUDA_CHECK(cudaSetDevice(ctx->device));
     CDVZ_CUDA_CHECK(cudaStreamSynchronize(ctx->st));
-    const Batch& b = ctx->bt;
+    const Lane& lane = ctx->lanes[ctx->last_lane];
+    const Batch& b = lane.bt;
     const std::string s(name);
     std::vector<double> v;
     auto get_int = [&](const int* p) {
@@ -602,7 +692,7 @@ int cdvz_gpu_debug_get(cdvz_gpu_ctx* ctx, const char* name, int frame, double* d
       if (!ctx->debug) throw UsageError("per-octave lists need cdvz_gpu_set_debug(ctx, 1) before the batch");
       const int o = std::stoi(s.substr(8));
       if (o < b.n_oct) {
-        const KP* base = ctx->dbg_oct.as<KP>() + (long long)o * b.cap_acc * ctx->geo_frames + (long long)frame * b.cap_acc;
+        const KP* base = lane.dbg_oct.as<KP>() + (long long)o * b.cap_acc * lane.geo_frames + (long long)frame * b.cap_acc;
         for (const KP& k : get_kps(base, get_int(b.oct_count + frame * b.n_oct + o))) put_kp(k);
       }
     } else if (s == "keypoints") {

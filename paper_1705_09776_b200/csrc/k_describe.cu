@@ -225,15 +225,15 @@ __global__ void __launch_bounds__(1024) k_expand(Batch bt) {
 // cv0 likewise in j), so the samples feeding cell c form a rectangle in index
 // space; the thread walks it in row-major order, which is exactly the order
 // the reference adds them, and each sample adds to exactly one of its bins.
-constexpr int kMaxSamples = 33;  // samples per axis (ceil(12 sigma) for sigma <= 2.75)
+constexpr int kMaxSamples = 32;  // samples per axis: ceil(12 sigma) for sigma <= 2.66 (radius-8 detector)
 
-__global__ void __launch_bounds__(128) k_describe(Batch bt, DetConst dc, Model md, EncodeConst ec) {
+__global__ void __launch_bounds__(128, 5) k_describe(Batch bt, DetConst dc, Model md, EncodeConst ec) {
   __shared__ double s_w[kMaxSamples * kMaxSamples];       // weight; +0 for a skipped sample
   __shared__ double s_wo[2][kMaxSamples * kMaxSamples];   // wo for the bin of parity 0 / 1
   __shared__ uint8_t s_slot[kMaxSamples * kMaxSamples];   // bin >> 1 for parity 0 (bits 0-1) / 1 (bits 2-3)
   __shared__ double s_wu[2][kMaxSamples], s_wv[2][kMaxSamples];  // [du][i]: 1 - fu, fu
   __shared__ int s_cu[kMaxSamples], s_cv[kMaxSamples];
-  __shared__ double part[16][128];
+  __shared__ double part[4][128];  // <= 2x2 sub-patches of 16x16 samples
   __shared__ double sq[128], red[4], tv[128], vec[128];
   __shared__ uint8_t sym[128];
   const int tid = threadIdx.x;
@@ -328,6 +328,7 @@ __global__ void __launch_bounds__(128) k_describe(Batch bt, DetConst dc, Model m
         for (int j = ja; j < jb; ++j) {
           const double wv = s_wv[cy - s_cv[j]][j];
           const int row = j * samples;
+#pragma unroll 4
           for (int i = ia; i < ib; ++i) {
             const int q = row + i;
             // A skipped sample has weight +0: the add leaves the (non-negative) sum unchanged.
