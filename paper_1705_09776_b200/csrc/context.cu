@@ -143,8 +143,24 @@ struct cdvz_gpu_ctx {
   Lane lanes[2];
   int last_lane = 0;
   DeviceBuffer stage_in, stage_out, stage_len;
-  std::vector<uint8_t> host_out;
-  std::vector<uint32_t> host_len;
+  uint8_t* pin_out = nullptr;    // pinned container slots (D2H target)
+  uint32_t* pin_len = nullptr;
+  size_t pin_out_bytes = 0, pin_len_count = 0;
+
+  void ensure_pinned_out(size_t bytes, size_t count) {
+    if (bytes > pin_out_bytes) {
+      if (pin_out) cudaFreeHost(pin_out);
+      pin_out = nullptr;
+      CDVZ_CUDA_CHECK(cudaMallocHost(&pin_out, bytes));
+      pin_out_bytes = bytes;
+    }
+    if (count > pin_len_count) {
+      if (pin_len) cudaFreeHost(pin_len);
+      pin_len = nullptr;
+      CDVZ_CUDA_CHECK(cudaMallocHost(&pin_len, count * sizeof(uint32_t)));
+      pin_len_count = count;
+    }
+  }
   int last_frames = 0, last_mode = -1;
 
   cudaEvent_t ev[6] = {};
@@ -160,6 +176,8 @@ struct cdvz_gpu_ctx {
     stage_in.release();
     stage_out.release();
     stage_len.release();
+    if (pin_out) cudaFreeHost(pin_out);
+    if (pin_len) cudaFreeHost(pin_len);
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
     for (auto& e : evp)
@@ -360,8 +378,12 @@ struct cdvz_gpu_ctx {
   // w x h and writes containers into fixed slots of d_out. Ordered after
   // everything already enqueued on the context stream; the context stream
   // waits for the result.
+  // With host pointers (h_pix / h_out / h_len), each chunk's frames are copied
+  // in on its blur stream and its containers copied out on its describe
+  // stream, so the copies of one chunk overlap the kernels of the other lane.
   void run(const uint8_t* d_pix, int w, int h, long long stride, int frames, int mode_id, int max_side, uint8_t* d_out,
-           uint32_t* d_len) {
+           uint32_t* d_len, const uint8_t* h_pix = nullptr, size_t h_stride = 0, uint8_t* h_out = nullptr,
+           uint32_t* h_len = nullptr) {
     if (w < 8 || h < 8) throw DataError("image smaller than 8 px per side");
     int W, H;
     prepared_dims(w, h, max_side, W, H);
@@ -398,6 +420,9 @@ struct cdvz_gpu_ctx {
       b.frame_bytes8 = (long long)h * stride;
       CDVZ_CUDA_CHECK(cudaStreamWaitEvent(L.sA, ev[0], 0));
       CDVZ_CUDA_CHECK(cudaStreamWaitEvent(sB, ev[0], 0));
+      if (h_pix)
+        CDVZ_CUDA_CHECK(cudaMemcpy2DAsync(const_cast<uint8_t*>(b.pix8), size_t(stride), h_pix + size_t(base) * h * h_stride,
+                                          h_stride, size_t(w), size_t(h) * nf, cudaMemcpyHostToDevice, L.sA));
       CDVZ_CUDA_CHECK(cudaEventRecord(L.start, L.sA));
       CDVZ_CUDA_CHECK(cudaMemsetAsync(b.status, 0, sizeof(int) * nf, L.sA));
       ++launches;
@@ -440,6 +465,11 @@ struct cdvz_gpu_ctx {
       CDVZ_CUDA_CHECK(cudaEventRecord(L.stage[3], sB));
       CDVZ_CUDA_CHECK(launch_scfv_pack(b, md, ec, d_out + (long long)base * ec.slot_bytes, d_len + base, sB, L.stage[4]));
       CDVZ_CUDA_CHECK(cudaEventRecord(L.stage[5], sB));
+      if (h_out) {
+        CDVZ_CUDA_CHECK(cudaMemcpyAsync(h_out + size_t(base) * ec.slot_bytes, d_out + size_t(base) * ec.slot_bytes,
+                                        size_t(nf) * ec.slot_bytes, cudaMemcpyDeviceToHost, sB));
+        CDVZ_CUDA_CHECK(cudaMemcpyAsync(h_len + base, d_len + base, sizeof(uint32_t) * nf, cudaMemcpyDeviceToHost, sB));
+      }
       CDVZ_CUDA_CHECK(cudaEventRecord(L.done, sB));
       // The next chunk on this lane's stream A must not overwrite the pyramid
       // before stream B is done with it.
@@ -599,39 +629,35 @@ int cdvz_gpu_encode_batch(cdvz_gpu_ctx* ctx, const uint8_t* pixels, int width, i
       throw DataError("image smaller than 8 px per side");
     }
     CDVZ_CUDA_CHECK(cudaSetDevice(ctx->device));
-    const int chunk = ctx->max_batch;
     const size_t frame_bytes = size_t(width) * height;
-    ctx->stage_in.ensure(frame_bytes * std::min(count, chunk));
-    ctx->stage_out.ensure(slot * std::min(count, chunk));
-    ctx->stage_len.ensure(sizeof(uint32_t) * std::min(count, chunk));
-    ctx->host_out.resize(slot * std::min(count, chunk));
-    ctx->host_len.resize(std::min(count, chunk));
+    // Frames per call to run(): bounded so the device staging stays < 4 GB.
+    const int group = int(std::max<size_t>(1, std::min<size_t>(size_t(count), (size_t(4) << 30) / frame_bytes)));
+    ctx->stage_in.ensure(frame_bytes * group);
+    ctx->stage_out.ensure(slot * group);
+    ctx->stage_len.ensure(sizeof(uint32_t) * group);
+    ctx->ensure_pinned_out(slot * group, group);
     size_t written = 0;
     double acc_ms[5] = {0, 0, 0, 0, 0};
     double acc_pyr_ms = 0, acc_pyr_bytes = 0;
     int acc_launches = 0;
-    for (int base = 0; base < count; base += chunk) {
-      const int nf = std::min(chunk, count - base);
-      CDVZ_CUDA_CHECK(cudaMemcpy2DAsync(ctx->stage_in.p, width, pixels + size_t(base) * height * stride, stride, width,
-                                        size_t(height) * nf, cudaMemcpyHostToDevice, ctx->st));
+    for (int base = 0; base < count; base += group) {
+      const int nf = std::min(group, count - base);
       ctx->run(ctx->stage_in.as<uint8_t>(), width, height, width, nf, mode_id, max_side, ctx->stage_out.as<uint8_t>(),
-               ctx->stage_len.as<uint32_t>());
+               ctx->stage_len.as<uint32_t>(), pixels + size_t(base) * height * stride, stride, ctx->pin_out, ctx->pin_len);
+      CDVZ_CUDA_CHECK(cudaStreamSynchronize(ctx->st));
       for (int i = 0; i < 5; ++i) acc_ms[i] += ctx->stage_ms[i];
       acc_pyr_ms += ctx->pyr_ms;
       acc_pyr_bytes += ctx->pyr_bytes;
       acc_launches += ctx->launches;
-      CDVZ_CUDA_CHECK(cudaMemcpyAsync(ctx->host_len.data(), ctx->stage_len.p, sizeof(uint32_t) * nf, cudaMemcpyDeviceToHost, ctx->st));
-      CDVZ_CUDA_CHECK(cudaMemcpyAsync(ctx->host_out.data(), ctx->stage_out.p, slot * nf, cudaMemcpyDeviceToHost, ctx->st));
-      CDVZ_CUDA_CHECK(cudaStreamSynchronize(ctx->st));
       for (int i = 0; i < nf; ++i) {
-        const size_t len = ctx->host_len[size_t(i)];
+        const size_t len = ctx->pin_len[size_t(i)];
         const int fi = base + i;
         if (len == 0) {
           status[fi] = CDVZ_GPU_INTERNAL;
         } else if (written + len > out_cap) {
           status[fi] = CDVZ_GPU_USAGE;
         } else {
-          std::memcpy(out + written, ctx->host_out.data() + size_t(i) * slot, len);
+          std::memcpy(out + written, ctx->pin_out + size_t(i) * slot, len);
           written += len;
           status[fi] = CDVZ_GPU_OK;
         }
