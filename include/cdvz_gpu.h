@@ -120,7 +120,8 @@ int cdvz_gpu_debug_get(cdvz_gpu_ctx* ctx, const char* name, int frame, double* d
  * off the FP32 pre-screen of the extrema kernel so every pixel takes the
  * exact FP64 test (used to prove the screen never drops a candidate). Bit 2
  * runs a batch's kernels on one stream, unoverlapped, so per-kernel event
- * times are standalone (bench.py's roofline measurement). */
+ * times are standalone (bench.py's roofline measurement). Bit 3 disables the
+ * TMA tile loads of the extrema kernel (plain loads instead; parity tests). */
 int cdvz_gpu_set_debug(cdvz_gpu_ctx* ctx, int on);
 
 /* CUDA events on the context's stream (slots 0..3), for callers timing the

@@ -16,13 +16,16 @@
 #include <string>
 #include <vector>
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "../../include/cdvz_gpu.h"
 #include "bundle.hpp"
 #include "common.cuh"
 
 namespace cdvz_gpu {
 cudaError_t launch_octave(const Batch& bt, const DetConst& dc, int o, int src, cudaStream_t st);
-cudaError_t launch_detect(const Batch& bt, const DetConst& dc, int o, cudaStream_t st);
+cudaError_t launch_detect(const Batch& bt, const DetConst& dc, int o, const CUtensorMap* tmap, cudaStream_t st);
 cudaError_t launch_merge(const Batch& bt, int o, cudaStream_t st);
 cudaError_t launch_select(const Batch& bt, const Model& md, const EncodeConst& ec, cudaStream_t st);
 cudaError_t launch_describe(const Batch& bt, const DetConst& dc, const Model& md, const EncodeConst& ec, cudaStream_t st);
@@ -98,6 +101,8 @@ struct Lane {
   cudaEvent_t start = nullptr, done = nullptr;
   cudaEvent_t stage[6] = {};
   cudaEvent_t blur[2 * kMaxOctaves] = {}, det[2 * kMaxOctaves] = {};
+  CUtensorMap tmap[kMaxOctaves];   // 4-D view (x, y, level, frame) of each octave's G planes
+  bool tmap_ok[kMaxOctaves] = {};
   bool pending = false;   // events of an enqueued chunk not yet folded into the stats
   int pending_oct = 0;
   double pending_bytes = 0.0;
@@ -139,6 +144,7 @@ struct cdvz_gpu_ctx {
   std::vector<DeviceBuffer> model_bufs;
   bool debug = false;
   bool serial = false;
+  bool tma_disabled = false;
 
   Lane lanes[2];
   int last_lane = 0;
@@ -328,6 +334,28 @@ struct cdvz_gpu_ctx {
     CDVZ_CUDA_CHECK(cudaMemset(nb.bitmap, 0, sizeof(uint32_t) * F * nb.bitmap_words));
     CDVZ_CUDA_CHECK(cudaMemset(nb.acc_count, 0, sizeof(int) * F * 2));
     if (debug) L.dbg_oct.ensure(sizeof(KP) * F * std::max(1, n_oct) * nb.cap_acc);
+    // TMA views of the pyramid for k_detect: needs 16-byte row strides (even
+    // widths); other sizes use the plain load path.
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+      void* fn = nullptr;
+      cudaDriverEntryPointQueryResult q{};
+      if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+          q != cudaDriverEntryPointSuccess)
+        fn = nullptr;
+      return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }();
+    for (int o = 0; o < n_oct; ++o) {
+      L.tmap_ok[o] = false;
+      if (!encode || (nb.ow[o] & 1) || tma_disabled) continue;
+      const cuuint64_t dims[4] = {cuuint64_t(nb.ow[o]), cuuint64_t(nb.oh[o]), 4, cuuint64_t(frames)};
+      const cuuint64_t strides[3] = {cuuint64_t(nb.ow[o]) * 8, cuuint64_t(nb.ow[o]) * nb.oh[o] * 8,
+                                     cuuint64_t(nb.frame_doubles) * 8};
+      const cuuint32_t box[4] = {68, 20, 4, 1}, estr[4] = {1, 1, 1, 1};
+      const CUresult r = encode(&L.tmap[o], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, nb.pyr + nb.plane_off[o][0], dims, strides,
+                                box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      L.tmap_ok[o] = (r == CUDA_SUCCESS);
+    }
     L.bt = nb;
     L.geo_w = W;
     L.geo_h = H;
@@ -438,7 +466,7 @@ struct cdvz_gpu_ctx {
         CDVZ_CUDA_CHECK(cudaEventRecord(L.blur[2 * o + 1], L.sA));
         CDVZ_CUDA_CHECK(cudaStreamWaitEvent(sB, L.blur[2 * o + 1], 0));
         CDVZ_CUDA_CHECK(cudaEventRecord(L.det[2 * o], sB));
-        CDVZ_CUDA_CHECK(launch_detect(b, dc, o, sB));
+        CDVZ_CUDA_CHECK(launch_detect(b, dc, o, L.tmap_ok[o] ? &L.tmap[o] : nullptr, sB));
         CDVZ_CUDA_CHECK(cudaEventRecord(L.det[2 * o + 1], sB));
         CDVZ_CUDA_CHECK(launch_merge(b, o, sB));
         launches += 3;
@@ -594,6 +622,10 @@ int cdvz_gpu_set_debug(cdvz_gpu_ctx* ctx, int on) {
   ctx->debug = (on & 1) != 0;
   ctx->dc.screen = (on & 2) ? 0 : 1;
   ctx->serial = (on & 4) != 0;
+  if (ctx->tma_disabled != ((on & 8) != 0)) {
+    ctx->tma_disabled = (on & 8) != 0;
+    for (auto& l : ctx->lanes) l.geo_w = 0;  // rebuild the tensor maps
+  }
   return CDVZ_GPU_OK;
 }
 

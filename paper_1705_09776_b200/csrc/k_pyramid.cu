@@ -29,6 +29,8 @@
 // ((up+down)+left)+right-4c, alpha in column order) with separately rounded
 // multiplies and adds (--fmad=false), so G, alpha and every candidate are
 // bit-identical to the oracle.
+#include <cuda.h>
+
 #include "common.cuh"
 
 namespace cdvz_gpu {
@@ -301,18 +303,44 @@ constexpr int kDetW = 64, kDetH = 16, kDetThreads = 256;
 constexpr int kGW = kDetW + 4, kGH = kDetH + 4;  // G region
 constexpr int kAW = kDetW + 2, kAH = kDetH + 2;  // alpha region
 
-__global__ void __launch_bounds__(kDetThreads, 2) k_detect(Batch bt, DetConst dc, int o) {
-  extern __shared__ double dsm[];
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return uint32_t(__cvta_generic_to_shared(p)); }
+
+__global__ void __launch_bounds__(kDetThreads, 2)
+    k_detect(Batch bt, DetConst dc, int o, const __grid_constant__ CUtensorMap tmap, int use_tma) {
+  extern __shared__ __align__(128) double dsm[];
   double* Gt = dsm;                      // [4][kGH][kGW]
   double* At = Gt + 4 * kGH * kGW;       // [kAH][4][kAW]
   __shared__ int q_count;
   __shared__ uint16_t queue[kDetW * kDetH];
+  __shared__ __align__(8) uint64_t tma_bar;
   const int f = blockIdx.z, tid = threadIdx.x;
   const int w = bt.ow[o], h = bt.oh[o], m = dc.margin;
   const int tx0 = m + blockIdx.x * kDetW, ty0 = m + blockIdx.y * kDetH;
   const double* pyr = bt.pyr + f * bt.frame_doubles;
   if (tid == 0) q_count = 0;
-  {
+  if (use_tma) {
+    // One 4-D TMA box (68 x 20 x 4 levels x 1 frame) brings the tile's G
+    // levels into shared memory; rows/columns past the image arrive as zeros
+    // and only feed alpha outside the detection window.
+    if (tid == 0) {
+      const uint32_t bar = smem_u32(&tma_bar);
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(uint32_t(sizeof(double) * 4 * kGH * kGW)) : "memory");
+      asm volatile(
+          "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];"
+          ::"r"(smem_u32(Gt)), "l"(&tmap), "r"(tx0 - 2), "r"(ty0 - 2), "r"(0), "r"(f), "r"(bar)
+          : "memory");
+    }
+    __syncthreads();  // barrier initialised before anyone polls it
+    const uint32_t bar = smem_u32(&tma_bar);
+    uint32_t done = 0;
+    while (!done) {
+      asm volatile(
+          "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n selp.u32 %0, 1, 0, p;\n}"
+          : "=r"(done) : "r"(bar) : "memory");
+    }
+  } else {
     constexpr int N = 4 * kGH * kGW, PER = (N + kDetThreads - 1) / kDetThreads;
     double v[PER];
 #pragma unroll
@@ -329,8 +357,8 @@ __global__ void __launch_bounds__(kDetThreads, 2) k_detect(Batch bt, DetConst dc
       const int q = tid + k * kDetThreads;
       if (q < N) Gt[q] = v[k];
     }
+    __syncthreads();
   }
-  __syncthreads();
   // Laplacian x sigma^2 then alpha, for the tile + 1 halo (scale_space.cpp:148-170);
   // a fixed, unrolled set of positions per thread so loads and the four
   // independent alpha sums of several positions overlap.
@@ -360,14 +388,24 @@ __global__ void __launch_bounds__(kDetThreads, 2) k_detect(Batch bt, DetConst dc
     }
   }
   __syncthreads();
+  static_assert((kDetW * kDetH) % kDetThreads == 0, "uniform screen loop");
+  const int lane = tid & 31;
   for (int q = tid; q < kDetW * kDetH; q += kDetThreads) {
     const int r = q / kDetW, cc = q % kDetW;
     const int yd = ty0 + r, xd = tx0 + cc;
+    bool push = false;
     if (yd < h - m && xd < w - m) {
       const double* a = At + ((r + 1) * 4) * kAW + cc + 1;
       const double av[4] = {a[0], a[kAW], a[2 * kAW], a[3 * kAW]};
-      if (!dc.screen || screen_pixel(av, dc)) queue[atomicAdd(&q_count, 1)] = uint16_t(q);
+      push = !dc.screen || screen_pixel(av, dc);
     }
+    // One shared-memory atomic per warp (queue order is irrelevant: the merge
+    // kernel restores raster order from the bitmap).
+    const unsigned bal = __ballot_sync(0xffffffffu, push);
+    int base = 0;
+    if (lane == 0 && bal) base = atomicAdd(&q_count, __popc(bal));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (push) queue[base + __popc(bal & ((1u << lane) - 1u))] = uint16_t(q);
   }
   __syncthreads();
   const int nq = q_count;
@@ -381,6 +419,7 @@ __global__ void __launch_bounds__(kDetThreads, 2) k_detect(Batch bt, DetConst dc
 }
 
 constexpr size_t kDetSmem = sizeof(double) * (4 * kGH * kGW + kAH * 4 * kAW);
+static_assert((kGW * sizeof(double)) % 16 == 0, "TMA box rows must be 16-byte multiples");
 
 template <int R0, int R1, int R2, int R3>
 cudaError_t launch_octave_variant(const Batch& bt, const DetConst& dc, int o, int src, cudaStream_t st) {
@@ -391,7 +430,7 @@ cudaError_t launch_octave_variant(const Batch& bt, const DetConst& dc, int o, in
   return cudaGetLastError();
 }
 
-cudaError_t launch_detect(const Batch& bt, const DetConst& dc, int o, cudaStream_t st) {
+cudaError_t launch_detect(const Batch& bt, const DetConst& dc, int o, const CUtensorMap* tmap, cudaStream_t st) {
   const int ww = bt.ow[o] - 2 * dc.margin, hh = bt.oh[o] - 2 * dc.margin;
   if (ww <= 0 || hh <= 0) return cudaSuccess;  // detect_extrema: empty window (scale_space.cpp:159)
   static bool configured = false;
@@ -401,7 +440,8 @@ cudaError_t launch_detect(const Batch& bt, const DetConst& dc, int o, cudaStream
     configured = true;
   }
   dim3 grid((ww + kDetW - 1) / kDetW, (hh + kDetH - 1) / kDetH, bt.nframes);
-  k_detect<<<grid, kDetThreads, kDetSmem, st>>>(bt, dc, o);
+  CUtensorMap none{};
+  k_detect<<<grid, kDetThreads, kDetSmem, st>>>(bt, dc, o, tmap ? *tmap : none, tmap ? 1 : 0);
   return cudaGetLastError();
 }
 
