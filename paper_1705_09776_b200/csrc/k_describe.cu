@@ -25,9 +25,20 @@ namespace {
 constexpr double kTwoPi = 2.0 * 3.14159265358979323846;
 constexpr int kMaxPeaks = 36;
 
+// wrap_angle (descriptor.cpp:19-22) for |a| < 2 * 2pi without the general
+// fmod loop: fmod is exact, and on this range it is a itself or a +- 2pi,
+// which Sterbenz's lemma makes exact too (sign of the dividend kept).
 __device__ __forceinline__ double wrap_angle(double a) {
-  a = fmod(a, kTwoPi);
-  return a < 0.0 ? a + kTwoPi : a;
+  double r = a;
+  if (fabs(a) >= kTwoPi) {
+    if (fabs(a) < 2.0 * kTwoPi) {
+      r = a > 0.0 ? a - kTwoPi : a + kTwoPi;
+      if (r == 0.0) r = copysign(0.0, a);
+    } else {
+      r = fmod(a, kTwoPi);
+    }
+  }
+  return r < 0.0 ? r + kTwoPi : r;
 }
 
 // descriptor.cpp:25-35 — a term is skipped when its fraction is exactly 0.
@@ -214,32 +225,46 @@ __global__ void __launch_bounds__(1024) k_expand(Batch bt) {
   }
 }
 
-// One CTA per oriented point, grid-strided: description
-// (descriptor.cpp:47-145) + compression (transform_coding.cpp:81-217).
+// One WARP per oriented point: description (descriptor.cpp:47-145) +
+// compression (transform_coding.cpp:81-217), warp-synchronous (no block
+// barriers; the CTA is only a container of independent warps).
 //
-// Phase A: all samples of the patch are evaluated in parallel (bilinear
-// gradients, magnitude, Gaussian weight, orientation) and parked in shared
-// memory. Phase B: thread (sub-patch s, cell c, parity p) owns the 4
-// orientation bins of cell c with parity p for sub-patch s. A sample's cell
-// coordinates depend only on its index (cu0 = floor(u(i) / 3sigma + 1.5),
-// cv0 likewise in j), so the samples feeding cell c form a rectangle in index
-// space; the thread walks it in row-major order, which is exactly the order
-// the reference adds them, and each sample adds to exactly one of its bins.
+// The 12-sigma patch is sampled on a samples x samples grid (samples =
+// ceil(12 sigma) <= 32) and split into row bands of 16 sample rows — exactly
+// the rows of the reference's 16x16 sub-patches. Per band:
+//   Phase A: the warp evaluates every sample of the band (bilinear gradient,
+//     magnitude, Gaussian weight, orientation bin) with 32 samples in flight
+//     and parks (weight, fo, bin0) in shared memory;
+//   Phase B: lane (cell c, parity p) owns the four orientation bins of parity
+//     p of cell c. Cell coordinates depend on the sample index only, so the
+//     samples feeding cell c form a rectangle; the lane walks it in row-major
+//     order — the reference's add order — keeping separate partials for the
+//     left and right sub-patch of the band, and folds the band's partials into
+//     the running total in sub-patch index order (merge_and_normalize).
+// Every lane then holds 4 of the 128 bins for normalisation, transform and
+// ternary coding.
 constexpr int kMaxSamples = 32;  // samples per axis: ceil(12 sigma) for sigma <= 2.66 (radius-8 detector)
+constexpr int kBand = 16;        // kSubPatchSide (descriptor.cpp)
+constexpr int kDescWarps = 4;
 
-__global__ void __launch_bounds__(128, 5) k_describe(Batch bt, DetConst dc, Model md, EncodeConst ec) {
-  __shared__ double s_w[kMaxSamples * kMaxSamples];       // weight; +0 for a skipped sample
-  __shared__ double s_wo[2][kMaxSamples * kMaxSamples];   // wo for the bin of parity 0 / 1
-  __shared__ uint8_t s_slot[kMaxSamples * kMaxSamples];   // bin >> 1 for parity 0 (bits 0-1) / 1 (bits 2-3)
-  __shared__ double s_wu[2][kMaxSamples], s_wv[2][kMaxSamples];  // [du][i]: 1 - fu, fu
-  __shared__ int s_cu[kMaxSamples], s_cv[kMaxSamples];
-  __shared__ double part[4][128];  // <= 2x2 sub-patches of 16x16 samples
-  __shared__ double sq[128], red[4], tv[128], vec[128];
-  __shared__ uint8_t sym[128];
-  const int tid = threadIdx.x;
+struct DescWarpSmem {
+  double w[kBand * kMaxSamples];   // weight; +0 for a skipped sample. Reused as sq / tv after phase B.
+  double fo[kBand * kMaxSamples];  // fractional orientation bin
+  double u[kMaxSamples];           // (i + 0.5) * step - half (same for rows and columns)
+  double wf[2][kMaxSamples];       // [d][i]: 1 - f, f of the cell coordinate
+  uint8_t bin[kBand * kMaxSamples];
+  int c0[kMaxSamples];             // floor(u * inv_cell + 1.5)
+};
+
+__global__ void __launch_bounds__(32 * kDescWarps, 4) k_describe(Batch bt, DetConst dc, Model md, EncodeConst ec) {
+  __shared__ DescWarpSmem smem[kDescWarps];
+  const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  DescWarpSmem& S = smem[wi];
   const int f = blockIdx.y;
   const int n_or = bt.or_count[f];
-  for (int idx = blockIdx.x; idx < n_or; idx += gridDim.x) {
+  const int cell = lane >> 1, parity = lane & 1;
+  const int ccx = cell & 3, ccy = cell >> 2;
+  for (int idx = blockIdx.x * kDescWarps + wi; idx < n_or; idx += gridDim.x * kDescWarps) {
     const Oriented orp = bt.oriented[(long long)f * bt.cap_or + idx];
     const KP k = bt.sel[(long long)f * bt.select_n + orp.sel];
     const double theta = orp.theta;
@@ -247,158 +272,177 @@ __global__ void __launch_bounds__(128, 5) k_describe(Batch bt, DetConst dc, Mode
     // make_geometry (descriptor.cpp:47-58)
     const double half = 6.0 * fr.sigma;
     const int samples = max(1, static_cast<int>(ceil(12.0 * fr.sigma)));
+    if (samples > kMaxSamples) {  // outside the supported scale range: flag the frame
+      if (lane == 0) atomicOr(&bt.status[f], 8);
+      continue;
+    }
     const double step = 2.0 * half / samples;
-    const int spa = (samples + 15) / 16;
+    const int spa = (samples + kBand - 1) / kBand;
     const double cos_t = cos(theta), sin_t = sin(theta);
     const double inv_cell = 1.0 / (3.0 * fr.sigma);
     const double gauss_denom = 2.0 * half * half;
-    const int n_sub = spa * spa;
-    if (samples > kMaxSamples) {  // outside the supported scale range: flag the frame
-      if (tid == 0) atomicOr(&bt.status[f], 8);
-      continue;
-    }
-    // Per-axis cell coordinates (descriptor.cpp:89-96): cu depends on i only.
-    for (int i = tid; i < samples; i += blockDim.x) {
-      const double u = (i + 0.5) * step - half;
+    // Per-axis cell coordinates (descriptor.cpp:89-96): identical for u (i) and v (j).
+    int my_c0 = 0x7fff;
+    if (lane < samples) {
+      const double u = (lane + 0.5) * step - half;
       const double cu = u * inv_cell + 1.5;
-      const int cu0 = static_cast<int>(floor(cu));
-      const double fu = cu - cu0;
-      s_cu[i] = cu0;
-      s_wu[0][i] = 1.0 - fu;
-      s_wu[1][i] = fu;
+      my_c0 = static_cast<int>(floor(cu));
+      const double fu = cu - my_c0;
+      S.u[lane] = u;
+      S.c0[lane] = my_c0;
+      S.wf[0][lane] = 1.0 - fu;
+      S.wf[1][lane] = fu;
     }
-    for (int j = tid; j < samples; j += blockDim.x) {
-      const double v = (j + 0.5) * step - half;
-      const double cv = v * inv_cell + 1.5;
-      const int cv0 = static_cast<int>(floor(cv));
-      const double fv = cv - cv0;
-      s_cv[j] = cv0;
-      s_wv[0][j] = 1.0 - fv;
-      s_wv[1][j] = fv;
+    // This lane's rectangle: indices whose c0 is in {c - 1, c} (c0 is monotone).
+    int ia = samples, ib = samples, ja = samples, jb = samples;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const unsigned ge = __ballot_sync(0xffffffffu, lane < samples && my_c0 >= c - 1);
+      const unsigned gt = __ballot_sync(0xffffffffu, lane < samples && my_c0 > c);
+      const int lo = ge ? __ffs(ge) - 1 : samples, hi = gt ? __ffs(gt) - 1 : samples;
+      if (c == ccx) { ia = lo; ib = hi; }
+      if (c == ccy) { ja = lo; jb = hi; }
     }
-    // Phase A: every sample (descriptor.cpp:75-88).
-    const int ns = samples * samples;
-    for (int q = tid; q < ns; q += blockDim.x) {
-      const int j = q / samples, i = q - j * samples;
-      const double v = (j + 0.5) * step - half;
-      const double u = (i + 0.5) * step - half;
-      const double px = fr.x + u * cos_t - v * sin_t;
-      const double py = fr.y + u * sin_t + v * cos_t;
-      int bin0 = 0;
-      double wgt = 0.0, fo = 0.0;
-      if (!(px < 1.0 || px > fr.w - 2.0 || py < 1.0 || py > fr.h - 2.0)) {
-        const double gx = 0.5 * (sample_bilinear(fr.lvl, fr.w, px + 1.0, py) - sample_bilinear(fr.lvl, fr.w, px - 1.0, py));
-        const double gy = 0.5 * (sample_bilinear(fr.lvl, fr.w, px, py + 1.0) - sample_bilinear(fr.lvl, fr.w, px, py - 1.0));
-        const double mag = hypot(gx, gy);
-        if (mag != 0.0) {
-          wgt = mag * exp(-(u * u + v * v) / gauss_denom);
-          const double phi = wrap_angle(atan2(gy, gx) - theta);
-          const double obv = phi / kTwoPi * 8 - 0.5;
-          const int ob0 = static_cast<int>(floor(obv));
-          fo = obv - ob0;
-          bin0 = ((ob0 % 8) + 8) % 8;
-        }
-      }
-      // Of the sample's two orientation bins (bin0, bin0 + 1 mod 8), the one
-      // of parity p gets wo = 1 - fo if it is bin0, fo otherwise.
-      const int odd = bin0 & 1;
-      const int b_even = odd ? (bin0 + 1) & 7 : bin0, b_odd = odd ? bin0 : (bin0 + 1) & 7;
-      s_w[q] = wgt;
-      s_wo[0][q] = odd ? fo : 1.0 - fo;
-      s_wo[1][q] = odd ? 1.0 - fo : fo;
-      s_slot[q] = uint8_t((b_even >> 1) | ((b_odd >> 1) << 2));
-    }
-    __syncthreads();
-    // Phase B: ordered accumulation (descriptor.cpp:98-116).
-    {
-      const int sp = tid >> 5, cell = (tid >> 1) & 15, parity = tid & 1;
-      const int cx = cell & 3, cy = cell >> 2;
-      double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
-      if (sp < n_sub) {
-        const int i_lo = (sp % spa) * 16, j_lo = (sp / spa) * 16;
-        const int i_hi = min(samples, i_lo + 16), j_hi = min(samples, j_lo + 16);
-        // Samples with cu0 in {cx-1, cx} (du = 1, 0) and cv0 in {cy-1, cy}.
-        int ia = i_lo, ib = i_hi, ja = j_lo, jb = j_hi;
-        while (ia < ib && s_cu[ia] < cx - 1) ++ia;
-        while (ib > ia && s_cu[ib - 1] > cx) --ib;
-        while (ja < jb && s_cv[ja] < cy - 1) ++ja;
-        while (jb > ja && s_cv[jb - 1] > cy) --jb;
-        const double* wo_p = s_wo[parity];
-        const int shift = 2 * parity;
-        for (int j = ja; j < jb; ++j) {
-          const double wv = s_wv[cy - s_cv[j]][j];
-          const int row = j * samples;
-#pragma unroll 4
-          for (int i = ia; i < ib; ++i) {
-            const int q = row + i;
-            // A skipped sample has weight +0: the add leaves the (non-negative) sum unchanged.
-            const double add = s_w[q] * wv * s_wu[cx - s_cu[i]][i] * wo_p[q];
-            const int slot = (s_slot[q] >> shift) & 3;
-            acc0 += slot == 0 ? add : 0.0;
-            acc1 += slot == 1 ? add : 0.0;
-            acc2 += slot == 2 ? add : 0.0;
-            acc3 += slot == 3 ? add : 0.0;
+    __syncwarp();
+    double tot[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int band = 0; band < spa; ++band) {
+      const int j0 = band * kBand, j1 = min(samples, j0 + kBand);
+      const int n = (j1 - j0) * samples;
+      // Phase A (descriptor.cpp:75-88).
+      for (int q = lane; q < n; q += 32) {
+        const int jr = q / samples, i = q - jr * samples;
+        const double v = S.u[j0 + jr];
+        const double u = S.u[i];
+        const double px = fr.x + u * cos_t - v * sin_t;
+        const double py = fr.y + u * sin_t + v * cos_t;
+        int bin0 = 0;
+        double wgt = 0.0, fo = 0.0;
+        if (!(px < 1.0 || px > fr.w - 2.0 || py < 1.0 || py > fr.h - 2.0)) {
+          const double gx = 0.5 * (sample_bilinear(fr.lvl, fr.w, px + 1.0, py) - sample_bilinear(fr.lvl, fr.w, px - 1.0, py));
+          const double gy = 0.5 * (sample_bilinear(fr.lvl, fr.w, px, py + 1.0) - sample_bilinear(fr.lvl, fr.w, px, py - 1.0));
+          const double mag = hypot(gx, gy);
+          if (mag != 0.0) {
+            wgt = mag * exp(-(u * u + v * v) / gauss_denom);
+            const double phi = wrap_angle(atan2(gy, gx) - theta);
+            const double obv = phi / kTwoPi * 8 - 0.5;
+            const int ob0 = static_cast<int>(floor(obv));
+            fo = obv - ob0;
+            bin0 = ((ob0 % 8) + 8) % 8;
           }
         }
-        part[sp][cell * 8 + parity] = acc0;
-        part[sp][cell * 8 + parity + 2] = acc1;
-        part[sp][cell * 8 + parity + 4] = acc2;
-        part[sp][cell * 8 + parity + 6] = acc3;
+        S.w[q] = wgt;
+        S.fo[q] = fo;
+        S.bin[q] = uint8_t(bin0);
       }
-    }
-    __syncthreads();
-    // merge_and_normalize (descriptor.cpp:124-145): sum partials in order,
-    // then up to 5 rounds of L2 normalise + clamp at 0.2; the norm uses the
-    // Eigen SSE2 reduction order.
-    double v = part[0][tid];
-    for (int s = 1; s < n_sub; ++s) v = v + part[s][tid];
-    for (int round = 0; round < 5; ++round) {
-      sq[tid] = v * v;
-      __syncthreads();
-      if (tid < 4) {
-        double a = sq[tid];
-        for (int i = tid + 4; i < 128; i += 4) a = a + sq[i];
-        red[tid] = a;
+      __syncwarp();
+      // Phase B (descriptor.cpp:98-116): partials of the band's left (i < 16)
+      // and right sub-patch, each in row-major sample order.
+      double pa[4] = {0.0, 0.0, 0.0, 0.0}, pb[4] = {0.0, 0.0, 0.0, 0.0};
+      const int jlo = max(ja, j0), jhi = min(jb, j1);
+      const int ia0 = ia, ib0 = min(ib, kBand), ia1 = max(ia, kBand), ib1 = ib;
+      for (int j = jlo; j < jhi; ++j) {
+        const double wv = S.wf[ccy - S.c0[j]][j];
+        const int row = (j - j0) * samples;
+#define CDVZ_VISIT(ACC)                                                   \
+  {                                                                       \
+    const int q = row + i;                                                \
+    const int b0 = S.bin[q];                                              \
+    const bool own = (b0 & 1) == parity;                                  \
+    const double fo = S.fo[q];                                            \
+    const double wo = own ? 1.0 - fo : fo;                                \
+    const int slot = (own ? b0 : (b0 + 1) & 7) >> 1;                      \
+    const double add = S.w[q] * wv * S.wf[ccx - S.c0[i]][i] * wo;         \
+    ACC[0] += slot == 0 ? add : 0.0;                                      \
+    ACC[1] += slot == 1 ? add : 0.0;                                      \
+    ACC[2] += slot == 2 ? add : 0.0;                                      \
+    ACC[3] += slot == 3 ? add : 0.0;                                      \
+  }
+        for (int i = ia0; i < ib0; ++i) CDVZ_VISIT(pa)
+        for (int i = ia1; i < ib1; ++i) CDVZ_VISIT(pb)
+#undef CDVZ_VISIT
       }
-      __syncthreads();
-      const double norm = sqrt((red[0] + red[2]) + (red[1] + red[3]));
-      if (norm == 0.0) break;
-      v = v / norm;
-      bool clipped = false;
-      if (v > 0.2) { v = 0.2; clipped = true; }
-      if (!__syncthreads_or(clipped)) break;
-    }
-    bt.desc[((long long)f * bt.cap_or + idx) * 128 + tid] = v;
-    vec[tid] = v;
-    __syncthreads();
-    // transform_descriptor (transform_coding.cpp:81-91)
-    {
-      const int c = tid >> 3, i = tid & 7;
-      const int which = (((c % 4) + (c / 4)) & 1) == 0 ? 0 : 1;
-      double s = md.tr[which][i][0] * vec[c * 8];
+      // merge_and_normalize's ordered sum of partials (sub-patch index order).
 #pragma unroll
-      for (int kk = 1; kk < 8; ++kk) s = s + md.tr[which][i][kk] * vec[c * 8 + kk];
-      tv[tid] = md.tr_scale * s;
-    }
-    __syncthreads();
-    // quantize_ternary (transform_coding.cpp:202-217): 00 zero, 01 +1, 10 -1
-    if (tid < ec.elements) {
-      const int e = md.priority[tid];
-      const double val = tv[e];
-      sym[tid] = val < md.t0[e] ? 2 : (val > md.t1[e] ? 1 : 0);
-    }
-    __syncthreads();
-    uint8_t* code = bt.codes + ((long long)f * bt.cap_or + idx) * bt.code_stride;
-    const int nbytes = (ec.elements * 2 + 7) / 8;
-    if (tid < nbytes) {
-      uint8_t byte = 0;
-      for (int q = 0; q < 4; ++q) {
-        const int j = tid * 4 + q;
-        if (j < ec.elements) byte |= uint8_t(sym[j] << (2 * q));
+      for (int m = 0; m < 4; ++m) {
+        tot[m] = band == 0 ? pa[m] : tot[m] + pa[m];
+        if (spa > 1) tot[m] = tot[m] + pb[m];
       }
-      code[6 + tid] = byte;
+      __syncwarp();
     }
-    if (tid == 0) {
+    // normalize_descriptor (descriptor.cpp:124-145): up to 5 rounds of L2
+    // normalise + clamp at 0.2; the norm in the Eigen SSE2 reduction order
+    // (four stride-4 running sums, then (s0 + s2) + (s1 + s3)).
+    double* sq = S.w;
+    double* tv = S.w + 128;
+    const int bin_base = cell * 8 + parity;
+    for (int round = 0; round < 5; ++round) {
+#pragma unroll
+      for (int m = 0; m < 4; ++m) sq[bin_base + 2 * m] = tot[m] * tot[m];
+      __syncwarp();
+      double red = 0.0;
+      if (lane < 4) {
+        double t[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) t[i] = sq[lane + 4 * i];
+        red = t[0];
+#pragma unroll
+        for (int i = 1; i < 32; ++i) red = red + t[i];
+      }
+      const double r0 = __shfl_sync(0xffffffffu, red, 0), r1 = __shfl_sync(0xffffffffu, red, 1);
+      const double r2 = __shfl_sync(0xffffffffu, red, 2), r3 = __shfl_sync(0xffffffffu, red, 3);
+      __syncwarp();
+      const double norm = sqrt((r0 + r2) + (r1 + r3));
+      if (norm == 0.0) break;
+      bool clipped = false;
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        tot[m] = tot[m] / norm;
+        if (tot[m] > 0.2) { tot[m] = 0.2; clipped = true; }
+      }
+      if (!__any_sync(0xffffffffu, clipped)) break;
+    }
+    double* dout = bt.desc + ((long long)f * bt.cap_or + idx) * 128;
+#pragma unroll
+    for (int m = 0; m < 4; ++m) dout[bin_base + 2 * m] = tot[m];
+    // transform_descriptor (transform_coding.cpp:81-91): the cell's 8 values
+    // are split between this lane and its parity partner.
+    {
+      double vec[8];
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        const double other = __shfl_xor_sync(0xffffffffu, tot[m], 1);
+        vec[2 * m] = parity ? other : tot[m];
+        vec[2 * m + 1] = parity ? tot[m] : other;
+      }
+      const int which = ((ccx + ccy) & 1) == 0 ? 0 : 1;
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        const int i = parity + 2 * m;
+        double s = md.tr[which][i][0] * vec[0];
+#pragma unroll
+        for (int kk = 1; kk < 8; ++kk) s = s + md.tr[which][i][kk] * vec[kk];
+        tv[cell * 8 + i] = md.tr_scale * s;
+      }
+    }
+    __syncwarp();
+    // quantize_ternary (transform_coding.cpp:202-217): 00 zero, 01 +1, 10 -1;
+    // lane L packs symbols 4L .. 4L+3 into code byte L.
+    uint8_t* code = bt.codes + ((long long)f * bt.cap_or + idx) * bt.code_stride;
+    if (4 * lane < ec.elements) {
+      uint8_t byte = 0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int t = 4 * lane + q;
+        if (t < ec.elements) {
+          const int e = md.priority[t];
+          const double val = tv[e];
+          const uint8_t sym = val < md.t0[e] ? 2 : (val > md.t1[e] ? 1 : 0);
+          byte |= uint8_t(sym << (2 * q));
+        }
+      }
+      code[6 + lane] = byte;
+    }
+    if (lane == 0) {
       // quantize_coord / quantize_sigma_log / quantize_theta (transform_coding.cpp:173-200)
       const double cxq = fmin(fmax(k.x, 0.0), double(bt.W - 1));
       const double cyq = fmin(fmax(k.y, 0.0), double(bt.H - 1));
@@ -417,7 +461,7 @@ __global__ void __launch_bounds__(128, 5) k_describe(Batch bt, DetConst dc, Mode
       code[4] = uint8_t(sq8);
       code[5] = uint8_t(th8);
     }
-    __syncthreads();
+    __syncwarp();
   }
 }
 
@@ -428,7 +472,7 @@ cudaError_t launch_describe(const Batch& bt, const DetConst& dc, const Model& md
   k_expand<<<bt.nframes, 1024, 0, st>>>(bt);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  k_describe<<<dim3(96, bt.nframes), 128, 0, st>>>(bt, dc, md, ec);
+  k_describe<<<dim3(32, bt.nframes), 32 * kDescWarps, 0, st>>>(bt, dc, md, ec);
   return cudaGetLastError();
 }
 
