@@ -25,6 +25,15 @@ static_assert(sizeof(KP) == 64, "KP layout");
 
 struct Oriented { int sel; int pad; double theta; };
 
+// Sampling geometry of one oriented point (make_geometry + resolve_frame,
+// descriptor.cpp:47-58,149-170), shared by the sample and histogram kernels.
+struct DescGeo {
+  double x, y, cos_t, sin_t, step, half, inv_cell, gauss_denom;
+  long long lvl_off;   // doubles from the batch pyramid base to the level plane
+  int w, h, samples, pad;
+};
+static_assert(sizeof(DescGeo) == 88, "DescGeo layout");
+
 // Detector constants (ScaleSpaceConfig + derived; scale_space.hpp:16-27).
 struct DetConst {
   double taps[4][2 * kMaxTapRadius + 1];
@@ -75,6 +84,9 @@ struct Batch {
   int cap_or;
   Oriented* oriented;                  // [frame][cap_or]
   int* or_count;                       // [frame]
+  DescGeo* geo;                        // [frame][cap_or]
+  int smp_cap;                         // samples per oriented point (max samples^2)
+  double2* smp;                        // [frame][cap_or][smp_cap] {weight (+0: skipped), ob = phi/2pi*8 - 0.5}
   double* desc;                        // [frame][cap_or][128]
   uint8_t* codes;                      // [frame][cap_or][code_stride]
   int code_stride;

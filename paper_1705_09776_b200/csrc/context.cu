@@ -321,6 +321,14 @@ struct cdvz_gpu_ctx {
     nb.theta_count = static_cast<int*>(alloc(sizeof(int) * F * nb.select_n));
     nb.oriented = static_cast<Oriented*>(alloc(sizeof(Oriented) * F * nb.cap_or));
     nb.or_count = static_cast<int*>(alloc(sizeof(int) * F));
+    nb.geo = static_cast<DescGeo*>(alloc(sizeof(DescGeo) * F * nb.cap_or));
+    {
+      // samples per axis = ceil(12 sigma) with sigma <= sigma_3 (roots are
+      // clamped to [sigma_0, sigma_3]); larger patches are flagged per frame.
+      const int smax = std::min(32, std::max(1, static_cast<int>(std::ceil(12.0 * bundle.sigmas[3]))));
+      nb.smp_cap = smax * smax;
+    }
+    nb.smp = static_cast<double2*>(alloc(sizeof(double2) * F * nb.cap_or * nb.smp_cap));
     nb.desc = static_cast<double*>(alloc(sizeof(double) * F * nb.cap_or * 128));
     nb.codes = static_cast<uint8_t*>(alloc(F * nb.cap_or * nb.code_stride));
     nb.x = static_cast<double*>(alloc(sizeof(double) * F * nb.cap_or * 32));
@@ -453,7 +461,6 @@ struct cdvz_gpu_ctx {
                                           h_stride, size_t(w), size_t(h) * nf, cudaMemcpyHostToDevice, L.sA));
       CDVZ_CUDA_CHECK(cudaEventRecord(L.start, L.sA));
       CDVZ_CUDA_CHECK(cudaMemsetAsync(b.status, 0, sizeof(int) * nf, L.sA));
-      ++launches;
       if (resize) {
         CDVZ_CUDA_CHECK(launch_resize(b.pix8, stride, b.frame_bytes8, w, h, const_cast<double*>(b.pixf), W, H, nf, L.sA));
         ++launches;
@@ -502,7 +509,7 @@ struct cdvz_gpu_ctx {
       // The next chunk on this lane's stream A must not overwrite the pyramid
       // before stream B is done with it.
       CDVZ_CUDA_CHECK(cudaStreamWaitEvent(L.sA, L.done, 0));
-      launches += 1 + 3 + 5;
+      launches += 1 + 5 + 5;  // k_select; k_orient, k_expand, k_geometry, k_sample, k_describe; SCFV + pack
       L.pending = true;
       L.pending_oct = b.n_oct;
       L.pending_bytes = bytes;

@@ -225,241 +225,340 @@ __global__ void __launch_bounds__(1024) k_expand(Batch bt) {
   }
 }
 
-// One WARP per oriented point: description (descriptor.cpp:47-145) +
-// compression (transform_coding.cpp:81-217), warp-synchronous (no block
-// barriers; the CTA is only a container of independent warps).
-//
-// The 12-sigma patch is sampled on a samples x samples grid (samples =
-// ceil(12 sigma) <= 32) and split into row bands of 16 sample rows — exactly
-// the rows of the reference's 16x16 sub-patches. Per band:
-//   Phase A: the warp evaluates every sample of the band (bilinear gradient,
-//     magnitude, Gaussian weight, orientation bin) with 32 samples in flight
-//     and parks (weight, fo, bin0) in shared memory;
-//   Phase B: lane (cell c, parity p) owns the four orientation bins of parity
-//     p of cell c. Cell coordinates depend on the sample index only, so the
-//     samples feeding cell c form a rectangle; the lane walks it in row-major
-//     order — the reference's add order — keeping separate partials for the
-//     left and right sub-patch of the band, and folds the band's partials into
-//     the running total in sub-patch index order (merge_and_normalize).
-// Every lane then holds 4 of the 128 bins for normalisation, transform and
-// ternary coding.
+// Description (descriptor.cpp:47-145) + compression
+// (transform_coding.cpp:81-217) in three launches:
+//   k_geometry  thread per oriented point: resolve_frame + make_geometry.
+//   k_sample    Phase A, thread per patch sample (no shared memory, full
+//               occupancy): bilinear gradient, magnitude, Gaussian weight and
+//               orientation bin of every sample of the samples x samples grid
+//               (samples = ceil(12 sigma) <= 32), parked in HBM/L2 as
+//               (weight, fo, bin0) — descriptor.cpp:75-88.
+//   k_describe  Phase B + epilogue, one WARP per oriented point. Lane (cell c,
+//               parity p) owns the four orientation bins of parity p of cell
+//               c. Cell coordinates depend on the sample index only, so the
+//               samples feeding cell c form a rectangle, cut by the
+//               16-sample sub-patch grid into up to four sub-rectangles. The
+//               lane walks them in sub-patch index order, each in row-major
+//               order — the reference's add order within each sub-patch
+//               partial — and folds each partial into its running total in
+//               that order (merge_and_normalize). The walk is one flat loop
+//               per lane (a small state machine), so every lane stays busy
+//               until its own rectangle is done. Every lane then holds 4 of
+//               the 128 bins for normalisation, transform and ternary coding.
 constexpr int kMaxSamples = 32;  // samples per axis: ceil(12 sigma) for sigma <= 2.66 (radius-8 detector)
-constexpr int kBand = 16;        // kSubPatchSide (descriptor.cpp)
+constexpr int kSub = 16;         // kSubPatchSide (descriptor.cpp)
 constexpr int kDescWarps = 4;
 
+__global__ void __launch_bounds__(128) k_geometry(Batch bt, DetConst dc) {
+  const int f = blockIdx.y;
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= bt.or_count[f]) return;
+  const Oriented orp = bt.oriented[(long long)f * bt.cap_or + idx];
+  const KP k = bt.sel[(long long)f * bt.select_n + orp.sel];
+  const Frame fr = resolve(bt, dc, f, k);
+  DescGeo g;
+  g.x = fr.x;
+  g.y = fr.y;
+  g.half = 6.0 * fr.sigma;
+  g.samples = max(1, static_cast<int>(ceil(12.0 * fr.sigma)));
+  g.step = 2.0 * g.half / g.samples;
+  g.cos_t = cos(orp.theta);
+  g.sin_t = sin(orp.theta);
+  g.inv_cell = 1.0 / (3.0 * fr.sigma);
+  g.gauss_denom = 2.0 * g.half * g.half;
+  g.lvl_off = fr.lvl - bt.pyr;
+  g.w = fr.w;
+  g.h = fr.h;
+  g.pad = 0;
+  if (g.samples * g.samples > bt.smp_cap) {  // outside the supported scale range: flag the frame
+    atomicOr(&bt.status[f], 8);
+    g.samples = 0;
+  }
+  bt.geo[(long long)f * bt.cap_or + idx] = g;
+}
+
+__global__ void __launch_bounds__(256) k_sample(Batch bt) {
+  const int f = blockIdx.y;
+  const int n_or = bt.or_count[f];
+  for (int idx = blockIdx.x; idx < n_or; idx += gridDim.x) {
+    const long long slot = (long long)f * bt.cap_or + idx;
+    const DescGeo g = bt.geo[slot];
+    const double theta = bt.oriented[slot].theta;
+    const double* lvl = bt.pyr + g.lvl_off;
+    const int samples = g.samples, ns = samples * samples;
+    double2* out = bt.smp + slot * bt.smp_cap;
+    for (int q = threadIdx.x; q < ns; q += blockDim.x) {
+      const int j = q / samples, i = q - j * samples;
+      const double v = (j + 0.5) * g.step - g.half;
+      const double u = (i + 0.5) * g.step - g.half;
+      const double px = g.x + u * g.cos_t - v * g.sin_t;
+      const double py = g.y + u * g.sin_t + v * g.cos_t;
+      double wgt = 0.0, obv = 0.0;
+      if (!(px < 1.0 || px > g.w - 2.0 || py < 1.0 || py > g.h - 2.0)) {
+        const double gx = 0.5 * (sample_bilinear(lvl, g.w, px + 1.0, py) - sample_bilinear(lvl, g.w, px - 1.0, py));
+        const double gy = 0.5 * (sample_bilinear(lvl, g.w, px, py + 1.0) - sample_bilinear(lvl, g.w, px, py - 1.0));
+        const double mag = hypot(gx, gy);
+        if (mag != 0.0) {
+          wgt = mag * exp(-(u * u + v * v) / g.gauss_denom);
+          const double phi = wrap_angle(atan2(gy, gx) - theta);
+          obv = phi / kTwoPi * 8 - 0.5;
+        }
+      }
+      out[q] = make_double2(wgt, obv);
+    }
+  }
+}
+
+// Phase B + epilogue: TWO oriented points per warp, lane = (half, cell).
+// Lane (h, c) owns all 8 orientation bins of cell c of point h, kept in
+// shared memory as acc[bin][lane] (one sequential chain per bin, exactly the
+// reference's per-bin add order), so each sample costs one visit per cell
+// and two ordered adds (bins ob0 and ob0 + 1).
 struct DescWarpSmem {
-  double w[kBand * kMaxSamples];   // weight; +0 for a skipped sample. Reused as sq / tv after phase B.
-  double fo[kBand * kMaxSamples];  // fractional orientation bin
-  double u[kMaxSamples];           // (i + 0.5) * step - half (same for rows and columns)
-  double wf[2][kMaxSamples];       // [d][i]: 1 - f, f of the cell coordinate
-  uint8_t bin[kBand * kMaxSamples];
-  int c0[kMaxSamples];             // floor(u * inv_cell + 1.5)
+  double wf[2][2][kMaxSamples];  // [half][d][i]: 1 - f, f of the cell coordinate
+  double acc[8][32];             // [bin][lane]: current sub-patch partial
+  double buf[2][256];            // [half]: sq (0..127), tv (128..255)
 };
 
-__global__ void __launch_bounds__(32 * kDescWarps, 4) k_describe(Batch bt, DetConst dc, Model md, EncodeConst ec) {
+__global__ void __launch_bounds__(32 * kDescWarps) k_describe(Batch bt, DetConst dc, Model md, EncodeConst ec) {
   __shared__ DescWarpSmem smem[kDescWarps];
   const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
   DescWarpSmem& S = smem[wi];
   const int f = blockIdx.y;
   const int n_or = bt.or_count[f];
-  const int cell = lane >> 1, parity = lane & 1;
+  const int half = lane >> 4, cell = lane & 15;
   const int ccx = cell & 3, ccy = cell >> 2;
-  for (int idx = blockIdx.x * kDescWarps + wi; idx < n_or; idx += gridDim.x * kDescWarps) {
-    const Oriented orp = bt.oriented[(long long)f * bt.cap_or + idx];
-    const KP k = bt.sel[(long long)f * bt.select_n + orp.sel];
-    const double theta = orp.theta;
-    const Frame fr = resolve(bt, dc, f, k);
-    // make_geometry (descriptor.cpp:47-58)
-    const double half = 6.0 * fr.sigma;
-    const int samples = max(1, static_cast<int>(ceil(12.0 * fr.sigma)));
-    if (samples > kMaxSamples) {  // outside the supported scale range: flag the frame
-      if (lane == 0) atomicOr(&bt.status[f], 8);
-      continue;
-    }
-    const double step = 2.0 * half / samples;
-    const int spa = (samples + kBand - 1) / kBand;
-    const double cos_t = cos(theta), sin_t = sin(theta);
-    const double inv_cell = 1.0 / (3.0 * fr.sigma);
-    const double gauss_denom = 2.0 * half * half;
-    // Per-axis cell coordinates (descriptor.cpp:89-96): identical for u (i) and v (j).
-    int my_c0 = 0x7fff;
-    if (lane < samples) {
-      const double u = (lane + 0.5) * step - half;
-      const double cu = u * inv_cell + 1.5;
-      my_c0 = static_cast<int>(floor(cu));
-      const double fu = cu - my_c0;
-      S.u[lane] = u;
-      S.c0[lane] = my_c0;
-      S.wf[0][lane] = 1.0 - fu;
-      S.wf[1][lane] = fu;
-    }
-    // This lane's rectangle: indices whose c0 is in {c - 1, c} (c0 is monotone).
-    int ia = samples, ib = samples, ja = samples, jb = samples;
+  const unsigned hmask = 0xffffu << (16 * half);
+  for (int pair = blockIdx.x * kDescWarps + wi; 2 * pair < n_or; pair += gridDim.x * kDescWarps) {
+    const int idx = 2 * pair + half;
+    const bool live = idx < n_or;
+    const long long gslot = (long long)f * bt.cap_or + (live ? idx : 0);
+    const DescGeo g = bt.geo[gslot];
+    const int samples = live ? g.samples : 0;  // 0: no point, or flagged by k_geometry
+    const double2* smp = bt.smp + gslot * bt.smp_cap;
+    // Pull the point's sample records into L1 up front (one request per
+    // 128-byte line, all in flight together) so the walk below hits L1.
+    for (int l = cell * 8; l < samples * samples; l += 16 * 8)
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(smp + l));
+    // Per-axis cell coordinates (descriptor.cpp:89-96): identical for u (i)
+    // and v (j). Lane c of the half computes indices c and c + 16.
+    int c0lo = 0x7fff, c0hi = 0x7fff;
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const unsigned ge = __ballot_sync(0xffffffffu, lane < samples && my_c0 >= c - 1);
-      const unsigned gt = __ballot_sync(0xffffffffu, lane < samples && my_c0 > c);
-      const int lo = ge ? __ffs(ge) - 1 : samples, hi = gt ? __ffs(gt) - 1 : samples;
-      if (c == ccx) { ia = lo; ib = hi; }
-      if (c == ccy) { ja = lo; jb = hi; }
+    for (int r = 0; r < 2; ++r) {
+      const int ii = cell + 16 * r;
+      if (ii < samples) {
+        const double u = (ii + 0.5) * g.step - g.half;
+        const double cu = u * g.inv_cell + 1.5;
+        const int c0 = static_cast<int>(floor(cu));
+        const double fu = cu - c0;
+        S.wf[half][0][ii] = 1.0 - fu;
+        S.wf[half][1][ii] = fu;
+        (r ? c0hi : c0lo) = c0;
+      }
+    }
+    // first[v]: first index whose c0 >= v (c0 is monotone in the index).
+    // Cell c takes indices with c0 in {c - 1, c}: [first[c-1], first[c+1]),
+    // with weight f (d = 1) below first[c] and 1 - f (d = 0) from there.
+    int ia = 0, im = 0, ib = 0, ja = 0, jm = 0, jb = 0;
+#pragma unroll
+    for (int v = -1; v <= 4; ++v) {
+      const unsigned lo = __ballot_sync(0xffffffffu, c0lo != 0x7fff && c0lo >= v);
+      const unsigned hi = __ballot_sync(0xffffffffu, c0hi != 0x7fff && c0hi >= v);
+      const unsigned m = ((lo >> (16 * half)) & 0xffffu) | (((hi >> (16 * half)) & 0xffffu) << 16);
+      const int fv = m ? __ffs(m) - 1 : samples;
+      if (v == ccx - 1) ia = fv;
+      if (v == ccx) im = fv;
+      if (v == ccx + 1) ib = fv;
+      if (v == ccy - 1) ja = fv;
+      if (v == ccy) jm = fv;
+      if (v == ccy + 1) jb = fv;
+    }
+#pragma unroll
+    for (int b = 0; b < 8; ++b) S.acc[b][lane] = 0.0;
+    __syncwarp();
+    // Phase B (descriptor.cpp:98-116).
+    double tot[8];
+#pragma unroll
+    for (int b = 0; b < 8; ++b) tot[b] = 0.0;
+    {
+      const int spa = (samples + kSub - 1) / kSub;
+      const int n_sub = spa * spa;
+      auto bounds = [&](int s, int& ilo, int& ihi, int& jlo, int& jhi) {
+        const int sx = s % spa, sy = s / spa;
+        ilo = max(ia, sx * kSub);
+        ihi = min(ib, sx * kSub + kSub);
+        jlo = max(ja, sy * kSub);
+        jhi = min(jb, sy * kSub + kSub);
+      };
+      int T = 0;
+      for (int s = 0; s < n_sub; ++s) {
+        int ilo, ihi, jlo, jhi;
+        bounds(s, ilo, ihi, jlo, jhi);
+        if (ihi > ilo && jhi > jlo) T += (ihi - ilo) * (jhi - jlo);
+      }
+      const int Tmax = __reduce_max_sync(0xffffffffu, T);
+      int s = -1, ilo = 0, ihi = 0, jlo = 0, jhi = 0;
+      auto next_sub = [&]() {
+        do {
+          ++s;
+          if (s >= n_sub) return;
+          bounds(s, ilo, ihi, jlo, jhi);
+        } while (!(ihi > ilo && jhi > jlo));
+      };
+      next_sub();
+      int i = ilo, j = jlo, row = jlo * samples;
+      const double* wfh = &S.wf[half][0][0];
+      double wv = (T > 0) ? wfh[(j < jm ? kMaxSamples : 0) + j] : 0.0;
+      bool first = true;
+      double* accl = &S.acc[0][lane];
+      // One visit of look-ahead: the next sample's record is requested
+      // before the current one is accumulated.
+      double2 cur = T > 0 ? smp[row + i] : make_double2(0.0, 0.0);
+      int ci = i;
+      double cwv = wv;
+      for (int it = 0; it < Tmax; ++it) {
+        if (it < T) {
+          bool fold = false;
+          if (++i == ihi) {
+            i = ilo;
+            ++j;
+            row += samples;
+            if (j == jhi) {
+              fold = true;
+              next_sub();
+              i = ilo;
+              j = jlo;
+              row = jlo * samples;
+            }
+            if (j < samples) wv = wfh[(j < jm ? kMaxSamples : 0) + j];
+          }
+          const double2 nxt = it + 1 < T ? smp[row + i] : make_double2(0.0, 0.0);
+          // ob0 = floor(ob), fo = ob - ob0; bins ob0 and ob0 + 1 (mod 8) get
+          // weight * wv * wu * (1 - fo) and ... * fo (descriptor.cpp:93-113).
+          const double ob = cur.y;
+          const double obf = floor(ob);
+          const double fo = ob - obf;
+          const int b0 = static_cast<int>(obf) & 7, b1 = (b0 + 1) & 7;
+          const double base = cur.x * cwv * wfh[(ci < im ? kMaxSamples : 0) + ci];
+          const double add0 = base * (1.0 - fo);
+          const double add1 = base * fo;
+          accl[b0 * 32] += add0;
+          accl[b1 * 32] += add1;
+          if (fold) {
+            // This sub-patch's partial is complete: fold it in index order.
+#pragma unroll
+            for (int b = 0; b < 8; ++b) {
+              const double p = accl[b * 32];
+              tot[b] = first ? p : tot[b] + p;
+              accl[b * 32] = 0.0;
+            }
+            first = false;
+          }
+          cur = nxt;
+          ci = i;
+          cwv = wv;
+        }
+      }
     }
     __syncwarp();
-    double tot[4] = {0.0, 0.0, 0.0, 0.0};
-    for (int band = 0; band < spa; ++band) {
-      const int j0 = band * kBand, j1 = min(samples, j0 + kBand);
-      const int n = (j1 - j0) * samples;
-      // Phase A (descriptor.cpp:75-88).
-      for (int q = lane; q < n; q += 32) {
-        const int jr = q / samples, i = q - jr * samples;
-        const double v = S.u[j0 + jr];
-        const double u = S.u[i];
-        const double px = fr.x + u * cos_t - v * sin_t;
-        const double py = fr.y + u * sin_t + v * cos_t;
-        int bin0 = 0;
-        double wgt = 0.0, fo = 0.0;
-        if (!(px < 1.0 || px > fr.w - 2.0 || py < 1.0 || py > fr.h - 2.0)) {
-          const double gx = 0.5 * (sample_bilinear(fr.lvl, fr.w, px + 1.0, py) - sample_bilinear(fr.lvl, fr.w, px - 1.0, py));
-          const double gy = 0.5 * (sample_bilinear(fr.lvl, fr.w, px, py + 1.0) - sample_bilinear(fr.lvl, fr.w, px, py - 1.0));
-          const double mag = hypot(gx, gy);
-          if (mag != 0.0) {
-            wgt = mag * exp(-(u * u + v * v) / gauss_denom);
-            const double phi = wrap_angle(atan2(gy, gx) - theta);
-            const double obv = phi / kTwoPi * 8 - 0.5;
-            const int ob0 = static_cast<int>(floor(obv));
-            fo = obv - ob0;
-            bin0 = ((ob0 % 8) + 8) % 8;
-          }
-        }
-        S.w[q] = wgt;
-        S.fo[q] = fo;
-        S.bin[q] = uint8_t(bin0);
-      }
-      __syncwarp();
-      // Phase B (descriptor.cpp:98-116): partials of the band's left (i < 16)
-      // and right sub-patch, each in row-major sample order.
-      double pa[4] = {0.0, 0.0, 0.0, 0.0}, pb[4] = {0.0, 0.0, 0.0, 0.0};
-      const int jlo = max(ja, j0), jhi = min(jb, j1);
-      const int ia0 = ia, ib0 = min(ib, kBand), ia1 = max(ia, kBand), ib1 = ib;
-      for (int j = jlo; j < jhi; ++j) {
-        const double wv = S.wf[ccy - S.c0[j]][j];
-        const int row = (j - j0) * samples;
-#define CDVZ_VISIT(ACC)                                                   \
-  {                                                                       \
-    const int q = row + i;                                                \
-    const int b0 = S.bin[q];                                              \
-    const bool own = (b0 & 1) == parity;                                  \
-    const double fo = S.fo[q];                                            \
-    const double wo = own ? 1.0 - fo : fo;                                \
-    const int slot = (own ? b0 : (b0 + 1) & 7) >> 1;                      \
-    const double add = S.w[q] * wv * S.wf[ccx - S.c0[i]][i] * wo;         \
-    ACC[0] += slot == 0 ? add : 0.0;                                      \
-    ACC[1] += slot == 1 ? add : 0.0;                                      \
-    ACC[2] += slot == 2 ? add : 0.0;                                      \
-    ACC[3] += slot == 3 ? add : 0.0;                                      \
-  }
-        for (int i = ia0; i < ib0; ++i) CDVZ_VISIT(pa)
-        for (int i = ia1; i < ib1; ++i) CDVZ_VISIT(pb)
-#undef CDVZ_VISIT
-      }
-      // merge_and_normalize's ordered sum of partials (sub-patch index order).
-#pragma unroll
-      for (int m = 0; m < 4; ++m) {
-        tot[m] = band == 0 ? pa[m] : tot[m] + pa[m];
-        if (spa > 1) tot[m] = tot[m] + pb[m];
-      }
-      __syncwarp();
-    }
     // normalize_descriptor (descriptor.cpp:124-145): up to 5 rounds of L2
     // normalise + clamp at 0.2; the norm in the Eigen SSE2 reduction order
     // (four stride-4 running sums, then (s0 + s2) + (s1 + s3)).
-    double* sq = S.w;
-    double* tv = S.w + 128;
-    const int bin_base = cell * 8 + parity;
+    double* sq = S.buf[half];
+    double* tv = S.buf[half] + 128;
+    bool done = !live || samples == 0;
     for (int round = 0; round < 5; ++round) {
 #pragma unroll
-      for (int m = 0; m < 4; ++m) sq[bin_base + 2 * m] = tot[m] * tot[m];
+      for (int b = 0; b < 8; ++b) sq[cell * 8 + b] = tot[b] * tot[b];
       __syncwarp();
       double red = 0.0;
-      if (lane < 4) {
+      if (cell < 4) {
         double t[32];
 #pragma unroll
-        for (int i = 0; i < 32; ++i) t[i] = sq[lane + 4 * i];
+        for (int q = 0; q < 32; ++q) t[q] = sq[cell + 4 * q];
         red = t[0];
 #pragma unroll
-        for (int i = 1; i < 32; ++i) red = red + t[i];
+        for (int q = 1; q < 32; ++q) red = red + t[q];
       }
-      const double r0 = __shfl_sync(0xffffffffu, red, 0), r1 = __shfl_sync(0xffffffffu, red, 1);
-      const double r2 = __shfl_sync(0xffffffffu, red, 2), r3 = __shfl_sync(0xffffffffu, red, 3);
+      const int hb = 16 * half;
+      const double r0 = __shfl_sync(0xffffffffu, red, hb), r1 = __shfl_sync(0xffffffffu, red, hb + 1);
+      const double r2 = __shfl_sync(0xffffffffu, red, hb + 2), r3 = __shfl_sync(0xffffffffu, red, hb + 3);
       __syncwarp();
       const double norm = sqrt((r0 + r2) + (r1 + r3));
-      if (norm == 0.0) break;
       bool clipped = false;
+      if (!done) {
+        if (norm == 0.0) {
+          done = true;
+        } else {
 #pragma unroll
-      for (int m = 0; m < 4; ++m) {
-        tot[m] = tot[m] / norm;
-        if (tot[m] > 0.2) { tot[m] = 0.2; clipped = true; }
+          for (int b = 0; b < 8; ++b) {
+            tot[b] = tot[b] / norm;
+            if (tot[b] > 0.2) { tot[b] = 0.2; clipped = true; }
+          }
+        }
       }
-      if (!__any_sync(0xffffffffu, clipped)) break;
+      const unsigned cl = __ballot_sync(0xffffffffu, clipped);
+      if (!(cl & hmask)) done = true;
+      if (__all_sync(0xffffffffu, done)) break;
     }
-    double* dout = bt.desc + ((long long)f * bt.cap_or + idx) * 128;
+    if (live && samples > 0) {
+      double2* dout = reinterpret_cast<double2*>(bt.desc + ((long long)f * bt.cap_or + idx) * 128 + cell * 8);
 #pragma unroll
-    for (int m = 0; m < 4; ++m) dout[bin_base + 2 * m] = tot[m];
-    // transform_descriptor (transform_coding.cpp:81-91): the cell's 8 values
-    // are split between this lane and its parity partner.
-    {
-      double vec[8];
-#pragma unroll
-      for (int m = 0; m < 4; ++m) {
-        const double other = __shfl_xor_sync(0xffffffffu, tot[m], 1);
-        vec[2 * m] = parity ? other : tot[m];
-        vec[2 * m + 1] = parity ? tot[m] : other;
-      }
+      for (int b = 0; b < 4; ++b) dout[b] = make_double2(tot[2 * b], tot[2 * b + 1]);
+      // transform_descriptor (transform_coding.cpp:81-91) of this lane's cell.
       const int which = ((ccx + ccy) & 1) == 0 ? 0 : 1;
 #pragma unroll
-      for (int m = 0; m < 4; ++m) {
-        const int i = parity + 2 * m;
-        double s = md.tr[which][i][0] * vec[0];
+      for (int i = 0; i < 8; ++i) {
+        double s = md.tr[which][i][0] * tot[0];
 #pragma unroll
-        for (int kk = 1; kk < 8; ++kk) s = s + md.tr[which][i][kk] * vec[kk];
+        for (int kk = 1; kk < 8; ++kk) s = s + md.tr[which][i][kk] * tot[kk];
         tv[cell * 8 + i] = md.tr_scale * s;
       }
     }
     __syncwarp();
-    // quantize_ternary (transform_coding.cpp:202-217): 00 zero, 01 +1, 10 -1;
-    // lane L packs symbols 4L .. 4L+3 into code byte L.
-    uint8_t* code = bt.codes + ((long long)f * bt.cap_or + idx) * bt.code_stride;
-    if (4 * lane < ec.elements) {
-      uint8_t byte = 0;
+    if (live && samples > 0) {
+      // quantize_ternary (transform_coding.cpp:202-217): 00 zero, 01 +1,
+      // 10 -1; lane c packs symbols 8c .. 8c+7 into code bytes 2c, 2c + 1.
+      uint8_t* code = bt.codes + ((long long)f * bt.cap_or + idx) * bt.code_stride;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int t = 4 * lane + q;
-        if (t < ec.elements) {
-          const int e = md.priority[t];
-          const double val = tv[e];
-          const uint8_t sym = val < md.t0[e] ? 2 : (val > md.t1[e] ? 1 : 0);
-          byte |= uint8_t(sym << (2 * q));
+      for (int hb = 0; hb < 2; ++hb) {
+        const int t0 = 8 * cell + 4 * hb;
+        if (t0 < ec.elements) {
+          uint8_t byte = 0;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int t = t0 + q;
+            if (t < ec.elements) {
+              const int e = md.priority[t];
+              const double val = tv[e];
+              const uint8_t sym = val < md.t0[e] ? 2 : (val > md.t1[e] ? 1 : 0);
+              byte |= uint8_t(sym << (2 * q));
+            }
+          }
+          code[6 + 2 * cell + hb] = byte;
         }
       }
-      code[6 + lane] = byte;
-    }
-    if (lane == 0) {
-      // quantize_coord / quantize_sigma_log / quantize_theta (transform_coding.cpp:173-200)
-      const double cxq = fmin(fmax(k.x, 0.0), double(bt.W - 1));
-      const double cyq = fmin(fmax(k.y, 0.0), double(bt.H - 1));
-      const unsigned xq = (unsigned)llround(cxq / (bt.W - 1) * 65535.0);
-      const unsigned yq = (unsigned)llround(cyq / (bt.H - 1) * 65535.0);
-      const double sc = fmin(fmax(k.sigma, 0.5), 64.0);
-      const double tq = log2(sc / 0.5) / ec.log2_range;
-      const unsigned sq8 = (unsigned)llround(tq * 255.0);
-      double tt = theta / kTwoPi;
-      tt -= floor(tt);
-      const unsigned th8 = (unsigned)(llround(tt * 256.0) & 0xFF);
-      code[0] = uint8_t(xq & 0xFF);
-      code[1] = uint8_t(xq >> 8);
-      code[2] = uint8_t(yq & 0xFF);
-      code[3] = uint8_t(yq >> 8);
-      code[4] = uint8_t(sq8);
-      code[5] = uint8_t(th8);
+      if (cell == 0) {
+        // quantize_coord / quantize_sigma_log / quantize_theta (transform_coding.cpp:173-200)
+        const Oriented orp = bt.oriented[gslot];
+        const KP k = bt.sel[(long long)f * bt.select_n + orp.sel];
+        const double cxq = fmin(fmax(k.x, 0.0), double(bt.W - 1));
+        const double cyq = fmin(fmax(k.y, 0.0), double(bt.H - 1));
+        const unsigned xq = (unsigned)llround(cxq / (bt.W - 1) * 65535.0);
+        const unsigned yq = (unsigned)llround(cyq / (bt.H - 1) * 65535.0);
+        const double sc = fmin(fmax(k.sigma, 0.5), 64.0);
+        const double tq = log2(sc / 0.5) / ec.log2_range;
+        const unsigned sq8 = (unsigned)llround(tq * 255.0);
+        double tt = orp.theta / kTwoPi;
+        tt -= floor(tt);
+        const unsigned th8 = (unsigned)(llround(tt * 256.0) & 0xFF);
+        code[0] = uint8_t(xq & 0xFF);
+        code[1] = uint8_t(xq >> 8);
+        code[2] = uint8_t(yq & 0xFF);
+        code[3] = uint8_t(yq >> 8);
+        code[4] = uint8_t(sq8);
+        code[5] = uint8_t(th8);
+      }
     }
     __syncwarp();
   }
@@ -470,6 +569,12 @@ cudaError_t launch_describe(const Batch& bt, const DetConst& dc, const Model& md
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   k_expand<<<bt.nframes, 1024, 0, st>>>(bt);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  k_geometry<<<dim3((bt.cap_or + 127) / 128, bt.nframes), 128, 0, st>>>(bt, dc);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  k_sample<<<dim3(64, bt.nframes), 256, 0, st>>>(bt);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   k_describe<<<dim3(32, bt.nframes), 32 * kDescWarps, 0, st>>>(bt, dc, md, ec);
