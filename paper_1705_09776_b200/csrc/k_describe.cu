@@ -247,7 +247,6 @@ __global__ void __launch_bounds__(1024) k_expand(Batch bt) {
 //               the 128 bins for normalisation, transform and ternary coding.
 constexpr int kMaxSamples = 32;  // samples per axis: ceil(12 sigma) for sigma <= 2.66 (radius-8 detector)
 constexpr int kSub = 16;         // kSubPatchSide (descriptor.cpp)
-constexpr int kDescWarps = 4;
 
 __global__ void __launch_bounds__(128) k_geometry(Batch bt, DetConst dc) {
   const int f = blockIdx.y;
@@ -309,180 +308,165 @@ __global__ void __launch_bounds__(256) k_sample(Batch bt) {
   }
 }
 
-// Phase B + epilogue: TWO oriented points per warp, lane = (half, cell).
-// Lane (h, c) owns all 8 orientation bins of cell c of point h, kept in
-// shared memory as acc[bin][lane] (one sequential chain per bin, exactly the
-// reference's per-bin add order), so each sample costs one visit per cell
-// and two ordered adds (bins ob0 and ob0 + 1).
-struct DescWarpSmem {
-  double wf[2][2][kMaxSamples];  // [half][d][i]: 1 - f, f of the cell coordinate
-  double acc[8][32];             // [bin][lane]: current sub-patch partial
-  double buf[2][256];            // [half]: sq (0..127), tv (128..255)
+// Phase B + epilogue: TWO oriented points per warp, row-synchronous.
+// Lane (q, cx, dv, p) of point q walks every sample row j in order; in row j
+// it visits, in increasing i, the samples whose cell column is cx (c0[i] in
+// {cx - 1, cx}) and adds the contribution of whichever of the sample's two
+// orientation bins (ob0, ob0 + 1 mod 8) has parity p to cell (cx, c0[j] + dv).
+// Accumulators live in shared memory indexed by (set, cell, bin): at any
+// moment each (cell, bin) has exactly one owning lane, and a cell's chains
+// pass from lane dv = 1 to lane dv = 0 when the rows cross a cell boundary
+// with no exchange, so every bin is one sequential chain in the reference's
+// sample order (descriptor.cpp:98-116). Sets: the left (i < 16) and right
+// (i >= 16) sub-patch partials of the current 16-row band; the folded total
+// ((P0 + P1) + P2) + P3 of merge_and_normalize lives in registers.
+// Rows of (weight, ob) records stream into a 3-row shared ring with
+// cp.async, two rows ahead of the walk.
+constexpr int kPBWarps = 4;
+struct PhaseBSmem {
+  double2 ring[3][2][kMaxSamples];  // [slot][q][i]
+  double acc[2][2][128];            // [q][set: 0 left, 1 right][cell * 8 + bin]
+  double wf[2][2][kMaxSamples];     // [q][d][i]: 1 - f, f of the cell coordinate
+  int c0[2][kMaxSamples];           // [q][i]: floor(u * inv_cell + 1.5)
 };
 
-__global__ void __launch_bounds__(32 * kDescWarps) k_describe(Batch bt, DetConst dc, Model md, EncodeConst ec) {
-  __shared__ DescWarpSmem smem[kDescWarps];
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(uint32_t(__cvta_generic_to_shared(smem))), "l"(gmem)
+               : "memory");
+}
+
+__global__ void __launch_bounds__(32 * kPBWarps) k_describe(Batch bt, DetConst dc, Model md, EncodeConst ec) {
+  extern __shared__ __align__(16) uint8_t pb_smem[];
   const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  DescWarpSmem& S = smem[wi];
+  PhaseBSmem& S = reinterpret_cast<PhaseBSmem*>(pb_smem)[wi];
   const int f = blockIdx.y;
   const int n_or = bt.or_count[f];
-  const int half = lane >> 4, cell = lane & 15;
-  const int ccx = cell & 3, ccy = cell >> 2;
-  const unsigned hmask = 0xffffu << (16 * half);
-  for (int pair = blockIdx.x * kDescWarps + wi; 2 * pair < n_or; pair += gridDim.x * kDescWarps) {
-    const int idx = 2 * pair + half;
+  const int q = lane >> 4, hl = lane & 15;
+  const int cx = hl & 3, dv = (hl >> 2) & 1, par = hl >> 3;
+  const unsigned gmask = 0xffffu << (16 * q);
+  for (int pair = blockIdx.x * kPBWarps + wi; 2 * pair < n_or; pair += gridDim.x * kPBWarps) {
+    const int idx = 2 * pair + q;
     const bool live = idx < n_or;
     const long long gslot = (long long)f * bt.cap_or + (live ? idx : 0);
     const DescGeo g = bt.geo[gslot];
     const int samples = live ? g.samples : 0;  // 0: no point, or flagged by k_geometry
     const double2* smp = bt.smp + gslot * bt.smp_cap;
-    // Pull the point's sample records into L1 up front (one request per
-    // 128-byte line, all in flight together) so the walk below hits L1.
-    for (int l = cell * 8; l < samples * samples; l += 16 * 8)
-      asm volatile("prefetch.global.L1 [%0];" ::"l"(smp + l));
-    // Per-axis cell coordinates (descriptor.cpp:89-96): identical for u (i)
-    // and v (j). Lane c of the half computes indices c and c + 16.
-    int c0lo = 0x7fff, c0hi = 0x7fff;
-#pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      const int ii = cell + 16 * r;
-      if (ii < samples) {
-        const double u = (ii + 0.5) * g.step - g.half;
-        const double cu = u * g.inv_cell + 1.5;
-        const int c0 = static_cast<int>(floor(cu));
-        const double fu = cu - c0;
-        S.wf[half][0][ii] = 1.0 - fu;
-        S.wf[half][1][ii] = fu;
-        (r ? c0hi : c0lo) = c0;
+    auto fetch_row = [&](int j) {
+      if (j < samples) {
+        double2* dst = S.ring[j % 3][q];
+        const double2* src = smp + (long long)j * samples;
+        for (int i = hl; i < samples; i += 16) cp_async16(dst + i, src + i);
       }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    fetch_row(0);
+    fetch_row(1);
+    // Per-axis cell coordinates (descriptor.cpp:89-96): identical for u (i) and v (j).
+    for (int i = hl; i < samples; i += 16) {
+      const double u = (i + 0.5) * g.step - g.half;
+      const double cu = u * g.inv_cell + 1.5;
+      const int c0 = static_cast<int>(floor(cu));
+      const double fu = cu - c0;
+      S.c0[q][i] = c0;
+      S.wf[q][0][i] = 1.0 - fu;
+      S.wf[q][1][i] = fu;
     }
-    // first[v]: first index whose c0 >= v (c0 is monotone in the index).
-    // Cell c takes indices with c0 in {c - 1, c}: [first[c-1], first[c+1]),
-    // with weight f (d = 1) below first[c] and 1 - f (d = 0) from there.
-    int ia = 0, im = 0, ib = 0, ja = 0, jm = 0, jb = 0;
-#pragma unroll
-    for (int v = -1; v <= 4; ++v) {
-      const unsigned lo = __ballot_sync(0xffffffffu, c0lo != 0x7fff && c0lo >= v);
-      const unsigned hi = __ballot_sync(0xffffffffu, c0hi != 0x7fff && c0hi >= v);
-      const unsigned m = ((lo >> (16 * half)) & 0xffffu) | (((hi >> (16 * half)) & 0xffffu) << 16);
-      const int fv = m ? __ffs(m) - 1 : samples;
-      if (v == ccx - 1) ia = fv;
-      if (v == ccx) im = fv;
-      if (v == ccx + 1) ib = fv;
-      if (v == ccy - 1) ja = fv;
-      if (v == ccy) jm = fv;
-      if (v == ccy + 1) jb = fv;
-    }
-#pragma unroll
-    for (int b = 0; b < 8; ++b) S.acc[b][lane] = 0.0;
+    double* acc = S.acc[q][0];  // left set; the right set follows at +128
+    for (int e = hl; e < 256; e += 16) acc[e] = 0.0;
     __syncwarp();
-    // Phase B (descriptor.cpp:98-116).
-    double tot[8];
+    // Column range of cx: c0 in {cx - 1, cx}; weight f (d = 1) below im.
+    int ia = 0, im = 0, ib = 0;
+    for (int i = 0; i < samples; ++i) {
+      const int c = S.c0[q][i];
+      ia += c < cx - 1;
+      im += c < cx;
+      ib += c < cx + 1;
+    }
+    const int rows = __reduce_max_sync(0xffffffffu, samples);
+    double tot[8];  // lane hl's fold of cell hl (bins 8 hl .. 8 hl + 7)
 #pragma unroll
-    for (int b = 0; b < 8; ++b) tot[b] = 0.0;
-    {
-      const int spa = (samples + kSub - 1) / kSub;
-      const int n_sub = spa * spa;
-      auto bounds = [&](int s, int& ilo, int& ihi, int& jlo, int& jhi) {
-        const int sx = s % spa, sy = s / spa;
-        ilo = max(ia, sx * kSub);
-        ihi = min(ib, sx * kSub + kSub);
-        jlo = max(ja, sy * kSub);
-        jhi = min(jb, sy * kSub + kSub);
-      };
-      int T = 0;
-      for (int s = 0; s < n_sub; ++s) {
-        int ilo, ihi, jlo, jhi;
-        bounds(s, ilo, ihi, jlo, jhi);
-        if (ihi > ilo && jhi > jlo) T += (ihi - ilo) * (jhi - jlo);
-      }
-      const int Tmax = __reduce_max_sync(0xffffffffu, T);
-      int s = -1, ilo = 0, ihi = 0, jlo = 0, jhi = 0;
-      auto next_sub = [&]() {
-        do {
-          ++s;
-          if (s >= n_sub) return;
-          bounds(s, ilo, ihi, jlo, jhi);
-        } while (!(ihi > ilo && jhi > jlo));
-      };
-      next_sub();
-      int i = ilo, j = jlo, row = jlo * samples;
-      const double* wfh = &S.wf[half][0][0];
-      double wv = (T > 0) ? wfh[(j < jm ? kMaxSamples : 0) + j] : 0.0;
-      bool first = true;
-      double* accl = &S.acc[0][lane];
-      // One visit of look-ahead: the next sample's record is requested
-      // before the current one is accumulated.
-      double2 cur = T > 0 ? smp[row + i] : make_double2(0.0, 0.0);
-      int ci = i;
-      double cwv = wv;
-      for (int it = 0; it < Tmax; ++it) {
-        if (it < T) {
-          bool fold = false;
-          if (++i == ihi) {
-            i = ilo;
-            ++j;
-            row += samples;
-            if (j == jhi) {
-              fold = true;
-              next_sub();
-              i = ilo;
-              j = jlo;
-              row = jlo * samples;
-            }
-            if (j < samples) wv = wfh[(j < jm ? kMaxSamples : 0) + j];
-          }
-          const double2 nxt = it + 1 < T ? smp[row + i] : make_double2(0.0, 0.0);
-          // ob0 = floor(ob), fo = ob - ob0; bins ob0 and ob0 + 1 (mod 8) get
-          // weight * wv * wu * (1 - fo) and ... * fo (descriptor.cpp:93-113).
-          const double ob = cur.y;
-          const double obf = floor(ob);
-          const double fo = ob - obf;
-          const int b0 = static_cast<int>(obf) & 7, b1 = (b0 + 1) & 7;
-          const double base = cur.x * cwv * wfh[(ci < im ? kMaxSamples : 0) + ci];
-          const double add0 = base * (1.0 - fo);
-          const double add1 = base * fo;
-          accl[b0 * 32] += add0;
-          accl[b1 * 32] += add1;
-          if (fold) {
-            // This sub-patch's partial is complete: fold it in index order.
+    for (int k = 0; k < 8; ++k) tot[k] = 0.0;
+    for (int j = 0; j < rows; ++j) {
+      fetch_row(j + 2);
+      asm volatile("cp.async.wait_group 2;" ::: "memory");
+      __syncwarp();
+      if (j == kSub && samples > kSub) {
+        // Band boundary: the first two sub-patch partials are complete.
 #pragma unroll
-            for (int b = 0; b < 8; ++b) {
-              const double p = accl[b * 32];
-              tot[b] = first ? p : tot[b] + p;
-              accl[b * 32] = 0.0;
-            }
-            first = false;
-          }
-          cur = nxt;
-          ci = i;
-          cwv = wv;
+        for (int k = 0; k < 8; ++k) {
+          tot[k] = acc[8 * hl + k] + acc[128 + 8 * hl + k];
+          acc[8 * hl + k] = 0.0;
+          acc[128 + 8 * hl + k] = 0.0;
         }
       }
+      __syncwarp();
+      if (j < samples) {
+        const int cy = S.c0[q][j] + dv;
+        if (cy >= 0 && cy < 4) {
+          const double wv = S.wf[q][dv][j];
+          const double2* rowp = S.ring[j % 3][q];
+          const double* wfq = &S.wf[q][0][0];
+          const int cell8 = (cy * 4 + cx) * 8;
+          // Two-stage software pipeline: visit i + 1 is decoded while visit
+          // i's bin chain is updated, so a visit's critical path is one
+          // shared load -> add -> store.
+          auto decode = [&](int i, int& o, double& x) {
+            const double2 rec = rowp[i];
+            const double wu = wfq[(i < im ? kMaxSamples : 0) + i];
+            // ob0 = floor(ob), fo = ob - ob0 (descriptor.cpp:93-99); of the
+            // bins ob0 (weight 1 - fo) and ob0 + 1 (weight fo) take the one
+            // of parity p.
+            const double obf = floor(rec.y);
+            const double fo = rec.y - obf;
+            const int b0 = static_cast<int>(obf) & 7;
+            const bool own = (b0 & 1) == par;
+            const double base = rec.x * wv * wu;
+            o = cell8 + (i < kSub ? 0 : 128) + (own ? b0 : (b0 + 1) & 7);
+            x = base * (own ? 1.0 - fo : fo);
+          };
+          int o = 0;
+          double x = 0.0;
+          if (ia < ib) decode(ia, o, x);
+          for (int i = ia; i < ib; ++i) {
+            int no = o;
+            double nx = 0.0;
+            if (i + 1 < ib) decode(i + 1, no, nx);
+            acc[o] = acc[o] + x;
+            o = no;
+            x = nx;
+          }
+        }
+      }
+      __syncwarp();
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int e = 8 * hl + k;
+      tot[k] = samples > kSub ? (tot[k] + acc[e]) + acc[128 + e] : acc[e];
     }
     __syncwarp();
     // normalize_descriptor (descriptor.cpp:124-145): up to 5 rounds of L2
     // normalise + clamp at 0.2; the norm in the Eigen SSE2 reduction order
     // (four stride-4 running sums, then (s0 + s2) + (s1 + s3)).
-    double* sq = S.buf[half];
-    double* tv = S.buf[half] + 128;
-    bool done = !live || samples == 0;
+    double* sq = acc;
+    double* tv = acc + 128;
+    bool done = samples == 0;
     for (int round = 0; round < 5; ++round) {
 #pragma unroll
-      for (int b = 0; b < 8; ++b) sq[cell * 8 + b] = tot[b] * tot[b];
+      for (int k = 0; k < 8; ++k) sq[8 * hl + k] = tot[k] * tot[k];
       __syncwarp();
       double red = 0.0;
-      if (cell < 4) {
+      if (hl < 4) {
         double t[32];
 #pragma unroll
-        for (int q = 0; q < 32; ++q) t[q] = sq[cell + 4 * q];
+        for (int k = 0; k < 32; ++k) t[k] = sq[hl + 4 * k];
         red = t[0];
 #pragma unroll
-        for (int q = 1; q < 32; ++q) red = red + t[q];
+        for (int k = 1; k < 32; ++k) red = red + t[k];
       }
-      const int hb = 16 * half;
-      const double r0 = __shfl_sync(0xffffffffu, red, hb), r1 = __shfl_sync(0xffffffffu, red, hb + 1);
-      const double r2 = __shfl_sync(0xffffffffu, red, hb + 2), r3 = __shfl_sync(0xffffffffu, red, hb + 3);
+      const int gb = 16 * q;
+      const double r0 = __shfl_sync(0xffffffffu, red, gb), r1 = __shfl_sync(0xffffffffu, red, gb + 1);
+      const double r2 = __shfl_sync(0xffffffffu, red, gb + 2), r3 = __shfl_sync(0xffffffffu, red, gb + 3);
       __syncwarp();
       const double norm = sqrt((r0 + r2) + (r1 + r3));
       bool clipped = false;
@@ -491,54 +475,53 @@ __global__ void __launch_bounds__(32 * kDescWarps) k_describe(Batch bt, DetConst
           done = true;
         } else {
 #pragma unroll
-          for (int b = 0; b < 8; ++b) {
-            tot[b] = tot[b] / norm;
-            if (tot[b] > 0.2) { tot[b] = 0.2; clipped = true; }
+          for (int k = 0; k < 8; ++k) {
+            tot[k] = tot[k] / norm;
+            if (tot[k] > 0.2) { tot[k] = 0.2; clipped = true; }
           }
         }
       }
-      const unsigned cl = __ballot_sync(0xffffffffu, clipped);
-      if (!(cl & hmask)) done = true;
+      if (!(__ballot_sync(0xffffffffu, clipped) & gmask)) done = true;
       if (__all_sync(0xffffffffu, done)) break;
     }
-    if (live && samples > 0) {
-      double2* dout = reinterpret_cast<double2*>(bt.desc + ((long long)f * bt.cap_or + idx) * 128 + cell * 8);
+    if (samples > 0) {
+      double2* dout = reinterpret_cast<double2*>(bt.desc + ((long long)f * bt.cap_or + idx) * 128 + 8 * hl);
 #pragma unroll
-      for (int b = 0; b < 4; ++b) dout[b] = make_double2(tot[2 * b], tot[2 * b + 1]);
-      // transform_descriptor (transform_coding.cpp:81-91) of this lane's cell.
-      const int which = ((ccx + ccy) & 1) == 0 ? 0 : 1;
+      for (int k = 0; k < 4; ++k) dout[k] = make_double2(tot[2 * k], tot[2 * k + 1]);
+      // transform_descriptor (transform_coding.cpp:81-91) of cell hl.
+      const int which = (((hl & 3) + (hl >> 2)) & 1) == 0 ? 0 : 1;
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         double s = md.tr[which][i][0] * tot[0];
 #pragma unroll
         for (int kk = 1; kk < 8; ++kk) s = s + md.tr[which][i][kk] * tot[kk];
-        tv[cell * 8 + i] = md.tr_scale * s;
+        tv[hl * 8 + i] = md.tr_scale * s;
       }
     }
     __syncwarp();
-    if (live && samples > 0) {
+    if (samples > 0) {
       // quantize_ternary (transform_coding.cpp:202-217): 00 zero, 01 +1,
-      // 10 -1; lane c packs symbols 8c .. 8c+7 into code bytes 2c, 2c + 1.
+      // 10 -1; lane hl packs symbols 8 hl .. 8 hl + 7 into code bytes 2 hl, 2 hl + 1.
       uint8_t* code = bt.codes + ((long long)f * bt.cap_or + idx) * bt.code_stride;
 #pragma unroll
-      for (int hb = 0; hb < 2; ++hb) {
-        const int t0 = 8 * cell + 4 * hb;
+      for (int by = 0; by < 2; ++by) {
+        const int t0 = 8 * hl + 4 * by;
         if (t0 < ec.elements) {
           uint8_t byte = 0;
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const int t = t0 + q;
+          for (int k = 0; k < 4; ++k) {
+            const int t = t0 + k;
             if (t < ec.elements) {
               const int e = md.priority[t];
               const double val = tv[e];
               const uint8_t sym = val < md.t0[e] ? 2 : (val > md.t1[e] ? 1 : 0);
-              byte |= uint8_t(sym << (2 * q));
+              byte |= uint8_t(sym << (2 * k));
             }
           }
-          code[6 + 2 * cell + hb] = byte;
+          code[6 + 2 * hl + by] = byte;
         }
       }
-      if (cell == 0) {
+      if (hl == 0) {
         // quantize_coord / quantize_sigma_log / quantize_theta (transform_coding.cpp:173-200)
         const Oriented orp = bt.oriented[gslot];
         const KP k = bt.sel[(long long)f * bt.select_n + orp.sel];
@@ -577,7 +560,14 @@ cudaError_t launch_describe(const Batch& bt, const DetConst& dc, const Model& md
   k_sample<<<dim3(64, bt.nframes), 256, 0, st>>>(bt);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  k_describe<<<dim3(32, bt.nframes), 32 * kDescWarps, 0, st>>>(bt, dc, md, ec);
+  static bool configured = false;
+  constexpr int smem = int(sizeof(PhaseBSmem)) * kPBWarps;
+  if (!configured) {
+    e = cudaFuncSetAttribute(k_describe, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  k_describe<<<dim3(24, bt.nframes), 32 * kPBWarps, smem, st>>>(bt, dc, md, ec);
   return cudaGetLastError();
 }
 

@@ -160,21 +160,35 @@ __device__ __forceinline__ void exact_detect(const Batch& bt, const DetConst& dc
   }
 }
 
-// Conservative FP32 screen (runs on the FP32 pipe, beside the FP64 work): a
-// pixel is dropped only when no root of the derivative can lie in
-// [s_lo, s_hi] or no in-range root can reach |p| >= thr, with margins orders
-// of magnitude above the float error. Everything else gets the exact test.
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float rsqrt_approx(float x) {
+  float r;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+// Conservative FP32 screen (FP32 pipe + MUFU, beside the FP64 work): a pixel
+// is dropped only when the discriminant is negative (the reference's own
+// exact test, in FP64), or no float root lies within [s_lo - 0.05, s_hi + 0.05],
+// or no in-range root can reach |p| >= thr with a margin of 1e-5 of the
+// coefficient magnitudes — orders of magnitude above FP32 rounding of the
+// reference's own formulas. Near-double roots and degenerate cases go to the
+// exact path.
 __device__ __forceinline__ bool screen_pixel(const double a[4], const DetConst& dc) {
   const double qa = 3.0 * a[3], qb = 2.0 * a[2], qc = a[1];
   if (qa == 0.0) return true;
   const double disc = qb * qb - 4.0 * qa * qc;
   if (disc < 0.0) return false;  // exactly the reference's test: no real root
   if (!(disc > 1e-6 * (qb * qb))) return true;  // near-double root: let the exact path decide
-  const float fa = float(qa), fb = float(qb), fc = float(qc);
-  const float sq = sqrtf(float(disc));
+  const float fa = float(qa), fb = float(qb), fc = float(qc), fd = float(disc);
+  const float sq = fd * rsqrt_approx(fd);
   const float q = -0.5f * (fb + copysignf(sq, fb));
   if (!(fabsf(q) > 1e-30f)) return true;
-  const float r0 = q / fa, r1 = fc / q;
+  const float r0 = q * rcp_approx(fa), r1 = fc * rcp_approx(q);
   const float lo = float(dc.s_lo) - 0.05f, hi = float(dc.s_hi) + 0.05f;
   const float a0 = float(a[0]), a1 = float(a[1]), a2 = float(a[2]), a3 = float(a[3]);
   const float thr = float(dc.thr);
