@@ -44,6 +44,7 @@ struct DetConst {
   double thr, rho_limit, s_lo, s_hi;
   int margin;
   int screen;          // 1: FP32 pre-screen before the exact test; 0: exact test on every pixel
+  int walk;            // 1: warp column-walk extrema kernel; 0: TMA tile kernel
 };
 
 // Per-batch geometry and buffer map (device pointers). One instance lives in

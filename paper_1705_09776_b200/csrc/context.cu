@@ -222,6 +222,7 @@ struct cdvz_gpu_ctx {
     dc.s_hi = b.sigmas[3];
     dc.margin = b.margin;
     dc.screen = 1;
+    dc.walk = 1;
 
     for (int c = 0; c < 5; ++c) {
       md.rel_edges[c] = upload(b.relevance[std::size_t(c)].edges.data(), b.relevance[std::size_t(c)].edges.size());
@@ -629,6 +630,7 @@ int cdvz_gpu_set_debug(cdvz_gpu_ctx* ctx, int on) {
   ctx->debug = (on & 1) != 0;
   ctx->dc.screen = (on & 2) ? 0 : 1;
   ctx->serial = (on & 4) != 0;
+  ctx->dc.walk = (on & 16) ? 0 : 1;
   if (ctx->tma_disabled != ((on & 8) != 0)) {
     ctx->tma_disabled = (on & 8) != 0;
     for (auto& l : ctx->lanes) l.geo_w = 0;  // rebuild the tensor maps

@@ -222,40 +222,55 @@ template <int R, int SRC>
 __device__ __forceinline__ void blur_level(const Batch& bt, const double* __restrict__ taps, int f, int o, int lvl,
                                            double* brow /* [2][RS][NB] */) {
   constexpr int RS = kBlurRows, NB = kBlurCols + 2 * R, D = 2 * R + RS;
-  constexpr int PER = (RS * NB + kBlurCols - 1) / kBlurCols;  // staged elements per thread
   const int w = bt.ow[o], h = bt.oh[o];
   const int c = threadIdx.x;
   const int x0 = blockIdx.x * kBlurCols;
   const int cx = x0 + c;
   const bool store = cx < w;
   double* G = bt.pyr + f * bt.frame_doubles + bt.plane_off[o][lvl];
-  // Column mirror map for this thread's staging slots (fixed for the whole walk).
-  int scol[PER], srow[PER];
-#pragma unroll
-  for (int k = 0; k < PER; ++k) {
-    const int q = c + k * kBlurCols;
-    srow[k] = q / NB;
-    scol[k] = q < RS * NB ? mirror_near(x0 - R + (q - srow[k] * NB), w) : 0;
+  // Staging: thread c owns staged column c (x0 - R + c) and, for c < 2R, the
+  // halo column c + kBlurCols, in every staged row; columns are mirrored once
+  // here, rows once per step.
+  const bool halo = c < 2 * R;
+  const int sc0 = mirror_near(x0 - R + c, w), sc1 = halo ? mirror_near(x0 - R + c + kBlurCols, w) : 0;
+  using Raw = typename RawT<SRC>::type;
+  const Raw* src;
+  long long rstride;
+  int cmul;
+  if constexpr (SRC == 0) {
+    src = bt.pix8 + f * bt.frame_bytes8;
+    rstride = bt.stride8;
+    cmul = 1;
+  } else if constexpr (SRC == 1) {
+    src = bt.pixf + (long long)f * bt.W * bt.H;
+    rstride = bt.W;
+    cmul = 1;
+  } else {  // downsample_half(G3 of octave o-1): image.cpp:147-155
+    src = bt.pyr + f * bt.frame_doubles + bt.plane_off[o - 1][3];
+    rstride = 2LL * bt.ow[o - 1];
+    cmul = 2;
   }
+  const long long o0 = (long long)sc0 * cmul, o1 = (long long)sc1 * cmul;
   double t[R + 1];  // symmetric taps: t[|j|] = taps[R + |j|]
 #pragma unroll
   for (int j = 0; j <= R; ++j) t[j] = taps[R + j];
   double ring[D];
 #pragma unroll
   for (int i = 0; i < D; ++i) ring[i] = 0.0;
-  typename RawT<SRC>::type pre[PER];  // raw values in flight; converted when parked
+  Raw pre0[RS], pre1[RS];  // raw values in flight; converted when parked
   auto fetch = [&](int v0) {
 #pragma unroll
-    for (int k = 0; k < PER; ++k) {
-      const int q = c + k * kBlurCols;
-      if (q < RS * NB) pre[k] = load_raw<SRC>(bt, f, o, mirror_near(v0 + srow[k], h), scol[k]);
+    for (int i = 0; i < RS; ++i) {
+      const Raw* row = src + (long long)mirror_near(v0 + i, h) * rstride;
+      pre0[i] = row[o0];
+      if (halo) pre1[i] = row[o1];
     }
   };
   auto park = [&](double* dst) {
 #pragma unroll
-    for (int k = 0; k < PER; ++k) {
-      const int q = c + k * kBlurCols;
-      if (q < RS * NB) dst[q] = to_base<SRC>(pre[k]);
+    for (int i = 0; i < RS; ++i) {
+      dst[i * NB + c] = to_base<SRC>(pre0[i]);
+      if (halo) dst[i * NB + c + kBlurCols] = to_base<SRC>(pre1[i]);
     }
   };
   int buf = 0;
@@ -432,6 +447,133 @@ __global__ void __launch_bounds__(kDetThreads, 2)
   }
 }
 
+// ------------------------------------------------------- K1b v2: extrema walk
+// One WARP = a strip of 30 detection-window columns (lanes 1..30; lanes 0 and
+// 31 are the 1-column halo) walking a segment of kSegRows window rows top to
+// bottom. Per row the warp reads the four G levels of the next row once
+// (coalesced; the edge lanes also read their outer neighbour), slides the
+// Laplacian's up/centre/down rows in registers, takes left/right from a
+// per-warp row buffer, forms sigma^2 L and alpha = beta * L (the reference's
+// order) and parks alpha in a per-warp ring of kRing rows in shared memory.
+// Each window pixel is screened (FP32) as soon as its alpha exists; plausible
+// pixels are queued and the queue is drained in full-warp passes by the exact
+// FP64 test (exact_detect, reading the 3x3 alpha neighbourhood from the ring)
+// before the ring can overwrite any row a queued pixel needs.
+constexpr int kStripCols = 30, kSegRows = 64, kRing = 8, kDetWarps = 2;
+struct DetWarpSmem {
+  double ring[kRing][4][32];  // alpha rows: [row % kRing][coefficient][lane]
+  double row[4][34];          // centre G row per level: [k][1 + lane], edges at 0 and 33
+  uint16_t queue[64];         // ((row - y0 + 1) << 5) | lane
+};
+
+__global__ void __launch_bounds__(32 * kDetWarps) k_detect_walk(Batch bt, DetConst dc, int o) {
+  __shared__ DetWarpSmem smem[kDetWarps];
+  const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  DetWarpSmem& S = smem[wi];
+  const int f = blockIdx.z;
+  const int w = bt.ow[o], h = bt.oh[o], m = dc.margin;
+  const int xs0 = m + (blockIdx.x * kDetWarps + wi) * kStripCols;  // first window column of the strip
+  const int y0 = m + blockIdx.y * kSegRows, y1 = min(h - m, y0 + kSegRows);
+  if (xs0 >= w - m || y0 >= y1) return;  // warp-uniform
+  const int x = xs0 - 1 + lane;
+  const bool out_col = lane >= 1 && lane <= kStripCols && x < w - m;
+  const int xc = min(x, w - 1);
+  const bool edge = lane == 0 || lane == 31;
+  const int xe = lane == 0 ? x - 1 : min(x + 1, w - 1);  // edge lanes' outer neighbour
+  const int eslot = lane == 0 ? 0 : 33;
+  // Per-level column pointers, advanced one row per step.
+  const double* gp[4];
+  const double* ep[4];
+  {
+    const double* base = bt.pyr + f * bt.frame_doubles + (long long)(y0 - 2) * w;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      gp[k] = base + bt.plane_off[o][k] + xc;
+      ep[k] = base + bt.plane_off[o][k] + xe;
+    }
+  }
+  double gU[4], gC[4], gD[4], gN[4], eC[4], eD[4], eN[4];
+  auto load_row = [&](double* g, double* e) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      g[k] = __ldg(gp[k]);
+      e[k] = edge ? __ldg(ep[k]) : 0.0;
+      gp[k] += w;
+      ep[k] += w;
+    }
+  };
+  load_row(gU, eD);
+  load_row(gC, eC);
+  load_row(gN, eN);
+  const double oct_scale = ldexp(1.0, o);
+  int qn = 0, y_old = 0;
+  auto drain = [&]() {
+    for (int qi = lane; qi - lane < qn; qi += 32) {
+      if (qi < qn) {
+        const int e = S.queue[qi];
+        const int t = e & 31, yd = (e >> 5) + y0 - 1;
+        exact_detect(bt, dc, f, o, w, yd, xs0 - 1 + t, &S.ring[(yd - 1) % kRing][0][0], &S.ring[yd % kRing][0][0],
+                     &S.ring[(yd + 1) % kRing][0][0], 32, t, oct_scale);
+      }
+    }
+    qn = 0;
+    __syncwarp();
+  };
+  for (int ra = y0 - 1; ra <= y1; ++ra) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      gD[k] = gN[k];
+      eD[k] = eN[k];
+    }
+    if (ra + 2 <= y1 + 1) load_row(gN, eN);
+    // sigma^2-normalised Laplacian of row ra (image.cpp:220-238,
+    // scale_space.cpp:148-151), then alpha = beta * L in column order.
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      S.row[k][lane + 1] = gC[k];
+      if (edge) S.row[k][eslot] = eC[k];
+    }
+    __syncwarp();
+    double L[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const double lap = gU[k] + gD[k] + S.row[k][lane] + S.row[k][lane + 2] - 4.0 * gC[k];
+      L[k] = dc.s2[k] * lap;
+    }
+    double a[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      double sum = dc.beta[i][0] * L[0];
+      sum = sum + dc.beta[i][1] * L[1];
+      sum = sum + dc.beta[i][2] * L[2];
+      sum = sum + dc.beta[i][3] * L[3];
+      a[i] = sum;
+      S.ring[ra % kRing][i][lane] = sum;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      gU[k] = gC[k];
+      gC[k] = gD[k];
+      eC[k] = eD[k];
+    }
+    __syncwarp();
+    // Queued pixels (rows <= ra - 1) have their whole neighbourhood in the
+    // ring now; drain before the ring drops the oldest one's upper row.
+    if (qn >= 32 || (qn > 0 && ra - y_old >= kRing - 2)) drain();
+    if (ra >= y0 && ra < y1) {
+      const bool push = out_col && (!dc.screen || screen_pixel(a, dc));
+      const unsigned bal = __ballot_sync(0xffffffffu, push);
+      if (bal) {
+        if (qn == 0) y_old = ra;
+        if (push) S.queue[qn + __popc(bal & ((1u << lane) - 1u))] = uint16_t(((ra - y0 + 1) << 5) | lane);
+        qn += __popc(bal);
+      }
+      __syncwarp();
+    }
+  }
+  if (qn > 0) drain();
+}
+
 constexpr size_t kDetSmem = sizeof(double) * (4 * kGH * kGW + kAH * 4 * kAW);
 static_assert((kGW * sizeof(double)) % 16 == 0, "TMA box rows must be 16-byte multiples");
 
@@ -452,6 +594,12 @@ cudaError_t launch_detect(const Batch& bt, const DetConst& dc, int o, const CUte
     cudaError_t e = cudaFuncSetAttribute(k_detect, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kDetSmem));
     if (e != cudaSuccess) return e;
     configured = true;
+  }
+  if (dc.walk) {
+    const int strips = (ww + kStripCols - 1) / kStripCols;
+    dim3 grid((strips + kDetWarps - 1) / kDetWarps, (hh + kSegRows - 1) / kSegRows, bt.nframes);
+    k_detect_walk<<<grid, 32 * kDetWarps, 0, st>>>(bt, dc, o);
+    return cudaGetLastError();
   }
   dim3 grid((ww + kDetW - 1) / kDetW, (hh + kDetH - 1) / kDetH, bt.nframes);
   CUtensorMap none{};
