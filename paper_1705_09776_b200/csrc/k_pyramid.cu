@@ -466,7 +466,7 @@ struct DetWarpSmem {
   uint16_t queue[64];         // ((row - y0 + 1) << 5) | lane
 };
 
-__global__ void __launch_bounds__(32 * kDetWarps) k_detect_walk(Batch bt, DetConst dc, int o) {
+__global__ void __launch_bounds__(32 * kDetWarps, 8) k_detect_walk(Batch bt, DetConst dc, int o) {
   __shared__ DetWarpSmem smem[kDetWarps];
   const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
   DetWarpSmem& S = smem[wi];

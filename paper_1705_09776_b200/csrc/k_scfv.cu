@@ -81,52 +81,166 @@ __global__ void __launch_bounds__(128) k_pca(Batch bt, Model md) {
   }
 }
 
-// posteriors_matrix (scfv.cpp:140-164) + softmax_rows (scfv.cpp:40-48); one
-// warp per descriptor row, e[] parked in shared memory for the ordered sum.
-__global__ void __launch_bounds__(128) k_posterior(Batch bt, Model md) {
-  extern __shared__ double se[];
-  __shared__ double chain[4][4];
-  const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
+// posteriors_matrix (scfv.cpp:140-164) + softmax_rows (scfv.cpp:40-48).
+// One CTA owns a tile of kPM descriptor rows of one frame and all nc
+// components. Phase 1 is a register-tiled FP64 product over component tiles
+// of kPN: each thread holds a 4 x 4 block of (row, component) pairs and
+// accumulates a = sum_j x_j^2 / v_j and b = sum_j x_j m_j / v_j with the
+// inner index ascending and every multiply and add separately rounded (the
+// reference's arithmetic; the FP64 tensor-core MMA would fuse them, so it is
+// not used), then forms log p = -0.5 (a - 2b + c) + log_norm into the gamma
+// buffer while tracking the row maxima. Phase 2 exponentiates, sums each row
+// in Eigen's SSE2 packet order (four stride-4 chains) and normalises.
+constexpr int kPM = 64, kPN = 64;
+struct PostSmem {
+  double xs2[32][kPM];  // x^2, transposed
+  double xs[32][kPM];   // x, transposed
+  double iv[32][kPN];   // 1 / v, transposed
+  double mv[32][kPN];   // m / v, transposed
+  double cst[kPN];      // sum_j 1.0 * m^2 / v (the ones * (M^2/V)^T product)
+  double lnorm[kPN];
+  double rmax[16][kPM];
+  double chain[kPM][4];
+};
+
+__global__ void __launch_bounds__(256, 2) k_posterior(Batch bt, Model md) {
+  extern __shared__ __align__(16) uint8_t post_smem[];
+  PostSmem& S = *reinterpret_cast<PostSmem*>(post_smem);
   const int f = blockIdx.y;
   const int n = bt.or_count[f];
+  const int row0 = blockIdx.x * kPM;
+  if (row0 >= n) return;
   const int nc = md.nc;
-  double* e = se + wi * nc;
-  for (int t = blockIdx.x * 4 + wi; t < n; t += gridDim.x * 4) {
-    const double* x = bt.x + ((long long)f * bt.cap_or + t) * 32;
-    double peak = -INFINITY;
-    for (int i = lane; i < nc; i += 32) {
-      const double* iv = md.inv_var + i * 32;
-      const double* mv = md.m_over_v + i * 32;
-      const double* m2 = md.m2_over_v + i * 32;
-      double a = (x[0] * x[0]) * iv[0], b = x[0] * mv[0], c = 1.0 * m2[0];
-      for (int j = 1; j < 32; ++j) {
-        a = a + (x[j] * x[j]) * iv[j];
-        b = b + x[j] * mv[j];
-        c = c + 1.0 * m2[j];
+  const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
+  const double* X = bt.x + ((long long)f * bt.cap_or + row0) * 32;
+  double* gam = bt.gamma + ((long long)f * bt.cap_or + row0) * nc;
+  const int rows = min(kPM, n - row0);
+  for (int q = tid; q < kPM * 32; q += 256) {
+    const int t = q >> 5, j = q & 31;
+    const double v = t < rows ? X[t * 32 + j] : 0.0;
+    S.xs[j][t] = v;
+    S.xs2[j][t] = v * v;
+  }
+  double rm[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+  for (int c0 = 0; c0 < nc; c0 += kPN) {
+    __syncthreads();
+    for (int q = tid; q < kPN * 32; q += 256) {
+      const int i = q >> 5, j = q & 31;
+      const bool ok = c0 + i < nc;
+      S.iv[j][i] = ok ? md.inv_var[(c0 + i) * 32 + j] : 0.0;
+      S.mv[j][i] = ok ? md.m_over_v[(c0 + i) * 32 + j] : 0.0;
+    }
+    if (tid < kPN) {
+      const int i = c0 + tid;
+      double c = 0.0, ln = 0.0;
+      if (i < nc) {
+        const double* m2 = md.m2_over_v + i * 32;
+        c = 1.0 * m2[0];
+        for (int j = 1; j < 32; ++j) c = c + 1.0 * m2[j];
+        ln = md.log_norm[i];
       }
-      const double p = a - 2.0 * b + c;
-      const double lp = -0.5 * p + md.log_norm[i];
-      e[i] = lp;
-      peak = fmax(peak, lp);
+      S.cst[tid] = c;
+      S.lnorm[tid] = ln;
+    }
+    __syncthreads();
+    double a[4][4], b[4][4];
+    {
+      const double2 xa = *reinterpret_cast<const double2*>(&S.xs2[0][ty * 4]);
+      const double2 xb = *reinterpret_cast<const double2*>(&S.xs2[0][ty * 4 + 2]);
+      const double2 ya = *reinterpret_cast<const double2*>(&S.xs[0][ty * 4]);
+      const double2 yb = *reinterpret_cast<const double2*>(&S.xs[0][ty * 4 + 2]);
+      const double2 ia = *reinterpret_cast<const double2*>(&S.iv[0][tx * 4]);
+      const double2 ib = *reinterpret_cast<const double2*>(&S.iv[0][tx * 4 + 2]);
+      const double2 ma = *reinterpret_cast<const double2*>(&S.mv[0][tx * 4]);
+      const double2 mb = *reinterpret_cast<const double2*>(&S.mv[0][tx * 4 + 2]);
+      const double x2[4] = {xa.x, xa.y, xb.x, xb.y}, x1[4] = {ya.x, ya.y, yb.x, yb.y};
+      const double iv[4] = {ia.x, ia.y, ib.x, ib.y}, mv[4] = {ma.x, ma.y, mb.x, mb.y};
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          a[r][c] = x2[r] * iv[c];
+          b[r][c] = x1[r] * mv[c];
+        }
+    }
+#pragma unroll 4
+    for (int j = 1; j < 32; ++j) {
+      const double2 xa = *reinterpret_cast<const double2*>(&S.xs2[j][ty * 4]);
+      const double2 xb = *reinterpret_cast<const double2*>(&S.xs2[j][ty * 4 + 2]);
+      const double2 ya = *reinterpret_cast<const double2*>(&S.xs[j][ty * 4]);
+      const double2 yb = *reinterpret_cast<const double2*>(&S.xs[j][ty * 4 + 2]);
+      const double2 ia = *reinterpret_cast<const double2*>(&S.iv[j][tx * 4]);
+      const double2 ib = *reinterpret_cast<const double2*>(&S.iv[j][tx * 4 + 2]);
+      const double2 ma = *reinterpret_cast<const double2*>(&S.mv[j][tx * 4]);
+      const double2 mb = *reinterpret_cast<const double2*>(&S.mv[j][tx * 4 + 2]);
+      const double x2[4] = {xa.x, xa.y, xb.x, xb.y}, x1[4] = {ya.x, ya.y, yb.x, yb.y};
+      const double iv[4] = {ia.x, ia.y, ib.x, ib.y}, mv[4] = {ma.x, ma.y, mb.x, mb.y};
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          a[r][c] = a[r][c] + x2[r] * iv[c];
+          b[r][c] = b[r][c] + x1[r] * mv[c];
+        }
     }
 #pragma unroll
-    for (int d = 16; d > 0; d >>= 1) peak = fmax(peak, __shfl_xor_sync(0xffffffffu, peak, d));
-    __syncwarp();
-    for (int i = lane; i < nc; i += 32) e[i] = exp(e[i] - peak);
-    __syncwarp();
+    for (int r = 0; r < 4; ++r) {
+      const int t = ty * 4 + r;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int i = c0 + tx * 4 + c;
+        if (t < rows && i < nc) {
+          const double p = a[r][c] - 2.0 * b[r][c] + S.cst[tx * 4 + c];
+          const double lp = -0.5 * p + S.lnorm[tx * 4 + c];
+          gam[t * nc + i] = lp;
+          rm[r] = fmax(rm[r], lp);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < 4; ++r) S.rmax[tx][ty * 4 + r] = rm[r];
+  __syncthreads();
+  if (tid < kPM) {
+    double pk = S.rmax[0][tid];
+    for (int k = 1; k < 16; ++k) pk = fmax(pk, S.rmax[k][tid]);
+    S.rmax[0][tid] = pk;
+  }
+  __syncthreads();
+  // softmax_rows: e = exp(logp - peak) ...
+  for (int q = tid; q < rows * nc; q += 256) {
+    const int t = q / nc;
+    gam[q] = exp(gam[q] - S.rmax[0][t]);
+  }
+  __syncthreads();
+  // ... e.sum() in Eigen's packet order (packet_sum_seq) ...
+  {
+    const int t = tid >> 2, k = tid & 3;
+    if (t < rows && nc >= 4) {
+      const double* e = gam + t * nc;
+      const int e2 = nc / 4 * 4;
+      double acc = e[k];
+      int i = k + 4;
+      for (; i + 28 < e2; i += 32) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = e[i + 4 * u];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc = acc + v[u];
+      }
+      for (; i < e2; i += 4) acc = acc + e[i];
+      S.chain[t][k] = acc;
+    }
+  }
+  __syncthreads();
+  if (tid < rows) {
+    const double* e = gam + tid * nc;
     double total;
     if (nc < 4) {
       total = packet_sum_seq(e, nc);
     } else {
-      const int e2 = nc / 4 * 4;
-      if (lane < 4) {
-        double a = e[lane];
-        for (int i = lane + 4; i < e2; i += 4) a += e[i];
-        chain[wi][lane] = a;
-      }
-      __syncwarp();
-      double a0 = chain[wi][0] + chain[wi][2], a1 = chain[wi][1] + chain[wi][3];
-      const int e1 = nc / 2 * 2;
+      const int e2 = nc / 4 * 4, e1 = nc / 2 * 2;
+      double a0 = S.chain[tid][0] + S.chain[tid][2], a1 = S.chain[tid][1] + S.chain[tid][3];
       if (e1 > e2) {
         a0 += e[e2];
         a1 += e[e2 + 1];
@@ -134,10 +248,11 @@ __global__ void __launch_bounds__(128) k_posterior(Batch bt, Model md) {
       total = a0 + a1;
       for (int i = e1; i < nc; ++i) total += e[i];
     }
-    double* g = bt.gamma + ((long long)f * bt.cap_or + t) * nc;
-    for (int i = lane; i < nc; i += 32) g[i] = e[i] / total;
-    __syncwarp();
+    S.chain[tid][0] = total;
   }
+  __syncthreads();
+  // ... gamma = e / sum.
+  for (int q = tid; q < rows * nc; q += 256) gam[q] = gam[q] / S.chain[q / nc][0];
 }
 
 // fv_mean_matrix / fv_var_matrix (scfv.cpp:166-203), one thread per (i, j).
@@ -291,12 +406,13 @@ cudaError_t launch_scfv_pack(const Batch& bt, const Model& md, const EncodeConst
   k_pca<<<dim3(8, bt.nframes), 128, 0, st>>>(bt, md);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  const size_t psm = sizeof(double) * 4 * size_t(md.nc);
-  if (psm > 48 * 1024) {
-    e = cudaFuncSetAttribute(k_posterior, cudaFuncAttributeMaxDynamicSharedMemorySize, int(psm));
+  static bool post_configured = false;
+  if (!post_configured) {
+    e = cudaFuncSetAttribute(k_posterior, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(PostSmem)));
     if (e != cudaSuccess) return e;
+    post_configured = true;
   }
-  k_posterior<<<dim3(64, bt.nframes), 128, psm, st>>>(bt, md);
+  k_posterior<<<dim3((bt.cap_or + kPM - 1) / kPM, bt.nframes), 256, sizeof(PostSmem), st>>>(bt, md);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   k_fisher<<<dim3((md.nc * 32 + 127) / 128, bt.nframes), 128, 0, st>>>(bt, md, ec.variance);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
