@@ -208,9 +208,10 @@ __global__ void __launch_bounds__(256, 2) k_posterior(Batch bt, Model md) {
   }
   __syncthreads();
   // softmax_rows: e = exp(logp - peak) ...
-  for (int q = tid; q < rows * nc; q += 256) {
-    const int t = q / nc;
-    gam[q] = exp(gam[q] - S.rmax[0][t]);
+  const int wi = tid >> 5, lane = tid & 31;
+  for (int t = wi; t < rows; t += 8) {
+    const double pk = S.rmax[0][t];
+    for (int i = lane; i < nc; i += 32) gam[t * nc + i] = exp(gam[t * nc + i] - pk);
   }
   __syncthreads();
   // ... e.sum() in Eigen's packet order (packet_sum_seq) ...
@@ -252,39 +253,92 @@ __global__ void __launch_bounds__(256, 2) k_posterior(Batch bt, Model md) {
   }
   __syncthreads();
   // ... gamma = e / sum.
-  for (int q = tid; q < rows * nc; q += 256) gam[q] = gam[q] / S.chain[q / nc][0];
+  for (int t = wi; t < rows; t += 8) {
+    const double tot = S.chain[t][0];
+    for (int i = lane; i < nc; i += 32) gam[t * nc + i] = gam[t * nc + i] / tot;
+  }
 }
 
-// fv_mean_matrix / fv_var_matrix (scfv.cpp:166-203), one thread per (i, j).
-__global__ void __launch_bounds__(128) k_fisher(Batch bt, Model md, int variance) {
+// fv_mean_matrix / fv_var_matrix (scfv.cpp:166-203). gamma^T X (and
+// gamma^T X^2) as sums over the descriptor index t, ascending, one separately
+// rounded multiply and add per term. A CTA owns kFI components x all 32
+// dimensions; thread (g, j) accumulates components g*4 .. g*4+3 of
+// dimension j while the CTA streams gamma and X rows through shared memory.
+// gamma^T 1 is the same for every j: it is summed once per component.
+constexpr int kFI = 32, kFT = 64;
+__global__ void __launch_bounds__(256) k_fisher(Batch bt, Model md, int variance) {
+  __shared__ __align__(16) double sg[kFT][kFI];
+  __shared__ double sx[kFT][32];
+  __shared__ double qo_s[kFI];
   const int f = blockIdx.y;
   const int n = bt.or_count[f];
   const int nc = md.nc;
-  const int ij = blockIdx.x * blockDim.x + threadIdx.x;
-  if (ij >= nc * 32) return;
-  const int i = ij >> 5, j = ij & 31;
+  const int i0 = blockIdx.x * kFI;
+  const int tid = threadIdx.x, j = tid & 31, g = tid >> 5;
   double* gm = bt.gm + (long long)f * nc * 32;
   double* gv = bt.gv + (long long)f * nc * 32;
   if (n == 0) {
-    gm[ij] = 0.0;
-    gv[ij] = 0.0;
+    for (int q = tid; q < kFI * 32; q += 256)
+      if (i0 + q / 32 < nc) {
+        gm[(long long)i0 * 32 + q] = 0.0;
+        gv[(long long)i0 * 32 + q] = 0.0;
+      }
     return;
   }
   const double* G = bt.gamma + (long long)f * bt.cap_or * nc;
   const double* X = bt.x + (long long)f * bt.cap_or * 32;
-  const double scale = 1.0 / (double(n) * sqrt(md.weights[i]));
-  double qx = G[i] * X[j], qo = G[i] * 1.0, qx2 = G[i] * (X[j] * X[j]);
-  for (int t = 1; t < n; ++t) {
-    const double gti = G[(long long)t * nc + i], xtj = X[t * 32 + j];
-    qx = qx + gti * xtj;
-    qo = qo + gti * 1.0;
-    if (variance) qx2 = qx2 + gti * (xtj * xtj);
+  double qx[4], qx2[4], qo = 0.0;
+  for (int t0 = 0; t0 < n; t0 += kFT) {
+    const int tn = min(kFT, n - t0);
+    __syncthreads();
+    for (int q = tid; q < kFT * kFI; q += 256) {
+      const int t = q / kFI, i = q % kFI;
+      sg[t][i] = (t < tn && i0 + i < nc) ? G[(long long)(t0 + t) * nc + i0 + i] : 0.0;
+    }
+    for (int q = tid; q < kFT * 32; q += 256) {
+      const int t = q >> 5;
+      sx[t][q & 31] = t < tn ? X[(t0 + t) * 32 + (q & 31)] : 0.0;
+    }
+    __syncthreads();
+    for (int t = 0; t < tn; ++t) {
+      const double xt = sx[t][j];
+      const double xt2 = xt * xt;
+      const double2 ga = *reinterpret_cast<const double2*>(&sg[t][g * 4]);
+      const double2 gb = *reinterpret_cast<const double2*>(&sg[t][g * 4 + 2]);
+      const double gg[4] = {ga.x, ga.y, gb.x, gb.y};
+      if (t0 + t == 0) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          qx[c] = gg[c] * xt;
+          qx2[c] = gg[c] * xt2;
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          qx[c] = qx[c] + gg[c] * xt;
+          if (variance) qx2[c] = qx2[c] + gg[c] * xt2;
+        }
+      }
+    }
+    if (tid < kFI) {
+      for (int t = 0; t < tn; ++t) qo = (t0 + t == 0) ? sg[t][tid] * 1.0 : qo + sg[t][tid] * 1.0;
+    }
   }
-  const double m = md.means[ij], s = md.stds[ij];
-  gm[ij] = ((qx - qo * m) / s) * scale;
-  if (variance) {
-    const double var = s * s;
-    gv[ij] = ((qx2 - qx * (2.0 * m) + qo * (m * m - var)) / var) * scale;
+  if (tid < kFI) qo_s[tid] = qo;
+  __syncthreads();
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const int i = i0 + g * 4 + c;
+    if (i >= nc) continue;
+    const int ij = i * 32 + j;
+    const double scale = 1.0 / (double(n) * sqrt(md.weights[i]));
+    const double q1 = qo_s[g * 4 + c];
+    const double m = md.means[ij], s = md.stds[ij];
+    gm[ij] = ((qx[c] - q1 * m) / s) * scale;
+    if (variance) {
+      const double var = s * s;
+      gv[ij] = ((qx2[c] - qx[c] * (2.0 * m) + q1 * (m * m - var)) / var) * scale;
+    }
   }
 }
 
@@ -414,7 +468,7 @@ cudaError_t launch_scfv_pack(const Batch& bt, const Model& md, const EncodeConst
   }
   k_posterior<<<dim3((bt.cap_or + kPM - 1) / kPM, bt.nframes), 256, sizeof(PostSmem), st>>>(bt, md);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  k_fisher<<<dim3((md.nc * 32 + 127) / 128, bt.nframes), 128, 0, st>>>(bt, md, ec.variance);
+  k_fisher<<<dim3((md.nc + kFI - 1) / kFI, bt.nframes), 256, 0, st>>>(bt, md, ec.variance);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   const size_t esm = sizeof(double) * size_t(md.nc) + size_t(md.nc);
   if (esm > 48 * 1024) {
