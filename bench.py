@@ -100,14 +100,45 @@ def measured_peaks():
 
 
 def ncu_traffic():
-    """dram bytes per launch of the fused octave kernel from the committed ncu
-    --set full capture summary (profiles/), or None."""
+    """DRAM bytes per launch of the octave-0 kernel pair (k_blur<...,0> +
+    k_detect_walk) from the committed ncu --set full capture (profiles/), with
+    the algorithmic bytes of the same launches beside them, or None."""
     path = os.path.join(ROOT, "profiles", "octave_kernel_ncu.json")
     try:
         with open(path) as f:
-            return json.load(f).get("dram_bytes_per_launch")
+            return json.load(f)
     except (OSError, ValueError):
         return None
+
+
+def fp64_peak():
+    """Measured FP64 SIMT issue rate (separate DMUL/DADD, the pyramid's mix) from
+    tools/probe/fp64_peak on this B200 pool (profiles/fp64_peak.json), else the
+    nominal 64 FP64 lanes/clk/SM x 148 SMs x 1.965 GHz."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "fp64_peak.json")) as f:
+            return float(json.load(f)["dmul_dadd_tops"]), "measured"
+    except (OSError, KeyError, ValueError):
+        return 64 * 148 * 1.965e9 / 1e12, "nominal"
+
+
+def pyramid_fp64_ops(w, h, radii=(5, 5, 6, 8), margin=10, octaves=4):
+    """Separately rounded FP64 operations the octave pair must execute per frame
+    (DESIGN.md 2.3): blur x+y passes 8R+2 per level and pixel; sigma^2-Laplacian
+    (6 per level) + alpha (28) per alpha position (window + 1-pixel ring); the
+    screen's FP64 discriminant (7) per window pixel. The exact test on screened
+    pixels comes on top and is not counted."""
+    ops = 0
+    for _ in range(octaves):
+        if w < 16 or h < 16:
+            break
+        ops += w * h * sum(8 * r + 2 for r in radii)
+        ww, hh = w - 2 * margin, h - 2 * margin
+        if ww > 0 and hh > 0:
+            ops += (ww + 2) * (hh + 2) * 52 + ww * hh * 7
+        w //= 2
+        h //= 2
+    return ops
 
 
 def cpu_baseline(frames: np.ndarray, bundle: str, mode_id: int, sample: int):
@@ -173,6 +204,7 @@ def main():
     ap.add_argument("--bundle", default="b8")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-b512", action="store_true")
     args = ap.parse_args()
     rank, world, local = dist_env()
 
@@ -278,7 +310,27 @@ def main():
 
     hbm, peak_kind = measured_peaks()
     achieved = (pyr_bytes / (pyr_ms / 1000.0)) / 1e9 if pyr_ms > 0 else 0.0
-    traffic = ncu_traffic()
+    ncu = ncu_traffic()
+    traffic = ncu.get("dram_bytes_per_launch_pair") if ncu else None
+    f64_peak, f64_kind = fp64_peak()
+    f64_ops = pyramid_fp64_ops(FRAME_W, FRAME_H) * n
+    f64_achieved = f64_ops / (pyr_ms / 1000.0) / 1e12 if pyr_ms > 0 else 0.0
+    # Secondary workload: the paper's 512-component GMM bundle.
+    b512 = None
+    if args.bundle == "b8" and not args.no_b512:
+        with open(os.path.join(ROOT, "tests", "golden", "bundle_b512.txt")) as f:
+            ex512 = cg.Extractor(f.read(), device=device, max_batch=args.max_batch)
+        for _ in range(2):
+            ex512.encode_device(d_frames, n, FRAME_W, FRAME_H, mode, d_out, d_len)
+        ex512.sync()
+        ex512.event_record(0)
+        for _ in range(3):
+            ex512.encode_device(d_frames, n, FRAME_W, FRAME_H, mode, d_out, d_len)
+        ex512.event_record(1)
+        ms512 = max_over_ranks(ex512.event_elapsed(0, 1))
+        b512 = {"value": world * n * 3 / (ms512 / 1000.0), "unit": "frames/s", "steps": 3,
+                "note": "same frames and mode, B512 bundle (GMM 512 components, the paper's SCFV)"}
+        ex512.close()
     if rank != 0:
         return
     line = {
@@ -294,13 +346,22 @@ def main():
         "gpu_launches": launches,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": achieved / hbm if hbm else None, "traffic": traffic,
-                     "kernel": "octave pair k_blur (Gaussian scale space) + k_detect (LoG + ALP extrema + refinement)",
+                     "traffic_algorithmic": ncu.get("algorithmic_bytes_per_launch_pair") if ncu else None,
+                     "traffic_note": ncu.get("note") if ncu else None,
+                     "kernel": "octave pair k_blur (Gaussian scale space) + k_detect_walk (LoG + ALP extrema + "
+                               "refinement), all octaves, CUDA events in a serial (unoverlapped) step",
                      "peak_source": peak_kind,
                      "algorithmic_bytes": "per octave and frame: w*h*(b_in + 4*8) written by k_blur (b_in = 1 B u8 "
                                           "at octave 0, 8 B f64 G3 above) + 4*8 B per detection-window pixel read "
-                                          "back by k_detect; VGA = 26.0 MB/frame (DESIGN.md 2.2)"},
+                                          "back by k_detect_walk; VGA = 26.0 MB/frame (DESIGN.md 2.2)",
+                     "fp64": {"achieved": f64_achieved, "peak": f64_peak, "unit": "Tops/s (separately rounded "
+                              "DMUL/DADD)", "frac": f64_achieved / f64_peak, "peak_source": f64_kind,
+                              "ops_per_frame": pyramid_fp64_ops(FRAME_W, FRAME_H),
+                              "note": "the pair is FP64-issue-bound under the reference's double arithmetic "
+                                      "(DESIGN.md 2.3); ops exclude the exact test on screened pixels"}},
         "stage_ms_per_step_unoverlapped": {k: v for k, v in stage.items()},
         "frames_ok": ok_frames,
+        "secondary": {"b512": b512},
         "clocks": clk.summary(),
     }
     if not args.no_cpu:
