@@ -141,6 +141,43 @@ int cdvz_gpu_host_alloc(cdvz_gpu_ctx* ctx, size_t bytes, void** ptr);
 int cdvz_gpu_host_free(cdvz_gpu_ctx* ctx, void* ptr);
 int cdvz_gpu_copy(cdvz_gpu_ctx* ctx, void* dst, const void* src, size_t bytes, int kind /* 1 H2D, 2 D2H, 3 D2D */);
 
+/* ------------------------------------------------------------------------
+ * Compressed-domain matching and retrieval: an index of
+ * CDVZ1 containers decoded on the device, queried in batches.
+ * ------------------------------------------------------------------------ */
+typedef struct cdvz_gpu_index cdvz_gpu_index;
+
+/* Decodes `count` containers (blob + offsets[count+1]) on `device`: the
+ * reference's parse_container (proj/src/container.cpp:60-93) with
+ * parse_scfv / unpack_local (proj/src/scfv.cpp:300-326,
+ * proj/src/transform_coding.cpp:272-305) for a whole index. id_rank[i] is
+ * item i's rank in ascending id order — the tie-break retrieve applies to
+ * item ids (proj/src/eval.cpp:91-94); NULL means index order. Every container
+ * must pass the reference's checks (DataError otherwise, naming the item) and
+ * share one model bundle and mode. */
+int cdvz_gpu_index_create(int device, const uint8_t* blob, const size_t* offsets, int count, const int32_t* id_rank,
+                          cdvz_gpu_index** out);
+void cdvz_gpu_index_destroy(cdvz_gpu_index* idx);
+const char* cdvz_gpu_index_last_error(const cdvz_gpu_index* idx);
+int cdvz_gpu_index_info(const cdvz_gpu_index* idx, int* count, int* mode_id, uint32_t* model_crc, int* components,
+                        long long* total_codes);
+
+/* retrieve (proj/src/eval.cpp:76-124, proj/include/cdvz/eval.hpp:49-55) for
+ * `nq` query containers at once: rank the index by scfv_similarity, re-rank
+ * the top `rerank_depth` by count_local_matches(ratio_test), and write each
+ * query's first `max_results` (0 = all) ranked items and scores to
+ * out_items / out_scores (nq x max_results, row-major) with the reference's
+ * scores: local + (sim + 1) / 2 in the head, (sim + 1) / 2 - 1 beyond it. */
+int cdvz_gpu_retrieve(cdvz_gpu_index* idx, const uint8_t* query_blob, const size_t* query_offsets, int nq,
+                      double ratio_test, int rerank_depth, int max_results, int32_t* out_items, double* out_scores);
+
+/* match_pair (proj/src/eval.cpp:66-74, eval.hpp:44-47) for `np` pairs
+ * (query pairs[2k], index item pairs[2k+1]): global similarity
+ * (scfv_similarity, scfv.cpp:255-278) and mutual ratio-test local matches
+ * (count_local_matches, eval.cpp:47-64). */
+int cdvz_gpu_match_pairs(cdvz_gpu_index* idx, const uint8_t* query_blob, const size_t* query_offsets, int nq,
+                         const int32_t* pairs, int np, double ratio_test, double* global_sim, int32_t* local_matches);
+
 #ifdef __cplusplus
 }
 #endif

@@ -4,6 +4,7 @@
 // message in orc_last_error(): 1 usage, 2 data, 3 internal (the reference
 // CLI's exit-code contract, proj/tools/cdvz.cpp:308-317).
 #include <atomic>
+#include <cstdio>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -207,6 +208,49 @@ int orc_trace_get(void* handle, const char* name, double* dst, size_t cap, size_
     }
     *n = v.size();
     if (dst && cap >= v.size()) std::memcpy(dst, v.data(), v.size() * sizeof(double));
+  });
+}
+
+// retrieve(query, index) for nq queries over an index of n containers (all
+// given as CDVZ1 bytes: blob + offsets[count+1]). Item ids are "idx%08d" so the
+// reference's id tie-break is the index position. out_order / out_score are
+// nq x n (item index, score) in ranked order.
+int orc_retrieve(const uint8_t* index_blob, const size_t* index_off, int n, const uint8_t* query_blob,
+                 const size_t* query_off, int nq, double ratio, int depth, int32_t* out_order, double* out_score) {
+  return guarded([&] {
+    std::vector<EncodedImage> items(std::size_t(std::max(0, n)));
+    std::vector<std::pair<std::string, const EncodedImage*>> index;
+    char id[32];
+    for (int i = 0; i < n; ++i) {
+      items[std::size_t(i)] = parse_container(std::vector<uint8_t>(index_blob + index_off[i], index_blob + index_off[i + 1]));
+      std::snprintf(id, sizeof id, "idx%08d", i);
+      index.emplace_back(id, &items[std::size_t(i)]);
+    }
+    MatchOptions opts;
+    opts.ratio_test = ratio;
+    opts.rerank_depth = depth;
+    for (int q = 0; q < nq; ++q) {
+      const EncodedImage query =
+          parse_container(std::vector<uint8_t>(query_blob + query_off[q], query_blob + query_off[q + 1]));
+      const RankedList list = retrieve(query, index, opts);
+      for (std::size_t r = 0; r < list.items.size(); ++r) {
+        out_order[std::size_t(q) * n + r] = std::stoi(list.items[r].id.substr(3));
+        out_score[std::size_t(q) * n + r] = list.items[r].score;
+      }
+    }
+  });
+}
+
+// match_pair(a, b) on two CDVZ1 containers.
+int orc_match_pair(const uint8_t* a, size_t alen, const uint8_t* b, size_t blen, double ratio, double* global_sim,
+                   int* local_matches) {
+  return guarded([&] {
+    MatchOptions opts;
+    opts.ratio_test = ratio;
+    const MatchResult r = match_pair(parse_container(std::vector<uint8_t>(a, a + alen)),
+                                     parse_container(std::vector<uint8_t>(b, b + blen)), opts);
+    *global_sim = r.global_similarity;
+    *local_matches = r.local_match_count;
   });
 }
 

@@ -291,6 +291,16 @@ struct EncodeTrace {
 // pipeline.cpp:54-97
 EncodedImage encode_image(const Plane& img, const ModelBundle& b, const ModeSpec& mode,
                           int max_side = 640, StageTimes* times = nullptr, EncodeTrace* trace = nullptr);
+// ---------------------------------------------------------------- eval (eval.hpp)
+struct MatchOptions { double ratio_test = 0.85; int rerank_depth = 50; };   // eval.hpp:32-35
+struct MatchResult { double global_similarity = -1.0; int local_match_count = 0; };
+struct RankedItem { std::string id; double score = 0.0; };
+struct RankedList { std::vector<RankedItem> items; };
+int count_local_matches(const std::vector<TernaryCode>& a, const std::vector<TernaryCode>& b, double ratio = 0.85);
+MatchResult match_pair(const EncodedImage& a, const EncodedImage& b, const MatchOptions& opts = {});
+RankedList retrieve(const EncodedImage& query, const std::vector<std::pair<std::string, const EncodedImage*>>& index,
+                    const MatchOptions& opts = {});
+
 struct TrainOptions { uint64_t seed = 7; int gmm_components = 8; int em_iterations = 25;
                       int select_n = 300; int max_side = 640; int relevance_bins = 16; };
 ModelBundle train_model(const std::vector<Plane>& corpus, const TrainOptions& o);  // pipeline.cpp:99-166

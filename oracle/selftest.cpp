@@ -1137,6 +1137,73 @@ CASE("pipeline: every mode fits its budget; deterministic; self-similarity (test
   CHECK(tot > 0.0);
 }
 
+// ================================================================= eval (test_pipeline.cpp:110-205)
+
+namespace {
+const ModelBundle& eval_bundle() {
+  static const ModelBundle b = [] {
+    std::vector<Plane> corpus;
+    for (int i = 0; i < 20; ++i) corpus.push_back(synth_image(corpus_seed(401, i), 224, 168));
+    TrainOptions o;
+    o.seed = 11;
+    o.gmm_components = 8;
+    o.em_iterations = 15;
+    return train_model(corpus, o);
+  }();
+  return b;
+}
+}  // namespace
+
+CASE("eval: self match, disjoint noise, symmetric global score, mismatches (test_pipeline.cpp:110-146)") {
+  const ModelBundle& b = eval_bundle();
+  const EncodedImage enc = encode_image(synth_image(81, 320, 240), b, mode_by_name("4K"));
+  const MatchResult self = match_pair(enc, enc);
+  CHECK(self.global_similarity == 1.0);
+  CHECK(self.local_match_count == int(enc.codes.size()));
+  CHECK(enc.codes.size() > 20);
+  const EncodedImage ea = encode_image(synth_image(82, 320, 240), b, mode_by_name("4K"));
+  const EncodedImage eb = encode_image(synth_image(9999, 320, 240), b, mode_by_name("4K"));
+  CHECK(match_pair(ea, eb).local_match_count <= int(0.05 * double(ea.codes.size())));
+  const EncodedImage ec = encode_image(synth_image(83, 320, 240), b, mode_by_name("1K"));
+  const EncodedImage ed = encode_image(synth_image(84, 320, 240), b, mode_by_name("1K"));
+  CHECK(match_pair(ec, ed).global_similarity == match_pair(ed, ec).global_similarity);
+  const Plane img = synth_image(85, 320, 240);
+  const EncodedImage m1 = encode_image(img, b, mode_by_name("1K"));
+  const EncodedImage m2 = encode_image(img, b, mode_by_name("2K"));
+  CHECK_THROWS(match_pair(m1, m2), DataError);
+  EncodedImage m3 = m1;
+  m3.model_crc ^= 1;
+  CHECK_THROWS(match_pair(m1, m3), DataError);
+}
+
+CASE("eval: retrieval basics (test_pipeline.cpp:147-205)") {
+  const ModelBundle& b = eval_bundle();
+  std::vector<EncodedImage> encs;
+  std::vector<std::pair<std::string, const EncodedImage*>> index;
+  for (int i = 0; i < 6; ++i) encs.push_back(encode_image(synth_image(900 + uint64_t(i), 256, 192), b, mode_by_name("2K")));
+  for (int i = 0; i < 6; ++i) index.emplace_back("img" + std::to_string(i), &encs[std::size_t(i)]);
+  CHECK_THROWS(retrieve(encs[0], {}), DataError);
+  for (int i = 0; i < 6; ++i) CHECK(retrieve(encs[std::size_t(i)], index).items.front().id == "img" + std::to_string(i));
+  const RankedList one = retrieve(encs[0], {{"only", &encs[1]}});
+  CHECK(one.items.size() == 1 && one.items.front().id == "only");
+  const RankedList l2 = retrieve(encs[2], index);
+  for (std::size_t i = 1; i < l2.items.size(); ++i) CHECK(l2.items[i].score <= l2.items[i - 1].score);
+  MatchOptions r3;
+  r3.rerank_depth = 3;
+  MatchOptions r0;
+  r0.rerank_depth = 0;
+  const RankedList with = retrieve(encs[2], index, r3), without = retrieve(encs[2], index, r0);
+  std::vector<std::string> ha, hb;
+  for (int i = 0; i < 3; ++i) {
+    ha.push_back(with.items[std::size_t(i)].id);
+    hb.push_back(without.items[std::size_t(i)].id);
+  }
+  std::sort(ha.begin(), ha.end());
+  std::sort(hb.begin(), hb.end());
+  CHECK(ha == hb);
+  for (std::size_t i = 3; i < with.items.size(); ++i) CHECK(with.items[i].id == without.items[i].id);
+}
+
 int main(int argc, char** argv) {
   const std::string filter = argc > 1 ? argv[1] : "";
   int failed_cases = 0, run = 0, xfail = 0;

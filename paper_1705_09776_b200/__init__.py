@@ -111,6 +111,13 @@ def _lib() -> ctypes.CDLL:
         "cdvz_gpu_host_alloc": (I, [P, S, ctypes.POINTER(P)]),
         "cdvz_gpu_host_free": (I, [P, P]),
         "cdvz_gpu_copy": (I, [P, P, P, S, I]),
+        "cdvz_gpu_index_create": (I, [I, P, P, I, P, ctypes.POINTER(P)]),
+        "cdvz_gpu_index_destroy": (None, [P]),
+        "cdvz_gpu_index_last_error": (ctypes.c_char_p, [P]),
+        "cdvz_gpu_index_info": (I, [P, ctypes.POINTER(I), ctypes.POINTER(I), ctypes.POINTER(U32), ctypes.POINTER(I),
+                                    ctypes.POINTER(ctypes.c_longlong)]),
+        "cdvz_gpu_retrieve": (I, [P, P, P, I, ctypes.c_double, I, I, P, P]),
+        "cdvz_gpu_match_pairs": (I, [P, P, P, I, P, I, ctypes.c_double, P, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -311,6 +318,94 @@ class Extractor:
         return arr
 
 
+def _pack(containers) -> tuple:
+    """Concatenate container byte strings -> (uint8 blob, uint64 offsets[n+1])."""
+    offs = np.zeros(len(containers) + 1, dtype=np.uint64)
+    offs[1:] = np.cumsum([len(c) for c in containers], dtype=np.uint64)
+    blob = np.frombuffer(b"".join(containers), dtype=np.uint8) if containers else np.zeros(1, np.uint8)
+    if blob.size == 0:
+        blob = np.zeros(1, np.uint8)
+    return np.ascontiguousarray(blob), offs
+
+
+class Index:
+    """Compressed-domain retrieval index on one GPU: the
+    reference's retrieve / match_pair (proj/src/eval.cpp:66-124) over CDVZ1
+    containers decoded on the device (parse_container, container.cpp:60-93).
+
+    ids: optional item ids; their ascending order is the tie-break of equal
+    scores, as in the reference (default: index order)."""
+
+    def __init__(self, containers, device: int = 0, ids=None):
+        self._lib = _lib()
+        self._idx = ctypes.c_void_p()
+        self._blob, self._offs = _pack(list(containers))
+        n = len(self._offs) - 1
+        self.ids = list(ids) if ids is not None else None
+        rank = None
+        if ids is not None:
+            if len(ids) != n:
+                raise UsageError("one id per container")
+            order = sorted(range(n), key=lambda i: ids[i])
+            rank = np.empty(n, dtype=np.int32)
+            rank[np.array(order, dtype=np.int64)] = np.arange(n, dtype=np.int32)
+        code = self._lib.cdvz_gpu_index_create(device, self._blob.ctypes.data, self._offs.ctypes.data, n,
+                                               rank.ctypes.data if rank is not None else None, ctypes.byref(self._idx))
+        if code:
+            _raise(code, (self._lib.cdvz_gpu_index_last_error(None) or b"").decode())
+        self.count = n
+
+    def _check(self, code: int) -> None:
+        if code:
+            _raise(code, (self._lib.cdvz_gpu_index_last_error(self._idx) or b"").decode())
+
+    def info(self) -> dict:
+        n, m, nc = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+        crc, tot = ctypes.c_uint32(), ctypes.c_longlong()
+        self._check(self._lib.cdvz_gpu_index_info(self._idx, ctypes.byref(n), ctypes.byref(m), ctypes.byref(crc),
+                                                  ctypes.byref(nc), ctypes.byref(tot)))
+        return {"count": n.value, "mode_id": m.value, "model_crc": crc.value, "components": nc.value,
+                "total_codes": tot.value}
+
+    def retrieve_batch(self, queries, ratio_test: float = 0.85, rerank_depth: int = 50, max_results: int = 0):
+        """retrieve() for every query -> (items int32 [nq, k], scores float64 [nq, k])."""
+        blob, offs = _pack(list(queries))
+        nq = len(offs) - 1
+        k = self.count if max_results <= 0 else min(self.count, max_results)
+        items = np.empty((nq, k), dtype=np.int32)
+        scores = np.empty((nq, k), dtype=np.float64)
+        self._check(self._lib.cdvz_gpu_retrieve(self._idx, blob.ctypes.data, offs.ctypes.data, nq, ratio_test,
+                                                rerank_depth, max_results, items.ctypes.data, scores.ctypes.data))
+        return items, scores
+
+    def retrieve(self, query: bytes, ratio_test: float = 0.85, rerank_depth: int = 50) -> list:
+        """The reference's RankedList for one query: [(id, score), ...]."""
+        items, scores = self.retrieve_batch([query], ratio_test, rerank_depth)
+        ids = self.ids if self.ids is not None else list(range(self.count))
+        return [(ids[int(i)], float(s)) for i, s in zip(items[0], scores[0])]
+
+    def match_pairs(self, queries, pairs, ratio_test: float = 0.85):
+        """match_pair(queries[q], index[i]) for (q, i) in pairs -> (global_sim, local_matches)."""
+        blob, offs = _pack(list(queries))
+        pr = np.ascontiguousarray(np.asarray(pairs, dtype=np.int32).reshape(-1, 2))
+        sim = np.empty(len(pr), dtype=np.float64)
+        loc = np.empty(len(pr), dtype=np.int32)
+        self._check(self._lib.cdvz_gpu_match_pairs(self._idx, blob.ctypes.data, offs.ctypes.data, len(offs) - 1,
+                                                   pr.ctypes.data, len(pr), ratio_test, sim.ctypes.data, loc.ctypes.data))
+        return sim, loc
+
+    def close(self) -> None:
+        if self._idx:
+            self._lib.cdvz_gpu_index_destroy(self._idx)
+            self._idx = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 def container_slot(mode) -> int:
     m = mode if isinstance(mode, ModeSpec) else (mode_by_name(mode) if isinstance(mode, str) else mode_by_id(mode))
     return m.budget_bytes + 28
@@ -331,5 +426,5 @@ def parse_container_header(data: bytes) -> dict:
 
 __all__ = [
     "Extractor", "ModeSpec", "MODES", "mode_by_name", "mode_by_id", "UsageError", "DataError", "InternalError",
-    "bundle_check", "container_slot", "parse_container_header", "library_path",
+    "bundle_check", "container_slot", "parse_container_header", "library_path", "Index",
 ]

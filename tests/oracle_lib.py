@@ -39,6 +39,8 @@ def lib() -> ctypes.CDLL:
         L.orc_trace_u8.argtypes = [ctypes.c_char_p, S, P, I, I, I, I, ctypes.POINTER(P)]
         L.orc_trace_free.argtypes = [P]
         L.orc_trace_get.argtypes = [P, ctypes.c_char_p, P, S, ctypes.POINTER(S)]
+        L.orc_retrieve.argtypes = [P, P, I, P, P, I, ctypes.c_double, I, P, P]
+        L.orc_match_pair.argtypes = [P, S, P, S, ctypes.c_double, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(I)]
         _lib = L
     return _lib
 
@@ -118,3 +120,30 @@ class Trace:
             lib().orc_trace_free(self._h)
         except Exception:
             pass
+
+
+def _pack(containers):
+    offs = np.zeros(len(containers) + 1, dtype=np.uint64)
+    offs[1:] = np.cumsum([len(c) for c in containers], dtype=np.uint64)
+    blob = np.frombuffer(b"".join(containers) or b"\0", dtype=np.uint8).copy()
+    return blob, offs
+
+
+def retrieve(index: list, queries: list, ratio: float = 0.85, depth: int = 50):
+    """The oracle's retrieve (eval.cpp:76-124) for each query over `index`
+    (ids in index order) -> (items int32 [nq, n], scores float64 [nq, n])."""
+    ib, io = _pack(index)
+    qb, qo = _pack(queries)
+    n, nq = len(index), len(queries)
+    items = np.empty((nq, n), dtype=np.int32)
+    scores = np.empty((nq, n), dtype=np.float64)
+    _check(lib().orc_retrieve(ib.ctypes.data, io.ctypes.data, n, qb.ctypes.data, qo.ctypes.data, nq, ratio, depth,
+                              items.ctypes.data, scores.ctypes.data))
+    return items, scores
+
+
+def match_pair(a: bytes, b: bytes, ratio: float = 0.85):
+    """The oracle's match_pair (eval.cpp:66-74) -> (global_similarity, local_match_count)."""
+    sim, loc = ctypes.c_double(), ctypes.c_int()
+    _check(lib().orc_match_pair(a, len(a), b, len(b), ratio, ctypes.byref(sim), ctypes.byref(loc)))
+    return sim.value, loc.value

@@ -90,3 +90,18 @@ def test_bundle_canonicalisation(oracle):
     respelled = "\n".join(lines)
     assert cg.bundle_check(respelled) == cg.bundle_check(text)
     assert oracle_lib.bundle_crc(respelled) == oracle_lib.bundle_crc(text)
+
+
+def test_oracle_retrieval_basics(oracle, bundle_b8):
+    """The oracle's retrieve on its own containers (test_pipeline.cpp:147-205)."""
+    frames = oracle.synth_frames(900, 6, 256, 192)
+    blobs = [oracle.encode(bundle_b8, f, 2) for f in frames]
+    items, scores = oracle.retrieve(blobs, blobs, 0.85, 50)
+    assert list(items[:, 0]) == list(range(6))
+    assert np.all(np.diff(scores, axis=1) <= 0)
+    head3, _ = oracle.retrieve(blobs, blobs[2:3], 0.85, 3)
+    head0, _ = oracle.retrieve(blobs, blobs[2:3], 0.85, 0)
+    assert sorted(head3[0, :3]) == sorted(head0[0, :3])
+    assert list(head3[0, 3:]) == list(head0[0, 3:])
+    sim, loc = oracle.match_pair(blobs[0], blobs[0])
+    assert sim == 1.0 and loc > 0
