@@ -1,0 +1,101 @@
+"""Secondary workloads of BASELINE.json on one B200; one
+JSON line per measurement. The driver's headline stays bench.py (configs[1]).
+
+  config 3: synthetic 1920x1080 frames, resized on the device to 640x360
+            (resize_max_side, 640 max side), 16K mode, streamed from pinned
+            host memory in batches through cdvz_gpu_encode_batch (e2e), plus
+            the same frames device-resident.
+  config 5: the octave kernel pair alone (k_blur + k_detect_walk, every
+            octave) at native 320x240 ... 3840x2160: HBM GB/s of the
+            algorithmic bytes and FP64 Tops against the measured pipe peak.
+
+  python bench_configs.py [--only 3|5]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+import bench  # noqa: E402  (peaks, FP64 op counts)
+
+
+def config3(cg, oracle_lib, bundle, frames=1024, batch=256):
+    ex = cg.Extractor(bundle, max_batch=batch)
+    mode = cg.mode_by_name("16K")
+    w, h = 1920, 1080
+    d = ex.synth_frames_device(4000, frames, w, h)
+    host = ex.pinned_buffer(frames * w * h)
+    host.array[:] = d.to_host(frames * w * h)
+    fr = host.array.reshape(frames, h, w)
+    got, status = ex.encode_batch(fr[:2], mode)  # parity spot check vs the oracle
+    parity = got == oracle_lib.encode_batch(bundle, fr[:2], mode.id)
+    for _ in range(2):
+        ex.encode_batch(fr[:batch], mode)
+    t0 = time.perf_counter()
+    for s in range(0, frames, batch):
+        out, st = ex.encode_batch(fr[s:s + batch], mode)
+    e2e = frames / (time.perf_counter() - t0)
+    slot = cg.container_slot(mode)
+    d_out, d_len = ex.device_buffer(frames * slot), ex.device_buffer(frames * 4)
+    ex.encode_device(d, frames, w, h, mode, d_out, d_len)
+    ex.sync()
+    ex.event_record(0)
+    for _ in range(3):
+        ex.encode_device(d, frames, w, h, mode, d_out, d_len)
+    ex.event_record(1)
+    dev = 3 * frames / (ex.event_elapsed(0, 1) / 1000.0)
+    ex.close()
+    return {"config": "configs[2]: synthetic 1920x1080 stream -> 640x360, 16K mode, B8, 1 B200",
+            "metric": "frames/s", "e2e_value": e2e, "device_value": dev, "frames": frames, "batch": batch,
+            "h2d_bytes_per_frame": w * h, "parity_first_2_frames": bool(parity),
+            "note": "e2e: pinned host frames through cdvz_gpu_encode_batch in batches of 256 (copies inside); "
+                    "device: frames resident in HBM, CUDA events"}
+
+
+def config5(cg, bundle):
+    ex = cg.Extractor(bundle, max_batch=4096)
+    hbm, _ = bench.measured_peaks()
+    f64_peak, f64_kind = bench.fp64_peak()
+    out = []
+    for (w, h) in ((320, 240), (640, 480), (1280, 720), (1920, 1080), (3840, 2160)):
+        count = int(max(4, 512 * 307200 // (w * h)))  # ~512 VGA frames of pixels per pass
+        d = ex.synth_frames_device(5000, count, w, h)
+        ms, by = ex.pyramid_bench(d, count, w, h, iters=5)
+        d.free()
+        ops = bench.pyramid_fp64_ops(w, h, octaves=4) * count  # bundle num_octaves = 4
+        out.append({"size": f"{w}x{h}", "frames": count, "ms_per_pass": ms,
+                    "frames_per_s": count / (ms / 1000.0),
+                    "hbm": {"achieved_gbs": by / (ms / 1000.0) / 1e9, "peak_gbs": hbm,
+                            "frac": by / (ms / 1000.0) / 1e9 / hbm},
+                    "fp64": {"achieved_tops": ops / (ms / 1000.0) / 1e12, "peak_tops": f64_peak,
+                             "frac": ops / (ms / 1000.0) / 1e12 / f64_peak, "peak_source": f64_kind}})
+    ex.close()
+    return {"config": "configs[4]: octave kernel pair (k_blur + k_detect_walk, every octave) at native size",
+            "sweep": out}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--only", default="")
+    args = ap.parse_args()
+    import oracle_lib
+    import paper_1705_09776_b200 as cg
+
+    bundle = oracle_lib.bundle_text("b8")
+    if args.only in ("", "3"):
+        print(json.dumps(config3(cg, oracle_lib, bundle)), flush=True)
+    if args.only in ("", "5"):
+        print(json.dumps(config5(cg, bundle)), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -141,6 +141,14 @@ int cdvz_gpu_host_alloc(cdvz_gpu_ctx* ctx, size_t bytes, void** ptr);
 int cdvz_gpu_host_free(cdvz_gpu_ctx* ctx, void* ptr);
 int cdvz_gpu_copy(cdvz_gpu_ctx* ctx, void* dst, const void* src, size_t bytes, int kind /* 1 H2D, 2 D2H, 3 D2D */);
 
+/* Microbenchmark of the octave kernel pair alone (k_blur + k_detect_walk over
+ * every octave): `count` device-resident u8 frames
+ * of width x height at native size, `iters` timed passes after one warm-up.
+ * Returns the CUDA-event time per pass and the pair's algorithmic bytes per
+ * pass. No reference counterpart: a measurement hook. */
+int cdvz_gpu_pyramid_bench(cdvz_gpu_ctx* ctx, const uint8_t* d_pixels, int width, int height, int count, int iters,
+                           double* ms_per_iter, double* bytes_per_iter);
+
 /* ------------------------------------------------------------------------
  * Compressed-domain matching and retrieval: an index of
  * CDVZ1 containers decoded on the device, queried in batches.

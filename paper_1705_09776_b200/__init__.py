@@ -111,6 +111,7 @@ def _lib() -> ctypes.CDLL:
         "cdvz_gpu_host_alloc": (I, [P, S, ctypes.POINTER(P)]),
         "cdvz_gpu_host_free": (I, [P, P]),
         "cdvz_gpu_copy": (I, [P, P, P, S, I]),
+        "cdvz_gpu_pyramid_bench": (I, [P, P, I, I, I, I, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]),
         "cdvz_gpu_index_create": (I, [I, P, P, I, P, ctypes.POINTER(P)]),
         "cdvz_gpu_index_destroy": (None, [P]),
         "cdvz_gpu_index_last_error": (ctypes.c_char_p, [P]),
@@ -310,6 +311,13 @@ class Extractor:
         buf = DeviceBuffer(self, max(1, count * width * height))
         self._check(self._lib.cdvz_gpu_synth_frames(self._ctx, base_seed, count, width, height, buf.ptr))
         return buf
+
+    def pyramid_bench(self, d_frames: DeviceBuffer, count: int, width: int, height: int, iters: int = 5) -> tuple:
+        """(ms per pass, algorithmic bytes per pass) of the octave kernel pair at native size."""
+        ms, by = ctypes.c_double(), ctypes.c_double()
+        self._check(self._lib.cdvz_gpu_pyramid_bench(self._ctx, d_frames.ptr, width, height, count, iters,
+                                                     ctypes.byref(ms), ctypes.byref(by)))
+        return ms.value, by.value
 
     def synth_frames(self, base_seed: int, count: int, width: int, height: int) -> np.ndarray:
         buf = self.synth_frames_device(base_seed, count, width, height)

@@ -855,6 +855,46 @@ int cdvz_gpu_synth_frames(cdvz_gpu_ctx* ctx, uint64_t base_seed, int count, int 
   });
 }
 
+int cdvz_gpu_pyramid_bench(cdvz_gpu_ctx* ctx, const uint8_t* d_pixels, int width, int height, int count, int iters,
+                           double* ms_per_iter, double* bytes_per_iter) {
+  return guarded(ctx, [&] {
+    if (!ctx || !d_pixels || !ms_per_iter || !bytes_per_iter) throw UsageError("null argument");
+    if (width < 16 || height < 16 || count < 1 || iters < 1) throw UsageError("bad microbenchmark geometry");
+    CDVZ_CUDA_CHECK(cudaSetDevice(ctx->device));
+    Lane& L = ctx->lanes[0];
+    if (!L.sA) L.init();
+    ctx->plan(L, width, height, count, false);
+    Batch b = L.bt;
+    b.nframes = count;
+    b.pix8 = d_pixels;
+    b.stride8 = width;
+    b.frame_bytes8 = (long long)height * width;
+    double bytes = 0.0;
+    for (int o = 0; o < b.n_oct; ++o) {
+      const double px = double(b.ow[o]) * b.oh[o];
+      const int ww = std::max(0, b.ow[o] - 2 * ctx->dc.margin), hh = std::max(0, b.oh[o] - 2 * ctx->dc.margin);
+      bytes += double(count) * (px * ((o == 0 ? 1.0 : 8.0) + 32.0) + 32.0 * ww * hh);
+    }
+    auto pass = [&] {
+      CDVZ_CUDA_CHECK(cudaMemsetAsync(b.raw_count, 0, sizeof(int) * count * std::max(1, b.n_oct), L.sA));
+      for (int o = 0; o < b.n_oct; ++o) {
+        CDVZ_CUDA_CHECK(launch_octave(b, ctx->dc, o, o == 0 ? 0 : 2, L.sA));
+        CDVZ_CUDA_CHECK(launch_detect(b, ctx->dc, o, L.tmap_ok[o] ? &L.tmap[o] : nullptr, L.sA));
+      }
+    };
+    pass();  // warm-up
+    CDVZ_CUDA_CHECK(cudaEventRecord(L.start, L.sA));
+    for (int i = 0; i < iters; ++i) pass();
+    CDVZ_CUDA_CHECK(cudaEventRecord(L.done, L.sA));
+    CDVZ_CUDA_CHECK(cudaEventSynchronize(L.done));
+    float ms = 0.f;
+    CDVZ_CUDA_CHECK(cudaEventElapsedTime(&ms, L.start, L.done));
+    *ms_per_iter = double(ms) / iters;
+    *bytes_per_iter = bytes;
+    L.geo_w = 0;  // the next encode re-plans (raw lists and bitmaps were left dirty)
+  });
+}
+
 int cdvz_gpu_device_alloc(cdvz_gpu_ctx* ctx, size_t bytes, void** ptr) {
   return guarded(ctx, [&] {
     CDVZ_CUDA_CHECK(cudaSetDevice(ctx->device));
