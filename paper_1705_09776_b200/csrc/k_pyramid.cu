@@ -463,7 +463,7 @@ constexpr int kStripCols = 30, kSegRows = 64, kRing = 8, kDetWarps = 2;
 struct DetWarpSmem {
   double ring[kRing][4][32];  // alpha rows: [row % kRing][coefficient][lane]
   double row[4][34];          // centre G row per level: [k][1 + lane], edges at 0 and 33
-  uint16_t queue[64];         // ((row - y0 + 1) << 5) | lane
+  uint16_t queue[128];        // ((row - y0 + 2) << 5) | lane
 };
 
 __global__ void __launch_bounds__(32 * kDetWarps, 8) k_detect_walk(Batch bt, DetConst dc, int o) {
@@ -481,37 +481,36 @@ __global__ void __launch_bounds__(32 * kDetWarps, 8) k_detect_walk(Batch bt, Det
   const bool edge = lane == 0 || lane == 31;
   const int xe = lane == 0 ? x - 1 : min(x + 1, w - 1);  // edge lanes' outer neighbour
   const int eslot = lane == 0 ? 0 : 33;
-  // Per-level column pointers, advanced one row per step.
+  // Per-level column pointers, advanced one row per load.
   const double* gp[4];
-  const double* ep[4];
+  long long eoff = (long long)(xe - xc);
   {
     const double* base = bt.pyr + f * bt.frame_doubles + (long long)(y0 - 2) * w;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      gp[k] = base + bt.plane_off[o][k] + xc;
-      ep[k] = base + bt.plane_off[o][k] + xe;
-    }
+    for (int k = 0; k < 4; ++k) gp[k] = base + bt.plane_off[o][k] + xc;
   }
-  double gU[4], gC[4], gD[4], gN[4], eC[4], eD[4], eN[4];
-  auto load_row = [&](double* g, double* e) {
+  // Rows live in a 4-slot register ring per level (U, C, D and the row in
+  // flight); the walk is unrolled by 4 so every slot index is static.
+  double g[4][4], e[4][4];
+  auto load_row = [&](int slot) {
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      g[k] = __ldg(gp[k]);
-      e[k] = edge ? __ldg(ep[k]) : 0.0;
+      g[slot][k] = __ldg(gp[k]);
+      e[slot][k] = edge ? __ldg(gp[k] + eoff) : 0.0;
       gp[k] += w;
-      ep[k] += w;
     }
   };
-  load_row(gU, eD);
-  load_row(gC, eC);
-  load_row(gN, eN);
+  load_row(0);
+  load_row(1);
+  load_row(2);
   const double oct_scale = ldexp(1.0, o);
-  int qn = 0, y_old = 0;
+  double ap[2][4];  // own alpha of the previous two rows (screened one row late)
+  int qn = 0;
   auto drain = [&]() {
     for (int qi = lane; qi - lane < qn; qi += 32) {
       if (qi < qn) {
-        const int e = S.queue[qi];
-        const int t = e & 31, yd = (e >> 5) + y0 - 1;
+        const int ent = S.queue[qi];
+        const int t = ent & 31, yd = (ent >> 5) + y0 - 2;
         exact_detect(bt, dc, f, o, w, yd, xs0 - 1 + t, &S.ring[(yd - 1) % kRing][0][0], &S.ring[yd % kRing][0][0],
                      &S.ring[(yd + 1) % kRing][0][0], 32, t, oct_scale);
       }
@@ -519,59 +518,53 @@ __global__ void __launch_bounds__(32 * kDetWarps, 8) k_detect_walk(Batch bt, Det
     qn = 0;
     __syncwarp();
   };
-  for (int ra = y0 - 1; ra <= y1; ++ra) {
+  const int T = y1 - y0 + 2;  // alpha rows y0 - 1 .. y1
+  for (int t0 = 0; t0 < T; t0 += 4) {
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      gD[k] = gN[k];
-      eD[k] = eN[k];
-    }
-    if (ra + 2 <= y1 + 1) load_row(gN, eN);
-    // sigma^2-normalised Laplacian of row ra (image.cpp:220-238,
-    // scale_space.cpp:148-151), then alpha = beta * L in column order.
+    for (int ph = 0; ph < 4; ++ph) {
+      const int t = t0 + ph;
+      if (t >= T) break;
+      const int ra = y0 - 1 + t;
+      const int sU = ph & 3, sC = (ph + 1) & 3, sD = (ph + 2) & 3, sN = (ph + 3) & 3;
+      if (ra + 2 <= y1 + 1) load_row(sN);
+      // sigma^2-normalised Laplacian of row ra (image.cpp:220-238,
+      // scale_space.cpp:148-151), then alpha = beta * L in column order.
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      S.row[k][lane + 1] = gC[k];
-      if (edge) S.row[k][eslot] = eC[k];
-    }
-    __syncwarp();
-    double L[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const double lap = gU[k] + gD[k] + S.row[k][lane] + S.row[k][lane + 2] - 4.0 * gC[k];
-      L[k] = dc.s2[k] * lap;
-    }
-    double a[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      double sum = dc.beta[i][0] * L[0];
-      sum = sum + dc.beta[i][1] * L[1];
-      sum = sum + dc.beta[i][2] * L[2];
-      sum = sum + dc.beta[i][3] * L[3];
-      a[i] = sum;
-      S.ring[ra % kRing][i][lane] = sum;
-    }
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      gU[k] = gC[k];
-      gC[k] = gD[k];
-      eC[k] = eD[k];
-    }
-    __syncwarp();
-    // Queued pixels (rows <= ra - 1) have their whole neighbourhood in the
-    // ring now; drain before the ring drops the oldest one's upper row.
-    if (qn >= 32 || (qn > 0 && ra - y_old >= kRing - 2)) drain();
-    if (ra >= y0 && ra < y1) {
-      const bool push = out_col && (!dc.screen || screen_pixel(a, dc));
-      const unsigned bal = __ballot_sync(0xffffffffu, push);
-      if (bal) {
-        if (qn == 0) y_old = ra;
-        if (push) S.queue[qn + __popc(bal & ((1u << lane) - 1u))] = uint16_t(((ra - y0 + 1) << 5) | lane);
-        qn += __popc(bal);
+      for (int k = 0; k < 4; ++k) {
+        S.row[k][lane + 1] = g[sC][k];
+        if (edge) S.row[k][eslot] = e[sC][k];
       }
       __syncwarp();
+      double L[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const double lap = g[sU][k] + g[sD][k] + S.row[k][lane] + S.row[k][lane + 2] - 4.0 * g[sC][k];
+        L[k] = dc.s2[k] * lap;
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        double sum = dc.beta[i][0] * L[0];
+        sum = sum + dc.beta[i][1] * L[1];
+        sum = sum + dc.beta[i][2] * L[2];
+        sum = sum + dc.beta[i][3] * L[3];
+        ap[ph & 1][i] = sum;
+        S.ring[ra % kRing][i][lane] = sum;
+      }
+      __syncwarp();
+      // Screen row ra - 1, whose 3x3 alpha neighbourhood is now complete.
+      const int rs = ra - 1;
+      if (rs >= y0 && rs < y1) {
+        const bool push = out_col && (!dc.screen || screen_pixel(ap[(ph + 1) & 1], dc));
+        const unsigned bal = __ballot_sync(0xffffffffu, push);
+        if (push) S.queue[qn + __popc(bal & ((1u << lane) - 1u))] = uint16_t(((rs - y0 + 2) << 5) | lane);
+        qn += __popc(bal);
+      }
     }
+    __syncwarp();
+    // Every queued pixel (rows <= the last alpha row - 1) has its
+    // neighbourhood in the ring; the ring keeps the 6 rows they need.
+    if (qn > 0) drain();
   }
-  if (qn > 0) drain();
 }
 
 constexpr size_t kDetSmem = sizeof(double) * (4 * kGH * kGW + kAH * 4 * kAW);
