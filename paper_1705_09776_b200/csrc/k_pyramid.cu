@@ -459,17 +459,21 @@ __global__ void __launch_bounds__(kDetThreads, 2)
 // pixels are queued and the queue is drained in full-warp passes by the exact
 // FP64 test (exact_detect, reading the 3x3 alpha neighbourhood from the ring)
 // before the ring can overwrite any row a queued pixel needs.
-constexpr int kStripCols = 30, kSegRows = 64, kRing = 8, kDetWarps = 2;
+constexpr int kStripCols = 30, kSegRows = 64, kRing = 6, kDetWarps = 3, kGRows = 6, kPrefetch = 3;
 struct DetWarpSmem {
-  double ring[kRing][4][32];  // alpha rows: [row % kRing][coefficient][lane]
-  double row[4][34];          // centre G row per level: [k][1 + lane], edges at 0 and 33
-  uint16_t queue[128];        // ((row - y0 + 2) << 5) | lane
+  double grow[kGRows][4][34];  // G rows in flight: [row % kGRows][level][1 + lane], edges at 0 and 33
+  double ring[kRing][4][32];   // alpha rows: [row % kRing][coefficient][lane]
+  uint16_t queue[128];         // ((row - y0 + 2) << 5) | lane
 };
 
-__global__ void __launch_bounds__(32 * kDetWarps, 8) k_detect_walk(Batch bt, DetConst dc, int o) {
-  __shared__ DetWarpSmem smem[kDetWarps];
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
+
+__global__ void __launch_bounds__(32 * kDetWarps) k_detect_walk(Batch bt, DetConst dc, int o) {
+  extern __shared__ __align__(16) uint8_t det_smem[];
   const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  DetWarpSmem& S = smem[wi];
+  DetWarpSmem& S = reinterpret_cast<DetWarpSmem*>(det_smem)[wi];
   const int f = blockIdx.z;
   const int w = bt.ow[o], h = bt.oh[o], m = dc.margin;
   const int xs0 = m + (blockIdx.x * kDetWarps + wi) * kStripCols;  // first window column of the strip
@@ -481,30 +485,33 @@ __global__ void __launch_bounds__(32 * kDetWarps, 8) k_detect_walk(Batch bt, Det
   const bool edge = lane == 0 || lane == 31;
   const int xe = lane == 0 ? x - 1 : min(x + 1, w - 1);  // edge lanes' outer neighbour
   const int eslot = lane == 0 ? 0 : 33;
-  // Per-level column pointers, advanced one row per load.
+  // G rows stream into a kGRows-row shared ring with cp.async, kPrefetch
+  // rows ahead of the row being differentiated.
   const double* gp[4];
-  long long eoff = (long long)(xe - xc);
+  const long long eoff = (long long)(xe - xc);
   {
     const double* base = bt.pyr + f * bt.frame_doubles + (long long)(y0 - 2) * w;
 #pragma unroll
     for (int k = 0; k < 4; ++k) gp[k] = base + bt.plane_off[o][k] + xc;
   }
-  // Rows live in a 4-slot register ring per level (U, C, D and the row in
-  // flight); the walk is unrolled by 4 so every slot index is static.
-  double g[4][4], e[4][4];
-  auto load_row = [&](int slot) {
+  int next_row = y0 - 2;
+  auto issue = [&]() {  // next G row into its slot (or an empty group past the segment)
+    if (next_row <= y1 + 1) {
+      double(*dst)[34] = S.grow[next_row % kGRows];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      g[slot][k] = __ldg(gp[k]);
-      e[slot][k] = edge ? __ldg(gp[k] + eoff) : 0.0;
-      gp[k] += w;
+      for (int k = 0; k < 4; ++k) {
+        cp_async8(&dst[k][lane + 1], gp[k]);
+        if (edge) cp_async8(&dst[k][eslot], gp[k] + eoff);
+        gp[k] += w;
+      }
     }
+    ++next_row;
+    asm volatile("cp.async.commit_group;" ::: "memory");
   };
-  load_row(0);
-  load_row(1);
-  load_row(2);
+#pragma unroll
+  for (int i = 0; i < kPrefetch + 2; ++i) issue();  // rows y0 - 2 .. y0 + 2
   const double oct_scale = ldexp(1.0, o);
-  double ap[2][4];  // own alpha of the previous two rows (screened one row late)
+  double ap[4];  // own alpha of the previous row (screened one row late)
   int qn = 0;
   auto drain = [&]() {
     for (int qi = lane; qi - lane < qn; qi += 32) {
@@ -525,46 +532,50 @@ __global__ void __launch_bounds__(32 * kDetWarps, 8) k_detect_walk(Batch bt, Det
       const int t = t0 + ph;
       if (t >= T) break;
       const int ra = y0 - 1 + t;
-      const int sU = ph & 3, sC = (ph + 1) & 3, sD = (ph + 2) & 3, sN = (ph + 3) & 3;
-      if (ra + 2 <= y1 + 1) load_row(sN);
+      // Rows ra - 1 .. ra + 1 must have landed: rows up to ra + 1 + kPrefetch - 1
+      // may still be in flight.
+      asm volatile("cp.async.wait_group %0;" ::"n"(kPrefetch - 1) : "memory");
+      __syncwarp();
+      const double(*rU)[34] = S.grow[(ra - 1) % kGRows];
+      const double(*rC)[34] = S.grow[ra % kGRows];
+      const double(*rD)[34] = S.grow[(ra + 1) % kGRows];
       // sigma^2-normalised Laplacian of row ra (image.cpp:220-238,
       // scale_space.cpp:148-151), then alpha = beta * L in column order.
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        S.row[k][lane + 1] = g[sC][k];
-        if (edge) S.row[k][eslot] = e[sC][k];
-      }
-      __syncwarp();
       double L[4];
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        const double lap = g[sU][k] + g[sD][k] + S.row[k][lane] + S.row[k][lane + 2] - 4.0 * g[sC][k];
+        const double lap = rU[k][lane + 1] + rD[k][lane + 1] + rC[k][lane] + rC[k][lane + 2] - 4.0 * rC[k][lane + 1];
         L[k] = dc.s2[k] * lap;
       }
+      double an[4];
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         double sum = dc.beta[i][0] * L[0];
         sum = sum + dc.beta[i][1] * L[1];
         sum = sum + dc.beta[i][2] * L[2];
         sum = sum + dc.beta[i][3] * L[3];
-        ap[ph & 1][i] = sum;
+        an[i] = sum;
         S.ring[ra % kRing][i][lane] = sum;
       }
       __syncwarp();
+      issue();  // row ra + 4 into the slot of row ra - 2, no longer needed
       // Screen row ra - 1, whose 3x3 alpha neighbourhood is now complete.
       const int rs = ra - 1;
       if (rs >= y0 && rs < y1) {
-        const bool push = out_col && (!dc.screen || screen_pixel(ap[(ph + 1) & 1], dc));
+        const bool push = out_col && (!dc.screen || screen_pixel(ap, dc));
         const unsigned bal = __ballot_sync(0xffffffffu, push);
         if (push) S.queue[qn + __popc(bal & ((1u << lane) - 1u))] = uint16_t(((rs - y0 + 2) << 5) | lane);
         qn += __popc(bal);
       }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) ap[i] = an[i];
     }
     __syncwarp();
     // Every queued pixel (rows <= the last alpha row - 1) has its
     // neighbourhood in the ring; the ring keeps the 6 rows they need.
     if (qn > 0) drain();
   }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
 
 constexpr size_t kDetSmem = sizeof(double) * (4 * kGH * kGW + kAH * 4 * kAW);
@@ -591,7 +602,14 @@ cudaError_t launch_detect(const Batch& bt, const DetConst& dc, int o, const CUte
   if (dc.walk) {
     const int strips = (ww + kStripCols - 1) / kStripCols;
     dim3 grid((strips + kDetWarps - 1) / kDetWarps, (hh + kSegRows - 1) / kSegRows, bt.nframes);
-    k_detect_walk<<<grid, 32 * kDetWarps, 0, st>>>(bt, dc, o);
+    constexpr int smem = int(sizeof(DetWarpSmem)) * kDetWarps;
+    static bool walk_configured = false;
+    if (!walk_configured) {
+      cudaError_t e = cudaFuncSetAttribute(k_detect_walk, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      if (e != cudaSuccess) return e;
+      walk_configured = true;
+    }
+    k_detect_walk<<<grid, 32 * kDetWarps, smem, st>>>(bt, dc, o);
     return cudaGetLastError();
   }
   dim3 grid((ww + kDetW - 1) / kDetW, (hh + kDetH - 1) / kDetH, bt.nframes);
