@@ -78,14 +78,28 @@ __device__ __forceinline__ Frame resolve(const Batch& bt, const DetConst& dc, in
 
 }  // namespace
 
-// One warp per selected point (descriptor.cpp:172-232).
-__global__ void __launch_bounds__(128) k_orient(Batch bt, DetConst dc) {
-  __shared__ double sval[4][32];
-  __shared__ int sbin[4][32];
-  __shared__ double hist[4][36];
+// One warp per selected point (descriptor.cpp:172-232). The disk's samples
+// are evaluated 32 at a time and parked (bin, value) in shared memory; a
+// stable counting sort by bin (warp match + per-bin running offsets) then
+// gives every bin the list of its samples in raster order, and the lane that
+// owns a bin adds them in that order — the reference's per-bin add order —
+// touching only its own samples.
+constexpr int kOrientCap = 512;  // box of the 3.96-sigma disk: (2 * 10.5 + 1)^2 <= 484 for sigma <= 2.66
+constexpr int kOrientWarps = 4;
+struct OrientSmem {
+  double val[kOrientCap];
+  uint16_t list[kOrientCap];
+  uint8_t bin[kOrientCap];
+  int cnt[36], off[36], run[36];
+  double hist[36];
+};
+
+__global__ void __launch_bounds__(32 * kOrientWarps) k_orient(Batch bt, DetConst dc) {
+  __shared__ OrientSmem smem[kOrientWarps];
   const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  OrientSmem& S = smem[wi];
   const int f = blockIdx.y;
-  const int r = blockIdx.x * 4 + wi;
+  const int r = blockIdx.x * kOrientWarps + wi;
   if (r >= bt.sel_count[f]) return;  // warp-uniform; no block barrier below
   const KP k = bt.sel[(long long)f * bt.select_n + r];
   const Frame fr = resolve(bt, dc, f, k);
@@ -97,51 +111,76 @@ __global__ void __launch_bounds__(128) k_orient(Batch bt, DetConst dc) {
   const int y_lo = max(1, static_cast<int>(ceil(fr.y - radius)));
   const int y_hi = min(fr.h - 2, static_cast<int>(floor(fr.y + radius)));
   const int nx = x_hi - x_lo + 1, ny = y_hi - y_lo + 1;
-  const int npx = (nx > 0 && ny > 0) ? nx * ny : 0;
-  double acc0 = 0.0, acc1 = 0.0;  // bins lane and lane + 32
-  for (int base = 0; base < npx; base += 32) {
-    const int q = base + lane;
-    int bin = -1;
+  int npx = (nx > 0 && ny > 0) ? nx * ny : 0;
+  if (npx > kOrientCap) {  // outside the supported scale range: flag the frame
+    if (lane == 0) atomicOr(&bt.status[f], 8);
+    npx = 0;
+  }
+  for (int b = lane; b < 36; b += 32) S.cnt[b] = 0;
+  __syncwarp();
+  for (int q = lane; q < npx; q += 32) {
+    const int ix = x_lo + q % nx, iy = y_lo + q / nx;
+    const double dx = ix - fr.x, dy = iy - fr.y;
+    const double d2 = dx * dx + dy * dy;
+    int bin = 255;
     double val = 0.0;
-    if (q < npx) {
-      const int ix = x_lo + q % nx, iy = y_lo + q / nx;
-      const double dx = ix - fr.x, dy = iy - fr.y;
-      const double d2 = dx * dx + dy * dy;
-      if (!(d2 >= radius * radius)) {
-        const double* row = fr.lvl + (long long)iy * fr.w + ix;
-        const double gx = 0.5 * (row[1] - row[-1]);
-        const double gy = 0.5 * (row[fr.w] - row[-fr.w]);
-        const double mag = hypot(gx, gy);
-        if (mag != 0.0) {
-          const double ang = wrap_angle(atan2(gy, gx));
-          bin = static_cast<int>(floor(ang / kTwoPi * 36 + 0.5)) % 36;
-          val = mag * exp(-d2 / denom);
-        }
+    if (!(d2 >= radius * radius)) {
+      const double* row = fr.lvl + (long long)iy * fr.w + ix;
+      const double gx = 0.5 * (row[1] - row[-1]);
+      const double gy = 0.5 * (row[fr.w] - row[-fr.w]);
+      const double mag = hypot(gx, gy);
+      if (mag != 0.0) {
+        const double ang = wrap_angle(atan2(gy, gx));
+        bin = static_cast<int>(floor(ang / kTwoPi * 36 + 0.5)) % 36;
+        val = mag * exp(-d2 / denom);
+        atomicAdd(&S.cnt[bin], 1);
       }
     }
-    sbin[wi][lane] = bin;
-    sval[wi][lane] = val;
+    S.bin[q] = uint8_t(bin);
+    S.val[q] = val;
+  }
+  __syncwarp();
+  if (lane == 0) {
+    int o = 0;
+    for (int b = 0; b < 36; ++b) {
+      S.off[b] = o;
+      S.run[b] = 0;
+      o += S.cnt[b];
+    }
+  }
+  __syncwarp();
+  // Stable scatter of sample indices into per-bin lists (raster order kept).
+  for (int base = 0; base < npx; base += 32) {
+    const int q = base + lane;
+    const int b = q < npx ? S.bin[q] : 255;
+    const unsigned grp = __match_any_sync(0xffffffffu, b);
+    const int rank = __popc(grp & ((1u << lane) - 1u));
+    const int start = b < 36 ? S.off[b] + S.run[b] : 0;
     __syncwarp();
-    const int nsmp = min(32, npx - base);
-    for (int s = 0; s < nsmp; ++s) {
-      const int b = sbin[wi][s];
-      if (b == lane) acc0 += sval[wi][s];
-      else if (b == lane + 32) acc1 += sval[wi][s];
+    if (b < 36) {
+      S.list[start + rank] = uint16_t(q);
+      if (rank == 0) S.run[b] += __popc(grp);
     }
     __syncwarp();
   }
-  hist[wi][lane] = acc0;
-  if (lane < 4) hist[wi][lane + 32] = acc1;
+  // Ordered per-bin sums: lane L owns bins L and L + 32.
+  double acc0 = 0.0, acc1 = 0.0;
+  for (int i = S.off[lane], e = i + S.cnt[lane]; i < e; ++i) acc0 += S.val[S.list[i]];
+  if (lane < 4)
+    for (int i = S.off[lane + 32], e = i + S.cnt[lane + 32]; i < e; ++i) acc1 += S.val[S.list[i]];
+  double* hist_w = S.hist;
+  hist_w[lane] = acc0;
+  if (lane < 4) hist_w[lane + 32] = acc1;
   __syncwarp();
   for (int pass = 0; pass < 2; ++pass) {
-    double s0 = (hist[wi][(lane + 35) % 36] + hist[wi][lane] + hist[wi][(lane + 1) % 36]) / 3.0, s1 = 0.0;
-    if (lane < 4) s1 = (hist[wi][(lane + 32 + 35) % 36] + hist[wi][lane + 32] + hist[wi][(lane + 33) % 36]) / 3.0;
+    double s0 = (hist_w[(lane + 35) % 36] + hist_w[lane] + hist_w[(lane + 1) % 36]) / 3.0, s1 = 0.0;
+    if (lane < 4) s1 = (hist_w[(lane + 32 + 35) % 36] + hist_w[lane + 32] + hist_w[(lane + 33) % 36]) / 3.0;
     __syncwarp();
-    hist[wi][lane] = s0;
-    if (lane < 4) hist[wi][lane + 32] = s1;
+    hist_w[lane] = s0;
+    if (lane < 4) hist_w[lane + 32] = s1;
     __syncwarp();
   }
-  double peak = fmax(hist[wi][lane], lane < 4 ? hist[wi][lane + 32] : 0.0);
+  double peak = fmax(hist_w[lane], lane < 4 ? hist_w[lane + 32] : 0.0);
 #pragma unroll
   for (int d = 16; d > 0; d >>= 1) peak = fmax(peak, __shfl_xor_sync(0xffffffffu, peak, d));
   peak = fmax(peak, 0.0);
@@ -158,7 +197,7 @@ __global__ void __launch_bounds__(128) k_orient(Batch bt, DetConst dc) {
     bool is_peak = false;
     double theta = 0.0;
     if (b < 36) {
-      const double v = hist[wi][b], l = hist[wi][(b + 35) % 36], rr = hist[wi][(b + 1) % 36];
+      const double v = hist_w[b], l = hist_w[(b + 35) % 36], rr = hist_w[(b + 1) % 36];
       if (!(v <= 0.8 * peak || v < l || v < rr)) {
         const double fit = l - 2.0 * v + rr;
         const double delta = fabs(fit) > 1e-12 ? 0.5 * (l - rr) / fit : 0.0;
@@ -548,7 +587,7 @@ __global__ void __launch_bounds__(32 * kPBWarps) k_describe(Batch bt, DetConst d
 }
 
 cudaError_t launch_describe(const Batch& bt, const DetConst& dc, const Model& md, const EncodeConst& ec, cudaStream_t st) {
-  k_orient<<<dim3((bt.select_n + 3) / 4, bt.nframes), 128, 0, st>>>(bt, dc);
+  k_orient<<<dim3((bt.select_n + kOrientWarps - 1) / kOrientWarps, bt.nframes), 32 * kOrientWarps, 0, st>>>(bt, dc);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   k_expand<<<bt.nframes, 1024, 0, st>>>(bt);
