@@ -83,17 +83,32 @@ __global__ void __launch_bounds__(kMergeThreads) k_merge_octave(Batch bt, int o)
   const KP* raw = bt.raw + ((long long)f * bt.n_oct + o) * bt.cap_oct;
 
   // Exclusive popcount prefix of the bitmap, per word, in shared memory.
+  // Warp w owns a contiguous segment of words and reads it coalesced: pass 1
+  // counts the segment, a block scan places the segments, pass 2 re-reads
+  // each 32-word chunk and scans it across the lanes.
   int* prefix = sm;  // nwords
   {
-    const int per = (nwords + blockDim.x - 1) / blockDim.x;
-    const int lo = min(nwords, int(threadIdx.x) * per), hi = min(nwords, lo + per);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int seg = (nwords + nw - 1) / nw;
+    const int lo = min(nwords, wid * seg), hi = min(nwords, lo + seg);
     int cnt = 0;
-    for (int i = lo; i < hi; ++i) cnt += __popc(bm[i]);
+    for (int i = lo + lane; i < hi; i += 32) cnt += __popc(bm[i]);
+    cnt = __reduce_add_sync(0xffffffffu, cnt);
     int total = 0;
-    int run = block_exclusive_scan(cnt, warp_tot, total);
-    for (int i = lo; i < hi; ++i) {
-      prefix[i] = run;
-      run += __popc(bm[i]);
+    // One value per warp through the block scan (lanes other than 0 add 0).
+    int base = block_exclusive_scan(lane == 0 ? cnt : 0, warp_tot, total);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    for (int c = lo; c < hi; c += 32) {
+      const int i = c + lane;
+      const int v = i < hi ? __popc(bm[i]) : 0;
+      int incl = v;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, d);
+        if (lane >= d) incl += t;
+      }
+      if (i < hi) prefix[i] = base + incl - v;
+      base += __shfl_sync(0xffffffffu, incl, 31);
     }
   }
   __syncthreads();
