@@ -449,7 +449,7 @@ __global__ void __launch_bounds__(kDetThreads, 2)
 
 // ------------------------------------------------------- K1b v2: extrema walk
 // One WARP = a strip of 30 detection-window columns (lanes 1..30; lanes 0 and
-// 31 are the 1-column halo) walking a segment of kSegRows window rows top to
+// 31 are the 1-column halo) walking a segment of ~kSegTarget window rows top to
 // bottom. Per row the warp reads the four G levels of the next row once
 // (coalesced; the edge lanes also read their outer neighbour), slides the
 // Laplacian's up/centre/down rows in registers, takes left/right from a
@@ -459,7 +459,7 @@ __global__ void __launch_bounds__(kDetThreads, 2)
 // pixels are queued and the queue is drained in full-warp passes by the exact
 // FP64 test (exact_detect, reading the 3x3 alpha neighbourhood from the ring)
 // before the ring can overwrite any row a queued pixel needs.
-constexpr int kStripCols = 30, kSegRows = 64, kRing = 6, kDetWarps = 3, kGRows = 6, kPrefetch = 3;
+constexpr int kStripCols = 30, kSegTarget = 96, kRing = 6, kDetWarps = 3, kPrefetch = 3, kGRows = kPrefetch + 2;
 struct DetWarpSmem {
   double grow[kGRows][4][34];  // G rows in flight: [row % kGRows][level][1 + lane], edges at 0 and 33
   double ring[kRing][4][32];   // alpha rows: [row % kRing][coefficient][lane]
@@ -470,14 +470,14 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
 }
 
-__global__ void __launch_bounds__(32 * kDetWarps) k_detect_walk(Batch bt, DetConst dc, int o) {
+__global__ void __launch_bounds__(32 * kDetWarps) k_detect_walk(Batch bt, DetConst dc, int o, int seg_rows) {
   extern __shared__ __align__(16) uint8_t det_smem[];
   const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
   DetWarpSmem& S = reinterpret_cast<DetWarpSmem*>(det_smem)[wi];
   const int f = blockIdx.z;
   const int w = bt.ow[o], h = bt.oh[o], m = dc.margin;
   const int xs0 = m + (blockIdx.x * kDetWarps + wi) * kStripCols;  // first window column of the strip
-  const int y0 = m + blockIdx.y * kSegRows, y1 = min(h - m, y0 + kSegRows);
+  const int y0 = m + blockIdx.y * seg_rows, y1 = min(h - m, y0 + seg_rows);
   if (xs0 >= w - m || y0 >= y1) return;  // warp-uniform
   const int x = xs0 - 1 + lane;
   const bool out_col = lane >= 1 && lane <= kStripCols && x < w - m;
@@ -600,8 +600,11 @@ cudaError_t launch_detect(const Batch& bt, const DetConst& dc, int o, const CUte
     configured = true;
   }
   if (dc.walk) {
+    // Balanced row segments of about kSegTarget rows (each costs 4 extra G
+    // rows and 2 extra alpha rows at its ends).
     const int strips = (ww + kStripCols - 1) / kStripCols;
-    dim3 grid((strips + kDetWarps - 1) / kDetWarps, (hh + kSegRows - 1) / kSegRows, bt.nframes);
+    const int nseg = (hh + kSegTarget - 1) / kSegTarget, seg_rows = (hh + nseg - 1) / nseg;
+    dim3 grid((strips + kDetWarps - 1) / kDetWarps, nseg, bt.nframes);
     constexpr int smem = int(sizeof(DetWarpSmem)) * kDetWarps;
     static bool walk_configured = false;
     if (!walk_configured) {
@@ -609,7 +612,7 @@ cudaError_t launch_detect(const Batch& bt, const DetConst& dc, int o, const CUte
       if (e != cudaSuccess) return e;
       walk_configured = true;
     }
-    k_detect_walk<<<grid, 32 * kDetWarps, smem, st>>>(bt, dc, o);
+    k_detect_walk<<<grid, 32 * kDetWarps, smem, st>>>(bt, dc, o, seg_rows);
     return cudaGetLastError();
   }
   dim3 grid((ww + kDetW - 1) / kDetW, (hh + kDetH - 1) / kDetH, bt.nframes);
