@@ -277,11 +277,14 @@ class Extractor:
         self._check(self._lib.cdvz_gpu_kernel_stats(self._ctx, ctypes.byref(n), ctypes.byref(ms), ctypes.byref(by)))
         return {"launches": n.value, "pyramid_ms": ms.value, "pyramid_bytes": by.value}
 
-    def set_debug(self, on: bool = True, exact_only: bool = False, serial: bool = False, no_tma: bool = False) -> None:
+    def set_debug(self, on: bool = True, exact_only: bool = False, serial: bool = False, no_tma: bool = False,
+                  tile_detect: bool = False) -> None:
         """on: keep per-octave lists; exact_only: bypass the FP32 extrema screen;
-        serial: no kernel overlap (standalone per-kernel timing); no_tma: plain
-        loads instead of TMA in the extrema kernel."""
-        flags = (1 if on else 0) | (2 if exact_only else 0) | (4 if serial else 0) | (8 if no_tma else 0)
+        serial: no kernel overlap (standalone per-kernel timing); tile_detect:
+        the first-generation TMA tile extrema kernel instead of the column walk
+        (a cross-check); no_tma: that tile kernel with plain loads."""
+        flags = ((1 if on else 0) | (2 if exact_only else 0) | (4 if serial else 0) | (8 if no_tma else 0)
+                 | (16 if tile_detect else 0))
         self._check(self._lib.cdvz_gpu_set_debug(self._ctx, flags))
 
     def debug_get(self, name: str, frame: int) -> np.ndarray:
