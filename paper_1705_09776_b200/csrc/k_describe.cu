@@ -364,7 +364,7 @@ __global__ void __launch_bounds__(256) k_sample(Batch bt) {
 constexpr int kPBWarps = 4;
 struct PhaseBSmem {
   double2 ring[3][2][kMaxSamples];  // [slot][q][i]
-  double acc[2][2][128];            // [q][set: 0 left, 1 right][cell * 8 + bin]
+  double acc[2][2][128];            // [q][set: 0 left, 1 right][bin * 16 + cell] (cells on distinct banks)
   double wf[2][2][kMaxSamples];     // [q][d][i]: 1 - f, f of the cell coordinate
   int c0[2][kMaxSamples];           // [q][i]: floor(u * inv_cell + 1.5)
 };
@@ -433,9 +433,9 @@ __global__ void __launch_bounds__(32 * kPBWarps) k_describe(Batch bt, DetConst d
         // Band boundary: the first two sub-patch partials are complete.
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
-          tot[k] = acc[8 * hl + k] + acc[128 + 8 * hl + k];
-          acc[8 * hl + k] = 0.0;
-          acc[128 + 8 * hl + k] = 0.0;
+          tot[k] = acc[16 * k + hl] + acc[128 + 16 * k + hl];
+          acc[16 * k + hl] = 0.0;
+          acc[128 + 16 * k + hl] = 0.0;
         }
       }
       __syncwarp();
@@ -445,7 +445,7 @@ __global__ void __launch_bounds__(32 * kPBWarps) k_describe(Batch bt, DetConst d
           const double wv = S.wf[q][dv][j];
           const double2* rowp = S.ring[j % 3][q];
           const double* wfq = &S.wf[q][0][0];
-          const int cell8 = (cy * 4 + cx) * 8;
+          const int cell = cy * 4 + cx;
           // Two-stage software pipeline: visit i + 1 is decoded while visit
           // i's bin chain is updated, so a visit's critical path is one
           // shared load -> add -> store.
@@ -460,7 +460,7 @@ __global__ void __launch_bounds__(32 * kPBWarps) k_describe(Batch bt, DetConst d
             const int b0 = static_cast<int>(obf) & 7;
             const bool own = (b0 & 1) == par;
             const double base = rec.x * wv * wu;
-            o = cell8 + (i < kSub ? 0 : 128) + (own ? b0 : (b0 + 1) & 7);
+            o = cell + (i < kSub ? 0 : 128) + 16 * (own ? b0 : (b0 + 1) & 7);
             x = base * (own ? 1.0 - fo : fo);
           };
           int o = 0;
@@ -480,7 +480,7 @@ __global__ void __launch_bounds__(32 * kPBWarps) k_describe(Batch bt, DetConst d
     }
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
-      const int e = 8 * hl + k;
+      const int e = 16 * k + hl;
       tot[k] = samples > kSub ? (tot[k] + acc[e]) + acc[128 + e] : acc[e];
     }
     __syncwarp();
