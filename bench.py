@@ -318,6 +318,7 @@ def main():
     # Secondary workload: the paper's 512-component GMM bundle.
     b512 = None
     if args.bundle == "b8" and not args.no_b512:
+        ex.trim()  # one context's batch buffers at a time
         with open(os.path.join(ROOT, "tests", "golden", "bundle_b512.txt")) as f:
             ex512 = cg.Extractor(f.read(), device=device, max_batch=args.max_batch)
         for _ in range(2):

@@ -141,6 +141,10 @@ int cdvz_gpu_host_alloc(cdvz_gpu_ctx* ctx, size_t bytes, void** ptr);
 int cdvz_gpu_host_free(cdvz_gpu_ctx* ctx, void* ptr);
 int cdvz_gpu_copy(cdvz_gpu_ctx* ctx, void* dst, const void* src, size_t bytes, int kind /* 1 H2D, 2 D2H, 3 D2D */);
 
+/* Releases the context's per-batch device buffers (pyramid, lists, sample
+ * records; they are re-planned by the next call). The model tables stay. */
+int cdvz_gpu_trim(cdvz_gpu_ctx* ctx);
+
 /* Microbenchmark of the octave kernel pair alone (k_blur + k_detect_walk over
  * every octave): `count` device-resident u8 frames
  * of width x height at native size, `iters` timed passes after one warm-up.

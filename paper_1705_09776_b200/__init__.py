@@ -99,6 +99,7 @@ def _lib() -> ctypes.CDLL:
         "cdvz_gpu_encode_device": (I, [P, P, I, I, S, I, I, I, P, P]),
         "cdvz_gpu_container_slot": (S, [I]),
         "cdvz_gpu_sync": (I, [P]),
+        "cdvz_gpu_trim": (I, [P]),
         "cdvz_gpu_stage_times": (I, [P, P]),
         "cdvz_gpu_kernel_stats": (I, [P, ctypes.POINTER(I), ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]),
         "cdvz_gpu_debug_get": (I, [P, ctypes.c_char_p, I, P, S, ctypes.POINTER(S)]),
@@ -262,6 +263,10 @@ class Extractor:
         m = mode if isinstance(mode, ModeSpec) else (mode_by_name(mode) if isinstance(mode, str) else mode_by_id(mode))
         self._check(self._lib.cdvz_gpu_encode_device(self._ctx, d_frames.ptr, width, height, width, count, m.id,
                                                      max_side, d_out.ptr, d_lengths.ptr))
+
+    def trim(self) -> None:
+        """Free the per-batch device buffers (re-planned by the next encode)."""
+        self._check(self._lib.cdvz_gpu_trim(self._ctx))
 
     def sync(self) -> None:
         self._check(self._lib.cdvz_gpu_sync(self._ctx))

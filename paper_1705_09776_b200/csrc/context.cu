@@ -650,6 +650,22 @@ int cdvz_gpu_encode_device(cdvz_gpu_ctx* ctx, const uint8_t* d_pixels, int width
   });
 }
 
+int cdvz_gpu_trim(cdvz_gpu_ctx* ctx) {
+  return guarded(ctx, [&] {
+    if (!ctx) throw UsageError("null context");
+    CDVZ_CUDA_CHECK(cudaSetDevice(ctx->device));
+    CDVZ_CUDA_CHECK(cudaStreamSynchronize(ctx->st));
+    for (auto& l : ctx->lanes) {
+      if (l.sA) CDVZ_CUDA_CHECK(cudaStreamSynchronize(l.sA));
+      if (l.sB) CDVZ_CUDA_CHECK(cudaStreamSynchronize(l.sB));
+      l.release();
+    }
+    ctx->stage_in.release();
+    ctx->stage_out.release();
+    ctx->stage_len.release();
+  });
+}
+
 int cdvz_gpu_sync(cdvz_gpu_ctx* ctx) {
   return guarded(ctx, [&] { CDVZ_CUDA_CHECK(cudaStreamSynchronize(ctx->st)); });
 }
