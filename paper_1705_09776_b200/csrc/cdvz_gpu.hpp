@@ -9,6 +9,8 @@
 //   EncodedImage encode_image(img, bundle, mode,     std::vector<uint8_t> cdvz::gpu::encode_image(
 //       Engine, StageTimings*, EncodeOptions)            img, bundle, mode, timings, opts)
 //   serialize_container(enc)                         (returned directly: CDVZ1 bytes)
+//   RankedList retrieve(query, id, index, opts)      cdvz::gpu::retrieve({(id, bytes)...}, Index, opts)
+//   MatchResult match_pair(a, b, opts)               cdvz::gpu::match_pair(a_bytes, Index, item, opts)
 //
 // Images are 8-bit grey rasters (the byte/255 semantics of load_image,
 // image.cpp:79-87). Errors keep the reference's exception types: UsageError
@@ -17,6 +19,7 @@
 // meaning (results never depend on it, parallel.hpp:16-18) and is dropped.
 #pragma once
 
+#include <algorithm>
 #include <fstream>
 #include <map>
 #include <memory>
@@ -167,6 +170,93 @@ inline std::vector<std::vector<uint8_t>> encode_batch(const std::vector<const Gr
 inline std::vector<uint8_t> encode_image(const GrayImage8& img, const ModelBundle& bundle, const ModeSpec& mode,
                                          StageTimings* timings = nullptr, const EncodeOptions& opts = {}) {
   return encode_batch({&img}, bundle, mode, timings, opts)[0];
+}
+
+// ------------------------------------------------ retrieval (eval.hpp:17-55)
+struct MatchResult {  // eval.hpp:17-20
+  double global_similarity = -1.0;
+  int local_match_count = 0;
+};
+struct RankedItem {  // eval.hpp:22-25
+  std::string id;
+  double score = 0.0;
+};
+struct RankedList {  // eval.hpp:27-30
+  std::string query;
+  std::vector<RankedItem> items;
+};
+struct MatchOptions {  // eval.hpp:32-35
+  double ratio_test = 0.85;
+  int rerank_depth = 50;
+};
+
+// The `index` argument of retrieve (a vector of (id, container) pairs),
+// decoded once onto a device.
+class Index {
+ public:
+  Index(const std::vector<std::pair<std::string, std::vector<uint8_t>>>& items, int device = 0) {
+    std::vector<uint8_t> blob;
+    std::vector<std::size_t> off{0};
+    for (const auto& it : items) {
+      blob.insert(blob.end(), it.second.begin(), it.second.end());
+      off.push_back(blob.size());
+      ids_.push_back(it.first);
+    }
+    std::vector<int32_t> order(items.size()), rank(items.size());
+    for (std::size_t i = 0; i < order.size(); ++i) order[i] = int32_t(i);
+    std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return ids_[a] < ids_[b]; });
+    for (std::size_t r = 0; r < order.size(); ++r) rank[std::size_t(order[r])] = int32_t(r);
+    cdvz_gpu_index* idx = nullptr;
+    raise_for(cdvz_gpu_index_create(device, blob.empty() ? nullptr : blob.data(), off.data(), int(items.size()),
+                                    rank.data(), &idx),
+              cdvz_gpu_index_last_error(nullptr));
+    idx_.reset(idx, cdvz_gpu_index_destroy);
+  }
+  cdvz_gpu_index* handle() const { return idx_.get(); }
+  const std::vector<std::string>& ids() const { return ids_; }
+
+ private:
+  std::shared_ptr<cdvz_gpu_index> idx_;
+  std::vector<std::string> ids_;
+};
+
+// retrieve (eval.cpp:76-124) for a batch of query containers.
+inline std::vector<RankedList> retrieve(const std::vector<std::pair<std::string, std::vector<uint8_t>>>& queries,
+                                        const Index& index, const MatchOptions& opts = {}) {
+  std::vector<uint8_t> blob;
+  std::vector<std::size_t> off{0};
+  for (const auto& q : queries) {
+    blob.insert(blob.end(), q.second.begin(), q.second.end());
+    off.push_back(blob.size());
+  }
+  const std::size_t n = index.ids().size();
+  std::vector<int32_t> items(queries.size() * n);
+  std::vector<double> scores(queries.size() * n);
+  std::vector<RankedList> out(queries.size());
+  if (queries.empty()) return out;
+  raise_for(cdvz_gpu_retrieve(index.handle(), blob.data(), off.data(), int(queries.size()), opts.ratio_test,
+                              opts.rerank_depth, 0, items.data(), scores.data()),
+            cdvz_gpu_index_last_error(index.handle()));
+  for (std::size_t q = 0; q < queries.size(); ++q) {
+    out[q].query = queries[q].first;
+    for (std::size_t r = 0; r < n; ++r)
+      out[q].items.push_back({index.ids()[std::size_t(items[q * n + r])], scores[q * n + r]});
+  }
+  return out;
+}
+
+// match_pair (eval.cpp:66-74) of query container a and index item i.
+inline MatchResult match_pair(const std::vector<uint8_t>& a, const Index& index, int item,
+                              const MatchOptions& opts = {}) {
+  const std::size_t off[2] = {0, a.size()};
+  const int32_t pair[2] = {0, item};
+  MatchResult r;
+  int32_t local = 0;
+  raise_for(cdvz_gpu_match_pairs(index.handle(), a.data(), off, 1, pair, 1, opts.ratio_test, &r.global_similarity,
+                                 &local),
+            cdvz_gpu_index_last_error(index.handle()));
+  r.local_match_count = local;
+  return r;
 }
 
 }  // namespace gpu

@@ -82,3 +82,16 @@ def test_cpp_shim_compiles_and_validates_bundles(tmp_path):
     good = os.path.join(ROOT, "tests", "golden", "bundle_b8.txt")
     p = subprocess.run([str(exe), good, "3K", "x.pgm", "y.cdvz"], capture_output=True, text=True)
     assert p.returncode == 1 and "unknown mode" in p.stderr
+
+
+def test_cpp_retrieval_shim_compiles_and_links(tmp_path):
+    """examples/retrieve.cpp (the reference's run_retrieve over the shim)
+    builds against the library; without arguments it is a usage error."""
+    import subprocess
+
+    exe = tmp_path / "retrieve"
+    lib_dir = os.path.dirname(cg.library_path())
+    subprocess.run(["g++", "-std=c++17", "-O1", os.path.join(ROOT, "examples", "retrieve.cpp"), f"-L{lib_dir}",
+                    "-lcdvz_gpu", f"-Wl,-rpath,{lib_dir}", "-o", str(exe)], check=True)
+    p = subprocess.run([str(exe)], capture_output=True, text=True)
+    assert p.returncode == 1 and "usage" in p.stderr

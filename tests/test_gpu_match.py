@@ -134,3 +134,25 @@ def test_bundle_and_mode_mismatches_are_rejected(ex_b8, bundle_b512, corpus_4k):
     with pytest.raises(cg.DataError, match="model bundle"):
         cg.Index(corpus_4k[:2] + other_bundle)
     idx.close()
+
+
+def test_cpp_retrieval_example_matches_python(corpus_4k, tmp_path):
+    """examples/retrieve.cpp ranks like Index.retrieve (ids = file paths)."""
+    import os
+    import subprocess
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = tmp_path / "retrieve"
+    lib_dir = os.path.dirname(cg.library_path())
+    subprocess.run(["g++", "-std=c++17", "-O1", os.path.join(root, "examples", "retrieve.cpp"), f"-L{lib_dir}",
+                    "-lcdvz_gpu", f"-Wl,-rpath,{lib_dir}", "-o", str(exe)], check=True)
+    paths = []
+    for i, blob in enumerate(corpus_4k[:6]):
+        p = tmp_path / f"c{i}.cdvz"
+        p.write_bytes(blob)
+        paths.append(str(p))
+    out = subprocess.run([str(exe), paths[2], "--"] + paths, capture_output=True, text=True, check=True).stdout
+    got = [(tok.rsplit(":", 1)[0], float(tok.rsplit(":", 1)[1])) for tok in out.split()[1:]]
+    want = cg.Index(corpus_4k[:6], ids=paths).retrieve(corpus_4k[2])
+    assert [g[0] for g in got] == [w[0] for w in want]
+    assert all(abs(g[1] - w[1]) <= 1e-9 * max(1.0, abs(w[1])) for g, w in zip(got, want))
