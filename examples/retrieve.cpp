@@ -5,6 +5,7 @@
 //   ./retrieve q1.cdvz [q2.cdvz ...] -- idx1.cdvz idx2.cdvz ...
 #include <cstdio>
 #include <fstream>
+#include <iomanip>
 #include <iostream>
 #include <iterator>
 
@@ -32,6 +33,7 @@ int main(int argc, char** argv) {
     for (auto& q : queries) q.second = read_file(q.first);
     for (auto& it : index) it.second = read_file(it.first);
     const cdvz::gpu::Index gpu_index(index);
+    std::cout << std::setprecision(17);
     for (const auto& list : cdvz::gpu::retrieve(queries, gpu_index)) {
       std::cout << list.query;
       for (const auto& item : list.items) std::cout << " " << item.id << ":" << item.score;
