@@ -325,8 +325,11 @@ __global__ void __launch_bounds__(256) k_sample(Batch bt) {
     const double* lvl = bt.pyr + g.lvl_off;
     const int samples = g.samples, ns = samples * samples;
     double2* out = bt.smp + slot * bt.smp_cap;
+    // (q + 0.5) / samples is at least 1/64 away from an integer for q < 1024,
+    // far beyond the float error: an exact row index without integer division.
+    const float inv_samples = 1.0f / float(samples);
     for (int q = threadIdx.x; q < ns; q += blockDim.x) {
-      const int j = q / samples, i = q - j * samples;
+      const int j = int((float(q) + 0.5f) * inv_samples), i = q - j * samples;
       const double v = (j + 0.5) * g.step - g.half;
       const double u = (i + 0.5) * g.step - g.half;
       const double px = g.x + u * g.cos_t - v * g.sin_t;

@@ -386,6 +386,74 @@ __global__ void __launch_bounds__(256) k_scfv_encode(Batch bt, Model md, EncodeC
 }
 
 // serialize_container (container.cpp:32-58) into a fixed device slot.
+// CRC-32 (common.cpp:11-35) by a warp. The reflected CRC register update is
+// linear over GF(2), so raw(0, A || B) = Z^|B| raw(0, A) ^ raw(0, B) with Z the
+// "one zero byte" operator: lanes take 128-byte chunks, a shuffle tree merges
+// them with the precomputed operators Z^(2^k) (c_zeros), and the standard
+// init/final inversion is applied by linearity at the end.
+__constant__ uint32_t c_zeros[17][32];  // c_zeros[k][b] = Z^(2^k) applied to register 1 << b
+
+cudaError_t init_crc_zeros() {
+  static bool done = false;
+  if (done) return cudaSuccess;
+  uint32_t table[256];
+  for (uint32_t i = 0; i < 256; ++i) {
+    uint32_t c = i;
+    for (int k = 0; k < 8; ++k) c = (c & 1u) ? 0xEDB88320u ^ (c >> 1) : c >> 1;
+    table[i] = c;
+  }
+  uint32_t z[17][32];
+  for (int b = 0; b < 32; ++b) z[0][b] = table[(1u << b) & 0xFFu] ^ ((1u << b) >> 8);
+  for (int k = 1; k < 17; ++k)
+    for (int b = 0; b < 32; ++b) {  // Z^(2^k) = Z^(2^(k-1)) o Z^(2^(k-1))
+      uint32_t v = z[k - 1][b], r = 0;
+      for (int c = 0; c < 32; ++c)
+        if ((v >> c) & 1u) r ^= z[k - 1][c];
+      z[k][b] = r;
+    }
+  cudaError_t e = cudaMemcpyToSymbol(c_zeros, z, sizeof(z));
+  if (e == cudaSuccess) done = true;
+  return e;
+}
+
+__device__ __forceinline__ uint32_t crc_shift(uint32_t v, uint32_t nbytes) {
+  for (int k = 0; nbytes; ++k, nbytes >>= 1)
+    if (nbytes & 1u) {
+      uint32_t r = 0;
+#pragma unroll
+      for (int b = 0; b < 32; ++b) r ^= ((v >> b) & 1u) ? c_zeros[k][b] : 0u;
+      v = r;
+    }
+  return v;
+}
+
+// Whole warp calls; the CRC is returned on every lane.
+__device__ uint32_t warp_crc32(const uint8_t* buf, int n, const uint32_t* table) {
+  constexpr int C = 128;
+  const int lane = threadIdx.x & 31;
+  const int nfull = n / C;
+  uint32_t acc = 0;  // raw CRC (register from 0) of the chunks merged so far
+  for (int sb = 0; sb < nfull; sb += 32) {
+    const int nch = min(32, nfull - sb);
+    uint32_t r = 0;
+    if (lane < nch) {
+      const uint8_t* p = buf + (sb + lane) * C;
+      for (int i = 0; i < C; ++i) r = table[(r ^ p[i]) & 0xFFu] ^ (r >> 8);
+    }
+    for (int st = 1; st < 32; st <<= 1) {
+      const uint32_t rr = __shfl_down_sync(0xffffffffu, r, st);
+      const int cnt = min(st, max(0, nch - (lane + st)));
+      if ((lane & (2 * st - 1)) == 0 && cnt > 0) r = crc_shift(r, uint32_t(cnt * C)) ^ rr;
+    }
+    r = __shfl_sync(0xffffffffu, r, 0);
+    acc = crc_shift(acc, uint32_t(nch * C)) ^ r;
+  }
+  if (lane == 0)
+    for (int i = nfull * C; i < n; ++i) acc = table[(acc ^ buf[i]) & 0xFFu] ^ (acc >> 8);
+  acc = __shfl_sync(0xffffffffu, acc, 0);
+  return ~(crc_shift(0xFFFFFFFFu, uint32_t(n)) ^ acc);
+}
+
 __global__ void __launch_bounds__(256) k_pack(Batch bt, Model md, EncodeConst ec, uint8_t* out, uint32_t* lengths) {
   extern __shared__ uint8_t buf[];
   __shared__ uint32_t table[256];
@@ -442,13 +510,13 @@ __global__ void __launch_bounds__(256) k_pack(Batch bt, Model md, EncodeConst ec
     buf[code_base + q] = codes[(long long)c * bt.code_stride + b];
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    uint32_t c = 0xFFFFFFFFu;
+  if (threadIdx.x < 32) {
     const int body = total - 4;
-    for (int i = 0; i < body; ++i) c = table[(c ^ buf[i]) & 0xFFu] ^ (c >> 8);
-    c ^= 0xFFFFFFFFu;
-    for (int b = 0; b < 4; ++b) buf[body + b] = uint8_t((c >> (8 * b)) & 0xFF);
-    lengths[f] = uint32_t(total);
+    const uint32_t c = warp_crc32(buf, body, table);
+    if (threadIdx.x == 0) {
+      for (int b = 0; b < 4; ++b) buf[body + b] = uint8_t((c >> (8 * b)) & 0xFF);
+      lengths[f] = uint32_t(total);
+    }
   }
   __syncthreads();
   uint8_t* dst = out + (long long)f * ec.slot_bytes;
@@ -457,8 +525,10 @@ __global__ void __launch_bounds__(256) k_pack(Batch bt, Model md, EncodeConst ec
 
 cudaError_t launch_scfv_pack(const Batch& bt, const Model& md, const EncodeConst& ec, uint8_t* out, uint32_t* lengths,
                              cudaStream_t st, cudaEvent_t after_aggregation) {
+  cudaError_t e = init_crc_zeros();
+  if (e != cudaSuccess) return e;
   k_pca<<<dim3(8, bt.nframes), 128, 0, st>>>(bt, md);
-  cudaError_t e = cudaGetLastError();
+  e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   static bool post_configured = false;
   if (!post_configured) {
