@@ -137,6 +137,8 @@ struct cdvz_gpu_ctx {
   int device = 0;
   int max_batch = 256;
   cudaStream_t st = nullptr;
+  cudaStream_t copy_st = nullptr;          // host->device frame copies (encode_batch)
+  std::vector<cudaEvent_t> copy_ev;        // one per chunk of a call
   std::string err;
   Bundle bundle;
   DetConst dc{};
@@ -190,6 +192,8 @@ struct cdvz_gpu_ctx {
       if (e) cudaEventDestroy(e);
     for (auto& e : user_ev)
       if (e) cudaEventDestroy(e);
+    for (auto& e : copy_ev) cudaEventDestroy(e);
+    if (copy_st) cudaStreamDestroy(copy_st);
     if (st) cudaStreamDestroy(st);
   }
 
@@ -415,9 +419,9 @@ struct cdvz_gpu_ctx {
   // w x h and writes containers into fixed slots of d_out. Ordered after
   // everything already enqueued on the context stream; the context stream
   // waits for the result.
-  // With host pointers (h_pix / h_out / h_len), each chunk's frames are copied
-  // in on its blur stream and its containers copied out on its describe
-  // stream, so the copies of one chunk overlap the kernels of the other lane.
+  // With host pointers (h_pix / h_out / h_len), the frames are copied in on a
+  // dedicated copy stream ahead of the kernels and each chunk's containers are
+  // copied out on its describe stream, overlapping the other lane's kernels.
   void run(const uint8_t* d_pix, int w, int h, long long stride, int frames, int mode_id, int max_side, uint8_t* d_out,
            uint32_t* d_len, const uint8_t* h_pix = nullptr, size_t h_stride = 0, uint8_t* h_out = nullptr,
            uint32_t* h_len = nullptr) {
@@ -431,7 +435,12 @@ struct cdvz_gpu_ctx {
     ec.half_diag = 0.5 * std::hypot(static_cast<double>(W - 1), static_cast<double>(H - 1));
     ec.log2_range = std::log2(64.0 / 0.5);
     const int per = std::min(frames, max_batch);
-    const int chunks = (frames + per - 1) / per;
+    // Chunk boundaries. With host frames the first chunk is a quarter chunk,
+    // so the only copy not hidden behind kernels is short.
+    std::vector<int> cb{0};
+    if (h_pix && frames > per) cb.push_back(std::max(1, per / 4));
+    while (cb.back() < frames) cb.push_back(std::min(frames, cb.back() + per));
+    const int chunks = int(cb.size()) - 1;
     const int n_lanes = serial ? 1 : 2;
     for (int l = 0; l < std::min(chunks, n_lanes); ++l) {
       if (!lanes[l].sA) lanes[l].init();
@@ -442,9 +451,28 @@ struct cdvz_gpu_ctx {
     pyr_bytes = 0.0;
     for (double& x : stage_ms) x = 0.0;
     CDVZ_CUDA_CHECK(cudaEventRecord(ev[0], st));  // everything before this call
+    // Host frames: every chunk's copy is queued up front on the copy stream
+    // (back to back at full link bandwidth); a chunk's kernels wait only for
+    // its own copy, so only the first chunk's copy is exposed.
+    if (h_pix) {
+      if (!copy_st) CDVZ_CUDA_CHECK(cudaStreamCreateWithFlags(&copy_st, cudaStreamNonBlocking));
+      while (int(copy_ev.size()) < chunks) {
+        cudaEvent_t e;
+        CDVZ_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        copy_ev.push_back(e);
+      }
+      CDVZ_CUDA_CHECK(cudaStreamWaitEvent(copy_st, ev[0], 0));
+      for (int c = 0; c < chunks; ++c) {
+        const int base = cb[size_t(c)], nf = cb[size_t(c) + 1] - base;
+        CDVZ_CUDA_CHECK(cudaMemcpy2DAsync(const_cast<uint8_t*>(d_pix) + (long long)base * h * stride, size_t(stride),
+                                          h_pix + size_t(base) * h * h_stride, h_stride, size_t(w), size_t(h) * nf,
+                                          cudaMemcpyHostToDevice, copy_st));
+        CDVZ_CUDA_CHECK(cudaEventRecord(copy_ev[size_t(c)], copy_st));
+      }
+    }
     for (int c = 0; c < chunks; ++c) {
-      const int base = c * per;
-      const int nf = std::min(per, frames - base);
+      const int base = cb[size_t(c)];
+      const int nf = cb[size_t(c) + 1] - base;
       Lane& L = lanes[serial ? 0 : (c & 1)];
       collect(L);
       // Serial mode (debug bit 2): one stream per lane, so kernels never
@@ -457,9 +485,7 @@ struct cdvz_gpu_ctx {
       b.frame_bytes8 = (long long)h * stride;
       CDVZ_CUDA_CHECK(cudaStreamWaitEvent(L.sA, ev[0], 0));
       CDVZ_CUDA_CHECK(cudaStreamWaitEvent(sB, ev[0], 0));
-      if (h_pix)
-        CDVZ_CUDA_CHECK(cudaMemcpy2DAsync(const_cast<uint8_t*>(b.pix8), size_t(stride), h_pix + size_t(base) * h * h_stride,
-                                          h_stride, size_t(w), size_t(h) * nf, cudaMemcpyHostToDevice, L.sA));
+      if (h_pix) CDVZ_CUDA_CHECK(cudaStreamWaitEvent(L.sA, copy_ev[size_t(c)], 0));
       CDVZ_CUDA_CHECK(cudaEventRecord(L.start, L.sA));
       CDVZ_CUDA_CHECK(cudaMemsetAsync(b.status, 0, sizeof(int) * nf, L.sA));
       if (resize) {
@@ -519,7 +545,7 @@ struct cdvz_gpu_ctx {
     for (int l = 0; l < 2; ++l)
       if (lanes[l].pending) CDVZ_CUDA_CHECK(cudaStreamWaitEvent(st, lanes[l].done, 0));
     for (int l = 0; l < 2; ++l) collect(lanes[l]);
-    last_frames = std::min(per, frames - (chunks - 1) * per);
+    last_frames = cb[size_t(chunks)] - cb[size_t(chunks) - 1];
     last_mode = mode_id;
   }
 };
