@@ -66,8 +66,11 @@ __device__ __forceinline__ int derivative_roots(const double a[4], double r[2]) 
 // -1 -> 0, n -> n-1 (common.hpp:24-30 restricted to the range the walks use).
 __device__ __forceinline__ int mirror_near(int i, int n) { return i < 0 ? -1 - i : (i >= n ? 2 * n - 1 - i : i); }
 
+// Base sources: 0 u8 frames (4-byte aligned rows), 3 u8 frames (unaligned
+// rows), 1 resized f64 frames, 2 G3 of the previous octave.
 template <int SRC> struct RawT { using type = double; };
 template <> struct RawT<0> { using type = uint8_t; };
+template <> struct RawT<3> { using type = uint8_t; };
 
 template <int SRC>
 __device__ __forceinline__ typename RawT<SRC>::type load_raw(const Batch& bt, int f, int o, int ry, int xx) {
@@ -208,117 +211,216 @@ __device__ __forceinline__ bool screen_pixel(const double a[4], const DetConst& 
 }
 
 // ---------------------------------------------------------------- K1a: blur
-// One CTA = one Gaussian level of one strip of kBlurCols columns of one frame.
-// Each thread owns a column and walks it top to bottom RS virtual rows per
-// step: x pass of the new rows into a register ring, y pass of RS output rows
-// (image.cpp:187-210), G rows stored to HBM. Base rows are double-buffered in
-// shared memory (next step's rows are fetched into registers while the
-// current step computes), so there is one barrier per step and no halo
-// columns: the strip is exactly the output.
-constexpr int kBlurCols = 128;
-constexpr int kBlurRows = 4;
+// One CTA (kBlurThreads threads) = one Gaussian level of a strip of
+// kBlurCols output columns of one frame; thread t owns the two adjacent
+// columns x0 + 2t, x0 + 2t + 1 and walks them top to bottom over the virtual
+// rows v = -R .. h-1+R (rows outside [0,h) are the mirror-reflected rows the
+// reference's y pass reads, image.cpp:187-210).
+//
+// x pass (gather): the strip's base row v sits in shared memory; the thread
+// reads its 2R+2 inputs with R+1 16-byte loads and forms both columns' sums
+// in the reference's tap order.
+//
+// y pass (scatter with shared products): output row y is
+// (((k_R r[y-R] + k_{R-1} r[y-R+1]) + ...) + k_R r[y+R]) and the taps are
+// symmetric bit for bit, so the rounded product k_j r[v] serves both output
+// rows v - j and v + j. Each new x-pass row v therefore costs R+1 multiplies
+// (not 2R+1): its products are added to the 2R+1 pending output rows
+// y = v-R .. v+R, each of which receives its terms in increasing v — exactly
+// the reference's add sequence, so every G value is bit-identical. The 2R+1
+// accumulators rotate through statically named registers: the row loop is
+// unrolled by one period (CH = 2R+1 rows).
+//
+// Base rows stream into a shared ring with cp.async kBlurAhead rows ahead (no
+// registers held): f64 sources straight into the staged layout, u8 frames as
+// raw 4-byte words, converted (b / 255, mirrored columns) one row ahead into
+// a 2-row f64 ring. Octave >= 1 reads G3 of the previous octave at even
+// coordinates directly (downsample_half, image.cpp:147-155).
+constexpr int kBlurThreads = 64;
+constexpr int kBlurCols = 2 * kBlurThreads;
+constexpr int kMaxBlurR = 8;                           // launch_octave instantiates radii <= 8
+constexpr int kBlurAhead = 6;                          // rows in flight
+constexpr int kBlurRaw = kBlurAhead + 1;               // raw ring slots
+constexpr int kBlurNS = kBlurCols + 2 * kMaxBlurR;     // staged doubles per row (max radius)
+constexpr int kBlurRawBytes = kBlurNS + 16;            // u8 raw row: aligned word superset (16-byte multiple)
 
-template <int R, int SRC>
-__device__ __forceinline__ void blur_level(const Batch& bt, const double* __restrict__ taps, int f, int o, int lvl,
-                                           double* brow /* [2][RS][NB] */) {
-  constexpr int RS = kBlurRows, NB = kBlurCols + 2 * R, D = 2 * R + RS;
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(uint32_t(__cvta_generic_to_shared(smem))), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async8b(void* smem, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(uint32_t(__cvta_generic_to_shared(smem))), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N> __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+static_assert(kBlurRawBytes * kBlurRaw % 16 == 0 && kBlurNS % 2 == 0, "16-byte aligned staged rows");
+struct BlurSmem {
+  union {
+    double f64[kBlurRaw][kBlurNS];  // f64 sources: the staged rows themselves
+    struct {
+      uint8_t raw[kBlurRaw][kBlurRawBytes];
+      double conv[2][kBlurNS];
+    } u8;
+  };
+};
+
+template <int R, int LVL, int SRC>
+__device__ __forceinline__ void blur_level(const Batch& bt, const DetConst& dc, int f, int o, BlurSmem& S) {
+  constexpr int CH = 2 * R + 1, NS = kBlurCols + 2 * R;
+  static_assert(NS >= 2 * kBlurThreads && NS <= 3 * kBlurThreads && NS <= kBlurNS, "staging layout");
   const int w = bt.ow[o], h = bt.oh[o];
-  const int c = threadIdx.x;
+  const int t = threadIdx.x;
   const int x0 = blockIdx.x * kBlurCols;
-  const int cx = x0 + c;
-  const bool store = cx < w;
-  double* G = bt.pyr + f * bt.frame_doubles + bt.plane_off[o][lvl];
-  // Staging: thread c owns staged column c (x0 - R + c) and, for c < 2R, the
-  // halo column c + kBlurCols, in every staged row; columns are mirrored once
-  // here, rows once per step.
-  const bool halo = c < 2 * R;
-  const int sc0 = mirror_near(x0 - R + c, w), sc1 = halo ? mirror_near(x0 - R + c + kBlurCols, w) : 0;
-  using Raw = typename RawT<SRC>::type;
-  const Raw* src;
+  const int cx = x0 + 2 * t;
+  double* G = bt.pyr + f * bt.frame_doubles + bt.plane_off[o][LVL];
+  // Staged column sc = t + k * kBlurThreads holds image column
+  // mirror(x0 - R + sc); the thread's own window is sc = 2t .. 2t + 2R + 1.
+  const bool third = t + 2 * kBlurThreads < NS;
+  int mc[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) mc[k] = mirror_index(x0 - R + min(t + k * kBlurThreads, NS - 1), w);
+  auto src_row = [&](int r) { return min(max(mirror_near(r - R, h), 0), h - 1); };  // rows past h-1+R are never stored
+  // ---- row sources
+  const uint8_t* s8 = nullptr;
+  const double* sf = nullptr;
   long long rstride;
-  int cmul;
-  if constexpr (SRC == 0) {
-    src = bt.pix8 + f * bt.frame_bytes8;
+  int lo = 0, nwords = 0;
+  if constexpr (SRC == 0 || SRC == 3) {
+    s8 = bt.pix8 + f * bt.frame_bytes8;
     rstride = bt.stride8;
-    cmul = 1;
+    // Bytes [lo, lo + 4 * nwords) cover every mirrored column of the strip.
+    const int clo = max(0, x0 - R), chi = min(w - 1, x0 + NS - 1 - R);
+    lo = clo & ~3;
+    nwords = (chi - lo) / 4 + 1;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) mc[k] -= lo;
   } else if constexpr (SRC == 1) {
-    src = bt.pixf + (long long)f * bt.W * bt.H;
+    sf = bt.pixf + (long long)f * bt.W * bt.H;
     rstride = bt.W;
-    cmul = 1;
-  } else {  // downsample_half(G3 of octave o-1): image.cpp:147-155
-    src = bt.pyr + f * bt.frame_doubles + bt.plane_off[o - 1][3];
+  } else {
+    sf = bt.pyr + f * bt.frame_doubles + bt.plane_off[o - 1][3];
     rstride = 2LL * bt.ow[o - 1];
-    cmul = 2;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) mc[k] *= 2;
   }
-  const long long o0 = (long long)sc0 * cmul, o1 = (long long)sc1 * cmul;
-  double t[R + 1];  // symmetric taps: t[|j|] = taps[R + |j|]
-#pragma unroll
-  for (int j = 0; j <= R; ++j) t[j] = taps[R + j];
-  double ring[D];
-#pragma unroll
-  for (int i = 0; i < D; ++i) ring[i] = 0.0;
-  Raw pre0[RS], pre1[RS];  // raw values in flight; converted when parked
-  auto fetch = [&](int v0) {
-#pragma unroll
-    for (int i = 0; i < RS; ++i) {
-      const Raw* row = src + (long long)mirror_near(v0 + i, h) * rstride;
-      pre0[i] = row[o0];
-      if (halo) pre1[i] = row[o1];
+  auto issue = [&](int r, int slot) {  // base row of virtual row r - R into raw slot r % kBlurRaw
+    const long long ro = (long long)src_row(r) * rstride;
+    if constexpr (SRC == 0) {
+      if (t < nwords) cp_async4(S.u8.raw[slot] + 4 * t, s8 + ro + lo + 4 * t);
+    } else if constexpr (SRC == 3) {  // unaligned rows: synchronous byte copies
+      for (int b = t; b < 4 * nwords; b += kBlurThreads)
+        if (lo + b < w) S.u8.raw[slot][b] = s8[ro + lo + b];
+    } else {
+      double* dst = S.f64[slot];
+      cp_async8b(dst + t, sf + ro + mc[0]);
+      cp_async8b(dst + t + kBlurThreads, sf + ro + mc[1]);
+      if (third) cp_async8b(dst + t + 2 * kBlurThreads, sf + ro + mc[2]);
+    }
+    cp_commit();
+  };
+  auto convert = [&](int r, int slot) {  // u8: raw row r -> f64 ring slot r & 1 (image.cpp:79-87: raw * (1.0 / 255.0))
+    if constexpr (SRC == 0 || SRC == 3) {
+      const uint8_t* rw = S.u8.raw[slot];
+      double* d = S.u8.conv[r & 1];
+      d[t] = rw[mc[0]] * (1.0 / 255.0);
+      d[t + kBlurThreads] = rw[mc[1]] * (1.0 / 255.0);
+      if (third) d[t + 2 * kBlurThreads] = rw[mc[2]] * (1.0 / 255.0);
     }
   };
-  auto park = [&](double* dst) {
+  // Prologue: rows 0 .. kBlurAhead-1 in flight; u8 converts row 0.
 #pragma unroll
-    for (int i = 0; i < RS; ++i) {
-      dst[i * NB + c] = to_base<SRC>(pre0[i]);
-      if (halo) dst[i * NB + c + kBlurCols] = to_base<SRC>(pre1[i]);
-    }
-  };
-  int buf = 0;
-  fetch(-R);
-  park(brow);
-  __syncthreads();
-  for (int v0 = -R; v0 <= h - 1 + R; v0 += RS) {
-    const bool more = v0 + RS <= h - 1 + R;
-    if (more) fetch(v0 + RS);
-    const double* b = brow + buf * RS * NB;
-    double acc[RS];
+  for (int r = 0; r < kBlurAhead; ++r) issue(r, r);
+  if constexpr (SRC == 0 || SRC == 3) {
+    cp_wait<kBlurAhead - 1>();
+    __syncthreads();
+    convert(0, 0);
+  }
+  auto next = [](int s) { return s + 1 == kBlurRaw ? 0 : s + 1; };
+  int rs = 0, is = kBlurAhead;  // raw slots of rows r and r + kBlurAhead
+  const double* tp = dc.taps[LVL] + R;  // tp[j] = tp[-j]: tap of offset j
+  double acc0[CH], acc1[CH];
 #pragma unroll
-    for (int i = 0; i < RS; ++i) {
-      const double* bp = b + i * NB + c + R;
-      acc[i] = t[R] * bp[-R];
+  for (int s = 0; s < CH; ++s) acc0[s] = acc1[s] = 0.0;
+  const bool col0 = cx < w, col1 = cx + 1 < w;
+  double* gcol = G + cx;
+  const bool vec = col1 && (w & 1) == 0 && (reinterpret_cast<uintptr_t>(gcol) & 15) == 0;
+  const int nrows = h + 2 * R;  // virtual rows r = 0 .. nrows-1 (v = r - R)
+  for (int rc = 0; rc < nrows; rc += CH) {
 #pragma unroll
-      for (int j = -R + 1; j <= R; ++j) acc[i] = acc[i] + t[j < 0 ? -j : j] * bp[j];
-    }
+    for (int i = 0; i < CH; ++i) {
+      const int r = rc + i;
+      const double* row;
+      if constexpr (SRC == 0 || SRC == 3) {
+        cp_wait<kBlurAhead - 2>();  // raw row r + 1 landed (own copies)
+        __syncthreads();            // ... everyone's; row r converted; slots of rows <= r - 1 free
+        issue(r + kBlurAhead, is);
+        convert(r + 1, next(rs));
+        row = S.u8.conv[r & 1];
+      } else {
+        cp_wait<kBlurAhead - 1>();  // row r landed (own copies)
+        __syncthreads();            // ... everyone's; slot of row r - 1 free
+        issue(r + kBlurAhead, is);
+        row = S.f64[rs];
+      }
+      double b[2 * R + 2];
+      const double2* sp = reinterpret_cast<const double2*>(row + 2 * t);
 #pragma unroll
-    for (int d = 0; d < D - RS; ++d) ring[d] = ring[d + RS];
+      for (int k = 0; k <= R; ++k) {
+        const double2 q = sp[k];
+        b[2 * k] = q.x;
+        b[2 * k + 1] = q.y;
+      }
+      double xa = tp[R] * b[0], xb = tp[R] * b[1];
 #pragma unroll
-    for (int i = 0; i < RS; ++i) ring[D - RS + i] = acc[i];
-    // ring[0] holds virtual row v0 - 2R; output row y_i = v0 + i - R.
+      for (int j = 1; j <= 2 * R; ++j) {
+        const double k = tp[j < R ? R - j : j - R];
+        xa = xa + k * b[j];
+        xb = xb + k * b[j + 1];
+      }
 #pragma unroll
-    for (int i = 0; i < RS; ++i) {
-      const int y = v0 + i - R;
-      if (y >= 0 && y < h && store) {
-        double g = t[R] * ring[i];
-#pragma unroll
-        for (int j = 1; j <= 2 * R; ++j) g = g + t[j < R ? R - j : j - R] * ring[i + j];
-        G[(long long)y * w + cx] = g;
+      for (int j = 0; j <= R; ++j) {
+        const double pa = tp[j] * xa, pb = tp[j] * xb;
+        // output rows y = v - j and v + j; slot of output row y is (y + R) mod CH
+        const int sm = ((i - j) % CH + CH) % CH, sp_ = (i + j) % CH;
+        acc0[sm] = acc0[sm] + pa;
+        acc1[sm] = acc1[sm] + pb;
+        if (j == R) {
+          acc0[sp_] = pa;  // first term of output row v + R
+          acc1[sp_] = pb;
+        } else if (j > 0) {
+          acc0[sp_] = acc0[sp_] + pa;
+          acc1[sp_] = acc1[sp_] + pb;
+        }
+      }
+      rs = next(rs);
+      is = next(is);
+      const int y = r - 2 * R;  // complete: its last term (row y + R) was just added
+      if (y >= 0 && y < h) {
+        const int so = ((i - R) % CH + CH) % CH;
+        double* gp = gcol + (long long)y * w;
+        if (vec) {
+          *reinterpret_cast<double2*>(gp) = make_double2(acc0[so], acc1[so]);
+        } else {
+          if (col0) gp[0] = acc0[so];
+          if (col1) gp[1] = acc1[so];
+        }
       }
     }
-    if (more) park(brow + (buf ^ 1) * RS * NB);
-    __syncthreads();
-    buf ^= 1;
   }
+  cp_wait<0>();
 }
 
 template <int R0, int R1, int R2, int R3, int SRC>
-__global__ void __launch_bounds__(kBlurCols, 4) k_blur(Batch bt, DetConst dc, int o) {
-  __shared__ double brow[2 * kBlurRows * (kBlurCols + 2 * R3)];
-  const int lvl = blockIdx.y, f = blockIdx.z;
-  switch (lvl) {
-    case 0: blur_level<R0, SRC>(bt, dc.taps[0], f, o, 0, brow); break;
-    case 1: blur_level<R1, SRC>(bt, dc.taps[1], f, o, 1, brow); break;
-    case 2: blur_level<R2, SRC>(bt, dc.taps[2], f, o, 2, brow); break;
-    default: blur_level<R3, SRC>(bt, dc.taps[3], f, o, 3, brow); break;
+__global__ void __launch_bounds__(kBlurThreads) k_blur(Batch bt, DetConst dc, int o) {
+  __shared__ __align__(16) BlurSmem S;
+  // Level-major grid (blockIdx.z = level): the CTAs resident on an SM at any
+  // moment mostly share one level's unrolled loop in the instruction cache.
+  const int f = blockIdx.y;
+  switch (blockIdx.z) {
+    case 0: blur_level<R0, 0, SRC>(bt, dc, f, o, S); break;
+    case 1: blur_level<R1, 1, SRC>(bt, dc, f, o, S); break;
+    case 2: blur_level<R2, 2, SRC>(bt, dc, f, o, S); break;
+    default: blur_level<R3, 3, SRC>(bt, dc, f, o, S); break;
   }
 }
 
@@ -583,10 +685,12 @@ static_assert((kGW * sizeof(double)) % 16 == 0, "TMA box rows must be 16-byte mu
 
 template <int R0, int R1, int R2, int R3>
 cudaError_t launch_octave_variant(const Batch& bt, const DetConst& dc, int o, int src, cudaStream_t st) {
-  dim3 grid((bt.ow[o] + kBlurCols - 1) / kBlurCols, 4, bt.nframes);
-  if (src == 0) k_blur<R0, R1, R2, R3, 0><<<grid, kBlurCols, 0, st>>>(bt, dc, o);
-  else if (src == 1) k_blur<R0, R1, R2, R3, 1><<<grid, kBlurCols, 0, st>>>(bt, dc, o);
-  else k_blur<R0, R1, R2, R3, 2><<<grid, kBlurCols, 0, st>>>(bt, dc, o);
+  dim3 grid((bt.ow[o] + kBlurCols - 1) / kBlurCols, bt.nframes, 4);
+  const bool aligned8 = ((reinterpret_cast<uintptr_t>(bt.pix8) | uintptr_t(bt.stride8) | uintptr_t(bt.frame_bytes8)) & 3) == 0;
+  if (src == 0 && aligned8) k_blur<R0, R1, R2, R3, 0><<<grid, kBlurThreads, 0, st>>>(bt, dc, o);
+  else if (src == 0) k_blur<R0, R1, R2, R3, 3><<<grid, kBlurThreads, 0, st>>>(bt, dc, o);
+  else if (src == 1) k_blur<R0, R1, R2, R3, 1><<<grid, kBlurThreads, 0, st>>>(bt, dc, o);
+  else k_blur<R0, R1, R2, R3, 2><<<grid, kBlurThreads, 0, st>>>(bt, dc, o);
   return cudaGetLastError();
 }
 
