@@ -124,7 +124,9 @@ def fp64_peak():
 
 def pyramid_fp64_ops(w, h, radii=(5, 5, 6, 8), margin=10, octaves=4):
     """Separately rounded FP64 operations the octave pair must execute per frame
-    (DESIGN.md 2.3): blur x+y passes 8R+2 per level and pixel; sigma^2-Laplacian
+    (DESIGN.md 2.3): blur 7R+2 per level and pixel (x pass 2R+1 multiplies and
+    2R adds; y pass R+1 multiplies, each product shared by the two output rows
+    it serves, and 2R adds); sigma^2-Laplacian
     (6 per level) + alpha (28) per alpha position (window + 1-pixel ring); the
     screen's FP64 discriminant (7) per window pixel. The exact test on screened
     pixels comes on top and is not counted."""
@@ -132,7 +134,7 @@ def pyramid_fp64_ops(w, h, radii=(5, 5, 6, 8), margin=10, octaves=4):
     for _ in range(octaves):
         if w < 16 or h < 16:
             break
-        ops += w * h * sum(8 * r + 2 for r in radii)
+        ops += w * h * sum(7 * r + 2 for r in radii)
         ww, hh = w - 2 * margin, h - 2 * margin
         if ww > 0 and hh > 0:
             ops += (ww + 2) * (hh + 2) * 52 + ww * hh * 7

@@ -350,26 +350,33 @@ __global__ void __launch_bounds__(256) k_sample(Batch bt) {
   }
 }
 
-// Phase B + epilogue: TWO oriented points per warp, row-synchronous.
-// Lane (q, cx, dv, p) of point q walks every sample row j in order; in row j
-// it visits, in increasing i, the samples whose cell column is cx (c0[i] in
-// {cx - 1, cx}) and adds the contribution of whichever of the sample's two
-// orientation bins (ob0, ob0 + 1 mod 8) has parity p to cell (cx, c0[j] + dv).
-// Accumulators live in shared memory indexed by (set, cell, bin): at any
+// Phase B + epilogue: FOUR oriented points per warp, row-synchronous.
+// Lane (q, cx, dv) of point q walks every sample row j in order; in row j it
+// visits, in increasing i, the samples whose cell column is cx (c0[i] in
+// {cx - 1, cx}), decodes each sample once and adds its two orientation
+// contributions (bins ob0 and ob0 + 1 mod 8) to cell (cx, c0[j] + dv).
+// Accumulators live in shared memory indexed by (set, bin, cell): at any
 // moment each (cell, bin) has exactly one owning lane, and a cell's chains
 // pass from lane dv = 1 to lane dv = 0 when the rows cross a cell boundary
 // with no exchange, so every bin is one sequential chain in the reference's
 // sample order (descriptor.cpp:98-116). Sets: the left (i < 16) and right
 // (i >= 16) sub-patch partials of the current 16-row band; the folded total
-// ((P0 + P1) + P2) + P3 of merge_and_normalize lives in registers.
-// Rows of (weight, ob) records stream into a 3-row shared ring with
-// cp.async, two rows ahead of the walk.
-constexpr int kPBWarps = 4;
+// ((P0 + P1) + P2) + P3 of merge_and_normalize lives in registers (lane hl
+// folds cells hl and hl + 8). Rows of (weight, ob) records stream into a
+// 2-row shared ring with cp.async, one row ahead of the walk.
+constexpr int kPBWarps = 2, kPBPts = 4, kPBLanes = 8;
+// Bank-conflict-free accumulator layout: the 16 lanes of a half-warp (points
+// q, q^1) touch cells (cx, cy) with distinct (q & 1, cy & 1, cx), which is the
+// double's bank slot (index mod 16); set, bin, cy >> 1 and q >> 1 select
+// 16-double rows.
+__device__ __forceinline__ int acc_index(int q, int set, int bin, int cy, int cx) {
+  return (q >> 1) * 512 + set * 256 + bin * 32 + (cy >> 1) * 16 + (q & 1) * 8 + (cy & 1) * 4 + cx;
+}
 struct PhaseBSmem {
-  double2 ring[3][2][kMaxSamples];  // [slot][q][i]
-  double acc[2][2][128];            // [q][set: 0 left, 1 right][bin * 16 + cell] (cells on distinct banks)
-  double wf[2][2][kMaxSamples];     // [q][d][i]: 1 - f, f of the cell coordinate
-  int c0[2][kMaxSamples];           // [q][i]: floor(u * inv_cell + 1.5)
+  double2 ring[2][kPBPts][kMaxSamples];  // [slot][q][i]
+  double acc[kPBPts * 256];              // acc_index(); after phase B: per-point scratch [q][256]
+  double wf[kPBPts][kMaxSamples];        // [q][i]: f of the cell coordinate (1 - f formed on use)
+  int8_t c0[kPBPts][kMaxSamples];        // [q][i]: floor(u * inv_cell + 1.5) in -1 .. 4
 };
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
@@ -377,17 +384,17 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
                : "memory");
 }
 
-__global__ void __launch_bounds__(32 * kPBWarps) k_describe(Batch bt, DetConst dc, Model md, EncodeConst ec) {
+__global__ void __launch_bounds__(32 * kPBWarps, 8) k_describe(Batch bt, DetConst dc, Model md, EncodeConst ec) {
   extern __shared__ __align__(16) uint8_t pb_smem[];
   const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
   PhaseBSmem& S = reinterpret_cast<PhaseBSmem*>(pb_smem)[wi];
   const int f = blockIdx.y;
   const int n_or = bt.or_count[f];
-  const int q = lane >> 4, hl = lane & 15;
-  const int cx = hl & 3, dv = (hl >> 2) & 1, par = hl >> 3;
-  const unsigned gmask = 0xffffu << (16 * q);
-  for (int pair = blockIdx.x * kPBWarps + wi; 2 * pair < n_or; pair += gridDim.x * kPBWarps) {
-    const int idx = 2 * pair + q;
+  const int q = lane >> 3, hl = lane & 7;
+  const int cx = hl & 3, dv = hl >> 2;
+  const unsigned gmask = 0xffu << (kPBLanes * q);
+  for (int grp = blockIdx.x * kPBWarps + wi; kPBPts * grp < n_or; grp += gridDim.x * kPBWarps) {
+    const int idx = kPBPts * grp + q;
     const bool live = idx < n_or;
     const long long gslot = (long long)f * bt.cap_or + (live ? idx : 0);
     const DescGeo g = bt.geo[gslot];
@@ -395,26 +402,24 @@ __global__ void __launch_bounds__(32 * kPBWarps) k_describe(Batch bt, DetConst d
     const double2* smp = bt.smp + gslot * bt.smp_cap;
     auto fetch_row = [&](int j) {
       if (j < samples) {
-        double2* dst = S.ring[j % 3][q];
+        double2* dst = S.ring[j & 1][q];
         const double2* src = smp + (long long)j * samples;
-        for (int i = hl; i < samples; i += 16) cp_async16(dst + i, src + i);
+        for (int i = hl; i < samples; i += kPBLanes) cp_async16(dst + i, src + i);
       }
       asm volatile("cp.async.commit_group;" ::: "memory");
     };
     fetch_row(0);
-    fetch_row(1);
     // Per-axis cell coordinates (descriptor.cpp:89-96): identical for u (i) and v (j).
-    for (int i = hl; i < samples; i += 16) {
+    for (int i = hl; i < samples; i += kPBLanes) {
       const double u = (i + 0.5) * g.step - g.half;
       const double cu = u * g.inv_cell + 1.5;
       const int c0 = static_cast<int>(floor(cu));
       const double fu = cu - c0;
       S.c0[q][i] = c0;
-      S.wf[q][0][i] = 1.0 - fu;
-      S.wf[q][1][i] = fu;
+      S.wf[q][i] = fu;
     }
-    double* acc = S.acc[q][0];  // left set; the right set follows at +128
-    for (int e = hl; e < 256; e += 16) acc[e] = 0.0;
+    double* acc = S.acc;
+    for (int e = lane; e < kPBPts * 256; e += 32) acc[e] = 0.0;
     __syncwarp();
     // Column range of cx: c0 in {cx - 1, cx}; weight f (d = 1) below im.
     int ia = 0, im = 0, ib = 0;
@@ -425,88 +430,114 @@ __global__ void __launch_bounds__(32 * kPBWarps) k_describe(Batch bt, DetConst d
       ib += c < cx + 1;
     }
     const int rows = __reduce_max_sync(0xffffffffu, samples);
-    double tot[8];  // lane hl's fold of cell hl (bins 8 hl .. 8 hl + 7)
+    double tot[2][8];  // lane hl's fold of cells hl and hl + 8
 #pragma unroll
-    for (int k = 0; k < 8; ++k) tot[k] = 0.0;
+    for (int c = 0; c < 2; ++c)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) tot[c][k] = 0.0;
     for (int j = 0; j < rows; ++j) {
-      fetch_row(j + 2);
-      asm volatile("cp.async.wait_group 2;" ::: "memory");
+      fetch_row(j + 1);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
       __syncwarp();
       if (j == kSub && samples > kSub) {
         // Band boundary: the first two sub-patch partials are complete.
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          tot[k] = acc[16 * k + hl] + acc[128 + 16 * k + hl];
-          acc[16 * k + hl] = 0.0;
-          acc[128 + 16 * k + hl] = 0.0;
-        }
+        for (int c = 0; c < 2; ++c)
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const int e = acc_index(q, 0, k, c * 2 + (hl >> 2), hl & 3);  // cell hl + 8c
+            tot[c][k] = acc[e] + acc[256 + e];
+            acc[e] = 0.0;
+            acc[256 + e] = 0.0;
+          }
       }
       __syncwarp();
       if (j < samples) {
         const int cy = S.c0[q][j] + dv;
         if (cy >= 0 && cy < 4) {
-          const double wv = S.wf[q][dv][j];
-          const double2* rowp = S.ring[j % 3][q];
-          const double* wfq = &S.wf[q][0][0];
-          const int cell = cy * 4 + cx;
-          // Two-stage software pipeline: visit i + 1 is decoded while visit
-          // i's bin chain is updated, so a visit's critical path is one
-          // shared load -> add -> store.
-          auto decode = [&](int i, int& o, double& x) {
+          const double fv = S.wf[q][j];
+          const double wv = dv ? fv : 1.0 - fv;
+          const double2* rowp = S.ring[j & 1][q];
+          const double* wfq = S.wf[q];
+          const int cell = acc_index(q, 0, 0, cy, cx);
+          // Visit i: weight * wv * wu * wo for wo = 1 - fo (bin ob0) and fo
+          // (bin ob0 + 1), descriptor.cpp:89-116. Two-stage software
+          // pipeline: visit i + 1 is decoded while visit i's two chains are
+          // updated.
+          auto decode = [&](int i, int& o0, int& o1, double& x0, double& x1) {
             const double2 rec = rowp[i];
-            const double wu = wfq[(i < im ? kMaxSamples : 0) + i];
-            // ob0 = floor(ob), fo = ob - ob0 (descriptor.cpp:93-99); of the
-            // bins ob0 (weight 1 - fo) and ob0 + 1 (weight fo) take the one
-            // of parity p.
+            const double fu = wfq[i];
+            const double wu = i < im ? fu : 1.0 - fu;
             const double obf = floor(rec.y);
             const double fo = rec.y - obf;
             const int b0 = static_cast<int>(obf) & 7;
-            const bool own = (b0 & 1) == par;
             const double base = rec.x * wv * wu;
-            o = cell + (i < kSub ? 0 : 128) + 16 * (own ? b0 : (b0 + 1) & 7);
-            x = base * (own ? 1.0 - fo : fo);
+            const int so = cell + (i < kSub ? 0 : 256);
+            o0 = so + 32 * b0;
+            o1 = so + 32 * ((b0 + 1) & 7);
+            x0 = base * (1.0 - fo);
+            x1 = base * fo;
           };
-          int o = 0;
-          double x = 0.0;
-          if (ia < ib) decode(ia, o, x);
-          for (int i = ia; i < ib; ++i) {
-            int no = o;
-            double nx = 0.0;
-            if (i + 1 < ib) decode(i + 1, no, nx);
-            acc[o] = acc[o] + x;
-            o = no;
-            x = nx;
+          // The next visit's two loads are issued before this visit's
+          // stores; a load that hits a bin just updated takes the updated
+          // value from registers instead (o0 != o1 always), so each chain's
+          // critical path is one add.
+          if (ia < ib) {
+            int o0, o1;
+            double x0, x1;
+            decode(ia, o0, o1, x0, x1);
+            double a0 = acc[o0], a1 = acc[o1];
+            for (int i = ia; i < ib; ++i) {
+              const double s0 = a0 + x0, s1 = a1 + x1;
+              int n0 = o0, n1 = o1;
+              double y0 = 0.0, y1 = 0.0, b0 = 0.0, b1 = 0.0;
+              if (i + 1 < ib) {
+                decode(i + 1, n0, n1, y0, y1);
+                b0 = acc[n0];
+                b1 = acc[n1];
+              }
+              acc[o0] = s0;
+              acc[o1] = s1;
+              a0 = n0 == o0 ? s0 : (n0 == o1 ? s1 : b0);
+              a1 = n1 == o0 ? s0 : (n1 == o1 ? s1 : b1);
+              o0 = n0;
+              o1 = n1;
+              x0 = y0;
+              x1 = y1;
+            }
           }
         }
       }
       __syncwarp();
     }
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const int e = 16 * k + hl;
-      tot[k] = samples > kSub ? (tot[k] + acc[e]) + acc[128 + e] : acc[e];
-    }
+    for (int c = 0; c < 2; ++c)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int e = acc_index(q, 0, k, c * 2 + (hl >> 2), hl & 3);
+        tot[c][k] = samples > kSub ? (tot[c][k] + acc[e]) + acc[256 + e] : acc[e];
+      }
     __syncwarp();
     // normalize_descriptor (descriptor.cpp:124-145): up to 5 rounds of L2
     // normalise + clamp at 0.2; the norm in the Eigen SSE2 reduction order
     // (four stride-4 running sums, then (s0 + s2) + (s1 + s3)).
-    double* sq = acc;
-    double* tv = acc + 128;
+    // Element index of (cell, bin) is cell * 8 + bin.
+    double* sq = acc + 256 * q;
+    double* tv = sq + 128;
     bool done = samples == 0;
     for (int round = 0; round < 5; ++round) {
 #pragma unroll
-      for (int k = 0; k < 8; ++k) sq[8 * hl + k] = tot[k] * tot[k];
+      for (int c = 0; c < 2; ++c)
+#pragma unroll
+        for (int k = 0; k < 8; ++k) sq[8 * (hl + 8 * c) + k] = tot[c][k] * tot[c][k];
       __syncwarp();
       double red = 0.0;
       if (hl < 4) {
-        double t[32];
-#pragma unroll
-        for (int k = 0; k < 32; ++k) t[k] = sq[hl + 4 * k];
-        red = t[0];
-#pragma unroll
-        for (int k = 1; k < 32; ++k) red = red + t[k];
+        red = sq[hl];
+#pragma unroll 8
+        for (int k = 1; k < 32; ++k) red = red + sq[hl + 4 * k];
       }
-      const int gb = 16 * q;
+      const int gb = kPBLanes * q;
       const double r0 = __shfl_sync(0xffffffffu, red, gb), r1 = __shfl_sync(0xffffffffu, red, gb + 1);
       const double r2 = __shfl_sync(0xffffffffu, red, gb + 2), r3 = __shfl_sync(0xffffffffu, red, gb + 3);
       __syncwarp();
@@ -517,50 +548,61 @@ __global__ void __launch_bounds__(32 * kPBWarps) k_describe(Batch bt, DetConst d
           done = true;
         } else {
 #pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            tot[k] = tot[k] / norm;
-            if (tot[k] > 0.2) { tot[k] = 0.2; clipped = true; }
-          }
+          for (int c = 0; c < 2; ++c)
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              tot[c][k] = tot[c][k] / norm;
+              if (tot[c][k] > 0.2) { tot[c][k] = 0.2; clipped = true; }
+            }
         }
       }
       if (!(__ballot_sync(0xffffffffu, clipped) & gmask)) done = true;
       if (__all_sync(0xffffffffu, done)) break;
     }
     if (samples > 0) {
-      double2* dout = reinterpret_cast<double2*>(bt.desc + ((long long)f * bt.cap_or + idx) * 128 + 8 * hl);
 #pragma unroll
-      for (int k = 0; k < 4; ++k) dout[k] = make_double2(tot[2 * k], tot[2 * k + 1]);
-      // transform_descriptor (transform_coding.cpp:81-91) of cell hl.
-      const int which = (((hl & 3) + (hl >> 2)) & 1) == 0 ? 0 : 1;
+      for (int c = 0; c < 2; ++c) {
+        const int cl = hl + 8 * c;
+        double2* dout = reinterpret_cast<double2*>(bt.desc + ((long long)f * bt.cap_or + idx) * 128 + 8 * cl);
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        double s = md.tr[which][i][0] * tot[0];
+        for (int k = 0; k < 4; ++k) dout[k] = make_double2(tot[c][2 * k], tot[c][2 * k + 1]);
+        // transform_descriptor (transform_coding.cpp:81-91) of cell cl.
+        const int which = (((cl & 3) + (cl >> 2)) & 1) == 0 ? 0 : 1;
 #pragma unroll
-        for (int kk = 1; kk < 8; ++kk) s = s + md.tr[which][i][kk] * tot[kk];
-        tv[hl * 8 + i] = md.tr_scale * s;
+        for (int i = 0; i < 8; ++i) {
+          double s = md.tr[which][i][0] * tot[c][0];
+#pragma unroll
+          for (int kk = 1; kk < 8; ++kk) s = s + md.tr[which][i][kk] * tot[c][kk];
+          tv[cl * 8 + i] = md.tr_scale * s;
+        }
       }
     }
     __syncwarp();
     if (samples > 0) {
       // quantize_ternary (transform_coding.cpp:202-217): 00 zero, 01 +1,
-      // 10 -1; lane hl packs symbols 8 hl .. 8 hl + 7 into code bytes 2 hl, 2 hl + 1.
+      // 10 -1; lane hl packs symbols 8 cl .. 8 cl + 7 into code bytes 2 cl, 2 cl + 1
+      // for its cells cl = hl, hl + 8.
       uint8_t* code = bt.codes + ((long long)f * bt.cap_or + idx) * bt.code_stride;
 #pragma unroll
-      for (int by = 0; by < 2; ++by) {
-        const int t0 = 8 * hl + 4 * by;
-        if (t0 < ec.elements) {
-          uint8_t byte = 0;
+      for (int c = 0; c < 2; ++c) {
+        const int cl = hl + 8 * c;
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const int t = t0 + k;
-            if (t < ec.elements) {
-              const int e = md.priority[t];
-              const double val = tv[e];
-              const uint8_t sym = val < md.t0[e] ? 2 : (val > md.t1[e] ? 1 : 0);
-              byte |= uint8_t(sym << (2 * k));
+        for (int by = 0; by < 2; ++by) {
+          const int t0 = 8 * cl + 4 * by;
+          if (t0 < ec.elements) {
+            uint8_t byte = 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const int t = t0 + k;
+              if (t < ec.elements) {
+                const int e = md.priority[t];
+                const double val = tv[e];
+                const uint8_t sym = val < md.t0[e] ? 2 : (val > md.t1[e] ? 1 : 0);
+                byte |= uint8_t(sym << (2 * k));
+              }
             }
+            code[6 + 2 * cl + by] = byte;
           }
-          code[6 + 2 * hl + by] = byte;
         }
       }
       if (hl == 0) {
