@@ -315,7 +315,13 @@ __global__ void __launch_bounds__(128) k_geometry(Batch bt, DetConst dc) {
   bt.geo[(long long)f * bt.cap_or + idx] = g;
 }
 
-__global__ void __launch_bounds__(256) k_sample(Batch bt) {
+// The Gaussian weight exp(-(u*u + v*v) / denom) of sample (i, j) equals that
+// of (j, i) bit for bit (u_i == v_i, and the sum commutes), so each CTA first
+// tabulates the samples*(samples+1)/2 distinct values of its point in shared
+// memory, then runs the per-sample body.
+constexpr int kSampleThreads = 128;
+__global__ void __launch_bounds__(kSampleThreads) k_sample(Batch bt) {
+  __shared__ double gexp[kMaxSamples * (kMaxSamples + 1) / 2];  // [j * (j + 1) / 2 + i], i <= j
   const int f = blockIdx.y;
   const int n_or = bt.or_count[f];
   for (int idx = blockIdx.x; idx < n_or; idx += gridDim.x) {
@@ -325,10 +331,23 @@ __global__ void __launch_bounds__(256) k_sample(Batch bt) {
     const double* lvl = bt.pyr + g.lvl_off;
     const int samples = g.samples, ns = samples * samples;
     double2* out = bt.smp + slot * bt.smp_cap;
-    // (q + 0.5) / samples is at least 1/64 away from an integer for q < 1024,
-    // far beyond the float error: an exact row index without integer division.
+    // (q + 0.5) / n is at least 1/64 away from an integer for q < 1024, far
+    // beyond the float error: exact row indices without integer division.
+    const int nt = samples * (samples + 1) / 2;
+    __syncthreads();  // previous point's table fully read
+    for (int q = threadIdx.x; q < nt; q += kSampleThreads) {
+      // q = j (j + 1) / 2 + i with i <= j
+      int j = int((sqrtf(8.0f * float(q) + 1.0f) - 1.0f) * 0.5f);
+      j += (j + 1) * (j + 2) / 2 <= q;
+      j -= j * (j + 1) / 2 > q;
+      const int i = q - j * (j + 1) / 2;
+      const double v = (j + 0.5) * g.step - g.half;
+      const double u = (i + 0.5) * g.step - g.half;
+      gexp[q] = exp(-(u * u + v * v) / g.gauss_denom);
+    }
+    __syncthreads();
     const float inv_samples = 1.0f / float(samples);
-    for (int q = threadIdx.x; q < ns; q += blockDim.x) {
+    for (int q = threadIdx.x; q < ns; q += kSampleThreads) {
       const int j = int((float(q) + 0.5f) * inv_samples), i = q - j * samples;
       const double v = (j + 0.5) * g.step - g.half;
       const double u = (i + 0.5) * g.step - g.half;
@@ -340,7 +359,8 @@ __global__ void __launch_bounds__(256) k_sample(Batch bt) {
         const double gy = 0.5 * (sample_bilinear(lvl, g.w, px, py + 1.0) - sample_bilinear(lvl, g.w, px, py - 1.0));
         const double mag = hypot(gx, gy);
         if (mag != 0.0) {
-          wgt = mag * exp(-(u * u + v * v) / g.gauss_denom);
+          const int lo = min(i, j), hi = max(i, j);
+          wgt = mag * gexp[hi * (hi + 1) / 2 + lo];
           const double phi = wrap_angle(atan2(gy, gx) - theta);
           obv = phi / kTwoPi * 8 - 0.5;
         }
@@ -641,7 +661,7 @@ cudaError_t launch_describe(const Batch& bt, const DetConst& dc, const Model& md
   k_geometry<<<dim3((bt.cap_or + 127) / 128, bt.nframes), 128, 0, st>>>(bt, dc);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  k_sample<<<dim3(64, bt.nframes), 256, 0, st>>>(bt);
+  k_sample<<<dim3(128, bt.nframes), kSampleThreads, 0, st>>>(bt);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   static bool configured = false;
