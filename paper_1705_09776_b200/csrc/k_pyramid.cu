@@ -611,7 +611,7 @@ __global__ void __launch_bounds__(32 * kDetWarps) k_detect_walk(Batch bt, DetCon
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
 #pragma unroll
-  for (int i = 0; i < kPrefetch + 2; ++i) issue();  // rows y0 - 2 .. y0 + 2
+  for (int i = 0; i < kPrefetch + 2; ++i) issue();  // rows y0 - 2 .. y0 + kPrefetch - 1
   const double oct_scale = ldexp(1.0, o);
   double ap[4];  // own alpha of the previous row (screened one row late)
   int qn = 0;
@@ -628,49 +628,62 @@ __global__ void __launch_bounds__(32 * kDetWarps) k_detect_walk(Batch bt, DetCon
     __syncwarp();
   };
   const int T = y1 - y0 + 2;  // alpha rows y0 - 1 .. y1
-  for (int t0 = 0; t0 < T; t0 += 4) {
+  // sigma^2-normalised Laplacian of row ra (image.cpp:220-238,
+  // scale_space.cpp:148-151), then alpha = beta * L in column order.
+  auto alpha_row = [&](int ra, double an[4]) {
+    const double(*rU)[34] = S.grow[(ra - 1) % kGRows];
+    const double(*rC)[34] = S.grow[ra % kGRows];
+    const double(*rD)[34] = S.grow[(ra + 1) % kGRows];
+    double L[4];
 #pragma unroll
-    for (int ph = 0; ph < 4; ++ph) {
+    for (int k = 0; k < 4; ++k) {
+      const double lap = rU[k][lane + 1] + rD[k][lane + 1] + rC[k][lane] + rC[k][lane + 2] - 4.0 * rC[k][lane + 1];
+      L[k] = dc.s2[k] * lap;
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      double sum = dc.beta[i][0] * L[0];
+      sum = sum + dc.beta[i][1] * L[1];
+      sum = sum + dc.beta[i][2] * L[2];
+      sum = sum + dc.beta[i][3] * L[3];
+      an[i] = sum;
+    }
+  };
+  auto screen_row = [&](int rs, const double a[4]) {  // rs's 3x3 alpha neighbourhood is complete
+    if (rs >= y0 && rs < y1) {
+      const bool push = out_col && (!dc.screen || screen_pixel(a, dc));
+      const unsigned bal = __ballot_sync(0xffffffffu, push);
+      if (push) S.queue[qn + __popc(bal & ((1u << lane) - 1u))] = uint16_t(((rs - y0 + 2) << 5) | lane);
+      qn += __popc(bal);
+    }
+  };
+  for (int t0 = 0; t0 < T; t0 += 4) {
+    // Two alpha rows per step (independent FP64 chains side by side).
+#pragma unroll
+    for (int ph = 0; ph < 4; ph += 2) {
       const int t = t0 + ph;
       if (t >= T) break;
       const int ra = y0 - 1 + t;
-      // Rows ra - 1 .. ra + 1 must have landed: rows up to ra + 1 + kPrefetch - 1
+      // Rows ra - 1 .. ra + 2 must have landed: rows up to ra + kPrefetch
       // may still be in flight.
-      asm volatile("cp.async.wait_group %0;" ::"n"(kPrefetch - 1) : "memory");
+      asm volatile("cp.async.wait_group %0;" ::"n"(kPrefetch - 2) : "memory");
       __syncwarp();
-      const double(*rU)[34] = S.grow[(ra - 1) % kGRows];
-      const double(*rC)[34] = S.grow[ra % kGRows];
-      const double(*rD)[34] = S.grow[(ra + 1) % kGRows];
-      // sigma^2-normalised Laplacian of row ra (image.cpp:220-238,
-      // scale_space.cpp:148-151), then alpha = beta * L in column order.
-      double L[4];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const double lap = rU[k][lane + 1] + rD[k][lane + 1] + rC[k][lane] + rC[k][lane + 2] - 4.0 * rC[k][lane + 1];
-        L[k] = dc.s2[k] * lap;
-      }
-      double an[4];
+      double a0[4], a1[4];
+      alpha_row(ra, a0);
+      alpha_row(ra + 1, a1);
+      const bool second = t + 1 < T;
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        double sum = dc.beta[i][0] * L[0];
-        sum = sum + dc.beta[i][1] * L[1];
-        sum = sum + dc.beta[i][2] * L[2];
-        sum = sum + dc.beta[i][3] * L[3];
-        an[i] = sum;
-        S.ring[ra % kRing][i][lane] = sum;
+        S.ring[ra % kRing][i][lane] = a0[i];
+        if (second) S.ring[(ra + 1) % kRing][i][lane] = a1[i];
       }
       __syncwarp();
-      issue();  // row ra + 4 into the slot of row ra - 2, no longer needed
-      // Screen row ra - 1, whose 3x3 alpha neighbourhood is now complete.
-      const int rs = ra - 1;
-      if (rs >= y0 && rs < y1) {
-        const bool push = out_col && (!dc.screen || screen_pixel(ap, dc));
-        const unsigned bal = __ballot_sync(0xffffffffu, push);
-        if (push) S.queue[qn + __popc(bal & ((1u << lane) - 1u))] = uint16_t(((rs - y0 + 2) << 5) | lane);
-        qn += __popc(bal);
-      }
+      issue();  // rows ra + kPrefetch + 1, ra + kPrefetch + 2 into the slots of rows ra - 1, ra
+      issue();
+      screen_row(ra - 1, ap);
+      if (second) screen_row(ra, a0);
 #pragma unroll
-      for (int i = 0; i < 4; ++i) ap[i] = an[i];
+      for (int i = 0; i < 4; ++i) ap[i] = a1[i];
     }
     __syncwarp();
     // Every queued pixel (rows <= the last alpha row - 1) has its
