@@ -561,7 +561,7 @@ __global__ void __launch_bounds__(kDetThreads, 2)
 // pixels are queued and the queue is drained in full-warp passes by the exact
 // FP64 test (exact_detect, reading the 3x3 alpha neighbourhood from the ring)
 // before the ring can overwrite any row a queued pixel needs.
-constexpr int kStripCols = 30, kSegTarget = 96, kRing = 6, kDetWarps = 3, kPrefetch = 3, kGRows = kPrefetch + 2;
+constexpr int kStripCols = 30, kSegTarget = 96, kRing = 6, kDetWarps = 3, kPrefetch = 2, kGRows = kPrefetch + 2;
 struct DetWarpSmem {
   double grow[kGRows][4][34];  // G rows in flight: [row % kGRows][level][1 + lane], edges at 0 and 33
   double ring[kRing][4][32];   // alpha rows: [row % kRing][coefficient][lane]
@@ -726,6 +726,8 @@ cudaError_t launch_detect(const Batch& bt, const DetConst& dc, int o, const CUte
     static bool walk_configured = false;
     if (!walk_configured) {
       cudaError_t e = cudaFuncSetAttribute(k_detect_walk, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      if (e != cudaSuccess) return e;
+      e = cudaFuncSetAttribute(k_detect_walk, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
       if (e != cudaSuccess) return e;
       walk_configured = true;
     }
