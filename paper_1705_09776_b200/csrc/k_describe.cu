@@ -46,11 +46,11 @@ __device__ __forceinline__ double sample_bilinear(const double* img, int w, doub
   const int x0 = static_cast<int>(floor(qx));
   const int y0 = static_cast<int>(floor(qy));
   const double fx = qx - x0, fy = qy - y0;
-  const double* p = img + (long long)y0 * w + x0;
-  double v = (1.0 - fy) * (1.0 - fx) * p[0];
-  if (fx > 0.0) v += (1.0 - fy) * fx * p[1];
-  if (fy > 0.0) v += fy * (1.0 - fx) * p[w];
-  if (fx > 0.0 && fy > 0.0) v += fy * fx * p[w + 1];
+  const double* p = img + (long long)y0 * w + x0;  // read-only here: the non-coherent (texture) path
+  double v = (1.0 - fy) * (1.0 - fx) * __ldg(p);
+  if (fx > 0.0) v += (1.0 - fy) * fx * __ldg(p + 1);
+  if (fy > 0.0) v += fy * (1.0 - fx) * __ldg(p + w);
+  if (fx > 0.0 && fy > 0.0) v += fy * fx * __ldg(p + w + 1);
   return v;
 }
 

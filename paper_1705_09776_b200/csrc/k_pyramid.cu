@@ -211,8 +211,8 @@ __device__ __forceinline__ bool screen_pixel(const double a[4], const DetConst& 
 }
 
 // ---------------------------------------------------------------- K1a: blur
-// One CTA (kBlurThreads threads) = one Gaussian level of a strip of
-// kBlurCols output columns of one frame; thread t owns the two adjacent
+// One CTA (NT = 64 or 32 threads) = one Gaussian level of a strip of 2 NT
+// output columns of one frame; thread t owns the two adjacent
 // columns x0 + 2t, x0 + 2t + 1 and walks them top to bottom over the virtual
 // rows v = -R .. h-1+R (rows outside [0,h) are the mirror-reflected rows the
 // reference's y pass reads, image.cpp:187-210).
@@ -236,8 +236,8 @@ __device__ __forceinline__ bool screen_pixel(const double a[4], const DetConst& 
 // raw 4-byte words, converted (b / 255, mirrored columns) one row ahead into
 // a 2-row f64 ring. Octave >= 1 reads G3 of the previous octave at even
 // coordinates directly (downsample_half, image.cpp:147-155).
-constexpr int kBlurThreads = 64;
-constexpr int kBlurCols = 2 * kBlurThreads;
+constexpr int kBlurThreadsMax = 64;                    // 64 (octave 0) or 32 threads (smaller octaves)
+constexpr int kBlurCols = 2 * kBlurThreadsMax;
 constexpr int kMaxBlurR = 8;                           // launch_octave instantiates radii <= 8
 constexpr int kBlurAhead = 6;                          // rows in flight
 constexpr int kBlurRaw = kBlurAhead + 1;               // raw ring slots
@@ -264,21 +264,21 @@ struct BlurSmem {
   };
 };
 
-template <int R, int LVL, int SRC>
+template <int R, int LVL, int SRC, int NT>
 __device__ __forceinline__ void blur_level(const Batch& bt, const DetConst& dc, int f, int o, BlurSmem& S) {
-  constexpr int CH = 2 * R + 1, NS = kBlurCols + 2 * R;
-  static_assert(NS >= 2 * kBlurThreads && NS <= 3 * kBlurThreads && NS <= kBlurNS, "staging layout");
+  constexpr int CH = 2 * R + 1, NS = 2 * NT + 2 * R;
+  static_assert(NS >= 2 * NT && NS <= 3 * NT && NS <= kBlurNS, "staging layout");
   const int w = bt.ow[o], h = bt.oh[o];
   const int t = threadIdx.x;
-  const int x0 = blockIdx.x * kBlurCols;
+  const int x0 = blockIdx.x * 2 * NT;
   const int cx = x0 + 2 * t;
   double* G = bt.pyr + f * bt.frame_doubles + bt.plane_off[o][LVL];
-  // Staged column sc = t + k * kBlurThreads holds image column
+  // Staged column sc = t + k * NT holds image column
   // mirror(x0 - R + sc); the thread's own window is sc = 2t .. 2t + 2R + 1.
-  const bool third = t + 2 * kBlurThreads < NS;
+  const bool third = t + 2 * NT < NS;
   int mc[3];
 #pragma unroll
-  for (int k = 0; k < 3; ++k) mc[k] = mirror_index(x0 - R + min(t + k * kBlurThreads, NS - 1), w);
+  for (int k = 0; k < 3; ++k) mc[k] = mirror_index(x0 - R + min(t + k * NT, NS - 1), w);
   auto src_row = [&](int r) { return min(max(mirror_near(r - R, h), 0), h - 1); };  // rows past h-1+R are never stored
   // ---- row sources
   const uint8_t* s8 = nullptr;
@@ -308,13 +308,13 @@ __device__ __forceinline__ void blur_level(const Batch& bt, const DetConst& dc, 
     if constexpr (SRC == 0) {
       if (t < nwords) cp_async4(S.u8.raw[slot] + 4 * t, s8 + ro + lo + 4 * t);
     } else if constexpr (SRC == 3) {  // unaligned rows: synchronous byte copies
-      for (int b = t; b < 4 * nwords; b += kBlurThreads)
+      for (int b = t; b < 4 * nwords; b += NT)
         if (lo + b < w) S.u8.raw[slot][b] = s8[ro + lo + b];
     } else {
       double* dst = S.f64[slot];
       cp_async8b(dst + t, sf + ro + mc[0]);
-      cp_async8b(dst + t + kBlurThreads, sf + ro + mc[1]);
-      if (third) cp_async8b(dst + t + 2 * kBlurThreads, sf + ro + mc[2]);
+      cp_async8b(dst + t + NT, sf + ro + mc[1]);
+      if (third) cp_async8b(dst + t + 2 * NT, sf + ro + mc[2]);
     }
     cp_commit();
   };
@@ -323,8 +323,8 @@ __device__ __forceinline__ void blur_level(const Batch& bt, const DetConst& dc, 
       const uint8_t* rw = S.u8.raw[slot];
       double* d = S.u8.conv[r & 1];
       d[t] = rw[mc[0]] * (1.0 / 255.0);
-      d[t + kBlurThreads] = rw[mc[1]] * (1.0 / 255.0);
-      if (third) d[t + 2 * kBlurThreads] = rw[mc[2]] * (1.0 / 255.0);
+      d[t + NT] = rw[mc[1]] * (1.0 / 255.0);
+      if (third) d[t + 2 * NT] = rw[mc[2]] * (1.0 / 255.0);
     }
   };
   // Prologue: rows 0 .. kBlurAhead-1 in flight; u8 converts row 0.
@@ -410,17 +410,17 @@ __device__ __forceinline__ void blur_level(const Batch& bt, const DetConst& dc, 
   cp_wait<0>();
 }
 
-template <int R0, int R1, int R2, int R3, int SRC>
-__global__ void __launch_bounds__(kBlurThreads) k_blur(Batch bt, DetConst dc, int o) {
+template <int R0, int R1, int R2, int R3, int SRC, int NT>
+__global__ void __launch_bounds__(NT) k_blur(Batch bt, DetConst dc, int o) {
   __shared__ __align__(16) BlurSmem S;
   // Level-major grid (blockIdx.z = level): the CTAs resident on an SM at any
   // moment mostly share one level's unrolled loop in the instruction cache.
   const int f = blockIdx.y;
   switch (blockIdx.z) {
-    case 0: blur_level<R0, 0, SRC>(bt, dc, f, o, S); break;
-    case 1: blur_level<R1, 1, SRC>(bt, dc, f, o, S); break;
-    case 2: blur_level<R2, 2, SRC>(bt, dc, f, o, S); break;
-    default: blur_level<R3, 3, SRC>(bt, dc, f, o, S); break;
+    case 0: blur_level<R0, 0, SRC, NT>(bt, dc, f, o, S); break;
+    case 1: blur_level<R1, 1, SRC, NT>(bt, dc, f, o, S); break;
+    case 2: blur_level<R2, 2, SRC, NT>(bt, dc, f, o, S); break;
+    default: blur_level<R3, 3, SRC, NT>(bt, dc, f, o, S); break;
   }
 }
 
@@ -698,12 +698,18 @@ static_assert((kGW * sizeof(double)) % 16 == 0, "TMA box rows must be 16-byte mu
 
 template <int R0, int R1, int R2, int R3>
 cudaError_t launch_octave_variant(const Batch& bt, const DetConst& dc, int o, int src, cudaStream_t st) {
-  dim3 grid((bt.ow[o] + kBlurCols - 1) / kBlurCols, bt.nframes, 4);
+  // 128-column strips at octave 0 (640 = 5 strips), 64-column strips (one
+  // warp) above, where the planes are narrow.
+  const int nt = src == 2 ? 32 : 64;
+  dim3 grid((bt.ow[o] + 2 * nt - 1) / (2 * nt), bt.nframes, 4);
   const bool aligned8 = ((reinterpret_cast<uintptr_t>(bt.pix8) | uintptr_t(bt.stride8) | uintptr_t(bt.frame_bytes8)) & 3) == 0;
-  if (src == 0 && aligned8) k_blur<R0, R1, R2, R3, 0><<<grid, kBlurThreads, 0, st>>>(bt, dc, o);
-  else if (src == 0) k_blur<R0, R1, R2, R3, 3><<<grid, kBlurThreads, 0, st>>>(bt, dc, o);
-  else if (src == 1) k_blur<R0, R1, R2, R3, 1><<<grid, kBlurThreads, 0, st>>>(bt, dc, o);
-  else k_blur<R0, R1, R2, R3, 2><<<grid, kBlurThreads, 0, st>>>(bt, dc, o);
+  const int s = src == 0 ? (aligned8 ? 0 : 3) : src;
+#define CDVZ_BLUR(S, N) k_blur<R0, R1, R2, R3, S, N><<<grid, N, 0, st>>>(bt, dc, o)
+  if (s == 0) CDVZ_BLUR(0, 64);       // octave 0: u8 frames
+  else if (s == 3) CDVZ_BLUR(3, 64);  // octave 0: u8 frames, unaligned rows
+  else if (s == 1) CDVZ_BLUR(1, 64);  // octave 0: resized f64 frames
+  else CDVZ_BLUR(2, 32);              // octaves >= 1: G3 of the previous octave
+#undef CDVZ_BLUR
   return cudaGetLastError();
 }
 
