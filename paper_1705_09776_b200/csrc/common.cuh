@@ -44,6 +44,7 @@ struct DetConst {
   double thr, rho_limit, s_lo, s_hi;
   int margin;
   int screen;          // 1: FP32 pre-screen before the exact test; 0: exact test on every pixel
+  float scr_lo, scr_hi, scr_thr;  // screen constants: s_lo - 0.05, s_hi + 0.05, thr (FP32)
   int walk;            // 1: warp column-walk extrema kernel; 0: TMA tile kernel
 };
 

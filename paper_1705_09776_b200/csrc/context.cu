@@ -224,6 +224,9 @@ struct cdvz_gpu_ctx {
     dc.rho_limit = b.rho_limit;
     dc.s_lo = b.sigmas[0];
     dc.s_hi = b.sigmas[3];
+    dc.scr_lo = float(dc.s_lo) - 0.05f;
+    dc.scr_hi = float(dc.s_hi) + 0.05f;
+    dc.scr_thr = float(b.response_threshold);
     dc.margin = b.margin;
     dc.screen = 1;
     dc.walk = 1;

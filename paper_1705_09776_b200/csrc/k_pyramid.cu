@@ -187,25 +187,25 @@ __device__ __forceinline__ bool screen_pixel(const double a[4], const DetConst& 
   const double disc = qb * qb - 4.0 * qa * qc;
   if (disc < 0.0) return false;  // exactly the reference's test: no real root
   if (!(disc > 1e-6 * (qb * qb))) return true;  // near-double root: let the exact path decide
+  // FP32 from here on (fused multiply-adds are fine: this only screens, and
+  // its margins dwarf FP32 rounding).
   const float fa = float(qa), fb = float(qb), fc = float(qc), fd = float(disc);
   const float sq = fd * rsqrt_approx(fd);
   const float q = -0.5f * (fb + copysignf(sq, fb));
   if (!(fabsf(q) > 1e-30f)) return true;
   const float r0 = q * rcp_approx(fa), r1 = fc * rcp_approx(q);
-  const float lo = float(dc.s_lo) - 0.05f, hi = float(dc.s_hi) + 0.05f;
   const float a0 = float(a[0]), a1 = float(a[1]), a2 = float(a[2]), a3 = float(a[3]);
-  const float thr = float(dc.thr);
   bool any = false;
 #pragma unroll
   for (int k = 0; k < 2; ++k) {
     const float r = k ? r1 : r0;
-    if (!(r >= lo && r <= hi)) {
+    if (!(r >= dc.scr_lo && r <= dc.scr_hi)) {
       if (!isfinite(r)) any = true;
       continue;
     }
-    const float p = a0 + r * (a1 + r * (a2 + r * a3));
-    const float bound = fabsf(a0) + r * (fabsf(a1) + r * (fabsf(a2) + r * fabsf(a3)));
-    if (fabsf(p) + 1e-5f * bound + 1e-6f >= thr) any = true;
+    const float p = __fmaf_rn(r, __fmaf_rn(r, __fmaf_rn(r, a3, a2), a1), a0);
+    const float bound = __fmaf_rn(r, __fmaf_rn(r, __fmaf_rn(r, fabsf(a3), fabsf(a2)), fabsf(a1)), fabsf(a0));
+    if (__fmaf_rn(1e-5f, bound, fabsf(p) + 1e-6f) >= dc.scr_thr) any = true;
   }
   return any;
 }
@@ -599,7 +599,7 @@ __global__ void __launch_bounds__(32 * kDetWarps) k_detect_walk(Batch bt, DetCon
   int next_row = y0 - 2;
   auto issue = [&]() {  // next G row into its slot (or an empty group past the segment)
     if (next_row <= y1 + 1) {
-      double(*dst)[34] = S.grow[next_row % kGRows];
+      double(*dst)[34] = S.grow[unsigned(next_row) % kGRows];
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         cp_async8(&dst[k][lane + 1], gp[k]);
@@ -631,9 +631,9 @@ __global__ void __launch_bounds__(32 * kDetWarps) k_detect_walk(Batch bt, DetCon
   // sigma^2-normalised Laplacian of row ra (image.cpp:220-238,
   // scale_space.cpp:148-151), then alpha = beta * L in column order.
   auto alpha_row = [&](int ra, double an[4]) {
-    const double(*rU)[34] = S.grow[(ra - 1) % kGRows];
-    const double(*rC)[34] = S.grow[ra % kGRows];
-    const double(*rD)[34] = S.grow[(ra + 1) % kGRows];
+    const double(*rU)[34] = S.grow[unsigned(ra - 1) % kGRows];
+    const double(*rC)[34] = S.grow[unsigned(ra) % kGRows];
+    const double(*rD)[34] = S.grow[unsigned(ra + 1) % kGRows];
     double L[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
@@ -674,8 +674,8 @@ __global__ void __launch_bounds__(32 * kDetWarps) k_detect_walk(Batch bt, DetCon
       const bool second = t + 1 < T;
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        S.ring[ra % kRing][i][lane] = a0[i];
-        if (second) S.ring[(ra + 1) % kRing][i][lane] = a1[i];
+        S.ring[unsigned(ra) % kRing][i][lane] = a0[i];
+        if (second) S.ring[unsigned(ra + 1) % kRing][i][lane] = a1[i];
       }
       __syncwarp();
       issue();  // rows ra + kPrefetch + 1, ra + kPrefetch + 2 into the slots of rows ra - 1, ra
