@@ -561,7 +561,7 @@ __global__ void __launch_bounds__(kDetThreads, 2)
 // pixels are queued and the queue is drained in full-warp passes by the exact
 // FP64 test (exact_detect, reading the 3x3 alpha neighbourhood from the ring)
 // before the ring can overwrite any row a queued pixel needs.
-constexpr int kStripCols = 30, kSegTarget = 96, kRing = 6, kDetWarps = 3, kPrefetch = 2, kGRows = kPrefetch + 2;
+constexpr int kStripCols = 30, kSegTarget = 96, kRing = 6, kDetWarps = 3, kPrefetch = 2, kGRows = kPrefetch + 2;  // kDetWarps: max warps per CTA
 struct DetWarpSmem {
   double grow[kGRows][4][34];  // G rows in flight: [row % kGRows][level][1 + lane], edges at 0 and 33
   double ring[kRing][4][32];   // alpha rows: [row % kRing][coefficient][lane]
@@ -578,7 +578,7 @@ __global__ void __launch_bounds__(32 * kDetWarps) k_detect_walk(Batch bt, DetCon
   DetWarpSmem& S = reinterpret_cast<DetWarpSmem*>(det_smem)[wi];
   const int f = blockIdx.z;
   const int w = bt.ow[o], h = bt.oh[o], m = dc.margin;
-  const int xs0 = m + (blockIdx.x * kDetWarps + wi) * kStripCols;  // first window column of the strip
+  const int xs0 = m + (blockIdx.x * int(blockDim.x >> 5) + wi) * kStripCols;  // first window column of the strip
   const int y0 = m + blockIdx.y * seg_rows, y1 = min(h - m, y0 + seg_rows);
   if (xs0 >= w - m || y0 >= y1) return;  // warp-uniform
   const int x = xs0 - 1 + lane;
@@ -727,7 +727,10 @@ cudaError_t launch_detect(const Batch& bt, const DetConst& dc, int o, const CUte
     // rows and 2 extra alpha rows at its ends).
     const int strips = (ww + kStripCols - 1) / kStripCols;
     const int nseg = (hh + kSegTarget - 1) / kSegTarget, seg_rows = (hh + nseg - 1) / nseg;
-    dim3 grid((strips + kDetWarps - 1) / kDetWarps, nseg, bt.nframes);
+    // 2 or 3 warps (strips) per CTA, whichever leaves fewer idle warps
+    // (octave 0 of VGA: 21 strips -> 3; octave 1: 10 strips -> 2).
+    const int nw = ((strips + 2) / 3 * 3 - strips) <= ((strips + 1) / 2 * 2 - strips) ? 3 : 2;
+    dim3 grid((strips + nw - 1) / nw, nseg, bt.nframes);
     constexpr int smem = int(sizeof(DetWarpSmem)) * kDetWarps;
     static bool walk_configured = false;
     if (!walk_configured) {
@@ -737,7 +740,7 @@ cudaError_t launch_detect(const Batch& bt, const DetConst& dc, int o, const CUte
       if (e != cudaSuccess) return e;
       walk_configured = true;
     }
-    k_detect_walk<<<grid, 32 * kDetWarps, smem, st>>>(bt, dc, o, seg_rows);
+    k_detect_walk<<<grid, 32 * nw, int(sizeof(DetWarpSmem)) * nw, st>>>(bt, dc, o, seg_rows);
     return cudaGetLastError();
   }
   dim3 grid((ww + kDetW - 1) / kDetW, (hh + kDetH - 1) / kDetH, bt.nframes);
