@@ -56,6 +56,21 @@ __device__ __forceinline__ double sample_bilinear(const double* img, int w, doub
 
 struct Frame { const double* lvl; int w, h; double x, y, sigma; };
 
+// Orientation bin floor(wrap_angle(atan2(gy, gx)) / 2pi * 36 + 0.5) % 36
+// (descriptor.cpp:196-199). Only the integer bin is used, so an FP32 atan2
+// decides it whenever the value lies farther than 1e-3 bins from a bin edge
+// (its error is below 1e-5 bins); otherwise the FP64 expression runs, so the
+// bin is always the one the double computation gives.
+__device__ __forceinline__ int orient_bin(double gx, double gy) {
+  float a = atan2f(float(gy), float(gx));
+  if (a < 0.0f) a += 6.28318548f;
+  const float t = a * 5.72957795f + 0.5f;  // 36 / 2pi
+  const float fl = floorf(t), fr = t - fl;
+  if (fr > 1e-3f && fr < 1.0f - 1e-3f) return int(fl) % 36;
+  const double ang = wrap_angle(atan2(gy, gx));
+  return static_cast<int>(floor(ang / kTwoPi * 36 + 0.5)) % 36;
+}
+
 // resolve_frame (descriptor.cpp:149-170): nearest scale node, first minimum.
 __device__ __forceinline__ Frame resolve(const Batch& bt, const DetConst& dc, int f, const KP& k) {
   Frame fr;
@@ -118,8 +133,11 @@ __global__ void __launch_bounds__(32 * kOrientWarps) k_orient(Batch bt, DetConst
   }
   for (int b = lane; b < 36; b += 32) S.cnt[b] = 0;
   __syncwarp();
+  // (q + 0.5) / nx is at least 1/(2 nx) from an integer: exact row index.
+  const float inv_nx = nx > 0 ? 1.0f / float(nx) : 0.0f;
   for (int q = lane; q < npx; q += 32) {
-    const int ix = x_lo + q % nx, iy = y_lo + q / nx;
+    const int qy = int((float(q) + 0.5f) * inv_nx);
+    const int ix = x_lo + q - qy * nx, iy = y_lo + qy;
     const double dx = ix - fr.x, dy = iy - fr.y;
     const double d2 = dx * dx + dy * dy;
     int bin = 255;
@@ -130,8 +148,7 @@ __global__ void __launch_bounds__(32 * kOrientWarps) k_orient(Batch bt, DetConst
       const double gy = 0.5 * (row[fr.w] - row[-fr.w]);
       const double mag = hypot(gx, gy);
       if (mag != 0.0) {
-        const double ang = wrap_angle(atan2(gy, gx));
-        bin = static_cast<int>(floor(ang / kTwoPi * 36 + 0.5)) % 36;
+        bin = orient_bin(gx, gy);
         val = mag * exp(-d2 / denom);
         atomicAdd(&S.cnt[bin], 1);
       }
