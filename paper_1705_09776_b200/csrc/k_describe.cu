@@ -62,6 +62,10 @@ struct Frame { const double* lvl; int w, h; double x, y, sigma; };
 // (its error is below 1e-5 bins); otherwise the FP64 expression runs, so the
 // bin is always the one the double computation gives.
 __device__ __forceinline__ int orient_bin(double gx, double gy) {
+  if (fmax(fabs(gx), fabs(gy)) < 1e-30) {  // outside FP32's comfortable range: FP64 only
+    const double ang = wrap_angle(atan2(gy, gx));
+    return static_cast<int>(floor(ang / kTwoPi * 36 + 0.5)) % 36;
+  }
   float a = atan2f(float(gy), float(gx));
   if (a < 0.0f) a += 6.28318548f;
   const float t = a * 5.72957795f + 0.5f;  // 36 / 2pi
