@@ -81,6 +81,28 @@ int cdvz_gpu_encode_batch(cdvz_gpu_ctx* ctx, const uint8_t* pixels, int width, i
                           int count, int mode_id, int max_side, uint8_t* out, size_t out_cap,
                           size_t* offsets, int* status);
 
+/* PPM form of cdvz_gpu_encode_batch: `count` interleaved 8-bit RGB frames
+ * (row stride `stride` >= 3*width bytes). Each pixel becomes the grey value
+ * (0.299 r + 0.587 g + 0.114 b) * (1/255) on the device, exactly as
+ * load_image reads a P6 file (proj/src/image.cpp:82-87); resize_max_side then
+ * runs on that grey plane and the rest of the pipeline is unchanged. Same
+ * outputs and error behaviour as cdvz_gpu_encode_batch. */
+int cdvz_gpu_encode_batch_rgb(cdvz_gpu_ctx* ctx, const uint8_t* rgb, int width, int height, size_t stride,
+                              int count, int mode_id, int max_side, uint8_t* out, size_t out_cap,
+                              size_t* offsets, int* status);
+
+/* Header of an in-memory binary PGM (P5) or PPM (P6) file, parsed like
+ * load_image (proj/src/image.cpp:53-77; read_pnm_token :17-36): whitespace
+ * and '#' comments skipped between fields, maxval must be 255, both sides
+ * >= 8, one whitespace byte before the raster, and the raster must be
+ * complete. Sets *channels to 1 (P5) or 3 (P6) and *raster_offset to the
+ * raster's byte offset in `file` (pass file + offset to cdvz_gpu_encode_batch
+ * or cdvz_gpu_encode_batch_rgb with stride = width * channels). Host-only; no
+ * context. Returns CDVZ_GPU_DATA for a malformed file (message in
+ * cdvz_gpu_last_error(NULL)). */
+int cdvz_gpu_pnm_parse(const uint8_t* file, size_t len, int* width, int* height, int* channels,
+                       size_t* raster_offset);
+
 /* Same pipeline on frames already resident in device memory (d_pixels is a
  * device pointer to count*height*stride bytes). Containers stay on the device
  * in fixed slots of cdvz_gpu_container_slot(mode) bytes; d_lengths[count]

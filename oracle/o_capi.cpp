@@ -114,6 +114,27 @@ int orc_encode_u8(const char* bundle_text, size_t len, const uint8_t* px, int w,
   });
 }
 
+// encode_image(load_image(P6)) on interleaved RGB bytes -> CDVZ1 container bytes.
+int orc_encode_rgb(const char* bundle_text, size_t len, const uint8_t* rgb, int w, int h, size_t stride, int mode_id,
+                   int max_side, uint8_t* out, size_t cap, size_t* out_len) {
+  return guarded([&] {
+    const ModelBundle b = parse_model(std::string(bundle_text, len));
+    const EncodedImage e = encode_image(plane_from_rgb(rgb, w, h, stride), b, mode_by_id(mode_id), max_side, nullptr);
+    const auto bytes = serialize_container(e);
+    *out_len = bytes.size();
+    if (cap < bytes.size()) throw DataError("output buffer too small");
+    std::memcpy(out, bytes.data(), bytes.size());
+  });
+}
+
+// The grey plane load_image makes of RGB bytes (image.cpp:82-86).
+int orc_grey_rgb(const uint8_t* rgb, int w, int h, size_t stride, double* out) {
+  return guarded([&] {
+    const Plane p = plane_from_rgb(rgb, w, h, stride);
+    std::memcpy(out, p.px.data(), sizeof(double) * p.px.size());
+  });
+}
+
 // Frame-parallel batch encode (BASELINE.md CPU mode B): `threads` workers each
 // running a single-threaded encode. out is count * slot bytes; lens[count].
 int orc_encode_batch_u8(const char* bundle_text, size_t len, const uint8_t* px, int count, int w, int h,

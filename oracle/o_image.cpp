@@ -89,6 +89,18 @@ Plane plane_from_u8(const uint8_t* bytes, int w, int h, std::size_t stride) {
   return img;
 }
 
+// proj/src/image.cpp:82-86 (load_image, P6 branch)
+Plane plane_from_rgb(const uint8_t* rgb, int w, int h, std::size_t stride) {
+  Plane img(w, h);
+  const double inv = 1.0 / 255.0;
+  for (int y = 0; y < h; ++y)
+    for (int x = 0; x < w; ++x) {
+      const uint8_t* p = rgb + std::size_t(y) * stride + std::size_t(3) * x;
+      img.at(y, x) = (0.299 * p[0] + 0.587 * p[1] + 0.114 * p[2]) * inv;
+    }
+  return img;
+}
+
 // proj/src/image.cpp:101-102
 std::vector<uint8_t> plane_to_u8(const Plane& img) {
   std::vector<uint8_t> out(img.px.size());

@@ -64,6 +64,7 @@ struct Plane {
 
 void validate_plane(const Plane& img);                                  // image.cpp:46-51
 Plane plane_from_u8(const uint8_t* bytes, int w, int h, std::size_t stride);  // image.cpp:79-87
+Plane plane_from_rgb(const uint8_t* rgb, int w, int h, std::size_t stride);    // image.cpp:82-86
 std::vector<uint8_t> plane_to_u8(const Plane& img);                     // image.cpp:101-102 (save_pgm)
 Plane rescale_bilinear(const Plane& img, int out_w, int out_h);         // image.cpp:107-129
 Plane resize_max_side(const Plane& img, int limit = 640);               // image.cpp:131-145

@@ -96,6 +96,8 @@ def _lib() -> ctypes.CDLL:
         "cdvz_gpu_bundle_check": (I, [ctypes.c_char_p, S, ctypes.POINTER(U32), ctypes.POINTER(I)]),
         "cdvz_gpu_bundle_info": (I, [P, ctypes.POINTER(U32), ctypes.POINTER(I), ctypes.POINTER(I)]),
         "cdvz_gpu_encode_batch": (I, [P, P, I, I, S, I, I, I, P, S, P, P]),
+        "cdvz_gpu_encode_batch_rgb": (I, [P, P, I, I, S, I, I, I, P, S, P, P]),
+        "cdvz_gpu_pnm_parse": (I, [P, S, ctypes.POINTER(I), ctypes.POINTER(I), ctypes.POINTER(I), ctypes.POINTER(S)]),
         "cdvz_gpu_encode_device": (I, [P, P, I, I, S, I, I, I, P, P]),
         "cdvz_gpu_container_slot": (S, [I]),
         "cdvz_gpu_sync": (I, [P]),
@@ -197,6 +199,19 @@ class PinnedBuffer:
             self.ptr = None
 
 
+def parse_pnm(data: bytes):
+    """The header of a binary PGM/PPM held in memory, parsed like load_image
+    (proj/src/image.cpp:53-77): returns (width, height, channels, raster_offset);
+    raises DataError for a malformed file."""
+    lib = _lib()
+    buf = ctypes.create_string_buffer(bytes(data), len(data))
+    w, h, ch, off = ctypes.c_int(), ctypes.c_int(), ctypes.c_int(), ctypes.c_size_t()
+    code = lib.cdvz_gpu_pnm_parse(ctypes.addressof(buf), len(data), ctypes.byref(w), ctypes.byref(h), ctypes.byref(ch),
+                                  ctypes.byref(off))
+    _raise(code, lib.cdvz_gpu_last_error(None).decode())
+    return w.value, h.value, ch.value, off.value
+
+
 class Extractor:
     """One GPU context holding a model bundle: the reference's
     ``encode_image(img, bundle, mode)`` for batches of 8-bit frames."""
@@ -232,24 +247,38 @@ class Extractor:
 
     # -- reference API
     def encode_batch(self, frames: np.ndarray, mode, max_side: int = 640):
-        """Encodes ``frames`` (uint8, [N, H, W]) and returns (containers, status):
-        ``containers[i]`` is frame i's CDVZ1 byte string (b"" on failure)."""
+        """Encodes ``frames`` (uint8, [N, H, W] grey, or [N, H, W, 3] RGB as in a
+        PPM) and returns (containers, status): ``containers[i]`` is frame i's
+        CDVZ1 byte string (b"" on failure)."""
         m = mode if isinstance(mode, ModeSpec) else (mode_by_name(mode) if isinstance(mode, str) else mode_by_id(mode))
         frames = np.ascontiguousarray(frames, dtype=np.uint8)
         if frames.ndim == 2:
             frames = frames[None]
-        if frames.ndim != 3:
-            raise UsageError("frames must be [N, H, W] uint8")
-        n, h, w = frames.shape
+        rgb = frames.ndim == 4
+        if frames.ndim not in (3, 4) or (rgb and frames.shape[-1] != 3):
+            raise UsageError("frames must be [N, H, W] or [N, H, W, 3] uint8")
+        n, h, w = frames.shape[:3]
+        ch = 3 if rgb else 1
         slot = m.budget_bytes + 28
         out = np.empty(max(1, n * slot), dtype=np.uint8)
         offsets = np.zeros(n + 1, dtype=np.uint64)
         status = np.zeros(max(1, n), dtype=np.int32)
-        self._check(self._lib.cdvz_gpu_encode_batch(self._ctx, frames.ctypes.data, w, h, w, n, m.id, max_side,
-                                                    out.ctypes.data, out.nbytes, offsets.ctypes.data,
-                                                    status.ctypes.data))
+        fn = self._lib.cdvz_gpu_encode_batch_rgb if rgb else self._lib.cdvz_gpu_encode_batch
+        self._check(fn(self._ctx, frames.ctypes.data, w, h, w * ch, n, m.id, max_side, out.ctypes.data, out.nbytes,
+                       offsets.ctypes.data, status.ctypes.data))
         res = [out[int(offsets[i]):int(offsets[i + 1])].tobytes() for i in range(n)]
         return res, status[:n].copy()
+
+    def encode_pnm(self, data: bytes, mode, max_side: int = 640) -> bytes:
+        """load_image + encode_image + serialize_container for one in-memory
+        PGM/PPM file (proj/src/image.cpp:53-92)."""
+        w, h, ch, off = parse_pnm(data)
+        raster = np.frombuffer(data, dtype=np.uint8, count=w * h * ch, offset=off)
+        frames = raster.reshape(1, h, w, 3) if ch == 3 else raster.reshape(1, h, w)
+        res, status = self.encode_batch(frames, mode, max_side)
+        if status[0] != 0:
+            _raise(int(status[0]), self._lib.cdvz_gpu_last_error(self._ctx).decode() or "frame failed")
+        return res[0]
 
     def encode_image(self, frame: np.ndarray, mode, max_side: int = 640) -> bytes:
         """encode_image + serialize_container for one frame; raises on failure."""

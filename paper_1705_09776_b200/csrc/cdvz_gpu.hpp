@@ -21,6 +21,7 @@
 
 #include <algorithm>
 #include <fstream>
+#include <iterator>
 #include <map>
 #include <memory>
 #include <sstream>
@@ -170,6 +171,44 @@ inline std::vector<std::vector<uint8_t>> encode_batch(const std::vector<const Gr
 inline std::vector<uint8_t> encode_image(const GrayImage8& img, const ModelBundle& bundle, const ModeSpec& mode,
                                          StageTimings* timings = nullptr, const EncodeOptions& opts = {}) {
   return encode_batch({&img}, bundle, mode, timings, opts)[0];
+}
+
+// ------------------------------------------------ ingest (image.cpp:53-92)
+// A binary PGM (channels 1) or PPM (channels 3) raster as load_image reads it;
+// the grey conversion of a PPM happens on the device.
+struct PnmImage {
+  int width = 0, height = 0, channels = 1;
+  std::vector<uint8_t> raster;  // width * height * channels bytes, row-major
+};
+
+inline PnmImage load_pnm(const std::string& path) {  // load_image's file handling and header checks
+  std::ifstream in(path, std::ios::binary);
+  if (!in) throw DataError("cannot open image file: " + path);
+  const std::string bytes((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+  PnmImage img;
+  std::size_t off = 0;
+  raise_for(cdvz_gpu_pnm_parse(reinterpret_cast<const uint8_t*>(bytes.data()), bytes.size(), &img.width, &img.height,
+                               &img.channels, &off),
+            cdvz_gpu_last_error(nullptr));
+  img.raster.assign(bytes.begin() + long(off), bytes.begin() + long(off) + long(img.width) * img.height * img.channels);
+  return img;
+}
+
+// encode_image(load_image(path), ...) for an in-memory PGM/PPM raster.
+inline std::vector<uint8_t> encode_image(const PnmImage& img, const ModelBundle& bundle, const ModeSpec& mode,
+                                         const EncodeOptions& opts = {}, int device = 0) {
+  cdvz_gpu_ctx* ctx = bundle.context(device);
+  std::vector<uint8_t> buf(cdvz_gpu_container_slot(mode.id));
+  std::size_t offsets[2] = {0, 0};
+  int status = 0;
+  const std::size_t stride = std::size_t(img.width) * img.channels;
+  auto fn = img.channels == 3 ? cdvz_gpu_encode_batch_rgb : cdvz_gpu_encode_batch;
+  raise_for(fn(ctx, img.raster.data(), img.width, img.height, stride, 1, mode.id, opts.max_side, buf.data(), buf.size(),
+               offsets, &status),
+            cdvz_gpu_last_error(ctx));
+  raise_for(status, "frame failed on the device");
+  buf.resize(offsets[1]);
+  return buf;
 }
 
 // ------------------------------------------------ retrieval (eval.hpp:17-55)

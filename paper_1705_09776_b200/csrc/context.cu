@@ -8,6 +8,7 @@
 // failures (capacity overflow) are flagged on the device and surface as
 // status 3 for that frame only.
 #include <algorithm>
+#include <cctype>
 #include <cmath>
 #include <cstring>
 #include <memory>
@@ -31,6 +32,10 @@ cudaError_t launch_select(const Batch& bt, const Model& md, const EncodeConst& e
 cudaError_t launch_describe(const Batch& bt, const DetConst& dc, const Model& md, const EncodeConst& ec, cudaStream_t st);
 cudaError_t launch_scfv_pack(const Batch& bt, const Model& md, const EncodeConst& ec, uint8_t* out, uint32_t* lengths,
                              cudaStream_t st, cudaEvent_t after_aggregation);
+cudaError_t launch_resize_f64(const double* grey, int w_in, int h_in, double* out, int w_out, int h_out, int frames,
+                              cudaStream_t st);
+cudaError_t launch_grey_rgb(const uint8_t* rgb, long long stride, long long frame_bytes, int w, int h, double* out,
+                            int frames, cudaStream_t st);
 cudaError_t launch_resize(const uint8_t* pix, long long stride, long long frame_bytes, int w_in, int h_in, double* out,
                           int w_out, int h_out, int frames, cudaStream_t st);
 struct SynthParams {
@@ -97,6 +102,8 @@ struct Lane {
   DeviceBuffer dbg_oct;
   int geo_w = 0, geo_h = 0, geo_frames = 0;
   bool geo_resize = false, geo_debug = false;
+  long long geo_grey = 0;  // doubles of the original-size grey plane buffer (RGB input + resize)
+  double* grey = nullptr;  // [frame][h][w] grey plane of RGB frames before resize
   cudaStream_t sA = nullptr, sB = nullptr;
   cudaEvent_t start = nullptr, done = nullptr;
   cudaEvent_t stage[6] = {};
@@ -273,8 +280,12 @@ struct cdvz_gpu_ctx {
   }
 
   // Sizes every per-batch buffer for `frames` frames of prepared size W x H.
-  void plan(Lane& L, int W, int H, int frames, bool need_resize) {
-    if (W == L.geo_w && H == L.geo_h && frames <= L.geo_frames && (!need_resize || L.geo_resize) && L.geo_debug == debug)
+  // need_resize: octave 0 reads an f64 plane (pixf) of the prepared size,
+  // because the frames are resized or RGB. grey_px: pixels of an
+  // original-size grey plane per frame (RGB frames that are also resized), or 0.
+  void plan(Lane& L, int W, int H, int frames, bool need_resize, long long grey_px = 0) {
+    if (W == L.geo_w && H == L.geo_h && frames <= L.geo_frames && (!need_resize || L.geo_resize) && L.geo_debug == debug &&
+        grey_px * frames <= L.geo_grey)
       return;
     CDVZ_CUDA_CHECK(cudaStreamSynchronize(L.sA));
     CDVZ_CUDA_CHECK(cudaStreamSynchronize(L.sB));
@@ -312,6 +323,7 @@ struct cdvz_gpu_ctx {
     };
     nb.pyr = static_cast<double*>(alloc(sizeof(double) * F * nb.frame_doubles));
     nb.pixf = need_resize ? static_cast<double*>(alloc(sizeof(double) * F * W * H)) : nullptr;
+    L.grey = grey_px ? static_cast<double*>(alloc(sizeof(double) * F * grey_px)) : nullptr;
     nb.raw = static_cast<KP*>(alloc(sizeof(KP) * F * std::max(1, n_oct) * nb.cap_oct));
     nb.raw_count = static_cast<int*>(alloc(sizeof(int) * F * std::max(1, n_oct)));
     nb.oct_count = static_cast<int*>(alloc(sizeof(int) * F * std::max(1, n_oct)));
@@ -378,6 +390,7 @@ struct cdvz_gpu_ctx {
     L.geo_h = H;
     L.geo_frames = frames;
     L.geo_resize = need_resize;
+    L.geo_grey = grey_px * F;
     L.geo_debug = debug;
   }
 
@@ -426,13 +439,17 @@ struct cdvz_gpu_ctx {
   // With host pointers (h_pix / h_out / h_len), the frames are copied in on a
   // dedicated copy stream ahead of the kernels and each chunk's containers are
   // copied out on its describe stream, overlapping the other lane's kernels.
+  // channels: 1 = grey bytes (PGM), 3 = interleaved RGB bytes (PPM), whose
+  // grey plane is formed on the device first.
   void run(const uint8_t* d_pix, int w, int h, long long stride, int frames, int mode_id, int max_side, uint8_t* d_out,
            uint32_t* d_len, const uint8_t* h_pix = nullptr, size_t h_stride = 0, uint8_t* h_out = nullptr,
-           uint32_t* h_len = nullptr) {
+           uint32_t* h_len = nullptr, int channels = 1) {
     if (w < 8 || h < 8) throw DataError("image smaller than 8 px per side");
     int W, H;
     prepared_dims(w, h, max_side, W, H);
     const bool resize = (W != w || H != h);
+    const bool rgb = channels == 3;
+    const bool f64_base = resize || rgb;  // octave 0 reads the f64 plane pixf
     EncodeConst ec = encode_const(mode_id);
     ec.cx = (W - 1) / 2.0;
     ec.cy = (H - 1) / 2.0;
@@ -448,7 +465,7 @@ struct cdvz_gpu_ctx {
     const int n_lanes = serial ? 1 : kLanes;
     for (int l = 0; l < std::min(chunks, n_lanes); ++l) {
       if (!lanes[l].sA) lanes[l].init();
-      plan(lanes[l], W, H, per, resize);
+      plan(lanes[l], W, H, per, f64_base, rgb && resize ? (long long)w * h : 0);
     }
     launches = 0;
     pyr_ms = 0.0;
@@ -469,7 +486,7 @@ struct cdvz_gpu_ctx {
       for (int c = 0; c < chunks; ++c) {
         const int base = cb[size_t(c)], nf = cb[size_t(c) + 1] - base;
         CDVZ_CUDA_CHECK(cudaMemcpy2DAsync(const_cast<uint8_t*>(d_pix) + (long long)base * h * stride, size_t(stride),
-                                          h_pix + size_t(base) * h * h_stride, h_stride, size_t(w), size_t(h) * nf,
+                                          h_pix + size_t(base) * h * h_stride, h_stride, size_t(w) * channels, size_t(h) * nf,
                                           cudaMemcpyHostToDevice, copy_st));
         CDVZ_CUDA_CHECK(cudaEventRecord(copy_ev[size_t(c)], copy_st));
       }
@@ -492,13 +509,21 @@ struct cdvz_gpu_ctx {
       if (h_pix) CDVZ_CUDA_CHECK(cudaStreamWaitEvent(L.sA, copy_ev[size_t(c)], 0));
       CDVZ_CUDA_CHECK(cudaEventRecord(L.start, L.sA));
       CDVZ_CUDA_CHECK(cudaMemsetAsync(b.status, 0, sizeof(int) * nf, L.sA));
-      if (resize) {
+      if (rgb) {  // load_image's PPM branch, then resize_max_side on the grey plane
+        double* grey = resize ? L.grey : const_cast<double*>(b.pixf);
+        CDVZ_CUDA_CHECK(launch_grey_rgb(b.pix8, stride, b.frame_bytes8, w, h, grey, nf, L.sA));
+        ++launches;
+        if (resize) {
+          CDVZ_CUDA_CHECK(launch_resize_f64(grey, w, h, const_cast<double*>(b.pixf), W, H, nf, L.sA));
+          ++launches;
+        }
+      } else if (resize) {
         CDVZ_CUDA_CHECK(launch_resize(b.pix8, stride, b.frame_bytes8, w, h, const_cast<double*>(b.pixf), W, H, nf, L.sA));
         ++launches;
       }
       double bytes = 0.0;
       for (int o = 0; o < b.n_oct; ++o) {
-        const int src = o == 0 ? (resize ? 1 : 0) : 2;
+        const int src = o == 0 ? (f64_base ? 1 : 0) : 2;
         CDVZ_CUDA_CHECK(cudaEventRecord(L.blur[2 * o], L.sA));
         CDVZ_CUDA_CHECK(launch_octave(b, dc, o, src, L.sA));
         CDVZ_CUDA_CHECK(cudaEventRecord(L.blur[2 * o + 1], L.sA));
@@ -517,7 +542,7 @@ struct cdvz_gpu_ctx {
         // the base (1 B/px u8 at octave 0, 8 B/px f64 above) and writes 4 G
         // levels (32 B/px); K1b reads the 4 G levels of its window back.
         const double px = double(b.ow[o]) * b.oh[o];
-        const double in_b = (o == 0) ? (resize ? 8.0 : 1.0) : 8.0;
+        const double in_b = (o == 0) ? (f64_base ? 8.0 : 1.0) : 8.0;
         const int ww = std::max(0, b.ow[o] - 2 * dc.margin), hh = std::max(0, b.oh[o] - 2 * dc.margin);
         bytes += double(nf) * (px * (in_b + 32.0) + 32.0 * ww * hh);
       }
@@ -700,11 +725,18 @@ int cdvz_gpu_sync(cdvz_gpu_ctx* ctx) {
   return guarded(ctx, [&] { CDVZ_CUDA_CHECK(cudaStreamSynchronize(ctx->st)); });
 }
 
-int cdvz_gpu_encode_batch(cdvz_gpu_ctx* ctx, const uint8_t* pixels, int width, int height, size_t stride, int count,
-                          int mode_id, int max_side, uint8_t* out, size_t out_cap, size_t* offsets, int* status) {
+}  // extern "C"
+
+namespace {
+
+// Host-frame batch encode of grey (channels 1) or RGB (channels 3) rasters.
+int encode_host_batch(cdvz_gpu_ctx* ctx, const uint8_t* pixels, int width, int height, size_t stride, int count,
+                      int mode_id, int max_side, uint8_t* out, size_t out_cap, size_t* offsets, int* status,
+                      int channels) {
   return guarded(ctx, [&] {
     if (!ctx || (!pixels && count > 0) || !offsets || !status) throw UsageError("null argument");
     if (count < 0) throw UsageError("negative frame count");
+    if (stride < size_t(width) * channels) throw UsageError("row stride shorter than a row");
     offsets[0] = 0;
     if (count == 0) return;
     const size_t slot = mode_by_id(mode_id).budget + 28;
@@ -716,7 +748,7 @@ int cdvz_gpu_encode_batch(cdvz_gpu_ctx* ctx, const uint8_t* pixels, int width, i
       throw DataError("image smaller than 8 px per side");
     }
     CDVZ_CUDA_CHECK(cudaSetDevice(ctx->device));
-    const size_t frame_bytes = size_t(width) * height;
+    const size_t frame_bytes = size_t(width) * height * channels;
     // Frames per call to run(): bounded so the device staging stays < 4 GB.
     const int group = int(std::max<size_t>(1, std::min<size_t>(size_t(count), (size_t(4) << 30) / frame_bytes)));
     ctx->stage_in.ensure(frame_bytes * group);
@@ -729,8 +761,9 @@ int cdvz_gpu_encode_batch(cdvz_gpu_ctx* ctx, const uint8_t* pixels, int width, i
     int acc_launches = 0;
     for (int base = 0; base < count; base += group) {
       const int nf = std::min(group, count - base);
-      ctx->run(ctx->stage_in.as<uint8_t>(), width, height, width, nf, mode_id, max_side, ctx->stage_out.as<uint8_t>(),
-               ctx->stage_len.as<uint32_t>(), pixels + size_t(base) * height * stride, stride, ctx->pin_out, ctx->pin_len);
+      ctx->run(ctx->stage_in.as<uint8_t>(), width, height, (long long)width * channels, nf, mode_id, max_side,
+               ctx->stage_out.as<uint8_t>(), ctx->stage_len.as<uint32_t>(), pixels + size_t(base) * height * stride, stride,
+               ctx->pin_out, ctx->pin_len, channels);
       CDVZ_CUDA_CHECK(cudaStreamSynchronize(ctx->st));
       for (int i = 0; i < 5; ++i) acc_ms[i] += ctx->stage_ms[i];
       acc_pyr_ms += ctx->pyr_ms;
@@ -756,6 +789,75 @@ int cdvz_gpu_encode_batch(cdvz_gpu_ctx* ctx, const uint8_t* pixels, int width, i
     ctx->pyr_bytes = acc_pyr_bytes;
     ctx->launches = acc_launches;
   });
+}
+
+}  // namespace
+
+extern "C" {
+
+// load_image's header parse (proj/src/image.cpp:53-77; read_pnm_token
+// :17-36) on an in-memory file.
+int cdvz_gpu_pnm_parse(const uint8_t* file, size_t len, int* width, int* height, int* channels, size_t* raster_offset) {
+  return guarded(nullptr, [&] {
+    if (!file || !width || !height || !channels || !raster_offset) throw UsageError("null argument");
+    size_t pos = 0;
+    if (len < 2 || file[0] != 'P' || (file[1] != '5' && file[1] != '6'))
+      throw DataError("unsupported image format (expected binary PGM/PPM)");
+    const bool color = file[1] == '6';
+    pos = 2;
+    auto token = [&](const char* what) {
+      for (;;) {  // whitespace and '#' comments (to the end of the line)
+        if (pos >= len) throw DataError(std::string("truncated header while reading ") + what);
+        const int c = file[pos];
+        if (std::isspace(c)) {
+          ++pos;
+          continue;
+        }
+        if (c == '#') {
+          while (pos < len && file[pos] != '\n') ++pos;
+          if (pos < len) ++pos;
+          continue;
+        }
+        break;
+      }
+      // operator>>(int): optional sign, then at least one digit, no overflow.
+      size_t p = pos;
+      bool neg = false;
+      if (file[p] == '+' || file[p] == '-') neg = file[p++] == '-';
+      long long v = 0;
+      size_t digits = 0;
+      while (p < len && file[p] >= '0' && file[p] <= '9') {
+        v = v * 10 + (file[p++] - '0');
+        if (v > 2147483647LL) throw DataError(std::string("invalid header field: ") + what);
+        ++digits;
+      }
+      if (digits == 0 || (neg && v > 0)) throw DataError(std::string("invalid header field: ") + what);
+      pos = p;
+      return int(v);
+    };
+    const int w = token("width");
+    const int h = token("height");
+    const int maxval = token("maxval");
+    if (maxval != 255) throw DataError("only maxval 255 is supported");
+    if (w < 8 || h < 8) throw DataError("image smaller than 8 px per side");
+    ++pos;  // the single whitespace byte before the raster
+    const size_t ch = color ? 3 : 1;
+    if (pos > len || len - pos < size_t(w) * size_t(h) * ch) throw DataError("truncated raster data");
+    *width = w;
+    *height = h;
+    *channels = int(ch);
+    *raster_offset = pos;
+  });
+}
+
+int cdvz_gpu_encode_batch(cdvz_gpu_ctx* ctx, const uint8_t* pixels, int width, int height, size_t stride, int count,
+                          int mode_id, int max_side, uint8_t* out, size_t out_cap, size_t* offsets, int* status) {
+  return encode_host_batch(ctx, pixels, width, height, stride, count, mode_id, max_side, out, out_cap, offsets, status, 1);
+}
+
+int cdvz_gpu_encode_batch_rgb(cdvz_gpu_ctx* ctx, const uint8_t* rgb, int width, int height, size_t stride, int count,
+                              int mode_id, int max_side, uint8_t* out, size_t out_cap, size_t* offsets, int* status) {
+  return encode_host_batch(ctx, rgb, width, height, stride, count, mode_id, max_side, out, out_cap, offsets, status, 3);
 }
 
 int cdvz_gpu_stage_times(cdvz_gpu_ctx* ctx, double ms[5]) {

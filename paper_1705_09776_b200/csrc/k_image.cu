@@ -1,4 +1,5 @@
-// K0 — ingest: bilinear resize of u8 frames to the prepared raster
+// K0 — ingest: PPM RGB -> grey conversion (load_image, proj/src/image.cpp:79-87),
+// bilinear resize of u8 or f64 grey frames to the prepared raster
 // (resize_max_side / rescale_bilinear, proj/src/image.cpp:107-145), and the
 // deterministic synthetic frame generator used by the benchmarks
 // (synth_image / synth_corpus, proj/src/synthetic.cpp:11-61).
@@ -6,14 +7,23 @@
 
 namespace cdvz_gpu {
 
-// One thread per output pixel; frames along grid.z.
-__global__ void k_resize(const uint8_t* pix, long long stride, long long frame_bytes, int w_in, int h_in, double* out,
+// One thread per output pixel; frames along grid.z. Source values are u8
+// bytes read as b / 255 (load_image of a PGM) or an f64 grey plane (a
+// converted PPM).
+template <class T>
+__device__ __forceinline__ double src_value(const T* row, int x) {
+  if constexpr (sizeof(T) == 1) return row[x] * (1.0 / 255.0);  // image.cpp:79-87
+  else return row[x];
+}
+
+template <class T>
+__global__ void k_resize(const T* pix, long long stride, long long frame_elems, int w_in, int h_in, double* out,
                          int w_out, int h_out, double sx, double sy) {
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
   const int y = blockIdx.y;
   const int f = blockIdx.z;
   if (x >= w_out) return;
-  const uint8_t* img = pix + f * frame_bytes;
+  const T* img = pix + f * frame_elems;
   double src_y = (y + 0.5) * sy - 0.5;
   src_y = fmin(fmax(src_y, 0.0), double(h_in - 1));
   const int y0 = static_cast<int>(src_y);
@@ -24,9 +34,10 @@ __global__ void k_resize(const uint8_t* pix, long long stride, long long frame_b
   const int x0 = static_cast<int>(src_x);
   const int x1 = min(x0 + 1, w_in - 1);
   const double fx = src_x - x0;
-  const double inv = 1.0 / 255.0;
-  const double p00 = img[(long long)y0 * stride + x0] * inv, p01 = img[(long long)y0 * stride + x1] * inv;
-  const double p10 = img[(long long)y1 * stride + x0] * inv, p11 = img[(long long)y1 * stride + x1] * inv;
+  const T* r0 = img + (long long)y0 * stride;
+  const T* r1 = img + (long long)y1 * stride;
+  const double p00 = src_value(r0, x0), p01 = src_value(r0, x1);
+  const double p10 = src_value(r1, x0), p11 = src_value(r1, x1);
   out[(long long)f * w_out * h_out + (long long)y * w_out + x] =
       (1.0 - fy) * ((1.0 - fx) * p00 + fx * p01) + fy * ((1.0 - fx) * p10 + fx * p11);
 }
@@ -35,7 +46,35 @@ cudaError_t launch_resize(const uint8_t* pix, long long stride, long long frame_
                           int w_out, int h_out, int frames, cudaStream_t st) {
   const double sx = static_cast<double>(w_in) / w_out, sy = static_cast<double>(h_in) / h_out;
   dim3 grid((w_out + 127) / 128, h_out, frames);
-  k_resize<<<grid, 128, 0, st>>>(pix, stride, frame_bytes, w_in, h_in, out, w_out, h_out, sx, sy);
+  k_resize<uint8_t><<<grid, 128, 0, st>>>(pix, stride, frame_bytes, w_in, h_in, out, w_out, h_out, sx, sy);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_resize_f64(const double* grey, int w_in, int h_in, double* out, int w_out, int h_out, int frames,
+                              cudaStream_t st) {
+  const double sx = static_cast<double>(w_in) / w_out, sy = static_cast<double>(h_in) / h_out;
+  dim3 grid((w_out + 127) / 128, h_out, frames);
+  k_resize<double><<<grid, 128, 0, st>>>(grey, w_in, (long long)w_in * h_in, w_in, h_in, out, w_out, h_out, sx, sy);
+  return cudaGetLastError();
+}
+
+// PPM ingest: interleaved 8-bit RGB -> grey f64, (0.299 r + 0.587 g + 0.114 b)
+// * (1 / 255) in this order (load_image, image.cpp:82-86). One thread per
+// pixel, frames along grid.z; `out` is a dense w x h plane per frame.
+__global__ void k_grey_rgb(const uint8_t* rgb, long long stride, long long frame_bytes, int w, int h, double* out) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int y = blockIdx.y;
+  const int f = blockIdx.z;
+  if (x >= w) return;
+  const uint8_t* p = rgb + f * frame_bytes + (long long)y * stride + 3LL * x;
+  const double inv = 1.0 / 255.0;
+  out[(long long)f * w * h + (long long)y * w + x] = (0.299 * p[0] + 0.587 * p[1] + 0.114 * p[2]) * inv;
+}
+
+cudaError_t launch_grey_rgb(const uint8_t* rgb, long long stride, long long frame_bytes, int w, int h, double* out,
+                            int frames, cudaStream_t st) {
+  dim3 grid((w + 127) / 128, h, frames);
+  k_grey_rgb<<<grid, 128, 0, st>>>(rgb, stride, frame_bytes, w, h, out);
   return cudaGetLastError();
 }
 

@@ -36,6 +36,8 @@ def lib() -> ctypes.CDLL:
         L.orc_bundle_crc.argtypes = [ctypes.c_char_p, S, ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(I)]
         L.orc_encode_u8.argtypes = [ctypes.c_char_p, S, P, I, I, S, I, I, P, S, ctypes.POINTER(S), P]
         L.orc_encode_batch_u8.argtypes = [ctypes.c_char_p, S, P, I, I, I, I, I, I, P, S, P]
+        L.orc_encode_rgb.argtypes = [ctypes.c_char_p, S, P, I, I, S, I, I, P, S, ctypes.POINTER(S)]
+        L.orc_grey_rgb.argtypes = [P, I, I, S, P]
         L.orc_trace_u8.argtypes = [ctypes.c_char_p, S, P, I, I, I, I, ctypes.POINTER(P)]
         L.orc_trace_free.argtypes = [P]
         L.orc_trace_get.argtypes = [P, ctypes.c_char_p, P, S, ctypes.POINTER(S)]
@@ -84,6 +86,35 @@ def encode(text: str, frame: np.ndarray, mode_id: int, max_side: int = 640) -> b
     _check(lib().orc_encode_u8(raw, len(raw), frame.ctypes.data, w, h, w, mode_id, max_side, out.ctypes.data, cap,
                                ctypes.byref(n), None))
     return out[: n.value].tobytes()
+
+
+def encode_rgb(text: str, frame: np.ndarray, mode_id: int, max_side: int = 640) -> bytes:
+    """encode_image(load_image(P6 raster)) for one [H, W, 3] uint8 frame."""
+    frame = np.ascontiguousarray(frame, dtype=np.uint8)
+    h, w, _ = frame.shape
+    cap = 16384 + 64
+    out = np.empty(cap, dtype=np.uint8)
+    n = ctypes.c_size_t()
+    raw = text.encode()
+    _check(lib().orc_encode_rgb(raw, len(raw), frame.ctypes.data, w, h, 3 * w, mode_id, max_side, out.ctypes.data, cap,
+                                ctypes.byref(n)))
+    return out[: n.value].tobytes()
+
+
+def grey_rgb(frame: np.ndarray) -> np.ndarray:
+    """The grey plane load_image makes of a P6 raster ([H, W, 3] uint8)."""
+    frame = np.ascontiguousarray(frame, dtype=np.uint8)
+    h, w, _ = frame.shape
+    out = np.empty((h, w), dtype=np.float64)
+    _check(lib().orc_grey_rgb(frame.ctypes.data, w, h, 3 * w, out.ctypes.data))
+    return out
+
+
+def synth_rgb(base_seed: int, count: int, w: int, h: int) -> np.ndarray:
+    """[count, h, w, 3] colour frames whose channels are three synthetic grey
+    frames (synth_corpus seeds base, base + count, base + 2 count)."""
+    g = synth_frames(base_seed, 3 * count, w, h)
+    return np.stack([g[:count], g[count:2 * count], g[2 * count:]], axis=-1)
 
 
 def encode_batch(text: str, frames: np.ndarray, mode_id: int, max_side: int = 640, threads: int = 8) -> list:

@@ -1,0 +1,50 @@
+"""GPU PPM ingest: cdvz_gpu_encode_batch_rgb (grey conversion on the device,
+then resize_max_side on the grey plane) byte-identical to the oracle's
+encode_image(load_image(P6)) (proj/src/image.cpp:53-92, pipeline.cpp:54-97)."""
+import numpy as np
+import pytest
+
+import oracle_lib
+import paper_1705_09776_b200 as cg
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ex(bundle_b8):
+    e = cg.Extractor(bundle_b8, max_batch=4)
+    yield e
+    e.close()
+
+
+@pytest.mark.parametrize("w,h,mode", [(640, 480, 3), (333, 257, 1), (1280, 720, 5)])
+def test_rgb_containers_match_oracle(ex, bundle_b8, w, h, mode):
+    frames = oracle_lib.synth_rgb(900 + w, 3, w, h)
+    got, status = ex.encode_batch(frames, mode)
+    assert (status == 0).all()
+    for i in range(3):
+        assert got[i] == oracle_lib.encode_rgb(bundle_b8, frames[i], mode), (w, h, i)
+
+
+def test_grey_rgb_keeps_the_ppm_arithmetic(ex):
+    """r = g = b = v: load_image's P6 grey ((0.299 v + 0.587 v) + 0.114 v) / 255
+    is not always v / 255 bit for bit, so the RGB path must not shortcut to
+    the PGM path; the containers follow the P6 arithmetic."""
+    g = oracle_lib.synth_frames(31, 2, 320, 240)
+    rgb = np.repeat(g[..., None], 3, axis=-1)
+    v = np.arange(256, dtype=np.float64)
+    assert not np.array_equal(((0.299 * v + 0.587 * v) + 0.114 * v) * (1.0 / 255.0), v * (1.0 / 255.0))
+    got, status = ex.encode_batch(rgb, "4K")
+    assert (status == 0).all()
+    assert got[0] == oracle_lib.encode_rgb(oracle_lib.bundle_text("b8"), rgb[0], 3)
+
+
+def test_encode_pnm_files(ex, bundle_b8):
+    grey = oracle_lib.synth_frames(77, 1, 160, 120)[0]
+    pgm = b"P5\n# synthetic\n160 120\n255\n" + grey.tobytes()
+    assert ex.encode_pnm(pgm, "2K") == oracle_lib.encode(bundle_b8, grey, 2)
+    rgb = oracle_lib.synth_rgb(78, 1, 160, 120)[0]
+    ppm = b"P6 160 120 255\n" + rgb.tobytes()
+    assert ex.encode_pnm(ppm, "2K") == oracle_lib.encode_rgb(bundle_b8, rgb, 2)
+    with pytest.raises(cg.DataError):
+        ex.encode_pnm(b"P6 160 120 255\n" + rgb.tobytes()[:-1], "2K")
