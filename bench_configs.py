@@ -40,10 +40,13 @@ def config3(cg, oracle_lib, bundle, frames=1024, batch=256):
     parity = got == oracle_lib.encode_batch(bundle, fr[:2], mode.id)
     for _ in range(2):
         ex.encode_batch(fr[:batch], mode)
-    t0 = time.perf_counter()
-    for s in range(0, frames, batch):
-        out, st = ex.encode_batch(fr[s:s + batch], mode)
-    e2e = frames / (time.perf_counter() - t0)
+    rates = []
+    for _ in range(3):  # median of three passes over the stream
+        t0 = time.perf_counter()
+        for s in range(0, frames, batch):
+            out, st = ex.encode_batch(fr[s:s + batch], mode)
+        rates.append(frames / (time.perf_counter() - t0))
+    e2e = sorted(rates)[1]
     slot = cg.container_slot(mode)
     d_out, d_len = ex.device_buffer(frames * slot), ex.device_buffer(frames * 4)
     ex.encode_device(d, frames, w, h, mode, d_out, d_len)
@@ -57,7 +60,9 @@ def config3(cg, oracle_lib, bundle, frames=1024, batch=256):
     return {"config": "configs[2]: synthetic 1920x1080 stream -> 640x360, 16K mode, B8, 1 B200",
             "metric": "frames/s", "e2e_value": e2e, "device_value": dev, "frames": frames, "batch": batch,
             "h2d_bytes_per_frame": w * h, "parity_first_2_frames": bool(parity),
-            "note": "e2e: pinned host frames through cdvz_gpu_encode_batch in batches of 256 (copies inside); "
+            "e2e_passes": rates,
+            "note": "e2e: pinned host frames through cdvz_gpu_encode_batch in batches of 256 (copies inside; each "
+                    "call splits into >= 4 chunks so copies overlap kernels), median of 3 passes; "
                     "device: frames resident in HBM, CUDA events"}
 
 

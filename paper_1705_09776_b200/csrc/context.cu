@@ -455,7 +455,11 @@ struct cdvz_gpu_ctx {
     ec.cy = (H - 1) / 2.0;
     ec.half_diag = 0.5 * std::hypot(static_cast<double>(W - 1), static_cast<double>(H - 1));
     ec.log2_range = std::log2(64.0 / 0.5);
-    const int per = std::min(frames, max_batch);
+    int per = std::min(frames, max_batch);
+    // Host frames much larger than the prepared raster (e.g. 1080p -> 640x360)
+    // make the copy the long pole: at least four chunks per call, so each
+    // chunk's copy overlaps the previous chunk's kernels.
+    if (h_pix && double(w) * h * channels > 2.0 * double(W) * H) per = std::min(per, std::max(32, (frames + 3) / 4));
     // Chunk boundaries. With host frames the first chunk is 1/16 of a chunk,
     // so the only copy not hidden behind kernels is short (1/4 and 1/8
     // measured 2-3% slower end to end).
