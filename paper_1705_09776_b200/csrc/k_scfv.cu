@@ -259,6 +259,65 @@ __global__ void __launch_bounds__(256, 2) k_posterior(Batch bt, Model md) {
   }
 }
 
+// posteriors_matrix + softmax_rows for small mixtures (nc <= 32, e.g. the
+// 8-component bundles): the 64-component tiles of k_posterior would be mostly
+// padding. Thread (t, i) of a CTA forms logp of row t and component i with
+// exactly k_posterior's arithmetic (sums over j ascending, separately
+// rounded); the CTA's first warp then runs the row softmax (peak, exp, the
+// packet-order sum of eigen_sum, division) one row per lane.
+constexpr int kSmallRows = 32;
+__global__ void __launch_bounds__(1024) k_posterior_small(Batch bt, Model md) {
+  __shared__ double xs[kSmallRows][33];
+  __shared__ double lp[kSmallRows][33];
+  __shared__ double cst[32], lnorm[32];
+  const int f = blockIdx.y;
+  const int n = bt.or_count[f];
+  const int nc = md.nc;
+  const int row0 = blockIdx.x * kSmallRows;
+  if (row0 >= n) return;
+  const int rows = min(kSmallRows, n - row0);
+  const int tid = threadIdx.x;
+  const double* X = bt.x + ((long long)f * bt.cap_or + row0) * 32;
+  for (int q = tid; q < kSmallRows * 32; q += blockDim.x) {
+    const int t = q >> 5, j = q & 31;
+    xs[t][j] = t < rows ? X[t * 32 + j] : 0.0;
+  }
+  if (tid < nc) {
+    const double* m2 = md.m2_over_v + tid * 32;
+    double c = 1.0 * m2[0];
+    for (int j = 1; j < 32; ++j) c = c + 1.0 * m2[j];
+    cst[tid] = c;
+    lnorm[tid] = md.log_norm[tid];
+  }
+  __syncthreads();
+  {
+    const int t = tid / nc, i = tid - t * nc;
+    if (t < rows) {
+      const double* iv = md.inv_var + i * 32;
+      const double* mv = md.m_over_v + i * 32;
+      double a = (xs[t][0] * xs[t][0]) * iv[0];
+      double b = xs[t][0] * mv[0];
+      for (int j = 1; j < 32; ++j) {
+        const double x = xs[t][j];
+        a = a + (x * x) * iv[j];
+        b = b + x * mv[j];
+      }
+      const double p = a - 2.0 * b + cst[i];
+      lp[t][i] = -0.5 * p + lnorm[i];
+    }
+  }
+  __syncthreads();
+  if (tid < rows) {
+    double* e = lp[tid];
+    double pk = e[0];
+    for (int i = 1; i < nc; ++i) pk = fmax(pk, e[i]);
+    for (int i = 0; i < nc; ++i) e[i] = exp(e[i] - pk);
+    const double tot = packet_sum_seq(e, nc);
+    double* gam = bt.gamma + ((long long)f * bt.cap_or + row0 + tid) * nc;
+    for (int i = 0; i < nc; ++i) gam[i] = e[i] / tot;
+  }
+}
+
 // fv_mean_matrix / fv_var_matrix (scfv.cpp:166-203). gamma^T X (and
 // gamma^T X^2) as sums over the descriptor index t, ascending, one separately
 // rounded multiply and add per term. A CTA owns kFI components x all 32
@@ -536,7 +595,10 @@ cudaError_t launch_scfv_pack(const Batch& bt, const Model& md, const EncodeConst
     if (e != cudaSuccess) return e;
     post_configured = true;
   }
-  k_posterior<<<dim3((bt.cap_or + kPM - 1) / kPM, bt.nframes), 256, sizeof(PostSmem), st>>>(bt, md);
+  if (md.nc <= 32)
+    k_posterior_small<<<dim3((bt.cap_or + kSmallRows - 1) / kSmallRows, bt.nframes), kSmallRows * md.nc, 0, st>>>(bt, md);
+  else
+    k_posterior<<<dim3((bt.cap_or + kPM - 1) / kPM, bt.nframes), 256, sizeof(PostSmem), st>>>(bt, md);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   k_fisher<<<dim3((md.nc + kFI - 1) / kFI, bt.nframes), 256, 0, st>>>(bt, md, ec.variance);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
