@@ -11,6 +11,7 @@
 #include <cctype>
 #include <cmath>
 #include <cstring>
+#include <functional>
 #include <memory>
 #include <random>
 #include <stdexcept>
@@ -146,6 +147,7 @@ struct cdvz_gpu_ctx {
   cudaStream_t st = nullptr;
   cudaStream_t copy_st = nullptr;          // host->device frame copies (encode_batch)
   std::vector<cudaEvent_t> copy_ev;        // one per chunk of a call
+  std::vector<cudaEvent_t> out_ev;         // one per chunk: its containers are in host memory
   std::string err;
   Bundle bundle;
   DetConst dc{};
@@ -201,6 +203,7 @@ struct cdvz_gpu_ctx {
     for (auto& e : user_ev)
       if (e) cudaEventDestroy(e);
     for (auto& e : copy_ev) cudaEventDestroy(e);
+    for (auto& e : out_ev) cudaEventDestroy(e);
     if (copy_st) cudaStreamDestroy(copy_st);
     if (st) cudaStreamDestroy(st);
   }
@@ -443,7 +446,8 @@ struct cdvz_gpu_ctx {
   // grey plane is formed on the device first.
   void run(const uint8_t* d_pix, int w, int h, long long stride, int frames, int mode_id, int max_side, uint8_t* d_out,
            uint32_t* d_len, const uint8_t* h_pix = nullptr, size_t h_stride = 0, uint8_t* h_out = nullptr,
-           uint32_t* h_len = nullptr, int channels = 1) {
+           uint32_t* h_len = nullptr, int channels = 1,
+           const std::function<void(int, int)>& on_chunk = nullptr) {
     if (w < 8 || h < 8) throw DataError("image smaller than 8 px per side");
     int W, H;
     prepared_dims(w, h, max_side, W, H);
@@ -565,6 +569,12 @@ struct cdvz_gpu_ctx {
         CDVZ_CUDA_CHECK(cudaMemcpyAsync(h_out + size_t(base) * ec.slot_bytes, d_out + size_t(base) * ec.slot_bytes,
                                         size_t(nf) * ec.slot_bytes, cudaMemcpyDeviceToHost, sB));
         CDVZ_CUDA_CHECK(cudaMemcpyAsync(h_len + base, d_len + base, sizeof(uint32_t) * nf, cudaMemcpyDeviceToHost, sB));
+        while (int(out_ev.size()) <= c) {
+          cudaEvent_t e;
+          CDVZ_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+          out_ev.push_back(e);
+        }
+        CDVZ_CUDA_CHECK(cudaEventRecord(out_ev[size_t(c)], sB));
       }
       CDVZ_CUDA_CHECK(cudaEventRecord(L.done, sB));
       // The next chunk on this lane's stream A must not overwrite the pyramid
@@ -576,6 +586,13 @@ struct cdvz_gpu_ctx {
       L.pending_bytes = bytes;
       last_lane = serial ? 0 : (c % kLanes);
     }
+    // Host outputs: hand each chunk's containers to the caller in frame order
+    // as soon as they land, while later chunks are still on the device.
+    if (h_out && on_chunk)
+      for (int c = 0; c < chunks; ++c) {
+        CDVZ_CUDA_CHECK(cudaEventSynchronize(out_ev[size_t(c)]));
+        on_chunk(cb[size_t(c)], cb[size_t(c) + 1] - cb[size_t(c)]);
+      }
     for (int l = 0; l < kLanes; ++l)
       if (lanes[l].pending) CDVZ_CUDA_CHECK(cudaStreamWaitEvent(st, lanes[l].done, 0));
     for (int l = 0; l < kLanes; ++l) collect(lanes[l]);
@@ -766,28 +783,32 @@ int encode_host_batch(cdvz_gpu_ctx* ctx, const uint8_t* pixels, int width, int h
     int acc_launches = 0;
     for (int base = 0; base < count; base += group) {
       const int nf = std::min(group, count - base);
+      // Containers of frames [c0, c0 + cn) of this group are in pinned memory:
+      // copied out in frame order while later chunks still run.
+      auto copy_out = [&](int c0, int cn) {
+        for (int i = c0; i < c0 + cn; ++i) {
+          const size_t len = ctx->pin_len[size_t(i)];
+          const int fi = base + i;
+          if (len == 0) {
+            status[fi] = CDVZ_GPU_INTERNAL;
+          } else if (written + len > out_cap) {
+            status[fi] = CDVZ_GPU_USAGE;
+          } else {
+            std::memcpy(out + written, ctx->pin_out + size_t(i) * slot, len);
+            written += len;
+            status[fi] = CDVZ_GPU_OK;
+          }
+          offsets[fi + 1] = written;
+        }
+      };
       ctx->run(ctx->stage_in.as<uint8_t>(), width, height, (long long)width * channels, nf, mode_id, max_side,
                ctx->stage_out.as<uint8_t>(), ctx->stage_len.as<uint32_t>(), pixels + size_t(base) * height * stride, stride,
-               ctx->pin_out, ctx->pin_len, channels);
+               ctx->pin_out, ctx->pin_len, channels, copy_out);
       CDVZ_CUDA_CHECK(cudaStreamSynchronize(ctx->st));
       for (int i = 0; i < 5; ++i) acc_ms[i] += ctx->stage_ms[i];
       acc_pyr_ms += ctx->pyr_ms;
       acc_pyr_bytes += ctx->pyr_bytes;
       acc_launches += ctx->launches;
-      for (int i = 0; i < nf; ++i) {
-        const size_t len = ctx->pin_len[size_t(i)];
-        const int fi = base + i;
-        if (len == 0) {
-          status[fi] = CDVZ_GPU_INTERNAL;
-        } else if (written + len > out_cap) {
-          status[fi] = CDVZ_GPU_USAGE;
-        } else {
-          std::memcpy(out + written, ctx->pin_out + size_t(i) * slot, len);
-          written += len;
-          status[fi] = CDVZ_GPU_OK;
-        }
-        offsets[fi + 1] = written;
-      }
     }
     for (int i = 0; i < 5; ++i) ctx->stage_ms[i] = acc_ms[i];
     ctx->pyr_ms = acc_pyr_ms;
