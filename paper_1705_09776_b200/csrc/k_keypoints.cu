@@ -54,18 +54,21 @@ __device__ int block_exclusive_scan(int v, int* warp_tot, int& total) {
 }
 
 // Order-preserving compaction of `n` flags (keep != 0) into dst positions:
-// pos[i] = number of kept before i (contiguous chunk per thread).
+// pos[i] = number of kept before i. Elements go in rounds of blockDim.x
+// consecutive indices (thread t takes element round + t), so the emits of a
+// warp touch consecutive records.
 template <class Keep, class Emit>
 __device__ int compact(int n, Keep keep, Emit emit, int* warp_tot) {
-  const int per = (n + blockDim.x - 1) / blockDim.x;
-  const int lo = min(n, int(threadIdx.x) * per), hi = min(n, lo + per);
-  int cnt = 0;
-  for (int i = lo; i < hi; ++i) cnt += keep(i) ? 1 : 0;
-  int total = 0;
-  int pos = block_exclusive_scan(cnt, warp_tot, total);
-  for (int i = lo; i < hi; ++i)
-    if (keep(i)) emit(i, pos++);
-  return total;
+  int base = 0;
+  for (int r0 = 0; r0 < n; r0 += blockDim.x) {
+    const int i = r0 + threadIdx.x;
+    const bool k = i < n && keep(i);
+    int total = 0;
+    const int pos = block_exclusive_scan(k ? 1 : 0, warp_tot, total);
+    if (k) emit(i, base + pos);
+    base += total;
+  }
+  return base;
 }
 
 }  // namespace
