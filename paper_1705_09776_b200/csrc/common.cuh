@@ -67,6 +67,8 @@ struct Batch {
   int* raw_count;                      // [frame][octave]
   int* oct_count;                      // [frame][octave] survivors per octave (after ordering)
   uint32_t* bitmap;                    // [frame][bitmap_words]
+  int* bm_prefix;                      // [frame][bitmap_words] word prefix counts when they exceed shared memory
+  int merge_cell;                      // dedup grid cell side in px (8, doubled until the grid fits shared memory)
   long long bm_off[kMaxOctaves];       // word offset of each octave's bitmap in a frame
   long long bitmap_words;              // per frame
   int cap_acc;

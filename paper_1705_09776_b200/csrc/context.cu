@@ -29,6 +29,7 @@ namespace cdvz_gpu {
 cudaError_t launch_octave(const Batch& bt, const DetConst& dc, int o, int src, cudaStream_t st);
 cudaError_t launch_detect(const Batch& bt, const DetConst& dc, int o, const CUtensorMap* tmap, cudaStream_t st);
 cudaError_t launch_merge(const Batch& bt, int o, cudaStream_t st);
+int merge_cell_px(int W, int H);
 cudaError_t launch_select(const Batch& bt, const Model& md, const EncodeConst& ec, cudaStream_t st);
 cudaError_t launch_describe(const Batch& bt, const DetConst& dc, const Model& md, const EncodeConst& ec, cudaStream_t st);
 cudaError_t launch_scfv_pack(const Batch& bt, const Model& md, const EncodeConst& ec, uint8_t* out, uint32_t* lengths,
@@ -144,6 +145,7 @@ struct Lane {
 struct cdvz_gpu_ctx {
   int device = 0;
   int max_batch = 256;
+  size_t device_mem = 0;  // total device memory (queried once)
   cudaStream_t st = nullptr;
   cudaStream_t copy_st = nullptr;          // host->device frame copies (encode_batch)
   std::vector<cudaEvent_t> copy_ev;        // one per chunk of a call
@@ -331,6 +333,8 @@ struct cdvz_gpu_ctx {
     nb.raw_count = static_cast<int*>(alloc(sizeof(int) * F * std::max(1, n_oct)));
     nb.oct_count = static_cast<int*>(alloc(sizeof(int) * F * std::max(1, n_oct)));
     nb.bitmap = static_cast<uint32_t*>(alloc(sizeof(uint32_t) * F * nb.bitmap_words));
+    nb.bm_prefix = static_cast<int*>(alloc(sizeof(int) * F * nb.bitmap_words));
+    nb.merge_cell = merge_cell_px(W, H);
     nb.acc[0] = static_cast<KP*>(alloc(sizeof(KP) * F * nb.cap_acc));
     nb.acc[1] = static_cast<KP*>(alloc(sizeof(KP) * F * nb.cap_acc));
     nb.acc_count = static_cast<int*>(alloc(sizeof(int) * F * 2));
@@ -460,6 +464,20 @@ struct cdvz_gpu_ctx {
     ec.half_diag = 0.5 * std::hypot(static_cast<double>(W - 1), static_cast<double>(H - 1));
     ec.log2_range = std::log2(64.0 / 0.5);
     int per = std::min(frames, max_batch);
+    {
+      // Each lane holds its chunk's pyramid (4 levels x 4/3 of the prepared
+      // raster, f64), the f64 base planes and ~20 MB of keypoint/descriptor
+      // lists per frame: keep a lane under 35% of the device memory (a 4K
+      // frame needs ~370 MB; VGA ~33 MB).
+      if (!device_mem) {
+        size_t free_b = 0;
+        CDVZ_CUDA_CHECK(cudaMemGetInfo(&free_b, &device_mem));
+      }
+      const double px = double(W) * H;
+      const double per_frame = 8.0 * (4.0 * px * 4.0 / 3.0 + (resize || channels == 3 ? px : 0.0) +
+                                      (channels == 3 && resize ? double(w) * h : 0.0)) + 20e6;
+      per = std::min(per, std::max(1, int(0.35 * double(device_mem) / per_frame)));
+    }
     // Host frames much larger than the prepared raster (e.g. 1080p -> 640x360)
     // make the copy the long pole: at least four chunks per call, so each
     // chunk's copy overlaps the previous chunk's kernels.

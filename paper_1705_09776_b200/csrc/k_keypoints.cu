@@ -22,6 +22,7 @@ namespace cdvz_gpu {
 namespace {
 
 constexpr int kMergeThreads = 1024;
+constexpr size_t kMergeSmemBudget = 200 * 1024;  // dynamic shared memory of k_merge_octave
 
 // Block-wide exclusive scan over one int per thread (1024 threads).
 __device__ int block_exclusive_scan(int v, int* warp_tot, int& total) {
@@ -89,7 +90,8 @@ __global__ void __launch_bounds__(kMergeThreads) k_merge_octave(Batch bt, int o)
   // Warp w owns a contiguous segment of words and reads it coalesced: pass 1
   // counts the segment, a block scan places the segments, pass 2 re-reads
   // each 32-word chunk and scans it across the lanes.
-  int* prefix = sm;  // nwords
+  // In shared memory when it fits (merge_smem_bytes), else in global scratch.
+  int* prefix = (size_t(nwords) * sizeof(int) <= kMergeSmemBudget) ? sm : bt.bm_prefix + f * bt.bitmap_words + bt.bm_off[o];
   {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int seg = (nwords + nw - 1) / nw;
@@ -141,14 +143,16 @@ __global__ void __launch_bounds__(kMergeThreads) k_merge_octave(Batch bt, int o)
   const int np = bt.acc_count[f * 2 + src];
   const KP* cur = out_sorted;
   const int nc = n;
-  const int gw = bt.W / 8 + 3, gh = bt.H / 8 + 3;
+  const int cell_px = bt.merge_cell;
+  const double inv_cell = 1.0 / cell_px;
+  const int gw = bt.W / cell_px + 3, gh = bt.H / cell_px + 3;
   int* cell_start = sm;                  // gw*gh + 1 (reuses the prefix space)
   int* cell_fill = sm + gw * gh + 1;     // gw*gh
   uint8_t* drop_prev = bt.flags + (long long)f * 2 * bt.cap_acc;
   uint8_t* drop_cur = drop_prev + bt.cap_acc;
   int* sorted_idx = bt.scratch_idx + (long long)f * bt.cap_acc;
   auto cell_of = [&](double x, double y) {
-    int cxi = int(floor(x * 0.125)) + 1, cyi = int(floor(y * 0.125)) + 1;
+    int cxi = int(floor(x * inv_cell)) + 1, cyi = int(floor(y * inv_cell)) + 1;
     cxi = max(0, min(gw - 1, cxi));
     cyi = max(0, min(gh - 1, cyi));
     return cyi * gw + cxi;
@@ -226,13 +230,22 @@ __global__ void __launch_bounds__(kMergeThreads) k_merge_octave(Batch bt, int o)
   }
 }
 
+// Dedup grid cell side: 8 px, doubled until the two per-cell int arrays fit
+// the shared-memory budget (any side >= 2 keeps every pair with |dx|, |dy| < 2
+// inside the 3x3 neighbourhood of cells).
+int merge_cell_px(int W, int H) {
+  int c = 8;
+  while (sizeof(int) * (2 * size_t(W / c + 3) * size_t(H / c + 3) + 1) > kMergeSmemBudget) c *= 2;
+  return c;
+}
+
 size_t merge_smem_bytes(const Batch& bt) {
   size_t need = 0;
   for (int o = 0; o < bt.n_oct; ++o) {
     const size_t words = (size_t(2) * bt.ow[o] * bt.oh[o] + 31) / 32;
-    need = need > words ? need : words;
+    if (words * sizeof(int) <= kMergeSmemBudget) need = need > words ? need : words;  // else global prefix
   }
-  const size_t cells = size_t(bt.W / 8 + 3) * (bt.H / 8 + 3);
+  const size_t cells = size_t(bt.W / bt.merge_cell + 3) * (bt.H / bt.merge_cell + 3);
   const size_t grid = 2 * cells + 1;
   return sizeof(int) * (need > grid ? need : grid);
 }
