@@ -314,8 +314,10 @@ struct cdvz_gpu_ctx {
     nb.n_oct = n_oct;
     nb.frame_doubles = std::max<long long>(pd, 1);
     nb.bitmap_words = std::max<long long>(bw, 1);
-    nb.cap_oct = 32768;
-    nb.cap_acc = 32768;
+    // Survivor capacities per frame: a synthetic 1080p octave keeps ~1% of its
+    // pixels (21k); 1/16 of the prepared raster leaves 6x headroom.
+    nb.cap_oct = std::max(32768, int(std::min<long long>(1LL << 26, (long long)W * H / 16)));
+    nb.cap_acc = nb.cap_oct;
     nb.select_n = bundle.select_n;
     nb.cap_or = std::max(64, bundle.select_n * 4);
     nb.code_stride = 40;
@@ -466,16 +468,19 @@ struct cdvz_gpu_ctx {
     int per = std::min(frames, max_batch);
     {
       // Each lane holds its chunk's pyramid (4 levels x 4/3 of the prepared
-      // raster, f64), the f64 base planes and ~20 MB of keypoint/descriptor
-      // lists per frame: keep a lane under 35% of the device memory (a 4K
-      // frame needs ~370 MB; VGA ~33 MB).
+      // raster, f64), the f64 base planes, the survivor lists (raw per octave,
+      // accumulated x2, current) and ~8 MB of descriptor buffers per frame:
+      // keep a lane under 35% of the device memory (VGA ~30 MB per frame, a
+      // 4K frame ~600 MB).
       if (!device_mem) {
         size_t free_b = 0;
         CDVZ_CUDA_CHECK(cudaMemGetInfo(&free_b, &device_mem));
       }
       const double px = double(W) * H;
+      const double cap = std::max(32768.0, px / 16.0);  // survivor capacity (plan())
       const double per_frame = 8.0 * (4.0 * px * 4.0 / 3.0 + (resize || channels == 3 ? px : 0.0) +
-                                      (channels == 3 && resize ? double(w) * h : 0.0)) + 20e6;
+                                      (channels == 3 && resize ? double(w) * h : 0.0)) +
+                               cap * (64.0 * 7.0 + 14.0) + 8e6;
       per = std::min(per, std::max(1, int(0.35 * double(device_mem) / per_frame)));
     }
     // Host frames much larger than the prepared raster (e.g. 1080p -> 640x360)
