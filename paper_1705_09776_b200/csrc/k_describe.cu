@@ -692,7 +692,7 @@ cudaError_t launch_describe(const Batch& bt, const DetConst& dc, const Model& md
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  k_describe<<<dim3(24, bt.nframes), 32 * kPBWarps, smem, st>>>(bt, dc, md, ec);
+  k_describe<<<dim3((bt.cap_or + kPBPts * kPBWarps - 1) / (kPBPts * kPBWarps), bt.nframes), 32 * kPBWarps, smem, st>>>(bt, dc, md, ec);
   return cudaGetLastError();
 }
 
