@@ -682,7 +682,7 @@ cudaError_t launch_describe(const Batch& bt, const DetConst& dc, const Model& md
   k_geometry<<<dim3((bt.cap_or + 127) / 128, bt.nframes), 128, 0, st>>>(bt, dc);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  k_sample<<<dim3(128, bt.nframes), kSampleThreads, 0, st>>>(bt);
+  k_sample<<<dim3(256, bt.nframes), kSampleThreads, 0, st>>>(bt);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   static bool configured = false;
