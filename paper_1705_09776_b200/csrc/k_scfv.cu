@@ -52,8 +52,10 @@ __device__ __forceinline__ double packet_sum_seq(const double* v, int n) {
 // The basis is staged transposed in shared memory; each thread carries four
 // descriptor rows so four independent sums hide the FP64 add latency.
 __global__ void __launch_bounds__(128) k_pca(Batch bt, Model md) {
-  __shared__ double bT[128][32];   // basis transposed (lanes read consecutive r)
-  __shared__ double cen[16][128];  // 16 centred rows (broadcast reads)
+  extern __shared__ __align__(16) double pca_sm[];
+  double(*bT)[33] = reinterpret_cast<double(*)[33]>(pca_sm);              // [128][33] basis transposed (lanes read
+                                                                           // consecutive r); padded: conflict-free transpose
+  double(*cen)[128] = reinterpret_cast<double(*)[128]>(pca_sm + 128 * 33);  // [16][128] centred rows (broadcast reads)
   const int f = blockIdx.y;
   const int n = bt.or_count[f];
   const int tid = threadIdx.x, r = tid & 31, grp = tid >> 5;
@@ -586,7 +588,14 @@ cudaError_t launch_scfv_pack(const Batch& bt, const Model& md, const EncodeConst
                              cudaStream_t st, cudaEvent_t after_aggregation) {
   cudaError_t e = init_crc_zeros();
   if (e != cudaSuccess) return e;
-  k_pca<<<dim3(8, bt.nframes), 128, 0, st>>>(bt, md);
+  constexpr int pca_smem = int(sizeof(double)) * (128 * 33 + 16 * 128);
+  static bool pca_configured = false;
+  if (!pca_configured) {
+    e = cudaFuncSetAttribute(k_pca, cudaFuncAttributeMaxDynamicSharedMemorySize, pca_smem);
+    if (e != cudaSuccess) return e;
+    pca_configured = true;
+  }
+  k_pca<<<dim3(16, bt.nframes), 128, pca_smem, st>>>(bt, md);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   static bool post_configured = false;
