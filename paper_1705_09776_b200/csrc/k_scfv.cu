@@ -94,6 +94,7 @@ __global__ void __launch_bounds__(128) k_pca(Batch bt, Model md) {
 // buffer while tracking the row maxima. Phase 2 exponentiates, sums each row
 // in Eigen's SSE2 packet order (four stride-4 chains) and normalises.
 constexpr int kPM = 64, kPN = 64;
+constexpr int kSoftmaxRowMax = 1024;  // fused per-row softmax: 8 warps x 1024 doubles of the operand tiles
 struct PostSmem {
   double xs2[32][kPM];  // x^2, transposed
   double xs[32][kPM];   // x, transposed
@@ -104,6 +105,9 @@ struct PostSmem {
   double rmax[16][kPM];
   double chain[kPM][4];
 };
+
+static_assert(sizeof(double) * (4 * 32 * kPM) >= sizeof(double) * 8 * kSoftmaxRowMax && kPM == kPN,
+              "the operand tiles xs2..mv hold the 8 warps' softmax rows");
 
 __global__ void __launch_bounds__(256, 2) k_posterior(Batch bt, Model md) {
   extern __shared__ __align__(16) uint8_t post_smem[];
@@ -209,8 +213,48 @@ __global__ void __launch_bounds__(256, 2) k_posterior(Batch bt, Model md) {
     S.rmax[0][tid] = pk;
   }
   __syncthreads();
-  // softmax_rows: e = exp(logp - peak) ...
   const int wi = tid >> 5, lane = tid & 31;
+  if (nc <= kSoftmaxRowMax) {
+    // softmax_rows fused per row: a warp stages its row's e = exp(logp - peak)
+    // in shared memory (the phase-1 operand tiles are free now), four lanes
+    // sum it in Eigen's packet order (four stride-4 chains, then
+    // (c0 + c2) + (c1 + c3), the odd pair and the tail), and the warp writes
+    // gamma = e / sum: one read and one write of each gamma row.
+    double* buf = reinterpret_cast<double*>(&S.xs2[0][0]) + wi * kSoftmaxRowMax;
+    for (int t = wi; t < rows; t += 8) {
+      const double pk = S.rmax[0][t];
+      double* g = gam + t * nc;
+      for (int i = lane; i < nc; i += 32) buf[i] = exp(g[i] - pk);
+      __syncwarp();
+      double total = 0.0;
+      if (nc < 4) {
+        if (lane == 0) total = packet_sum_seq(buf, nc);
+      } else {
+        const int e2 = nc / 4 * 4, e1 = nc / 2 * 2;
+        double c = 0.0;
+        if (lane < 4) {
+          c = buf[lane];
+          for (int i = lane + 4; i < e2; i += 4) c = c + buf[i];
+        }
+        const double c0 = __shfl_sync(0xffffffffu, c, 0), c1 = __shfl_sync(0xffffffffu, c, 1);
+        const double c2 = __shfl_sync(0xffffffffu, c, 2), c3 = __shfl_sync(0xffffffffu, c, 3);
+        if (lane == 0) {
+          double a0 = c0 + c2, a1 = c1 + c3;
+          if (e1 > e2) {
+            a0 += buf[e2];
+            a1 += buf[e2 + 1];
+          }
+          total = a0 + a1;
+          for (int i = e1; i < nc; ++i) total += buf[i];
+        }
+      }
+      total = __shfl_sync(0xffffffffu, total, 0);
+      for (int i = lane; i < nc; i += 32) g[i] = buf[i] / total;
+      __syncwarp();
+    }
+    return;
+  }
+  // softmax_rows: e = exp(logp - peak) ...
   for (int t = wi; t < rows; t += 8) {
     const double pk = S.rmax[0][t];
     for (int i = lane; i < nc; i += 32) gam[t * nc + i] = exp(gam[t * nc + i] - pk);
