@@ -121,6 +121,10 @@ struct Model {
   const double* inv_var;    // nc x 32  1/(s*s)
   const double* m_over_v;   // nc x 32  m/(s*s)
   const double* m2_over_v;  // nc x 32  (m*m)/(s*s)
+  const double* inv_var_t;  // 32 x ncp  transposed, rows padded to ncp = nc rounded up to 64 (zeros)
+  const double* m_over_v_t; // 32 x ncp
+  const double* cst;        // ncp      sum_j 1.0 * m2_over_v[i][j], j ascending (0 past nc)
+  int ncp;
   const double* log_norm;   // nc       log w - sum log s - 16 log 2pi
   const double* means;      // nc x 32
   const double* stds;       // nc x 32

@@ -278,6 +278,22 @@ struct cdvz_gpu_ctx {
     md.inv_var = upload(iv.data(), iv.size());
     md.m_over_v = upload(mv.data(), mv.size());
     md.m2_over_v = upload(m2.data(), m2.size());
+    // Transposed copies for k_posterior's cp.async tile loads, and the
+    // ones * (M^2/V)^T column (sum_j 1.0 * m2, j ascending, separately rounded).
+    md.ncp = (b.nc + 63) / 64 * 64;
+    std::vector<double> ivt(std::size_t(md.ncp) * 32, 0.0), mvt(ivt.size(), 0.0), cst(std::size_t(md.ncp), 0.0);
+    for (int i = 0; i < b.nc; ++i) {
+      double c = 1.0 * m2[std::size_t(i) * 32];
+      for (int j = 1; j < 32; ++j) c = c + 1.0 * m2[std::size_t(i) * 32 + j];
+      cst[std::size_t(i)] = c;
+      for (int j = 0; j < 32; ++j) {
+        ivt[std::size_t(j) * md.ncp + i] = iv[std::size_t(i) * 32 + j];
+        mvt[std::size_t(j) * md.ncp + i] = mv[std::size_t(i) * 32 + j];
+      }
+    }
+    md.inv_var_t = upload(ivt.data(), ivt.size());
+    md.m_over_v_t = upload(mvt.data(), mvt.size());
+    md.cst = upload(cst.data(), cst.size());
     md.log_norm = upload(ln.data(), ln.size());
     md.means = upload(b.means.data(), b.means.size());
     md.stds = upload(b.stds.data(), b.stds.size());

@@ -93,6 +93,11 @@ __global__ void __launch_bounds__(128) k_pca(Batch bt, Model md) {
 // not used), then forms log p = -0.5 (a - 2b + c) + log_norm into the gamma
 // buffer while tracking the row maxima. Phase 2 exponentiates, sums each row
 // in Eigen's SSE2 packet order (four stride-4 chains) and normalises.
+__device__ __forceinline__ void cp_async16_post(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(uint32_t(__cvta_generic_to_shared(smem))), "l"(gmem)
+               : "memory");
+}
+
 constexpr int kPM = 64, kPN = 64;
 constexpr int kSoftmaxRowMax = 1024;  // fused per-row softmax: 8 warps x 1024 doubles of the operand tiles
 struct PostSmem {
@@ -100,6 +105,8 @@ struct PostSmem {
   double xs[32][kPM];   // x, transposed
   double iv[32][kPN];   // 1 / v, transposed
   double mv[32][kPN];   // m / v, transposed
+  double iv2[32][kPN];  // the next component tile (cp.async double buffer)
+  double mv2[32][kPN];
   double cst[kPN];      // sum_j 1.0 * m^2 / v (the ones * (M^2/V)^T product)
   double lnorm[kPN];
   double rmax[16][kPM];
@@ -128,37 +135,44 @@ __global__ void __launch_bounds__(256, 2) k_posterior(Batch bt, Model md) {
     S.xs2[j][t] = v * v;
   }
   double rm[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-  for (int c0 = 0; c0 < nc; c0 += kPN) {
-    __syncthreads();
-    for (int q = tid; q < kPN * 32; q += 256) {
-      const int i = q >> 5, j = q & 31;
-      const bool ok = c0 + i < nc;
-      S.iv[j][i] = ok ? md.inv_var[(c0 + i) * 32 + j] : 0.0;
-      S.mv[j][i] = ok ? md.m_over_v[(c0 + i) * 32 + j] : 0.0;
+  // Component tiles stream through a double buffer with cp.async from the
+  // transposed (and zero-padded) tables: tile k + 1 loads while tile k is
+  // multiplied.
+  auto load_tile = [&](int c0, double (*iv)[kPN], double (*mv)[kPN]) {
+    for (int q = tid; q < 32 * (kPN / 2); q += 256) {  // 16-byte chunks: (j, column pair)
+      const int j = q / (kPN / 2), c = 2 * (q % (kPN / 2));
+      cp_async16_post(&iv[j][c], md.inv_var_t + (long long)j * md.ncp + c0 + c);
+      cp_async16_post(&mv[j][c], md.m_over_v_t + (long long)j * md.ncp + c0 + c);
     }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  load_tile(0, S.iv, S.mv);
+  int buf = 0;
+  for (int c0 = 0; c0 < nc; c0 += kPN) {
+    __syncthreads();  // everyone is done with the tile buffer loaded next
+    const bool more = c0 + kPN < nc;
+    if (more) load_tile(c0 + kPN, buf ? S.iv : S.iv2, buf ? S.mv : S.mv2);
+    if (more) asm volatile("cp.async.wait_group 1;" ::: "memory");
+    else asm volatile("cp.async.wait_group 0;" ::: "memory");
     if (tid < kPN) {
       const int i = c0 + tid;
-      double c = 0.0, ln = 0.0;
-      if (i < nc) {
-        const double* m2 = md.m2_over_v + i * 32;
-        c = 1.0 * m2[0];
-        for (int j = 1; j < 32; ++j) c = c + 1.0 * m2[j];
-        ln = md.log_norm[i];
-      }
-      S.cst[tid] = c;
-      S.lnorm[tid] = ln;
+      S.cst[tid] = md.cst[i];
+      S.lnorm[tid] = i < nc ? md.log_norm[i] : 0.0;
     }
     __syncthreads();
+    const double(*TIV)[kPN] = buf ? S.iv2 : S.iv;
+    const double(*TMV)[kPN] = buf ? S.mv2 : S.mv;
+    buf ^= 1;
     double a[4][4], b[4][4];
     {
       const double2 xa = *reinterpret_cast<const double2*>(&S.xs2[0][ty * 4]);
       const double2 xb = *reinterpret_cast<const double2*>(&S.xs2[0][ty * 4 + 2]);
       const double2 ya = *reinterpret_cast<const double2*>(&S.xs[0][ty * 4]);
       const double2 yb = *reinterpret_cast<const double2*>(&S.xs[0][ty * 4 + 2]);
-      const double2 ia = *reinterpret_cast<const double2*>(&S.iv[0][tx * 4]);
-      const double2 ib = *reinterpret_cast<const double2*>(&S.iv[0][tx * 4 + 2]);
-      const double2 ma = *reinterpret_cast<const double2*>(&S.mv[0][tx * 4]);
-      const double2 mb = *reinterpret_cast<const double2*>(&S.mv[0][tx * 4 + 2]);
+      const double2 ia = *reinterpret_cast<const double2*>(&TIV[0][tx * 4]);
+      const double2 ib = *reinterpret_cast<const double2*>(&TIV[0][tx * 4 + 2]);
+      const double2 ma = *reinterpret_cast<const double2*>(&TMV[0][tx * 4]);
+      const double2 mb = *reinterpret_cast<const double2*>(&TMV[0][tx * 4 + 2]);
       const double x2[4] = {xa.x, xa.y, xb.x, xb.y}, x1[4] = {ya.x, ya.y, yb.x, yb.y};
       const double iv[4] = {ia.x, ia.y, ib.x, ib.y}, mv[4] = {ma.x, ma.y, mb.x, mb.y};
 #pragma unroll
@@ -175,10 +189,10 @@ __global__ void __launch_bounds__(256, 2) k_posterior(Batch bt, Model md) {
       const double2 xb = *reinterpret_cast<const double2*>(&S.xs2[j][ty * 4 + 2]);
       const double2 ya = *reinterpret_cast<const double2*>(&S.xs[j][ty * 4]);
       const double2 yb = *reinterpret_cast<const double2*>(&S.xs[j][ty * 4 + 2]);
-      const double2 ia = *reinterpret_cast<const double2*>(&S.iv[j][tx * 4]);
-      const double2 ib = *reinterpret_cast<const double2*>(&S.iv[j][tx * 4 + 2]);
-      const double2 ma = *reinterpret_cast<const double2*>(&S.mv[j][tx * 4]);
-      const double2 mb = *reinterpret_cast<const double2*>(&S.mv[j][tx * 4 + 2]);
+      const double2 ia = *reinterpret_cast<const double2*>(&TIV[j][tx * 4]);
+      const double2 ib = *reinterpret_cast<const double2*>(&TIV[j][tx * 4 + 2]);
+      const double2 ma = *reinterpret_cast<const double2*>(&TMV[j][tx * 4]);
+      const double2 mb = *reinterpret_cast<const double2*>(&TMV[j][tx * 4 + 2]);
       const double x2[4] = {xa.x, xa.y, xb.x, xb.y}, x1[4] = {ya.x, ya.y, yb.x, yb.y};
       const double iv[4] = {ia.x, ia.y, ib.x, ib.y}, mv[4] = {ma.x, ma.y, mb.x, mb.y};
 #pragma unroll
