@@ -343,16 +343,32 @@ __global__ void __launch_bounds__(kMergeThreads) k_select(Batch bt, Model md, En
           atomicAdd(&hist[(kk.k[word] >> shift) & 0xFF], 1);
         }
       __syncthreads();
-      if (threadIdx.x == 0) {
-        int run = 0, d = 0;
-        const int rem = s_remaining;
-        for (d = 0; d < 256; ++d) {
-          if (run + hist[d] >= rem) break;
-          run += hist[d];
+      if (threadIdx.x < 32) {
+        // First digit whose inclusive count reaches the remaining quota: lane l
+        // owns bins 8l .. 8l + 7; a warp scan of the lane sums finds the lane,
+        // which then walks its eight bins (the sequential scan's answer).
+        const int l = threadIdx.x, rem = s_remaining;
+        int own = 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) own += hist[8 * l + q];
+        int incl = own;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          const int v = __shfl_up_sync(0xffffffffu, incl, d);
+          if (l >= d) incl += v;
         }
-        s_digit = d;
-        s_remaining = rem - run;
-        if (hist[d] == rem - run) s_done = 2;  // the whole bucket fits exactly
+        const unsigned hit = __ballot_sync(0xffffffffu, incl >= rem);
+        const int first = __ffs(hit) - 1;  // rem <= alive count, so some lane reaches it
+        if (l == first) {
+          int run = incl - own, d = 8 * l;
+          for (; d < 8 * l + 7; ++d) {
+            if (run + hist[d] >= rem) break;
+            run += hist[d];
+          }
+          s_digit = d;
+          s_remaining = rem - run;
+          if (hist[d] == rem - run) s_done = 2;  // the whole bucket fits exactly
+        }
       }
       __syncthreads();
       const int dsel = s_digit;
