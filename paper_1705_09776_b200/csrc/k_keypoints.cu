@@ -337,11 +337,13 @@ __global__ void __launch_bounds__(kMergeThreads) k_select(Batch bt, Model md, En
       const int word = digit >> 3, shift = 56 - 8 * (digit & 7);
       for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
       __syncthreads();
+      // Word 0 (the score) needs no keypoint record.
+      auto key_word = [&](int i) {
+        return word == 0 ? ~static_cast<unsigned long long>(__double_as_longlong(score[i]))
+                         : sel_key(score[i], acc[i], i).k[word];
+      };
       for (int i = threadIdx.x; i < n; i += blockDim.x)
-        if (state[i] == 0) {
-          const SelKey kk = sel_key(score[i], acc[i], i);
-          atomicAdd(&hist[(kk.k[word] >> shift) & 0xFF], 1);
-        }
+        if (state[i] == 0) atomicAdd(&hist[(key_word(i) >> shift) & 0xFF], 1);
       __syncthreads();
       if (threadIdx.x < 32) {
         // First digit whose inclusive count reaches the remaining quota: lane l
@@ -375,8 +377,7 @@ __global__ void __launch_bounds__(kMergeThreads) k_select(Batch bt, Model md, En
       const bool take_bucket = s_done == 2;
       for (int i = threadIdx.x; i < n; i += blockDim.x)
         if (state[i] == 0) {
-          const SelKey kk = sel_key(score[i], acc[i], i);
-          const int dv = int((kk.k[word] >> shift) & 0xFF);
+          const int dv = int((key_word(i) >> shift) & 0xFF);
           if (dv < dsel || (dv == dsel && take_bucket)) state[i] = 1;
           else if (dv > dsel) state[i] = 2;
         }
