@@ -15,6 +15,8 @@
 // the reference's total order (score desc, |p| desc, y, x, index;
 // relevance.cpp:71-93) with an exact MSB-first radix select on the 5-field
 // key, then a bitonic sort of the winners.
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace cdvz_gpu {
@@ -239,21 +241,24 @@ int merge_cell_px(int W, int H) {
   return c;
 }
 
-size_t merge_smem_bytes(const Batch& bt) {
-  size_t need = 0;
-  for (int o = 0; o < bt.n_oct; ++o) {
-    const size_t words = (size_t(2) * bt.ow[o] * bt.oh[o] + 31) / 32;
-    if (words * sizeof(int) <= kMergeSmemBudget) need = need > words ? need : words;  // else global prefix
-  }
+// Dynamic shared memory of octave o's merge: its bitmap prefix (when it fits)
+// and, above octave 0, the dedup grid that reuses the same space.
+size_t merge_smem_bytes(const Batch& bt, int o) {
+  const size_t words = (size_t(2) * bt.ow[o] * bt.oh[o] + 31) / 32;
+  const size_t need = words * sizeof(int) <= kMergeSmemBudget ? words : 0;  // else global prefix
   const size_t cells = size_t(bt.W / bt.merge_cell + 3) * (bt.H / bt.merge_cell + 3);
-  const size_t grid = 2 * cells + 1;
-  return sizeof(int) * (need > grid ? need : grid);
+  const size_t grid = o > 0 ? 2 * cells + 1 : 0;
+  return sizeof(int) * std::max<size_t>(1, need > grid ? need : grid);
 }
 
 cudaError_t launch_merge(const Batch& bt, int o, cudaStream_t st) {
-  const size_t smem = merge_smem_bytes(bt);
-  cudaError_t e = cudaFuncSetAttribute(k_merge_octave, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  if (e != cudaSuccess) return e;
+  const size_t smem = merge_smem_bytes(bt, o);
+  static size_t configured = 0;
+  if (smem > configured) {
+    cudaError_t e = cudaFuncSetAttribute(k_merge_octave, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    configured = smem;
+  }
   k_merge_octave<<<bt.nframes, kMergeThreads, smem, st>>>(bt, o);
   return cudaGetLastError();
 }
