@@ -209,19 +209,28 @@ __global__ void __launch_bounds__(kMergeThreads) k_merge_octave(Batch bt, int o)
     drop_cur[i] = dc ? 1 : 0;
   }
   __syncthreads();
+  // Survivors: previous first, then current, each in order. The positions
+  // are scanned first (source index per output slot, in the now free
+  // sorted_idx scratch), then the 64-byte records move in 16-byte pieces by
+  // consecutive threads with no barrier in between.
   KP* out = bt.acc[dst] + (long long)f * bt.cap_acc;
+  const int cap = bt.cap_acc;
+  int* src_of = sorted_idx;
+  auto move = [&](const KP* from, int count, int at) {
+    const uint4* s4 = reinterpret_cast<const uint4*>(from);
+    uint4* d4 = reinterpret_cast<uint4*>(out + at);
+    const int m = min(count, cap - at);
+    for (int c = threadIdx.x; c < 4 * m; c += blockDim.x) d4[c] = s4[4 * src_of[c >> 2] + (c & 3)];
+  };
   const int kept_prev = compact(
-      np, [&](int i) { return drop_prev[i] == 0; }, [&](int i, int pos) { out[pos] = prev[i]; }, warp_tot);
-  int kept_cur = 0;
-  {
-    const int cap = bt.cap_acc;
-    kept_cur = compact(
-        nc, [&](int i) { return drop_cur[i] == 0; },
-        [&](int i, int pos) {
-          if (kept_prev + pos < cap) out[kept_prev + pos] = cur[i];
-        },
-        warp_tot);
-  }
+      np, [&](int i) { return drop_prev[i] == 0; }, [&](int i, int pos) { src_of[pos] = i; }, warp_tot);
+  __syncthreads();
+  move(prev, kept_prev, 0);
+  __syncthreads();
+  const int kept_cur = compact(
+      nc, [&](int i) { return drop_cur[i] == 0; }, [&](int i, int pos) { src_of[pos] = i; }, warp_tot);
+  __syncthreads();
+  if (kept_prev < cap) move(cur, kept_cur, kept_prev);
   if (threadIdx.x == 0) {
     int total = kept_prev + kept_cur;
     if (total > bt.cap_acc) {
