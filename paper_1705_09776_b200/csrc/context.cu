@@ -145,6 +145,7 @@ struct Lane {
 struct cdvz_gpu_ctx {
   int device = 0;
   int max_batch = 256;
+  int next_lane = 0;      // lane of the next call's first chunk
   size_t device_mem = 0;  // total device memory (queried once)
   cudaStream_t st = nullptr;
   cudaStream_t copy_st = nullptr;          // host->device frame copies (encode_batch)
@@ -507,13 +508,17 @@ struct cdvz_gpu_ctx {
     // so the only copy not hidden behind kernels is short (1/4 and 1/8
     // measured 2-3% slower end to end).
     std::vector<int> cb{0};
-    if (h_pix && frames > per) cb.push_back(std::max(1, per / 16));
+    if (h_pix && frames >= 32) cb.push_back(std::max(1, per / 16));
     while (cb.back() < frames) cb.push_back(std::min(frames, cb.back() + per));
     const int chunks = int(cb.size()) - 1;
     const int n_lanes = serial ? 1 : kLanes;
+    // Lanes rotate across calls too, so back-to-back asynchronous calls
+    // (encode_device) overlap one call's tail with the next call's head.
+    const int lane0 = serial ? 0 : next_lane;
     for (int l = 0; l < std::min(chunks, n_lanes); ++l) {
-      if (!lanes[l].sA) lanes[l].init();
-      plan(lanes[l], W, H, per, f64_base, rgb && resize ? (long long)w * h : 0);
+      Lane& L = lanes[(lane0 + l) % kLanes];
+      if (!L.sA) L.init();
+      plan(L, W, H, per, f64_base, rgb && resize ? (long long)w * h : 0);
     }
     launches = 0;
     pyr_ms = 0.0;
@@ -542,7 +547,7 @@ struct cdvz_gpu_ctx {
     for (int c = 0; c < chunks; ++c) {
       const int base = cb[size_t(c)];
       const int nf = cb[size_t(c) + 1] - base;
-      Lane& L = lanes[serial ? 0 : (c % kLanes)];
+      Lane& L = lanes[serial ? 0 : (lane0 + c) % kLanes];
       collect(L);
       // Serial mode (debug bit 2): one stream per lane, so kernels never
       // overlap and their event times are standalone (bench roofline).
@@ -623,8 +628,9 @@ struct cdvz_gpu_ctx {
       L.pending = true;
       L.pending_oct = b.n_oct;
       L.pending_bytes = bytes;
-      last_lane = serial ? 0 : (c % kLanes);
+      last_lane = serial ? 0 : (lane0 + c) % kLanes;
     }
+    if (!serial) next_lane = (lane0 + chunks) % kLanes;
     // Host outputs: hand each chunk's containers to the caller in frame order
     // as soon as they land, while later chunks are still on the device.
     if (h_out && on_chunk)
