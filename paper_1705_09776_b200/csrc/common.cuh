@@ -6,7 +6,9 @@
 // with the oracle follows wherever no libm call intervenes.
 #pragma once
 
+#include <cstddef>
 #include <cstdint>
+#include <mutex>
 #include <cuda_runtime.h>
 
 namespace cdvz_gpu {
@@ -151,6 +153,27 @@ __host__ __device__ inline int mirror_index(int i, int n) {
   int m = i % period;
   if (m < 0) m += period;
   return m < n ? m : period - 1 - m;
+}
+
+// Host-side setup that must happen once per device (kernel attributes,
+// __constant__ tables): runs `f` unless the current device has already been
+// set up with a value >= v (e.g. a dynamic shared-memory size). Thread-safe.
+constexpr int kMaxDevices = 64;
+inline std::mutex& device_setup_mutex() {
+  static std::mutex m;
+  return m;
+}
+template <class F>
+cudaError_t once_per_device(size_t (&seen)[kMaxDevices], size_t v, F&& f) {
+  int d = 0;
+  cudaError_t e = cudaGetDevice(&d);
+  if (e != cudaSuccess) return e;
+  if (d < 0 || d >= kMaxDevices) return f();
+  std::lock_guard<std::mutex> g(device_setup_mutex());
+  if (seen[d] >= v) return cudaSuccess;
+  e = f();
+  if (e == cudaSuccess) seen[d] = v;
+  return e;
 }
 
 #define CDVZ_CUDA_CHECK(expr)                                                              \

@@ -685,13 +685,10 @@ cudaError_t launch_describe(const Batch& bt, const DetConst& dc, const Model& md
   k_sample<<<dim3(256, bt.nframes), kSampleThreads, 0, st>>>(bt);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  static bool configured = false;
+  static size_t configured[kMaxDevices] = {};
   constexpr int smem = int(sizeof(PhaseBSmem)) * kPBWarps;
-  if (!configured) {
-    e = cudaFuncSetAttribute(k_describe, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  e = once_per_device(configured, 1, [&] { return cudaFuncSetAttribute(k_describe, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); });
+  if (e != cudaSuccess) return e;
   k_describe<<<dim3((bt.cap_or + kPBPts * kPBWarps - 1) / (kPBPts * kPBWarps), bt.nframes), 32 * kPBWarps, smem, st>>>(bt, dc, md, ec);
   return cudaGetLastError();
 }

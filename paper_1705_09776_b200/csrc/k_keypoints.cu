@@ -262,12 +262,11 @@ size_t merge_smem_bytes(const Batch& bt, int o) {
 
 cudaError_t launch_merge(const Batch& bt, int o, cudaStream_t st) {
   const size_t smem = merge_smem_bytes(bt, o);
-  static size_t configured = 0;
-  if (smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(k_merge_octave, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    if (e != cudaSuccess) return e;
-    configured = smem;
-  }
+  static size_t configured[kMaxDevices] = {};
+  const cudaError_t e = once_per_device(configured, smem, [&] {
+    return cudaFuncSetAttribute(k_merge_octave, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  });
+  if (e != cudaSuccess) return e;
   k_merge_octave<<<bt.nframes, kMergeThreads, smem, st>>>(bt, o);
   return cudaGetLastError();
 }

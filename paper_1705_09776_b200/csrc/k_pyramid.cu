@@ -716,12 +716,11 @@ cudaError_t launch_octave_variant(const Batch& bt, const DetConst& dc, int o, in
 cudaError_t launch_detect(const Batch& bt, const DetConst& dc, int o, const CUtensorMap* tmap, cudaStream_t st) {
   const int ww = bt.ow[o] - 2 * dc.margin, hh = bt.oh[o] - 2 * dc.margin;
   if (ww <= 0 || hh <= 0) return cudaSuccess;  // detect_extrema: empty window (scale_space.cpp:159)
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(k_detect, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kDetSmem));
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  static size_t configured[kMaxDevices] = {};
+  cudaError_t e0 = once_per_device(configured, 1, [&] {
+    return cudaFuncSetAttribute(k_detect, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kDetSmem));
+  });
+  if (e0 != cudaSuccess) return e0;
   if (dc.walk) {
     // Balanced row segments of about kSegTarget rows (each costs 4 extra G
     // rows and 2 extra alpha rows at its ends).
@@ -733,14 +732,12 @@ cudaError_t launch_detect(const Batch& bt, const DetConst& dc, int o, const CUte
     const int nw = 1;
     dim3 grid((strips + nw - 1) / nw, nseg, bt.nframes);
     constexpr int smem = int(sizeof(DetWarpSmem)) * kDetWarps;
-    static bool walk_configured = false;
-    if (!walk_configured) {
-      cudaError_t e = cudaFuncSetAttribute(k_detect_walk, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      if (e != cudaSuccess) return e;
-      e = cudaFuncSetAttribute(k_detect_walk, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-      if (e != cudaSuccess) return e;
-      walk_configured = true;
-    }
+    static size_t walk_configured[kMaxDevices] = {};
+    cudaError_t e = once_per_device(walk_configured, 1, [&] {
+      cudaError_t r = cudaFuncSetAttribute(k_detect_walk, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      return r != cudaSuccess ? r : cudaFuncSetAttribute(k_detect_walk, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    });
+    if (e != cudaSuccess) return e;
     k_detect_walk<<<grid, 32 * nw, int(sizeof(DetWarpSmem)) * nw, st>>>(bt, dc, o, seg_rows);
     return cudaGetLastError();
   }

@@ -513,26 +513,26 @@ __global__ void __launch_bounds__(256) k_scfv_encode(Batch bt, Model md, EncodeC
 __constant__ uint32_t c_zeros[17][32];  // c_zeros[k][b] = Z^(2^k) applied to register 1 << b
 
 cudaError_t init_crc_zeros() {
-  static bool done = false;
-  if (done) return cudaSuccess;
-  uint32_t table[256];
-  for (uint32_t i = 0; i < 256; ++i) {
-    uint32_t c = i;
-    for (int k = 0; k < 8; ++k) c = (c & 1u) ? 0xEDB88320u ^ (c >> 1) : c >> 1;
-    table[i] = c;
-  }
-  uint32_t z[17][32];
-  for (int b = 0; b < 32; ++b) z[0][b] = table[(1u << b) & 0xFFu] ^ ((1u << b) >> 8);
-  for (int k = 1; k < 17; ++k)
-    for (int b = 0; b < 32; ++b) {  // Z^(2^k) = Z^(2^(k-1)) o Z^(2^(k-1))
-      uint32_t v = z[k - 1][b], r = 0;
-      for (int c = 0; c < 32; ++c)
-        if ((v >> c) & 1u) r ^= z[k - 1][c];
-      z[k][b] = r;
+  // c_zeros is per device (constant memory of each device's module image).
+  static size_t done[kMaxDevices] = {};
+  return once_per_device(done, 1, [] {
+    uint32_t table[256];
+    for (uint32_t i = 0; i < 256; ++i) {
+      uint32_t c = i;
+      for (int k = 0; k < 8; ++k) c = (c & 1u) ? 0xEDB88320u ^ (c >> 1) : c >> 1;
+      table[i] = c;
     }
-  cudaError_t e = cudaMemcpyToSymbol(c_zeros, z, sizeof(z));
-  if (e == cudaSuccess) done = true;
-  return e;
+    uint32_t z[17][32];
+    for (int b = 0; b < 32; ++b) z[0][b] = table[(1u << b) & 0xFFu] ^ ((1u << b) >> 8);
+    for (int k = 1; k < 17; ++k)
+      for (int b = 0; b < 32; ++b) {  // Z^(2^k) = Z^(2^(k-1)) o Z^(2^(k-1))
+        uint32_t v = z[k - 1][b], r = 0;
+        for (int c = 0; c < 32; ++c)
+          if ((v >> c) & 1u) r ^= z[k - 1][c];
+        z[k][b] = r;
+      }
+    return cudaMemcpyToSymbol(c_zeros, z, sizeof(z));
+  });
 }
 
 __device__ __forceinline__ uint32_t crc_shift(uint32_t v, uint32_t nbytes) {
@@ -647,21 +647,17 @@ cudaError_t launch_scfv_pack(const Batch& bt, const Model& md, const EncodeConst
   cudaError_t e = init_crc_zeros();
   if (e != cudaSuccess) return e;
   constexpr int pca_smem = int(sizeof(double)) * (128 * 33 + 16 * 128);
-  static bool pca_configured = false;
-  if (!pca_configured) {
-    e = cudaFuncSetAttribute(k_pca, cudaFuncAttributeMaxDynamicSharedMemorySize, pca_smem);
-    if (e != cudaSuccess) return e;
-    pca_configured = true;
-  }
+  static size_t pca_configured[kMaxDevices] = {};
+  e = once_per_device(pca_configured, 1, [&] { return cudaFuncSetAttribute(k_pca, cudaFuncAttributeMaxDynamicSharedMemorySize, pca_smem); });
+  if (e != cudaSuccess) return e;
   k_pca<<<dim3(16, bt.nframes), 128, pca_smem, st>>>(bt, md);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  static bool post_configured = false;
-  if (!post_configured) {
-    e = cudaFuncSetAttribute(k_posterior, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(PostSmem)));
-    if (e != cudaSuccess) return e;
-    post_configured = true;
-  }
+  static size_t post_configured[kMaxDevices] = {};
+  e = once_per_device(post_configured, 1, [&] {
+    return cudaFuncSetAttribute(k_posterior, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(PostSmem)));
+  });
+  if (e != cudaSuccess) return e;
   if (md.nc <= 32)
     k_posterior_small<<<dim3((bt.cap_or + kSmallRows - 1) / kSmallRows, bt.nframes), kSmallRows * md.nc, 0, st>>>(bt, md);
   else
