@@ -48,3 +48,32 @@ def test_encode_pnm_files(ex, bundle_b8):
     assert ex.encode_pnm(ppm, "2K") == oracle_lib.encode_rgb(bundle_b8, rgb, 2)
     with pytest.raises(cg.DataError):
         ex.encode_pnm(b"P6 160 120 255\n" + rgb.tobytes()[:-1], "2K")
+
+
+def test_cpp_example_extracts_pgm_and_ppm_files(tmp_path, bundle_b8):
+    """examples/extract.cpp (the reference CLI's extract flow over the shim's
+    load_pnm + encode_image) writes the oracle's container for a PGM and a
+    PPM file; a truncated file is a data error (exit code 2)."""
+    import os
+    import subprocess
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    lib_dir = os.path.join(root, "paper_1705_09776_b200")
+    exe = str(tmp_path / "extract")
+    subprocess.run(["g++", "-std=c++17", "-O1", os.path.join(root, "examples", "extract.cpp"), f"-L{lib_dir}",
+                    "-lcdvz_gpu", f"-Wl,-rpath,{lib_dir}", "-o", exe], check=True)
+    bundle = tmp_path / "bundle.txt"
+    bundle.write_text(bundle_b8)
+    grey = oracle_lib.synth_frames(91, 1, 320, 240)[0]
+    rgb = oracle_lib.synth_rgb(92, 1, 320, 240)[0]
+    cases = [(b"P5\n320 240\n255\n" + grey.tobytes(), oracle_lib.encode(bundle_b8, grey, 3)),
+             (b"P6\n320 240\n255\n" + rgb.tobytes(), oracle_lib.encode_rgb(bundle_b8, rgb, 3))]
+    for k, (data, want) in enumerate(cases):
+        src, dst = tmp_path / f"in{k}.pnm", tmp_path / f"out{k}.cdvz"
+        src.write_bytes(data)
+        subprocess.run([exe, str(bundle), "4K", str(src), str(dst)], check=True, capture_output=True)
+        assert dst.read_bytes() == want
+    bad = tmp_path / "bad.ppm"
+    bad.write_bytes(cases[1][0][:-10])
+    r = subprocess.run([exe, str(bundle), "4K", str(bad), str(tmp_path / "x.cdvz")], capture_output=True)
+    assert r.returncode == 2
