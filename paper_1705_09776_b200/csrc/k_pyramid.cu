@@ -181,7 +181,8 @@ __device__ __forceinline__ float rsqrt_approx(float x) {
 // coefficient magnitudes — orders of magnitude above FP32 rounding of the
 // reference's own formulas. Near-double roots and degenerate cases go to the
 // exact path.
-__device__ __forceinline__ bool screen_pixel(const double a[4], const DetConst& dc) {
+__device__ __forceinline__ bool screen_pixel(const double a[4], const double up[4], const double dn[4],
+                                              const DetConst& dc) {
   const double qa = 3.0 * a[3], qb = 2.0 * a[2], qc = a[1];
   if (qa == 0.0) return true;
   const double disc = qb * qb - 4.0 * qa * qc;
@@ -195,6 +196,11 @@ __device__ __forceinline__ bool screen_pixel(const double a[4], const DetConst& 
   if (!(fabsf(q) > 1e-30f)) return true;
   const float r0 = q * rcp_approx(fa), r1 = fc * rcp_approx(q);
   const float a0 = float(a[0]), a1 = float(a[1]), a2 = float(a[2]), a3 = float(a[3]);
+  const float u0 = float(up[0]), u1 = float(up[1]), u2 = float(up[2]), u3 = float(up[3]);
+  const float d0 = float(dn[0]), d1 = float(dn[1]), d2 = float(dn[2]), d3 = float(dn[3]);
+  auto horner = [](float r, float c0, float c1, float c2, float c3) {
+    return __fmaf_rn(r, __fmaf_rn(r, __fmaf_rn(r, c3, c2), c1), c0);
+  };
   bool any = false;
 #pragma unroll
   for (int k = 0; k < 2; ++k) {
@@ -203,9 +209,22 @@ __device__ __forceinline__ bool screen_pixel(const double a[4], const DetConst& 
       if (!isfinite(r)) any = true;
       continue;
     }
-    const float p = __fmaf_rn(r, __fmaf_rn(r, __fmaf_rn(r, a3, a2), a1), a0);
-    const float bound = __fmaf_rn(r, __fmaf_rn(r, __fmaf_rn(r, fabsf(a3), fabsf(a2)), fabsf(a1)), fabsf(a0));
-    if (__fmaf_rn(1e-5f, bound, fabsf(p) + 1e-6f) >= dc.scr_thr) any = true;
+    const float p = horner(r, a0, a1, a2, a3);
+    const float bound = horner(r, fabsf(a0), fabsf(a1), fabsf(a2), fabsf(a3));
+    if (!(__fmaf_rn(1e-5f, bound, fabsf(p) + 1e-6f) >= dc.scr_thr)) continue;
+    // The exact test needs p above (p > 0) or below (p < 0) all eight
+    // neighbours' cubics at the same scale; drop the root only when the up or
+    // down neighbour is clearly past p. The float root is within ~1e-6 s of
+    // the exact one and p is stationary there, so a margin of 1e-4 of the
+    // magnitudes (values plus slopes) is far beyond the float error.
+    const float pu = horner(r, u0, u1, u2, u3), pd = horner(r, d0, d1, d2, d3);
+    const float bu = horner(r, fabsf(u0), fabsf(u1), fabsf(u2), fabsf(u3));
+    const float bd = horner(r, fabsf(d0), fabsf(d1), fabsf(d2), fabsf(d3));
+    const float su = __fmaf_rn(r, __fmaf_rn(r, 3.0f * fabsf(u3), 2.0f * fabsf(u2)), fabsf(u1));
+    const float sd = __fmaf_rn(r, __fmaf_rn(r, 3.0f * fabsf(d3), 2.0f * fabsf(d2)), fabsf(d1));
+    const float m = 1e-4f * (bound + bu + bd + su + sd) + 1e-7f;
+    const bool past = p > 0.0f ? (pu >= p + m || pd >= p + m) : (pu <= p - m || pd <= p - m);
+    if (!past) any = true;
   }
   return any;
 }
@@ -528,7 +547,11 @@ __global__ void __launch_bounds__(kDetThreads, 2)
     if (yd < h - m && xd < w - m) {
       const double* a = At + ((r + 1) * 4) * kAW + cc + 1;
       const double av[4] = {a[0], a[kAW], a[2 * kAW], a[3 * kAW]};
-      push = !dc.screen || screen_pixel(av, dc);
+      const double* au = a - 4 * kAW;
+      const double* ad = a + 4 * kAW;
+      const double uv[4] = {au[0], au[kAW], au[2 * kAW], au[3 * kAW]};
+      const double dv[4] = {ad[0], ad[kAW], ad[2 * kAW], ad[3 * kAW]};
+      push = !dc.screen || screen_pixel(av, uv, dv, dc);
     }
     // One shared-memory atomic per warp (queue order is irrelevant: the merge
     // kernel restores raster order from the bitmap).
@@ -649,9 +672,9 @@ __global__ void __launch_bounds__(32 * kDetWarps) k_detect_walk(Batch bt, DetCon
       an[i] = sum;
     }
   };
-  auto screen_row = [&](int rs, const double a[4]) {  // rs's 3x3 alpha neighbourhood is complete
+  auto screen_row = [&](int rs, const double a[4], const double up[4], const double dn[4]) {  // 3x3 neighbourhood complete
     if (rs >= y0 && rs < y1) {
-      const bool push = out_col && (!dc.screen || screen_pixel(a, dc));
+      const bool push = out_col && (!dc.screen || screen_pixel(a, up, dn, dc));
       const unsigned bal = __ballot_sync(0xffffffffu, push);
       if (push) S.queue[qn + __popc(bal & ((1u << lane) - 1u))] = uint16_t(((rs - y0 + 2) << 5) | lane);
       qn += __popc(bal);
@@ -680,8 +703,13 @@ __global__ void __launch_bounds__(32 * kDetWarps) k_detect_walk(Batch bt, DetCon
       __syncwarp();
       issue();  // rows ra + kPrefetch + 1, ra + kPrefetch + 2 into the slots of rows ra - 1, ra
       issue();
-      screen_row(ra - 1, ap);
-      if (second) screen_row(ra, a0);
+      {
+        double au[4];  // own alpha of row ra - 2 (the ring keeps it)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) au[i] = S.ring[unsigned(ra - 2) % kRing][i][lane];
+        screen_row(ra - 1, ap, au, a0);
+      }
+      if (second) screen_row(ra, a0, ap, a1);
 #pragma unroll
       for (int i = 0; i < 4; ++i) ap[i] = a1[i];
     }
