@@ -1,17 +1,25 @@
-"""Benchmark: CDVS frames/sec (VGA, 4 KB mode) — BASELINE.json configs[1]:
-a batch of 1024 synthetic 640x480 frames, 4K mode, B8 bundle, on 1 B200 per
-rank (frame-sharded with no collective for N > 1: scaling "weak").
+"""Benchmark: CDVS frames/sec (VGA, 4 KB mode).
 
   python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
 
+Workload: N = 1 runs BASELINE.json configs[1] (a batch of 1024 synthetic
+640x480 frames, 4K mode, B8 bundle); N > 1 runs configs[3] (65,536 distinct
+synthetic VGA frames frame-sharded in contiguous ranges over the N GPUs, no
+collective; one step = the whole pool, "strong" scaling). --workload forces
+either. Under torchrun (WORLD_SIZE set) each process drives its LOCAL_RANK
+GPU; `python bench.py --gpus N` alone drives N GPUs from one process, one host
+thread per GPU. Fewer visible GPUs than N is an error unless --share-devices.
+
 value: frames/s with the frames already resident in HBM (device synthetic
-generator), timed with CUDA events on the extractor's stream, max over ranks.
+generator), timed with CUDA events on each extractor's stream, max over ranks.
 e2e:   the same through the public C ABI cdvz_gpu_encode_batch with pinned host
-frames in and containers out (H2D + D2H inside the timed region).
+frames in and containers out (H2D + D2H inside the timed region); without
+torchrun at N > 1 through one multi-device context (cdvz_gpu_create_multi).
 roofline: the octave kernel pair (k_blur pyramid + k_detect extrema), timed
 standalone in one extra unoverlapped step, against measured HBM.
 cpu_baseline / --impl reference: the CPU oracle (an Eigen-free restatement of
-the reference; the reference itself cannot be built here) on the host cores.
+the reference) on the host cores, with the GPU's containers of the same frames
+compared byte for byte.
 """
 from __future__ import annotations
 
@@ -32,6 +40,8 @@ sys.path.insert(0, ROOT)
 METRIC = "CDVS frames/sec (VGA, 4KB mode) at 1/2/4/8 B200; pyramid HBM GB/s vs peak"
 FRAME_W, FRAME_H, BATCH, MODE = 640, 480, 1024, "4K"
 BASE_SEED = 1000
+GOLDEN = 0x9E3779B97F4A7C15
+POOL = 65536  # configs[3]
 
 
 def dist_env():
@@ -143,20 +153,48 @@ def pyramid_fp64_ops(w, h, radii=(5, 5, 6, 8), margin=10, octaves=4):
     return ops
 
 
-def cpu_baseline(frames: np.ndarray, bundle: str, mode_id: int, sample: int):
-    """The oracle on all host cores, frame-parallel (BASELINE.md CPU mode B)."""
+def cpu_model() -> str:
+    """The host CPU model string (lscpu's "Model name", from /proc/cpuinfo)."""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def cpu_baseline(frames: np.ndarray, bundle: str, mode_id: int, gpu_containers=None):
+    """The oracle on all host cores, frame-parallel (BASELINE.md CPU mode B),
+    over a bounded sample of the timed frames (one untimed pass first), plus
+    the reference's StageTimings split from a single-threaded pass over 4
+    frames. gpu_containers: the timed step's GPU containers of the same frames,
+    compared byte for byte with the oracle's (parity beside the timing)."""
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     import oracle_lib
 
     oracle_lib.build()
     cores = os.cpu_count() or 1
-    sub = frames[:sample]
-    t0 = time.perf_counter()
-    oracle_lib.encode_batch(bundle, sub, mode_id, threads=cores)
-    dt = time.perf_counter() - t0
-    return {"value": len(sub) / dt, "unit": "frames/s", "cores": cores, "kind": "port",
-            "sample": f"{len(sub)} of the {BATCH} synthetic 640x480 frames, 4K mode, B8 bundle, "
-                      f"frame-parallel on {cores} host threads (oracle restatement; reference unbuildable)"}
+    oracle_lib.encode_batch(bundle, frames[:cores], mode_id, threads=cores)  # untimed warm pass
+    times = []
+    want = None
+    for _ in range(2):
+        t0 = time.perf_counter()
+        want = oracle_lib.encode_batch(bundle, frames, mode_id, threads=cores)
+        times.append(time.perf_counter() - t0)
+    dt = min(times)
+    stages = oracle_lib.stage_ms(bundle, frames[:4], mode_id)
+    out = {"value": len(frames) / dt, "unit": "frames/s", "cores": cores, "kind": "port",
+           "cpu_model": cpu_model(),
+           "sample": f"{len(frames)} of the timed synthetic 640x480 frames, 4K mode, B8 bundle, frame-parallel on "
+                     f"{cores} host threads (BASELINE.md mode B; best of 2 timed passes after a warm pass)",
+           "stage_ms_per_frame_single_thread": stages}
+    if gpu_containers is not None:
+        same = sum(1 for a, b in zip(gpu_containers, want) if a == b)
+        out["parity"] = {"byte_identical": same, "of": len(want),
+                         "note": "the GPU's containers from the last timed step vs the oracle's, same frames"}
+    return out
 
 
 def run_reference(args, rank, world):
@@ -182,17 +220,90 @@ def run_reference(args, rank, world):
     total = sum(times)
     value = sample * args.steps / total
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world,
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * total / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"VGA 640x480 synthetic frames, 4K mode, B8 bundle; each step = {sample} frames "
                                f"(bounded sample of the {BATCH}-frame batch)", "frames_per_step": sample},
-        "cpu_baseline": {"value": value, "unit": "frames/s", "cores": cores, "kind": "port",
+        "cpu_baseline": {"value": value, "unit": "frames/s", "cores": cores, "kind": "port", "cpu_model": cpu_model(),
                          "sample": f"{sample} frames per step on {cores} host threads; oracle restatement "
                                    "(the reference needs Eigen3/doctest/CLI11, absent)"},
         "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
+
+
+def workload(args, world):
+    """(name, total frames per step, scaling) — configs[1] at N = 1, configs[3]
+    (65,536 frames sharded over the N GPUs) above, unless --workload says."""
+    w = args.workload
+    if w == "auto":
+        w = "configs1" if world == 1 else "configs3"
+    if w == "configs1":
+        return w, args.batch * world, "weak", args.batch
+    return w, POOL, "strong", None
+
+
+def shard(total: int, world: int, rank: int):
+    """Contiguous frame range of `rank` (the multi-device context splits host
+    batches the same way)."""
+    return total * rank // world, total * (rank + 1) // world
+
+
+def frame_seed(index: int) -> int:
+    """synth_corpus seed of global frame `index` (synthetic.cpp:55-61)."""
+    return (BASE_SEED + index * GOLDEN) % (1 << 64)
+
+
+class Rank:
+    """One device's share of the step: an Extractor, its resident frames and
+    output slots."""
+
+    def __init__(self, cg, bundle, device, max_batch, first, count, mode):
+        self.ex = cg.Extractor(bundle, device=device, max_batch=max_batch)
+        self.device, self.first, self.count, self.mode = device, first, count, mode
+        self.slot = cg.container_slot(mode)
+        self.d_frames = self.ex.synth_frames_device(frame_seed(first), count, FRAME_W, FRAME_H)
+        self.d_out = self.ex.device_buffer(count * self.slot)
+        self.d_len = self.ex.device_buffer(count * 4)
+
+    def step(self):
+        self.ex.encode_device(self.d_frames, self.count, FRAME_W, FRAME_H, self.mode, self.d_out, self.d_len)
+
+    def timed(self, steps):
+        self.ex.event_record(0)
+        for _ in range(steps):
+            self.step()
+        self.ex.event_record(1)
+        return self.ex.event_elapsed(0, 1)
+
+    def containers(self, n):
+        """Containers of the first n frames from the last step's output slots."""
+        lens = np.frombuffer(self.d_len.to_host(self.count * 4).tobytes(), dtype=np.uint32)
+        raw = self.d_out.to_host(n * self.slot)
+        return [raw[i * self.slot: i * self.slot + int(lens[i])].tobytes() for i in range(n)], lens
+
+
+def run_threads(fns):
+    """Runs callables on one host thread each (ctypes releases the GIL) and
+    returns their results in order; re-raises the first failure."""
+    res = [None] * len(fns)
+    err = []
+
+    def body(i):
+        try:
+            res[i] = fns[i]()
+        except BaseException as e:  # noqa: BLE001
+            err.append(e)
+
+    ths = [threading.Thread(target=body, args=(i,)) for i in range(len(fns))]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    if err:
+        raise err[0]
+    return res
 
 
 def main():
@@ -204,46 +315,57 @@ def main():
     ap.add_argument("--batch", type=int, default=BATCH)
     ap.add_argument("--max-batch", type=int, default=512)
     ap.add_argument("--bundle", default="b8")
+    ap.add_argument("--workload", default="auto", choices=["auto", "configs1", "configs3"])
+    ap.add_argument("--share-devices", action="store_true",
+                    help="allow more ranks than visible GPUs (ranks share devices round-robin; plumbing tests only)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-b512", action="store_true")
     args = ap.parse_args()
-    rank, world, local = dist_env()
+    rank, world_env, local = dist_env()
+    torchrun = "WORLD_SIZE" in os.environ
 
     if args.impl == "reference":
-        run_reference(args, rank, world)
+        run_reference(args, rank, world_env)
         return
 
+    if torchrun and world_env != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but torchrun started {world_env} ranks")
+    world = args.gpus
+    import paper_1705_09776_b200 as cg
+
+    ndev = cg.device_count()
+    need = world if not torchrun else local + 1
+    if ndev < need and not args.share_devices:
+        sys.exit(f"bench.py: --gpus {world} needs {need} visible GPUs, found {ndev} "
+                 "(pass --share-devices to run the ranks on fewer GPUs as a plumbing test)")
     dist = None
-    device = local
-    if world > 1:
+    if torchrun and world > 1:
         import torch
         import torch.distributed as tdist
 
-        # One process per GPU; with fewer visible GPUs than ranks (a plumbing
-        # test on a 1-GPU box) ranks share devices round-robin. The data path
-        # has no collective (frames are independent), so the only cross-rank
-        # traffic -- the timing barrier and the max over ranks -- goes over the
-        # host backend.
-        device = local % max(1, torch.cuda.device_count())
+        # One process per GPU. The data path has no collective (frames are
+        # independent); the only cross-rank traffic -- the timing barrier and
+        # the max over ranks -- goes over the host backend.
         tdist.init_process_group("gloo")
         dist = tdist
-
-    import paper_1705_09776_b200 as cg
+    # Ranks this process drives: its own under torchrun; all N (one host
+    # thread each) when `python bench.py --gpus N` runs alone.
+    my_ranks = [rank] if torchrun else list(range(world))
 
     with open(os.path.join(ROOT, "tests", "golden", f"bundle_{args.bundle}.txt")) as f:
         bundle = f.read()
-    ex = cg.Extractor(bundle, device=device, max_batch=args.max_batch)
     mode = cg.mode_by_name(MODE)
-    n = args.batch
-    slot = cg.container_slot(mode)
-    # Each rank encodes its own 1024-frame batch (distinct seeds per rank).
-    d_frames = ex.synth_frames_device(BASE_SEED + rank * 1_000_003, n, FRAME_W, FRAME_H)
-    d_out = ex.device_buffer(n * slot)
-    d_len = ex.device_buffer(n * 4)
+    wl_name, total, scaling, per_rank_fixed = workload(args, world)
+    ranks = []
+    for r in my_ranks:
+        first, last = (r * per_rank_fixed, (r + 1) * per_rank_fixed) if per_rank_fixed else shard(total, world, r)
+        dev = r % ndev if not torchrun else local % ndev
+        ranks.append(Rank(cg, bundle, dev, args.max_batch, first, last - first, mode))
 
     def barrier():
-        ex.sync()
+        for rk in ranks:
+            rk.ex.sync()
         if dist:
             dist.barrier()
 
@@ -256,95 +378,136 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    def sum_over_ranks(x):
+        if not dist:
+            return x
+        import torch
+
+        t = torch.tensor([x], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
     for _ in range(args.warmup):
-        ex.encode_device(d_frames, n, FRAME_W, FRAME_H, mode, d_out, d_len)
+        run_threads([rk.step for rk in ranks])
     barrier()
-    with ClockSampler(device) as clk:
-        ex.event_record(0)
-        launches = 0
-        for _ in range(args.steps):
-            ex.encode_device(d_frames, n, FRAME_W, FRAME_H, mode, d_out, d_len)
-            launches += ex.kernel_stats()["launches"]
-        ex.event_record(1)
-        ms = ex.event_elapsed(0, 1)
+    with ClockSampler(ranks[0].device) as clk:
+        per_rank_ms = run_threads([(lambda rk=rk: rk.timed(args.steps)) for rk in ranks])
     barrier()
+    ms = max_over_ranks(max(per_rank_ms))
+    frames_per_step = sum_over_ranks(sum(rk.count for rk in ranks))
+    value = frames_per_step * args.steps / (ms / 1000.0)
+    launches = int(sum_over_ranks(sum(rk.ex.kernel_stats()["launches"] for rk in ranks))) * args.steps
+    lead = ranks[0]
+    n_cpu = min(lead.count, 2 * (os.cpu_count() or 8))
+    gpu_sample, lengths = lead.containers(n_cpu)
+    ok_frames = int(sum_over_ranks(sum(int(np.count_nonzero(np.frombuffer(rk.d_len.to_host(rk.count * 4).tobytes(),
+                                                                              dtype=np.uint32))) for rk in ranks)))
     # Roofline of the octave kernel pair and the per-stage split, timed
     # standalone in one extra step with every kernel on one stream (no
-    # overlap), outside the timed region.
-    ex.set_debug(False, serial=True)
-    ex.encode_device(d_frames, n, FRAME_W, FRAME_H, mode, d_out, d_len)
-    stage = ex.stage_times()
-    ks = ex.kernel_stats()
+    # overlap), outside the timed region (rank 0's device).
+    lead.ex.set_debug(False, serial=True)
+    lead.step()
+    stage = lead.ex.stage_times()
+    ks = lead.ex.kernel_stats()
     pyr_ms, pyr_bytes = ks["pyramid_ms"], ks["pyramid_bytes"]
-    ex.set_debug(False)
-    ms = max_over_ranks(ms)
-    value = world * n * args.steps / (ms / 1000.0)
-    lengths = np.frombuffer(d_len.to_host(n * 4).tobytes(), dtype=np.uint32)
-    ok_frames = int(np.count_nonzero(lengths))
+    lead.ex.set_debug(False)
 
-    # e2e through the public C ABI with pinned host buffers.
+    # e2e through the public C ABI with host frames: a pinned pool of distinct
+    # frames per rank, cycled until the rank's share of the step is encoded.
+    # Without torchrun, one multi-device context (cdvz_gpu_create_multi) takes
+    # the pools of all ranks in one host batch and shards it itself.
     e2e = None
     if not args.no_e2e:
-        host_frames = ex.pinned_buffer(n * FRAME_W * FRAME_H)
-        host_frames.array[:] = d_frames.to_host(n * FRAME_W * FRAME_H)
-        frames_np = host_frames.array.reshape(n, FRAME_H, FRAME_W)
-        out = ex.pinned_buffer(n * slot)
-        offsets = np.zeros(n + 1, dtype=np.uint64)
-        status = np.zeros(n, dtype=np.int32)
-        lib = ex._lib
+        pool_n = min(lead.count, BATCH)
+        if torchrun or world == 1:
+            ctx = lead.ex
+            host = ctx.pinned_buffer(pool_n * FRAME_W * FRAME_H)
+            host.array[:] = lead.d_frames.to_host(pool_n * FRAME_W * FRAME_H)
+            calls = max(1, lead.count // pool_n)
+        else:
+            for rk in ranks:
+                rk.ex.trim()
+            ctx = cg.Extractor(bundle, max_batch=args.max_batch, devices=[rk.device for rk in ranks])
+            host = ctx.pinned_buffer(world * pool_n * FRAME_W * FRAME_H)
+            for i, rk in enumerate(ranks):
+                host.array[i * pool_n * FRAME_W * FRAME_H:(i + 1) * pool_n * FRAME_W * FRAME_H] = \
+                    rk.d_frames.to_host(pool_n * FRAME_W * FRAME_H)
+            calls = max(1, lead.count // pool_n)
+            pool_n *= world
+        frames_np = host.array.reshape(pool_n, FRAME_H, FRAME_W)
+        slot = cg.container_slot(mode)
+        out = ctx.pinned_buffer(pool_n * slot)
+        offsets = np.zeros(pool_n + 1, dtype=np.uint64)
+        status = np.zeros(pool_n, dtype=np.int32)
+        lib = ctx._lib
 
         def call():
-            ex._check(lib.cdvz_gpu_encode_batch(ex._ctx, frames_np.ctypes.data, FRAME_W, FRAME_H, FRAME_W, n, mode.id,
-                                                640, out.ptr, n * slot, offsets.ctypes.data, status.ctypes.data))
+            ctx._check(lib.cdvz_gpu_encode_batch(ctx._ctx, frames_np.ctypes.data, FRAME_W, FRAME_H, FRAME_W, pool_n,
+                                                 mode.id, 640, out.ptr, pool_n * slot, offsets.ctypes.data,
+                                                 status.ctypes.data))
 
         call()
-        barrier()
+        if dist:
+            dist.barrier()
         t0 = time.perf_counter()
         for _ in range(args.steps):
-            call()
+            for _ in range(calls):
+                call()
         e2e_s = max_over_ranks(time.perf_counter() - t0)
-        e2e = {"value": world * n * args.steps / e2e_s, "unit": "frames/s",
-               "h2d_bytes_per_step": n * FRAME_W * FRAME_H, "d2h_bytes_per_step": n * slot + 4 * n,
-               "note": "host wall clock around cdvz_gpu_encode_batch (returns after the D2H completes)"}
-        cpu_frames = frames_np.copy()
-    else:
-        cpu_frames = d_frames.to_host(min(n, 256) * FRAME_W * FRAME_H).reshape(-1, FRAME_H, FRAME_W)
+        e2e_frames = sum_over_ranks(pool_n * calls)
+        e2e = {"value": e2e_frames * args.steps / e2e_s, "unit": "frames/s",
+               "h2d_bytes_per_step": int(e2e_frames * FRAME_W * FRAME_H),
+               "d2h_bytes_per_step": int(e2e_frames * (slot + 4)),
+               "note": "host wall clock around cdvz_gpu_encode_batch (returns after the D2H completes); "
+                       + (f"{calls} call(s) per step over a pinned pool of {pool_n} distinct frames"
+                          + (f" on a {world}-device context (cdvz_gpu_create_multi)" if ctx is not lead.ex else ""))}
+        if ctx is not lead.ex:
+            ctx.close()
 
     hbm, peak_kind = measured_peaks()
     achieved = (pyr_bytes / (pyr_ms / 1000.0)) / 1e9 if pyr_ms > 0 else 0.0
     ncu = ncu_traffic()
     traffic = ncu.get("dram_bytes_per_launch_pair") if ncu else None
     f64_peak, f64_kind = fp64_peak()
-    f64_ops = pyramid_fp64_ops(FRAME_W, FRAME_H) * n
+    f64_ops = pyramid_fp64_ops(FRAME_W, FRAME_H) * lead.count
     f64_achieved = f64_ops / (pyr_ms / 1000.0) / 1e12 if pyr_ms > 0 else 0.0
     # Secondary workload: the paper's 512-component GMM bundle.
     b512 = None
-    if args.bundle == "b8" and not args.no_b512:
-        ex.trim()  # one context's batch buffers at a time
+    if args.bundle == "b8" and not args.no_b512 and world == 1:
+        lead.ex.trim()  # one context's batch buffers at a time
         with open(os.path.join(ROOT, "tests", "golden", "bundle_b512.txt")) as f:
-            ex512 = cg.Extractor(f.read(), device=device, max_batch=args.max_batch)
+            ex512 = cg.Extractor(f.read(), device=lead.device, max_batch=args.max_batch)
+        n = lead.count
         for _ in range(2):
-            ex512.encode_device(d_frames, n, FRAME_W, FRAME_H, mode, d_out, d_len)
+            ex512.encode_device(lead.d_frames, n, FRAME_W, FRAME_H, mode, lead.d_out, lead.d_len)
         ex512.sync()
         ex512.event_record(0)
         for _ in range(3):
-            ex512.encode_device(d_frames, n, FRAME_W, FRAME_H, mode, d_out, d_len)
+            ex512.encode_device(lead.d_frames, n, FRAME_W, FRAME_H, mode, lead.d_out, lead.d_len)
         ex512.event_record(1)
-        ms512 = max_over_ranks(ex512.event_elapsed(0, 1))
-        b512 = {"value": world * n * 3 / (ms512 / 1000.0), "unit": "frames/s", "steps": 3,
+        ms512 = ex512.event_elapsed(0, 1)
+        b512 = {"value": n * 3 / (ms512 / 1000.0), "unit": "frames/s", "steps": 3,
                 "note": "same frames and mode, B512 bundle (GMM 512 components, the paper's SCFV)"}
         ex512.close()
     if rank != 0:
         return
+    if wl_name == "configs1":
+        wl = (f"configs[1]: batch of {args.batch} synthetic 640x480 frames per GPU (synth_image seeds 1000+i*golden), "
+              "4KB mode, B8 bundle (train_model on synth_corpus(401,20,256,256), GMM 8)")
+    else:
+        wl = (f"configs[3]: {POOL} distinct synthetic 640x480 frames (synth_image seeds 1000+i*golden), 4KB mode, "
+              f"B8 bundle, frame-sharded in contiguous ranges over {world} GPU(s), resident in HBM; one step = the "
+              "whole pool")
     line = {
         "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": scaling,
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "configs[1]: batch of 1024 synthetic 640x480 frames (synth_image seeds 1000+i*golden), "
-                               "4KB mode, B8 bundle (train_model on synth_corpus(401,20,256,256), GMM 8)",
-                   "frames_per_step_per_gpu": n, "mode": MODE, "bundle": args.bundle,
-                   "l2": "inputs larger than L2 (315 MB of frames + 13 GB of pyramid writes per step)",
-                   "parallelism": f"frame-sharded x{world}, no collective"},
+        "config": {"workload": wl, "frames_per_step": int(frames_per_step), "mode": MODE, "bundle": args.bundle,
+                   "l2": "inputs larger than L2 (315 MB of frames + 13 GB of pyramid writes per 1024 frames)",
+                   "parallelism": f"frame-sharded x{world}, no collective"
+                                  + (" (torchrun, one process per GPU)" if torchrun else
+                                     " (one process, one host thread per GPU)" if world > 1 else "")},
+        "per_rank_ms": [round(float(x), 3) for x in per_rank_ms] if not dist else None,
         "e2e": e2e,
         "gpu_launches": launches,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
@@ -368,7 +531,8 @@ def main():
         "clocks": clk.summary(),
     }
     if not args.no_cpu:
-        line["cpu_baseline"] = cpu_baseline(cpu_frames, bundle, mode.id, sample=min(len(cpu_frames), 2 * (os.cpu_count() or 8)))
+        cpu_frames = lead.d_frames.to_host(n_cpu * FRAME_W * FRAME_H).reshape(n_cpu, FRAME_H, FRAME_W)
+        line["cpu_baseline"] = cpu_baseline(cpu_frames, bundle, mode.id, gpu_sample)
     print(json.dumps(line))
 
 

@@ -48,6 +48,26 @@ enum {
 int cdvz_gpu_create(const char* bundle_text, size_t bundle_len, int device, int max_batch,
                     cdvz_gpu_ctx** out_ctx);
 
+/* Multi-device form of cdvz_gpu_create (SURVEY.md §8(b) "create with a device
+ * list"): one single-device context per entry of devices[0..ndev), same
+ * bundle. Host batches passed to cdvz_gpu_encode_batch / _rgb / _f64 are split
+ * into contiguous frame ranges, one host thread per device (the GPU analogue
+ * of the reference's run_indexed fan-out, proj/src/parallel.cpp:40-78), and
+ * the containers are gathered in frame order: output is byte-identical to a
+ * single-device context's. There is no collective (frames are independent).
+ * Device-resident entry points (encode_device, debug_get, events, device
+ * allocations) need a single-device context and return CDVZ_GPU_USAGE here.
+ * A device index may repeat (several contexts on one GPU). */
+int cdvz_gpu_create_multi(const char* bundle_text, size_t bundle_len, const int* devices, int ndev, int max_batch,
+                          cdvz_gpu_ctx** out_ctx);
+
+/* Number of visible CUDA devices (0 when there is none). */
+int cdvz_gpu_visible_devices(void);
+
+/* Number of devices a context drives (1 for cdvz_gpu_create); their indices
+ * are written to devices[0..min(n, cap)). */
+int cdvz_gpu_device_count(const cdvz_gpu_ctx* ctx, int* devices, int cap);
+
 /* Releases every device and pinned host buffer of the context. */
 void cdvz_gpu_destroy(cdvz_gpu_ctx* ctx);
 
@@ -76,10 +96,25 @@ int cdvz_gpu_bundle_info(const cdvz_gpu_ctx* ctx, uint32_t* model_crc, int* comp
  *   result; a failing frame has an empty range and never aborts the batch.
  * Host buffers may be pageable or pinned (cdvz_gpu_host_alloc); both copies
  * (pixels in, containers out) happen inside the call. Returns 0 when the call
- * itself succeeded (check status[] per frame). */
+ * itself succeeded (check status[] per frame). A frame whose keypoint or
+ * orientation lists outgrow the batch capacities is re-encoded on its own with
+ * the largest counts the reference can produce, so content alone never fails
+ * a frame the reference encodes. */
 int cdvz_gpu_encode_batch(cdvz_gpu_ctx* ctx, const uint8_t* pixels, int width, int height, size_t stride,
                           int count, int mode_id, int max_side, uint8_t* out, size_t out_cap,
                           size_t* offsets, int* status);
+
+/* GrayImage form of cdvz_gpu_encode_batch — the reference's own input type
+ * (proj/include/cdvz/image.hpp:11-18: row-major doubles, rows = height): the
+ * raster an in-process producer hands to encode_image (synth_image,
+ * apply_transform, a decoder), with no 8-bit quantisation. `stride` is in
+ * doubles. Each frame is checked like validate() (proj/src/image.cpp:46-51)
+ * on the device: a non-finite value or one outside [0, 1] gives that frame
+ * status CDVZ_GPU_DATA and an empty range. Then resize_max_side and the rest
+ * of the pipeline run unchanged. */
+int cdvz_gpu_encode_batch_f64(cdvz_gpu_ctx* ctx, const double* pixels, int width, int height, size_t stride,
+                              int count, int mode_id, int max_side, uint8_t* out, size_t out_cap, size_t* offsets,
+                              int* status);
 
 /* PPM form of cdvz_gpu_encode_batch: `count` interleaved 8-bit RGB frames
  * (row stride `stride` >= 3*width bytes). Each pixel becomes the grey value
@@ -106,9 +141,11 @@ int cdvz_gpu_pnm_parse(const uint8_t* file, size_t len, int* width, int* height,
 /* Same pipeline on frames already resident in device memory (d_pixels is a
  * device pointer to count*height*stride bytes). Containers stay on the device
  * in fixed slots of cdvz_gpu_container_slot(mode) bytes; d_lengths[count]
- * (device) receives the lengths, 0 for a failed frame. Asynchronous on the
- * context's stream; cdvz_gpu_sync waits. This is the HBM-resident throughput
- * path used by bench.py's `value`. */
+ * (device) receives the lengths, 0 for a failed frame. Asynchronous: returns
+ * once the work is enqueued (ordered after earlier calls on this context);
+ * cdvz_gpu_sync waits. No capacity retry on this path (a frame that overflows
+ * gets length 0). This is the HBM-resident throughput path of bench.py's
+ * `value`. */
 int cdvz_gpu_encode_device(cdvz_gpu_ctx* ctx, const uint8_t* d_pixels, int width, int height, size_t stride,
                            int count, int mode_id, int max_side, uint8_t* d_out, uint32_t* d_lengths);
 size_t cdvz_gpu_container_slot(int mode_id);
@@ -117,12 +154,14 @@ int cdvz_gpu_sync(cdvz_gpu_ctx* ctx);
 /* Device time of the last batch per reference stage label, in order
  * detection, selection, description, compression, aggregation
  * (StageTimings, proj/include/cdvz/parallel.hpp:117-134; pipeline.cpp:19-94).
- * Measured with CUDA events around each stage's kernels. */
+ * Measured with CUDA events around each stage's kernels; waits for the
+ * context's enqueued work. On a multi-device context: the sum over devices. */
 int cdvz_gpu_stage_times(cdvz_gpu_ctx* ctx, double ms[5]);
 
-/* Launch/kernel bookkeeping for the last batch: number of kernel launches and
- * the measured time of the fused octave (pyramid + extrema) kernels, with the
- * algorithmic HBM bytes they moved. */
+/* Launch/kernel bookkeeping for the last batch: number of kernel launches
+ * (no synchronisation when pyramid_ms and pyramid_bytes are NULL) and the
+ * measured time of the octave (pyramid + extrema) kernels, with the
+ * algorithmic HBM bytes they moved (waits for enqueued work). */
 int cdvz_gpu_kernel_stats(cdvz_gpu_ctx* ctx, int* launches, double* pyramid_ms, double* pyramid_bytes);
 
 /* Stage-level results of frame `frame` of the last batch for parity tests,
@@ -133,6 +172,8 @@ int cdvz_gpu_kernel_stats(cdvz_gpu_ctx* ctx, int* launches, double* pyramid_ms, 
  *   "oriented"     keypoint layout + theta
  *   "descriptors"  128 per oriented point
  *   "x" "gamma" "gm" "gv"  SCFV matrices (row-major)
+ *   "norms"        SCFVDescriptor::norms: scfv_delta of each selected
+ *                  component, ascending component order (scfv.cpp:240-251)
  *   "gauss:<o>:<k>" octave o, level k raster
  * *n receives the element count; nothing is copied when cap is too small. */
 int cdvz_gpu_debug_get(cdvz_gpu_ctx* ctx, const char* name, int frame, double* dst, size_t cap, size_t* n);
@@ -143,7 +184,9 @@ int cdvz_gpu_debug_get(cdvz_gpu_ctx* ctx, const char* name, int frame, double* d
  * exact FP64 test (used to prove the screen never drops a candidate). Bit 2
  * runs a batch's kernels on one stream, unoverlapped, so per-kernel event
  * times are standalone (bench.py's roofline measurement). Bit 3 disables the
- * TMA tile loads of the extrema kernel (plain loads instead; parity tests). */
+ * TMA tile loads of the extrema kernel (plain loads instead; parity tests).
+ * Bit 5 plans tiny list capacities so ordinary frames overflow them and take
+ * the host path's capacity retry (tests of that path). */
 int cdvz_gpu_set_debug(cdvz_gpu_ctx* ctx, int on);
 
 /* CUDA events on the context's stream (slots 0..3), for callers timing the

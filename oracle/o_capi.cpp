@@ -127,6 +127,35 @@ int orc_encode_rgb(const char* bundle_text, size_t len, const uint8_t* rgb, int 
   });
 }
 
+// synth_image(seed, w, h) as doubles (the unquantised GrayImage).
+int orc_synth_f64(uint64_t seed, int w, int h, double* out) {
+  return guarded([&] {
+    const Plane p = synth_image(seed, w, h);
+    std::memcpy(out, p.px.data(), sizeof(double) * p.px.size());
+  });
+}
+
+// encode_image on an f64 GrayImage (validate() included) -> container bytes;
+// norms (optional, cap nc) receives SCFVDescriptor::norms, *n_norms its size.
+int orc_encode_f64(const char* bundle_text, size_t len, const double* px, int w, int h, int mode_id, int max_side,
+                   uint8_t* out, size_t cap, size_t* out_len, double* norms, size_t norms_cap, size_t* n_norms) {
+  return guarded([&] {
+    const ModelBundle b = parse_model(std::string(bundle_text, len));
+    Plane img;
+    img.w = w;
+    img.h = h;
+    img.px.assign(px, px + std::size_t(w) * h);
+    const EncodedImage e = encode_image(img, b, mode_by_id(mode_id), max_side, nullptr);
+    const auto bytes = serialize_container(e);
+    *out_len = bytes.size();
+    if (cap < bytes.size()) throw DataError("output buffer too small");
+    std::memcpy(out, bytes.data(), bytes.size());
+    if (n_norms) *n_norms = e.global_desc.norms.size();
+    if (norms && norms_cap >= e.global_desc.norms.size())
+      std::memcpy(norms, e.global_desc.norms.data(), sizeof(double) * e.global_desc.norms.size());
+  });
+}
+
 // The grey plane load_image makes of RGB bytes (image.cpp:82-86).
 int orc_grey_rgb(const uint8_t* rgb, int w, int h, size_t stride, double* out) {
   return guarded([&] {

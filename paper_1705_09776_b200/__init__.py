@@ -91,6 +91,10 @@ def _lib() -> ctypes.CDLL:
     P, S, I, U32, U64 = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_uint32, ctypes.c_uint64
     sig = {
         "cdvz_gpu_create": (I, [ctypes.c_char_p, S, I, I, ctypes.POINTER(P)]),
+        "cdvz_gpu_create_multi": (I, [ctypes.c_char_p, S, P, I, I, ctypes.POINTER(P)]),
+        "cdvz_gpu_device_count": (I, [P, P, I]),
+        "cdvz_gpu_visible_devices": (I, []),
+        "cdvz_gpu_encode_batch_f64": (I, [P, P, I, I, S, I, I, I, P, S, P, P]),
         "cdvz_gpu_destroy": (None, [P]),
         "cdvz_gpu_last_error": (ctypes.c_char_p, [P]),
         "cdvz_gpu_bundle_check": (I, [ctypes.c_char_p, S, ctypes.POINTER(U32), ctypes.POINTER(I)]),
@@ -139,6 +143,11 @@ def _raise(code: int, msg: str) -> None:
     if code == 2:
         raise DataError(msg)
     raise InternalError(msg)
+
+
+def device_count() -> int:
+    """Number of visible CUDA devices (0 without a GPU)."""
+    return int(_lib().cdvz_gpu_visible_devices())
 
 
 def bundle_check(bundle_text: str) -> tuple:
@@ -214,13 +223,23 @@ def parse_pnm(data: bytes):
 
 class Extractor:
     """One GPU context holding a model bundle: the reference's
-    ``encode_image(img, bundle, mode)`` for batches of 8-bit frames."""
+    ``encode_image(img, bundle, mode)`` for batches of frames (8-bit grey or
+    RGB rasters, or the reference's own f64 GrayImage values).
 
-    def __init__(self, bundle_text: str, device: int = 0, max_batch: int = 256):
+    ``devices``: a list of device indices makes a multi-device context
+    (``cdvz_gpu_create_multi``): host batches are frame-sharded across the
+    devices, one host thread each, and gathered in frame order."""
+
+    def __init__(self, bundle_text: str, device: int = 0, max_batch: int = 256, devices: Optional[Sequence[int]] = None):
         self._lib = _lib()
         raw = bundle_text.encode() if isinstance(bundle_text, str) else bytes(bundle_text)
         ctx = ctypes.c_void_p()
-        code = self._lib.cdvz_gpu_create(raw, len(raw), device, max_batch, ctypes.byref(ctx))
+        if devices is not None:
+            devs = np.ascontiguousarray(np.asarray(list(devices), dtype=np.int32))
+            code = self._lib.cdvz_gpu_create_multi(raw, len(raw), devs.ctypes.data, len(devs), max_batch, ctypes.byref(ctx))
+            device = int(devs[0]) if len(devs) else device
+        else:
+            code = self._lib.cdvz_gpu_create(raw, len(raw), device, max_batch, ctypes.byref(ctx))
         _raise(code, self._lib.cdvz_gpu_last_error(None).decode())
         self._ctx = ctx.value
         crc, nc, sel = ctypes.c_uint32(), ctypes.c_int(), ctypes.c_int()
@@ -228,6 +247,9 @@ class Extractor:
         self.model_crc, self.components, self.select_n = crc.value, nc.value, sel.value
         self.device = device
         self.max_batch = max_batch
+        devs = (ctypes.c_int * 64)()
+        n = self._lib.cdvz_gpu_device_count(self._ctx, devs, 64)
+        self.devices = [int(devs[i]) for i in range(min(n, 64))]
 
     # -- plumbing
     def _check(self, code: int) -> None:
@@ -247,24 +269,30 @@ class Extractor:
 
     # -- reference API
     def encode_batch(self, frames: np.ndarray, mode, max_side: int = 640):
-        """Encodes ``frames`` (uint8, [N, H, W] grey, or [N, H, W, 3] RGB as in a
-        PPM) and returns (containers, status): ``containers[i]`` is frame i's
-        CDVZ1 byte string (b"" on failure)."""
+        """Encodes ``frames`` and returns (containers, status):
+        ``containers[i]`` is frame i's CDVZ1 byte string (b"" on failure).
+        uint8 [N, H, W] grey (PGM bytes, read as b/255) or [N, H, W, 3] RGB (as
+        in a PPM); float64 [N, H, W] grey values in [0, 1] (the reference's
+        GrayImage, validated per frame like validate())."""
         m = mode if isinstance(mode, ModeSpec) else (mode_by_name(mode) if isinstance(mode, str) else mode_by_id(mode))
-        frames = np.ascontiguousarray(frames, dtype=np.uint8)
+        f64 = np.asarray(frames).dtype == np.float64
+        frames = np.ascontiguousarray(frames, dtype=np.float64 if f64 else np.uint8)
         if frames.ndim == 2:
             frames = frames[None]
         rgb = frames.ndim == 4
-        if frames.ndim not in (3, 4) or (rgb and frames.shape[-1] != 3):
-            raise UsageError("frames must be [N, H, W] or [N, H, W, 3] uint8")
+        if frames.ndim not in (3, 4) or (rgb and (frames.shape[-1] != 3 or f64)):
+            raise UsageError("frames must be [N, H, W] or [N, H, W, 3] uint8, or [N, H, W] float64")
         n, h, w = frames.shape[:3]
         ch = 3 if rgb else 1
         slot = m.budget_bytes + 28
         out = np.empty(max(1, n * slot), dtype=np.uint8)
         offsets = np.zeros(n + 1, dtype=np.uint64)
         status = np.zeros(max(1, n), dtype=np.int32)
-        fn = self._lib.cdvz_gpu_encode_batch_rgb if rgb else self._lib.cdvz_gpu_encode_batch
-        self._check(fn(self._ctx, frames.ctypes.data, w, h, w * ch, n, m.id, max_side, out.ctypes.data, out.nbytes,
+        if f64:
+            fn, stride = self._lib.cdvz_gpu_encode_batch_f64, w
+        else:
+            fn, stride = (self._lib.cdvz_gpu_encode_batch_rgb if rgb else self._lib.cdvz_gpu_encode_batch), w * ch
+        self._check(fn(self._ctx, frames.ctypes.data, w, h, stride, n, m.id, max_side, out.ctypes.data, out.nbytes,
                        offsets.ctypes.data, status.ctypes.data))
         res = [out[int(offsets[i]):int(offsets[i + 1])].tobytes() for i in range(n)]
         return res, status[:n].copy()
@@ -283,6 +311,8 @@ class Extractor:
     def encode_image(self, frame: np.ndarray, mode, max_side: int = 640) -> bytes:
         """encode_image + serialize_container for one frame; raises on failure."""
         res, status = self.encode_batch(np.asarray(frame)[None], mode, max_side)
+        if status[0] == 2:
+            raise DataError("image values must be finite and in [0, 1]")
         if status[0] != 0:
             _raise(int(status[0]), self._lib.cdvz_gpu_last_error(self._ctx).decode() or "frame failed")
         return res[0]
@@ -312,13 +342,14 @@ class Extractor:
         return {"launches": n.value, "pyramid_ms": ms.value, "pyramid_bytes": by.value}
 
     def set_debug(self, on: bool = True, exact_only: bool = False, serial: bool = False, no_tma: bool = False,
-                  tile_detect: bool = False) -> None:
+                  tile_detect: bool = False, tiny_caps: bool = False) -> None:
         """on: keep per-octave lists; exact_only: bypass the FP32 extrema screen;
         serial: no kernel overlap (standalone per-kernel timing); tile_detect:
         the first-generation TMA tile extrema kernel instead of the column walk
-        (a cross-check); no_tma: that tile kernel with plain loads."""
+        (a cross-check); no_tma: that tile kernel with plain loads; tiny_caps:
+        tiny list capacities, so frames take the capacity retry."""
         flags = ((1 if on else 0) | (2 if exact_only else 0) | (4 if serial else 0) | (8 if no_tma else 0)
-                 | (16 if tile_detect else 0))
+                 | (16 if tile_detect else 0) | (32 if tiny_caps else 0))
         self._check(self._lib.cdvz_gpu_set_debug(self._ctx, flags))
 
     def debug_get(self, name: str, frame: int) -> np.ndarray:
@@ -471,5 +502,5 @@ def parse_container_header(data: bytes) -> dict:
 
 __all__ = [
     "Extractor", "ModeSpec", "MODES", "mode_by_name", "mode_by_id", "UsageError", "DataError", "InternalError",
-    "bundle_check", "container_slot", "parse_container_header", "library_path", "Index",
+    "bundle_check", "container_slot", "device_count", "parse_container_header", "library_path", "Index",
 ]

@@ -373,7 +373,9 @@ Bundle parse_bundle(const std::string& text) {
     b.taps[k] = gaussian_taps(b.sigmas[std::size_t(k)]);
     b.radius[k] = int(b.taps[k].size() / 2);
   }
-  if (b.radius[3] > 16) throw UsageError("detector scales above sigma 5.33 are not supported by the GPU kernels");
+  // The blur kernels are instantiated for radii up to 8 (setup_model): one limit for
+  // cdvz_gpu_bundle_check and cdvz_gpu_create alike.
+  if (b.radius[3] > 8) throw UsageError("detector scales above sigma 2.66 (Gaussian radius > 8) are not supported by the GPU kernels");
   b.margin = static_cast<int>(std::ceil(3.0 * b.sigmas[3])) + 2;
   b.rho_limit = (b.edge_r + 1.0) * (b.edge_r + 1.0) / b.edge_r;
   const std::string canon = serialize_bundle(b);

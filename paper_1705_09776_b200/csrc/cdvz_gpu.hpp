@@ -6,20 +6,25 @@
 //   reference                                        this shim
 //   ModelBundle load_model(path)                     cdvz::gpu::ModelBundle::load(path)
 //   const ModeSpec& mode_by_name(name)               cdvz::gpu::mode_by_name(name)
-//   EncodedImage encode_image(img, bundle, mode,     std::vector<uint8_t> cdvz::gpu::encode_image(
-//       Engine, StageTimings*, EncodeOptions)            img, bundle, mode, timings, opts)
-//   serialize_container(enc)                         (returned directly: CDVZ1 bytes)
+//   EncodedImage encode_image(img, bundle, mode,     EncodedImage cdvz::gpu::encode_image(
+//       Engine, StageTimings*, EncodeOptions)            img, bundle, mode, Engine, StageTimings*, EncodeOptions)
+//                                                    (GrayImage of doubles, the same signature)
+//   serialize_container(enc) / parse_container(b)    cdvz::gpu::serialize_container / parse_container
+//   (8-bit / PGM / PPM / batch fast paths)           encode_image(GrayImage8 | PnmImage, ...) -> CDVZ1 bytes,
+//                                                    encode_batch(frames, ...) over one or several GPUs
 //   RankedList retrieve(query, id, index, opts)      cdvz::gpu::retrieve({(id, bytes)...}, Index, opts)
 //   MatchResult match_pair(a, b, opts)               cdvz::gpu::match_pair(a_bytes, Index, item, opts)
 //
-// Images are 8-bit grey rasters (the byte/255 semantics of load_image,
+// GrayImage holds the reference's doubles in [0, 1] (image.hpp:11-18); the
+// byte fast paths take 8-bit rasters read as b/255 (load_image,
 // image.cpp:79-87). Errors keep the reference's exception types: UsageError
 // (bad mode name), DataError (bad raster / bundle), std::runtime_error for
 // device failures (the CLI's exit code 3). The Engine argument has no GPU
-// meaning (results never depend on it, parallel.hpp:16-18) and is dropped.
+// meaning (results never depend on it, parallel.hpp:16-18) and is ignored.
 #pragma once
 
 #include <algorithm>
+#include <cstdint>
 #include <fstream>
 #include <iterator>
 #include <map>
@@ -83,6 +88,200 @@ struct EncodeOptions {  // pipeline.hpp:14-16
   int max_side = 640;
 };
 
+struct Engine {  // parallel.hpp:19-23 — accepted for signature parity; the GPU's results never depend on it
+  int workers = 0;
+  int tile_size = 32;
+};
+
+struct GrayImage {  // image.hpp:14-18: row-major doubles in [0, 1], rows = height
+  int w = 0, h = 0;
+  std::vector<double> pix;
+  int width() const { return w; }
+  int height() const { return h; }
+  double& operator()(int y, int x) { return pix[std::size_t(y) * std::size_t(w) + std::size_t(x)]; }
+  double operator()(int y, int x) const { return pix[std::size_t(y) * std::size_t(w) + std::size_t(x)]; }
+};
+
+inline GrayImage make_image(int width, int height, double fill = 0.0) {  // image.cpp:40-44
+  GrayImage img;
+  img.w = width;
+  img.h = height;
+  img.pix.assign(std::size_t(std::max(0, width)) * std::size_t(std::max(0, height)), fill);
+  return img;
+}
+
+struct TernaryCode {  // transform_coding.hpp:56-62
+  std::uint16_t xq = 0, yq = 0;
+  std::uint8_t sigma_q = 0;
+  std::uint8_t theta_q = 0;
+  std::uint8_t mode = 0;
+  std::vector<std::int8_t> symbols;
+};
+
+struct SCFVDescriptor {  // scfv.hpp:30-40
+  int n_components = 0;
+  bool has_variance = false;
+  std::vector<std::uint8_t> mask;
+  std::vector<std::uint32_t> mean_planes;
+  std::vector<std::uint32_t> var_planes;
+  std::vector<double> norms;  // scfv_delta of each selected component (not serialized)
+  bool selected(int c) const { return (mask[std::size_t(c / 8)] >> (c % 8)) & 1u; }
+  int popcount() const {
+    int n = 0;
+    for (auto b : mask) n += __builtin_popcount(b);
+    return n;
+  }
+};
+
+struct EncodedImage {  // container.hpp:19-25
+  int mode_id = 0;
+  int width = 0, height = 0;
+  std::uint32_t model_crc = 0;
+  SCFVDescriptor global_desc;
+  std::vector<TernaryCode> codes;
+};
+
+namespace detail {
+inline std::uint32_t crc32(const std::uint8_t* p, std::size_t n) {  // common.cpp:11-35
+  static const auto table = [] {
+    std::vector<std::uint32_t> t(256);
+    for (std::uint32_t i = 0; i < 256; ++i) {
+      std::uint32_t c = i;
+      for (int k = 0; k < 8; ++k) c = (c & 1u) ? 0xEDB88320u ^ (c >> 1) : c >> 1;
+      t[i] = c;
+    }
+    return t;
+  }();
+  std::uint32_t c = 0xFFFFFFFFu;
+  for (std::size_t i = 0; i < n; ++i) c = table[(c ^ p[i]) & 0xFFu] ^ (c >> 8);
+  return c ^ 0xFFFFFFFFu;
+}
+inline void put16(std::vector<std::uint8_t>& o, std::uint32_t v) {
+  o.push_back(std::uint8_t(v & 0xFF));
+  o.push_back(std::uint8_t((v >> 8) & 0xFF));
+}
+inline void put32(std::vector<std::uint8_t>& o, std::uint32_t v) {
+  put16(o, v & 0xFFFF);
+  put16(o, v >> 16);
+}
+inline std::uint32_t get16(const std::vector<std::uint8_t>& b, std::size_t o) { return b[o] | (std::uint32_t(b[o + 1]) << 8); }
+inline std::uint32_t get32(const std::vector<std::uint8_t>& b, std::size_t o) { return get16(b, o) | (get16(b, o + 2) << 16); }
+}  // namespace detail
+
+// serialize_container (container.cpp:32-58) with serialize_scfv
+// (scfv.cpp:285-298) and pack_local (transform_coding.cpp:232-270).
+inline std::vector<std::uint8_t> serialize_container(const EncodedImage& enc) {
+  const ModeSpec& mode = mode_by_id(enc.mode_id);
+  std::vector<std::uint8_t> global(enc.global_desc.mask);
+  for (std::size_t r = 0; r < enc.global_desc.mean_planes.size(); ++r) {
+    detail::put32(global, enc.global_desc.mean_planes[r]);
+    if (enc.global_desc.has_variance) detail::put32(global, enc.global_desc.var_planes[r]);
+  }
+  if (enc.codes.size() > 0xFFFF) throw DataError("too many codes for one local block");
+  std::vector<std::uint8_t> local{std::uint8_t(mode.id), std::uint8_t(mode.elements)};
+  detail::put16(local, std::uint32_t(enc.codes.size()));
+  for (const auto& c : enc.codes) {
+    if (c.mode != mode.id) throw DataError("code mode does not match block mode");
+    if (c.symbols.size() != std::size_t(mode.elements)) throw DataError("code symbol count does not match block mode");
+    detail::put16(local, c.xq);
+    detail::put16(local, c.yq);
+    local.push_back(c.sigma_q);
+    local.push_back(c.theta_q);
+    std::uint8_t packed = 0;
+    int filled = 0;
+    for (std::int8_t sym : c.symbols) {
+      if (sym < -1 || sym > 1) throw DataError("symbol outside {-1, 0, +1}");
+      packed |= std::uint8_t((sym == 0 ? 0 : sym == 1 ? 1 : 2) << (2 * filled));
+      if (++filled == 4) {
+        local.push_back(packed);
+        packed = 0;
+        filled = 0;
+      }
+    }
+    if (filled > 0) local.push_back(packed);
+  }
+  if (global.size() + local.size() > mode.budget_bytes) throw DataError("encoded payload exceeds the mode budget");
+  if (enc.width < 1 || enc.width > 0xFFFF || enc.height < 1 || enc.height > 0xFFFF)
+    throw DataError("image dimensions do not fit the container header");
+  if (enc.global_desc.n_components < 1 || enc.global_desc.n_components > 0xFFFF)
+    throw DataError("component count does not fit the container header");
+  std::vector<std::uint8_t> out{'C', 'D', 'V', 'Z', '1', std::uint8_t(enc.mode_id)};
+  detail::put16(out, std::uint32_t(enc.width));
+  detail::put16(out, std::uint32_t(enc.height));
+  detail::put16(out, std::uint32_t(enc.global_desc.n_components));
+  detail::put32(out, enc.model_crc);
+  detail::put32(out, std::uint32_t(global.size()));
+  detail::put32(out, std::uint32_t(local.size()));
+  out.insert(out.end(), global.begin(), global.end());
+  out.insert(out.end(), local.begin(), local.end());
+  detail::put32(out, detail::crc32(out.data(), out.size()));
+  return out;
+}
+
+// parse_container (container.cpp:60-93) with parse_scfv (scfv.cpp:300-326)
+// and unpack_local (transform_coding.cpp:272-305), the same checks.
+inline EncodedImage parse_container(const std::vector<std::uint8_t>& bytes) {
+  if (bytes.size() < 28) throw DataError("container truncated");
+  static const char magic[5] = {'C', 'D', 'V', 'Z', '1'};
+  for (int i = 0; i < 5; ++i)
+    if (bytes[std::size_t(i)] != std::uint8_t(magic[i])) throw DataError("container magic mismatch");
+  const std::size_t body = bytes.size() - 4;
+  if (detail::crc32(bytes.data(), body) != detail::get32(bytes, body)) throw DataError("container checksum mismatch");
+  EncodedImage enc;
+  enc.mode_id = bytes[5];
+  const ModeSpec& mode = mode_by_id(enc.mode_id);
+  enc.width = int(detail::get16(bytes, 6));
+  enc.height = int(detail::get16(bytes, 8));
+  const int nc = int(detail::get16(bytes, 10));
+  enc.model_crc = detail::get32(bytes, 12);
+  const std::size_t glen = detail::get32(bytes, 16), llen = detail::get32(bytes, 20);
+  if (24 + glen + llen != body) throw DataError("container section lengths disagree with its size");
+  SCFVDescriptor& d = enc.global_desc;
+  d.n_components = nc;
+  d.has_variance = mode.variance_planes;
+  const std::size_t mask_bytes = std::size_t((nc + 7) / 8);
+  if (glen < mask_bytes) throw DataError("global descriptor block truncated");
+  d.mask.assign(bytes.begin() + 24, bytes.begin() + 24 + long(mask_bytes));
+  const int sel = d.popcount();
+  if (glen != mask_bytes + std::size_t(sel) * (d.has_variance ? 8 : 4))
+    throw DataError("global descriptor length does not match its mask");
+  std::size_t off = 24 + mask_bytes;
+  for (int r = 0; r < sel; ++r) {
+    d.mean_planes.push_back(detail::get32(bytes, off));
+    off += 4;
+    if (d.has_variance) {
+      d.var_planes.push_back(detail::get32(bytes, off));
+      off += 4;
+    }
+  }
+  const std::size_t lb = 24 + glen;
+  if (llen < 4) throw DataError("local block truncated");
+  const int lmode = bytes[lb], elements = bytes[lb + 1];
+  const std::size_t count = detail::get16(bytes, lb + 2);
+  if (lmode > 5) throw DataError("local block has an unknown mode id");
+  if (elements < 1 || elements > 128) throw DataError("local block has an invalid element count");
+  const std::size_t per = 6 + (std::size_t(elements) * 2 + 7) / 8;
+  if (llen != 4 + count * per) throw DataError("local block length does not match its header");
+  off = lb + 4;
+  enc.codes.resize(count);
+  for (auto& c : enc.codes) {
+    c.mode = std::uint8_t(lmode);
+    c.xq = std::uint16_t(detail::get16(bytes, off));
+    c.yq = std::uint16_t(detail::get16(bytes, off + 2));
+    c.sigma_q = bytes[off + 4];
+    c.theta_q = bytes[off + 5];
+    off += 6;
+    c.symbols.resize(std::size_t(elements));
+    for (int i = 0; i < elements; ++i) {
+      const unsigned bits = (bytes[off + std::size_t(i / 4)] >> (2 * (i % 4))) & 3u;
+      if (bits == 3) throw DataError("reserved symbol pattern in local block");
+      c.symbols[std::size_t(i)] = std::int8_t(bits == 0 ? 0 : bits == 1 ? 1 : -1);
+    }
+    off += (std::size_t(elements) * 2 + 7) / 8;
+  }
+  return enc;
+}
+
 class StageTimings {  // parallel.hpp:117-134: device ms per label
  public:
   struct Entry { std::string stage; long long calls = 0; double total_ms = 0.0; };
@@ -126,18 +325,67 @@ class ModelBundle {
     ctx_[device] = std::shared_ptr<cdvz_gpu_ctx>(c, cdvz_gpu_destroy);
     return c;
   }
+  // A frame-sharded context over several devices (cdvz_gpu_create_multi).
+  cdvz_gpu_ctx* context(const std::vector<int>& devices, int max_batch = 256) const {
+    if (devices.size() == 1) return context(devices[0], max_batch);
+    auto it = multi_.find(devices);
+    if (it != multi_.end()) return it->second.get();
+    cdvz_gpu_ctx* c = nullptr;
+    raise_for(cdvz_gpu_create_multi(text_.data(), text_.size(), devices.data(), int(devices.size()), max_batch, &c),
+              cdvz_gpu_last_error(nullptr));
+    multi_[devices] = std::shared_ptr<cdvz_gpu_ctx>(c, cdvz_gpu_destroy);
+    return c;
+  }
  private:
   std::string text_;
   uint32_t crc_ = 0;
   int components_ = 0;
   mutable std::map<int, std::shared_ptr<cdvz_gpu_ctx>> ctx_;
+  mutable std::map<std::vector<int>, std::shared_ptr<cdvz_gpu_ctx>> multi_;
 };
 
-// Batch encode: frames of one size -> CDVZ1 containers in frame order.
+inline void add_timings(cdvz_gpu_ctx* ctx, StageTimings* timings) {
+  if (!timings) return;
+  double ms[5];
+  raise_for(cdvz_gpu_stage_times(ctx, ms), cdvz_gpu_last_error(ctx));
+  const char* labels[5] = {"detection", "selection", "description", "compression", "aggregation"};
+  for (int i = 0; i < 5; ++i) timings->add(labels[i], ms[i]);
+}
+
+// encode_image (pipeline.cpp:54-97) with the reference's signature: a
+// GrayImage of doubles in, the EncodedImage out (its bytes are the GPU's
+// container, decoded; norms come from the device's scfv_delta values).
+inline EncodedImage encode_image(const GrayImage& img, const ModelBundle& bundle, const ModeSpec& mode,
+                                 const Engine& eng = {}, StageTimings* timings = nullptr,
+                                 const EncodeOptions& opts = {}) {
+  (void)eng;
+  if (img.pix.size() != std::size_t(std::max(0, img.w)) * std::size_t(std::max(0, img.h)))
+    throw DataError("image raster size does not match its dimensions");
+  cdvz_gpu_ctx* ctx = bundle.context(0);
+  std::vector<uint8_t> buf(cdvz_gpu_container_slot(mode.id));
+  std::size_t offsets[2] = {0, 0};
+  int status = 0;
+  raise_for(cdvz_gpu_encode_batch_f64(ctx, img.pix.data(), img.w, img.h, std::size_t(img.w), 1, mode.id, opts.max_side,
+                                      buf.data(), buf.size(), offsets, &status),
+            cdvz_gpu_last_error(ctx));
+  if (status == CDVZ_GPU_DATA) throw DataError("image values must be finite and in [0, 1]");
+  raise_for(status, "frame failed on the device");
+  buf.resize(offsets[1]);
+  EncodedImage enc = parse_container(buf);
+  std::size_t n = 0;
+  raise_for(cdvz_gpu_debug_get(ctx, "norms", 0, nullptr, 0, &n), cdvz_gpu_last_error(ctx));
+  enc.global_desc.norms.resize(n);
+  raise_for(cdvz_gpu_debug_get(ctx, "norms", 0, enc.global_desc.norms.data(), n, &n), cdvz_gpu_last_error(ctx));
+  add_timings(ctx, timings);
+  return enc;
+}
+
+// Batch encode: frames of one size -> CDVZ1 containers in frame order, on one
+// device or frame-sharded over several (`devices`).
 inline std::vector<std::vector<uint8_t>> encode_batch(const std::vector<const GrayImage8*>& frames,
                                                       const ModelBundle& bundle, const ModeSpec& mode,
-                                                      StageTimings* timings = nullptr, const EncodeOptions& opts = {},
-                                                      int device = 0) {
+                                                      StageTimings* timings, const EncodeOptions& opts,
+                                                      const std::vector<int>& devices) {
   std::vector<std::vector<uint8_t>> out(frames.size());
   if (frames.empty()) return out;
   const int w = frames[0]->width, h = frames[0]->height;
@@ -146,7 +394,7 @@ inline std::vector<std::vector<uint8_t>> encode_batch(const std::vector<const Gr
     if (frames[i]->width != w || frames[i]->height != h) throw UsageError("frames of one batch must share a size");
     std::copy(frames[i]->pix.begin(), frames[i]->pix.end(), pix.begin() + long(i) * w * h);
   }
-  cdvz_gpu_ctx* ctx = bundle.context(device);
+  cdvz_gpu_ctx* ctx = bundle.context(devices);
   const std::size_t slot = cdvz_gpu_container_slot(mode.id);
   std::vector<uint8_t> buf(slot * frames.size());
   std::vector<std::size_t> offsets(frames.size() + 1);
@@ -158,13 +406,15 @@ inline std::vector<std::vector<uint8_t>> encode_batch(const std::vector<const Gr
     raise_for(status[i], "frame failed on the device");
     out[i].assign(buf.begin() + long(offsets[i]), buf.begin() + long(offsets[i + 1]));
   }
-  if (timings) {
-    double ms[5];
-    cdvz_gpu_stage_times(ctx, ms);
-    const char* labels[5] = {"detection", "selection", "description", "compression", "aggregation"};
-    for (int i = 0; i < 5; ++i) timings->add(labels[i], ms[i]);
-  }
+  add_timings(ctx, timings);
   return out;
+}
+
+inline std::vector<std::vector<uint8_t>> encode_batch(const std::vector<const GrayImage8*>& frames,
+                                                      const ModelBundle& bundle, const ModeSpec& mode,
+                                                      StageTimings* timings = nullptr, const EncodeOptions& opts = {},
+                                                      int device = 0) {
+  return encode_batch(frames, bundle, mode, timings, opts, std::vector<int>{device});
 }
 
 // encode_image + serialize_container (pipeline.cpp:54-97, container.cpp:32-58).

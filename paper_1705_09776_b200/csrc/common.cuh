@@ -105,6 +105,7 @@ struct Batch {
   uint8_t* mask;                       // [frame][mask_bytes] (selected components)
   uint32_t* mean_planes;               // [frame][nc] by component index
   uint32_t* var_planes;                // [frame][nc]
+  double* norms;                       // [frame][nc] scfv_delta of every component (SCFVDescriptor::norms)
 };
 
 // Model tables in global memory.

@@ -12,10 +12,12 @@
 #include <cmath>
 #include <cstring>
 #include <functional>
+#include <map>
 #include <memory>
 #include <random>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include <cuda.h>
@@ -38,6 +40,7 @@ cudaError_t launch_resize_f64(const double* grey, int w_in, int h_in, double* ou
                               cudaStream_t st);
 cudaError_t launch_grey_rgb(const uint8_t* rgb, long long stride, long long frame_bytes, int w, int h, double* out,
                             int frames, cudaStream_t st);
+cudaError_t launch_validate_f64(double* pix, int w, int h, int frames, int* status, cudaStream_t st);
 cudaError_t launch_resize(const uint8_t* pix, long long stride, long long frame_bytes, int w_in, int h_in, double* out,
                           int w_out, int h_out, int frames, cudaStream_t st);
 struct SynthParams {
@@ -113,8 +116,11 @@ struct Lane {
   CUtensorMap tmap[kMaxOctaves];   // 4-D view (x, y, level, frame) of each octave's G planes
   bool tmap_ok[kMaxOctaves] = {};
   bool pending = false;   // events of an enqueued chunk not yet folded into the stats
+  long long pending_call = 0;  // the call that enqueued it
   int pending_oct = 0;
   double pending_bytes = 0.0;
+  bool geo_boost = false;      // planned with the maximal capacities (capacity retry)
+  bool geo_tiny = false;
 
   void init() {
     CDVZ_CUDA_CHECK(cudaStreamCreateWithFlags(&sA, cudaStreamNonBlocking));
@@ -130,6 +136,7 @@ struct Lane {
     bufs.clear();
     dbg_oct.release();
     geo_w = geo_h = geo_frames = 0;
+    geo_boost = false;
   }
   void destroy() {
     release();
@@ -159,6 +166,11 @@ struct cdvz_gpu_ctx {
   bool debug = false;
   bool serial = false;
   bool tma_disabled = false;
+  bool cap_boost = false;  // plan the maximal survivor / orientation capacities (capacity retry of single frames)
+  bool tiny_caps = false;  // debug bit 5: tiny batch capacities, so ordinary frames exercise the capacity retry
+  // A multi-device context (cdvz_gpu_create_multi) owns one single-device
+  // context per device and shards host batches across them.
+  std::vector<std::unique_ptr<cdvz_gpu_ctx>> shards;
 
   static constexpr int kLanes = 2;  // chunks in flight (each lane: its own streams and batch buffers; 4 measured no faster)
   Lane lanes[kLanes];
@@ -166,6 +178,7 @@ struct cdvz_gpu_ctx {
   DeviceBuffer stage_in, stage_out, stage_len;
   uint8_t* pin_out = nullptr;    // pinned container slots (D2H target)
   uint32_t* pin_len = nullptr;
+  int* pin_status = nullptr;     // per-frame device status (2 data error, 4 capacity, 8 unsupported scale)
   size_t pin_out_bytes = 0, pin_len_count = 0;
 
   void ensure_pinned_out(size_t bytes, size_t count) {
@@ -177,8 +190,11 @@ struct cdvz_gpu_ctx {
     }
     if (count > pin_len_count) {
       if (pin_len) cudaFreeHost(pin_len);
+      if (pin_status) cudaFreeHost(pin_status);
       pin_len = nullptr;
+      pin_status = nullptr;
       CDVZ_CUDA_CHECK(cudaMallocHost(&pin_len, count * sizeof(uint32_t)));
+      CDVZ_CUDA_CHECK(cudaMallocHost(&pin_status, count * sizeof(int)));
       pin_len_count = count;
     }
   }
@@ -187,9 +203,19 @@ struct cdvz_gpu_ctx {
   cudaEvent_t ev[6] = {};
   cudaEvent_t user_ev[4] = {};
   cudaEvent_t evp[2 * kMaxOctaves] = {};
-  double stage_ms[5] = {0, 0, 0, 0, 0};
-  double pyr_ms = 0.0, pyr_bytes = 0.0;
-  int launches = 0;
+  // Statistics are folded from each chunk's events lazily (when its lane is
+  // reused, or when a caller asks for them), so encode_device returns as soon
+  // as its work is enqueued. `stats` is the last call whose chunks have all
+  // been folded; `open` holds calls with chunks still pending.
+  struct Stats {
+    double stage_ms[5] = {0, 0, 0, 0, 0};
+    double pyr_ms = 0.0, pyr_bytes = 0.0;
+    int chunks = 0;  // chunks not yet folded
+  };
+  long long call_seq = 0, stats_call = -1;
+  std::map<long long, Stats> open;
+  Stats stats;
+  int launches = 0;  // kernel launches of the last enqueued call (host-side count)
 
   ~cdvz_gpu_ctx() {
     for (auto& b : model_bufs) b.release();
@@ -199,6 +225,7 @@ struct cdvz_gpu_ctx {
     stage_len.release();
     if (pin_out) cudaFreeHost(pin_out);
     if (pin_len) cudaFreeHost(pin_len);
+    if (pin_status) cudaFreeHost(pin_status);
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
     for (auto& e : evp)
@@ -307,7 +334,7 @@ struct cdvz_gpu_ctx {
   // original-size grey plane per frame (RGB frames that are also resized), or 0.
   void plan(Lane& L, int W, int H, int frames, bool need_resize, long long grey_px = 0) {
     if (W == L.geo_w && H == L.geo_h && frames <= L.geo_frames && (!need_resize || L.geo_resize) && L.geo_debug == debug &&
-        grey_px * frames <= L.geo_grey)
+        grey_px * frames <= L.geo_grey && L.geo_boost == cap_boost && L.geo_tiny == tiny_caps)
       return;
     CDVZ_CUDA_CHECK(cudaStreamSynchronize(L.sA));
     CDVZ_CUDA_CHECK(cudaStreamSynchronize(L.sB));
@@ -328,6 +355,11 @@ struct cdvz_gpu_ctx {
       w /= 2;
       h /= 2;
     }
+    // detect_keypoints would keep halving (scale_space.cpp:304-326): refuse
+    // rather than silently drop octaves the reference computes.
+    if (n_oct == kMaxOctaves && n_oct < bundle.num_octaves && w >= 16 && h >= 16)
+      throw UsageError("the bundle asks for more than " + std::to_string(kMaxOctaves) +
+                       " octaves on a raster this large; the GPU kernels support at most " + std::to_string(kMaxOctaves));
     nb.n_oct = n_oct;
     nb.frame_doubles = std::max<long long>(pd, 1);
     nb.bitmap_words = std::max<long long>(bw, 1);
@@ -337,6 +369,21 @@ struct cdvz_gpu_ctx {
     nb.cap_acc = nb.cap_oct;
     nb.select_n = bundle.select_n;
     nb.cap_or = std::max(64, bundle.select_n * 4);
+    if (tiny_caps && !cap_boost) {
+      nb.cap_oct = nb.cap_acc = 256;
+      nb.cap_or = 64;
+    }
+    if (cap_boost) {
+      // Capacity retry: the largest counts the reference can produce. At most
+      // two candidates per pixel (two roots of the derivative), the
+      // accumulated list is bounded by the sum over octaves, and a point has at
+      // most 36 orientation peaks (one per histogram bin).
+      long long px_sum = 0;
+      for (int o = 0; o < n_oct; ++o) px_sum += (long long)nb.ow[o] * nb.oh[o];
+      nb.cap_oct = int(std::min<long long>(1LL << 28, 2LL * W * H + 64));
+      nb.cap_acc = int(std::min<long long>(1LL << 28, 2LL * px_sum + 64));
+      nb.cap_or = std::max(64, bundle.select_n * 36);
+    }
     nb.code_stride = 40;
     nb.nc = bundle.nc;
     const long long F = frames;
@@ -385,6 +432,7 @@ struct cdvz_gpu_ctx {
     nb.mask = static_cast<uint8_t*>(alloc(F * ((nb.nc + 7) / 8)));
     nb.mean_planes = static_cast<uint32_t*>(alloc(sizeof(uint32_t) * F * nb.nc));
     nb.var_planes = static_cast<uint32_t*>(alloc(sizeof(uint32_t) * F * nb.nc));
+    nb.norms = static_cast<double*>(alloc(sizeof(double) * F * nb.nc));
     CDVZ_CUDA_CHECK(cudaMemset(nb.raw_count, 0, sizeof(int) * F * std::max(1, n_oct)));
     CDVZ_CUDA_CHECK(cudaMemset(nb.bitmap, 0, sizeof(uint32_t) * F * nb.bitmap_words));
     CDVZ_CUDA_CHECK(cudaMemset(nb.acc_count, 0, sizeof(int) * F * 2));
@@ -418,6 +466,8 @@ struct cdvz_gpu_ctx {
     L.geo_resize = need_resize;
     L.geo_grey = grey_px * F;
     L.geo_debug = debug;
+    L.geo_boost = cap_boost;
+    L.geo_tiny = tiny_caps;
   }
 
   EncodeConst encode_const(int mode_id) const {
@@ -437,25 +487,40 @@ struct cdvz_gpu_ctx {
     return ec;
   }
 
-  // Folds a finished chunk's events into the stage / kernel statistics.
+  // Folds a finished chunk's events into its call's statistics (blocks until
+  // the chunk is done). Stage labels follow the reference's time_stage calls
+  // (pipeline.cpp:19-94): detection, selection, description (orientation +
+  // description), compression (transform + ternary + location quantisers,
+  // fused into the description kernel's epilogue: its own event pair), aggregation.
   void collect(Lane& L) {
     if (!L.pending) return;
     CDVZ_CUDA_CHECK(cudaEventSynchronize(L.done));
+    Stats& st_ = open[L.pending_call];
     float t[5];
     cudaEventElapsedTime(&t[0], L.start, L.stage[1]);
     cudaEventElapsedTime(&t[1], L.stage[1], L.stage[2]);
     cudaEventElapsedTime(&t[2], L.stage[2], L.stage[3]);
     cudaEventElapsedTime(&t[3], L.stage[4], L.stage[5]);
     cudaEventElapsedTime(&t[4], L.stage[3], L.stage[4]);
-    for (int i = 0; i < 5; ++i) stage_ms[i] += t[i];
+    for (int i = 0; i < 5; ++i) st_.stage_ms[i] += t[i];
     for (int o = 0; o < L.pending_oct; ++o) {
       float a = 0.f, b = 0.f;
       cudaEventElapsedTime(&a, L.blur[2 * o], L.blur[2 * o + 1]);
       cudaEventElapsedTime(&b, L.det[2 * o], L.det[2 * o + 1]);
-      pyr_ms += a + b;  // kernel time of the pair (they may overlap: conservative)
+      st_.pyr_ms += a + b;  // kernel time of the pair (they may overlap: conservative)
     }
-    pyr_bytes += L.pending_bytes;
+    st_.pyr_bytes += L.pending_bytes;
     L.pending = false;
+    if (--st_.chunks == 0) {
+      if (L.pending_call > stats_call) {
+        stats = st_;
+        stats_call = L.pending_call;
+      }
+      open.erase(L.pending_call);
+    }
+  }
+  void collect_all() {
+    for (auto& l : lanes) collect(l);
   }
 
   // Runs the whole pipeline for `frames` device-resident frames (u8) of size
@@ -465,18 +530,24 @@ struct cdvz_gpu_ctx {
   // With host pointers (h_pix / h_out / h_len), the frames are copied in on a
   // dedicated copy stream ahead of the kernels and each chunk's containers are
   // copied out on its describe stream, overlapping the other lane's kernels.
-  // channels: 1 = grey bytes (PGM), 3 = interleaved RGB bytes (PPM), whose
-  // grey plane is formed on the device first.
+  // kind: 1 = grey bytes (PGM), 3 = interleaved RGB bytes (PPM), whose
+  // grey plane is formed on the device first, 8 = f64 grey values (the
+  // reference's GrayImage), validated on the device; `stride` and `h_stride`
+  // are in bytes. h_status receives each frame's device status bits.
   void run(const uint8_t* d_pix, int w, int h, long long stride, int frames, int mode_id, int max_side, uint8_t* d_out,
            uint32_t* d_len, const uint8_t* h_pix = nullptr, size_t h_stride = 0, uint8_t* h_out = nullptr,
-           uint32_t* h_len = nullptr, int channels = 1,
-           const std::function<void(int, int)>& on_chunk = nullptr) {
+           uint32_t* h_len = nullptr, int kind = 1, const std::function<void(int, int)>& on_chunk = nullptr,
+           int* h_status = nullptr) {
     if (w < 8 || h < 8) throw DataError("image smaller than 8 px per side");
     int W, H;
     prepared_dims(w, h, max_side, W, H);
     const bool resize = (W != w || H != h);
-    const bool rgb = channels == 3;
-    const bool f64_base = resize || rgb;  // octave 0 reads the f64 plane pixf
+    const bool rgb = kind == 3;
+    const bool f64 = kind == 8;
+    const int channels = rgb ? 3 : 1;
+    const size_t elem = f64 ? sizeof(double) : 1;
+    if (f64 && stride != (long long)w * 8) throw UsageError("f64 frames must be packed on the device (stride = 8 * width)");
+    const bool f64_base = resize || rgb || f64;  // octave 0 reads the f64 plane pixf
     EncodeConst ec = encode_const(mode_id);
     ec.cx = (W - 1) / 2.0;
     ec.cy = (H - 1) / 2.0;
@@ -512,18 +583,17 @@ struct cdvz_gpu_ctx {
     while (cb.back() < frames) cb.push_back(std::min(frames, cb.back() + per));
     const int chunks = int(cb.size()) - 1;
     const int n_lanes = serial ? 1 : kLanes;
+    const long long call = ++call_seq;
+    open[call].chunks = chunks;  // folded one by one as lanes are collected
     // Lanes rotate across calls too, so back-to-back asynchronous calls
     // (encode_device) overlap one call's tail with the next call's head.
     const int lane0 = serial ? 0 : next_lane;
     for (int l = 0; l < std::min(chunks, n_lanes); ++l) {
       Lane& L = lanes[(lane0 + l) % kLanes];
       if (!L.sA) L.init();
-      plan(L, W, H, per, f64_base, rgb && resize ? (long long)w * h : 0);
+      plan(L, W, H, per, resize || rgb, rgb && resize ? (long long)w * h : 0);
     }
     launches = 0;
-    pyr_ms = 0.0;
-    pyr_bytes = 0.0;
-    for (double& x : stage_ms) x = 0.0;
     CDVZ_CUDA_CHECK(cudaEventRecord(ev[0], st));  // everything before this call
     // Host frames: every chunk's copy is queued up front on the copy stream
     // (back to back at full link bandwidth); a chunk's kernels wait only for
@@ -539,8 +609,8 @@ struct cdvz_gpu_ctx {
       for (int c = 0; c < chunks; ++c) {
         const int base = cb[size_t(c)], nf = cb[size_t(c) + 1] - base;
         CDVZ_CUDA_CHECK(cudaMemcpy2DAsync(const_cast<uint8_t*>(d_pix) + (long long)base * h * stride, size_t(stride),
-                                          h_pix + size_t(base) * h * h_stride, h_stride, size_t(w) * channels, size_t(h) * nf,
-                                          cudaMemcpyHostToDevice, copy_st));
+                                          h_pix + size_t(base) * h * h_stride, h_stride, size_t(w) * channels * elem,
+                                          size_t(h) * nf, cudaMemcpyHostToDevice, copy_st));
         CDVZ_CUDA_CHECK(cudaEventRecord(copy_ev[size_t(c)], copy_st));
       }
     }
@@ -562,7 +632,17 @@ struct cdvz_gpu_ctx {
       if (h_pix) CDVZ_CUDA_CHECK(cudaStreamWaitEvent(L.sA, copy_ev[size_t(c)], 0));
       CDVZ_CUDA_CHECK(cudaEventRecord(L.start, L.sA));
       CDVZ_CUDA_CHECK(cudaMemsetAsync(b.status, 0, sizeof(int) * nf, L.sA));
-      if (rgb) {  // load_image's PPM branch, then resize_max_side on the grey plane
+      if (f64) {  // validate (image.cpp:46-51), then resize_max_side on the caller's grey plane
+        double* src = reinterpret_cast<double*>(const_cast<uint8_t*>(b.pix8));
+        CDVZ_CUDA_CHECK(launch_validate_f64(src, w, h, nf, b.status, L.sA));
+        launches += 2;
+        if (resize) {
+          CDVZ_CUDA_CHECK(launch_resize_f64(src, w, h, const_cast<double*>(b.pixf), W, H, nf, L.sA));
+          ++launches;
+        } else {
+          b.pixf = src;  // octave 0 reads the validated plane in place
+        }
+      } else if (rgb) {  // load_image's PPM branch, then resize_max_side on the grey plane
         double* grey = resize ? L.grey : const_cast<double*>(b.pixf);
         CDVZ_CUDA_CHECK(launch_grey_rgb(b.pix8, stride, b.frame_bytes8, w, h, grey, nf, L.sA));
         ++launches;
@@ -613,6 +693,8 @@ struct cdvz_gpu_ctx {
         CDVZ_CUDA_CHECK(cudaMemcpyAsync(h_out + size_t(base) * ec.slot_bytes, d_out + size_t(base) * ec.slot_bytes,
                                         size_t(nf) * ec.slot_bytes, cudaMemcpyDeviceToHost, sB));
         CDVZ_CUDA_CHECK(cudaMemcpyAsync(h_len + base, d_len + base, sizeof(uint32_t) * nf, cudaMemcpyDeviceToHost, sB));
+        if (h_status)
+          CDVZ_CUDA_CHECK(cudaMemcpyAsync(h_status + base, b.status, sizeof(int) * nf, cudaMemcpyDeviceToHost, sB));
         while (int(out_ev.size()) <= c) {
           cudaEvent_t e;
           CDVZ_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -626,6 +708,7 @@ struct cdvz_gpu_ctx {
       CDVZ_CUDA_CHECK(cudaStreamWaitEvent(L.sA, L.done, 0));
       launches += 1 + 5 + 5;  // k_select; k_orient, k_expand, k_geometry, k_sample, k_describe; SCFV + pack
       L.pending = true;
+      L.pending_call = call;
       L.pending_oct = b.n_oct;
       L.pending_bytes = bytes;
       last_lane = serial ? 0 : (lane0 + c) % kLanes;
@@ -640,7 +723,7 @@ struct cdvz_gpu_ctx {
       }
     for (int l = 0; l < kLanes; ++l)
       if (lanes[l].pending) CDVZ_CUDA_CHECK(cudaStreamWaitEvent(st, lanes[l].done, 0));
-    for (int l = 0; l < kLanes; ++l) collect(lanes[l]);
+    // No collect() here: the call returns once its work is enqueued.
     last_frames = cb[size_t(chunks)] - cb[size_t(chunks) - 1];
     last_mode = mode_id;
   }
@@ -664,6 +747,12 @@ int guarded(cdvz_gpu_ctx* ctx, F&& f) {
     (ctx ? ctx->err : g_create_error) = e.what();
     return CDVZ_GPU_INTERNAL;
   }
+}
+
+// Entry points that act on one device's memory or stream.
+void require_single(const cdvz_gpu_ctx* ctx) {
+  if (!ctx) throw UsageError("null context");
+  if (!ctx->shards.empty()) throw UsageError("this call acts on one device: use a single-device context");
 }
 
 }  // namespace
@@ -695,10 +784,51 @@ int cdvz_gpu_create(const char* bundle_text, size_t bundle_len, int device, int 
   });
 }
 
+int cdvz_gpu_create_multi(const char* bundle_text, size_t bundle_len, const int* devices, int ndev, int max_batch,
+                          cdvz_gpu_ctx** out_ctx) {
+  return guarded(nullptr, [&] {
+    if (!out_ctx || !bundle_text || !devices) throw UsageError("null argument");
+    *out_ctx = nullptr;
+    if (ndev < 1) throw UsageError("at least one device is required");
+    Bundle parsed = parse_bundle(std::string(bundle_text, bundle_len));
+    auto ctx = std::make_unique<cdvz_gpu_ctx>();
+    ctx->device = devices[0];
+    ctx->max_batch = max_batch > 0 ? max_batch : 256;
+    ctx->bundle = std::move(parsed);
+    for (int d = 0; d < ndev; ++d) {
+      cdvz_gpu_ctx* sub = nullptr;
+      const int rc = cdvz_gpu_create(bundle_text, bundle_len, devices[d], max_batch, &sub);
+      if (rc != CDVZ_GPU_OK) {
+        const std::string msg = "device " + std::to_string(devices[d]) + ": " + g_create_error;
+        if (rc == CDVZ_GPU_USAGE) throw UsageError(msg);
+        if (rc == CDVZ_GPU_DATA) throw DataError(msg);
+        throw std::runtime_error(msg);
+      }
+      ctx->shards.emplace_back(sub);
+    }
+    *out_ctx = ctx.release();
+  });
+}
+
+int cdvz_gpu_visible_devices(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+  return n;
+}
+
+int cdvz_gpu_device_count(const cdvz_gpu_ctx* ctx, int* devices, int cap) {
+  if (!ctx) return -1;
+  const int n = ctx->shards.empty() ? 1 : int(ctx->shards.size());
+  for (int d = 0; d < n && devices && d < cap; ++d) devices[d] = ctx->shards.empty() ? ctx->device : ctx->shards[size_t(d)]->device;
+  return n;
+}
+
 void cdvz_gpu_destroy(cdvz_gpu_ctx* ctx) {
   if (!ctx) return;
-  cudaSetDevice(ctx->device);
-  cudaStreamSynchronize(ctx->st);
+  if (ctx->shards.empty()) {
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->st);
+  }
   delete ctx;
 }
 
@@ -715,7 +845,8 @@ int cdvz_gpu_bundle_check(const char* bundle_text, size_t bundle_len, uint32_t* 
 
 int cdvz_gpu_event_record(cdvz_gpu_ctx* ctx, int slot) {
   return guarded(ctx, [&] {
-    if (!ctx || slot < 0 || slot >= 4) throw UsageError("event slot out of range");
+    require_single(ctx);
+    if (slot < 0 || slot >= 4) throw UsageError("event slot out of range");
     if (!ctx->user_ev[slot]) CDVZ_CUDA_CHECK(cudaEventCreate(&ctx->user_ev[slot]));
     CDVZ_CUDA_CHECK(cudaEventRecord(ctx->user_ev[slot], ctx->st));
   });
@@ -723,7 +854,8 @@ int cdvz_gpu_event_record(cdvz_gpu_ctx* ctx, int slot) {
 
 int cdvz_gpu_event_elapsed(cdvz_gpu_ctx* ctx, int a, int b, double* ms) {
   return guarded(ctx, [&] {
-    if (!ctx || a < 0 || a >= 4 || b < 0 || b >= 4 || !ctx->user_ev[a] || !ctx->user_ev[b]) throw UsageError("event slot not recorded");
+    require_single(ctx);
+    if (a < 0 || a >= 4 || b < 0 || b >= 4 || !ctx->user_ev[a] || !ctx->user_ev[b]) throw UsageError("event slot not recorded");
     CDVZ_CUDA_CHECK(cudaEventSynchronize(ctx->user_ev[b]));
     float t = 0.f;
     CDVZ_CUDA_CHECK(cudaEventElapsedTime(&t, ctx->user_ev[a], ctx->user_ev[b]));
@@ -749,10 +881,12 @@ size_t cdvz_gpu_container_slot(int mode_id) {
 
 int cdvz_gpu_set_debug(cdvz_gpu_ctx* ctx, int on) {
   if (!ctx) return CDVZ_GPU_USAGE;
+  for (auto& sh : ctx->shards) cdvz_gpu_set_debug(sh.get(), on);
   ctx->debug = (on & 1) != 0;
   ctx->dc.screen = (on & 2) ? 0 : 1;
   ctx->serial = (on & 4) != 0;
   ctx->dc.walk = (on & 16) ? 0 : 1;
+  ctx->tiny_caps = (on & 32) != 0;
   if (ctx->tma_disabled != ((on & 8) != 0)) {
     ctx->tma_disabled = (on & 8) != 0;
     for (auto& l : ctx->lanes) l.geo_w = 0;  // rebuild the tensor maps
@@ -764,6 +898,7 @@ int cdvz_gpu_encode_device(cdvz_gpu_ctx* ctx, const uint8_t* d_pixels, int width
                            int mode_id, int max_side, uint8_t* d_out, uint32_t* d_lengths) {
   return guarded(ctx, [&] {
     if (!ctx) throw UsageError("null context");
+    if (!ctx->shards.empty()) throw UsageError("device-resident frames belong to one device: use a single-device context");
     if (count < 0) throw UsageError("negative frame count");
     if (count == 0) return;
     mode_by_id(mode_id);
@@ -775,6 +910,11 @@ int cdvz_gpu_encode_device(cdvz_gpu_ctx* ctx, const uint8_t* d_pixels, int width
 int cdvz_gpu_trim(cdvz_gpu_ctx* ctx) {
   return guarded(ctx, [&] {
     if (!ctx) throw UsageError("null context");
+    if (!ctx->shards.empty()) {
+      for (auto& sh : ctx->shards)
+        if (cdvz_gpu_trim(sh.get()) != CDVZ_GPU_OK) throw std::runtime_error(sh->err);
+      return;
+    }
     CDVZ_CUDA_CHECK(cudaSetDevice(ctx->device));
     CDVZ_CUDA_CHECK(cudaStreamSynchronize(ctx->st));
     for (auto& l : ctx->lanes) {
@@ -789,21 +929,117 @@ int cdvz_gpu_trim(cdvz_gpu_ctx* ctx) {
 }
 
 int cdvz_gpu_sync(cdvz_gpu_ctx* ctx) {
-  return guarded(ctx, [&] { CDVZ_CUDA_CHECK(cudaStreamSynchronize(ctx->st)); });
+  return guarded(ctx, [&] {
+    if (!ctx) throw UsageError("null context");
+    for (auto& sh : ctx->shards)
+      if (cdvz_gpu_sync(sh.get()) != CDVZ_GPU_OK) throw std::runtime_error(sh->err);
+    if (ctx->shards.empty()) {
+      CDVZ_CUDA_CHECK(cudaSetDevice(ctx->device));
+      CDVZ_CUDA_CHECK(cudaStreamSynchronize(ctx->st));
+    }
+  });
 }
 
 }  // extern "C"
 
 namespace {
 
-// Host-frame batch encode of grey (channels 1) or RGB (channels 3) rasters.
 int encode_host_batch(cdvz_gpu_ctx* ctx, const uint8_t* pixels, int width, int height, size_t stride, int count,
-                      int mode_id, int max_side, uint8_t* out, size_t out_cap, size_t* offsets, int* status,
-                      int channels) {
+                      int mode_id, int max_side, uint8_t* out, size_t out_cap, size_t* offsets, int* status, int kind);
+
+// Frame-sharded host batch on a multi-device context: contiguous frame ranges,
+// one host thread per device (the GPU analogue of the reference's
+// run_indexed fan-out, parallel.cpp:40-78), containers gathered in frame
+// order. The lowest-index failing device's error wins, as in run_indexed.
+void encode_multi(cdvz_gpu_ctx* ctx, const uint8_t* pixels, int width, int height, size_t stride, int count,
+                  int mode_id, int max_side, uint8_t* out, size_t out_cap, size_t* offsets, int* status, int kind) {
+  const int nd = int(ctx->shards.size());
+  const size_t slot = mode_by_id(mode_id).budget + 28;
+  std::vector<int> start(static_cast<size_t>(nd) + 1);
+  for (int d = 0; d <= nd; ++d) start[size_t(d)] = int((long long)count * d / nd);
+  // Each shard writes into its own region: in place in `out` when the caller
+  // left room for every frame at full slot size, else in a scratch buffer.
+  const bool in_place = out_cap >= size_t(count) * slot;
+  std::vector<std::vector<uint8_t>> scratch(in_place ? 0 : static_cast<size_t>(nd));
+  std::vector<std::vector<size_t>> off(static_cast<size_t>(nd));
+  std::vector<int> rc(static_cast<size_t>(nd), int(CDVZ_GPU_OK));
+  std::vector<std::thread> th;
+  for (int d = 0; d < nd; ++d) {
+    const int n = start[size_t(d) + 1] - start[size_t(d)];
+    off[size_t(d)].assign(size_t(n) + 1, 0);
+    uint8_t* region = nullptr;
+    if (in_place) {
+      region = out + size_t(start[size_t(d)]) * slot;
+    } else {
+      scratch[size_t(d)].resize(std::max<size_t>(1, size_t(n) * slot));
+      region = scratch[size_t(d)].data();
+    }
+    const uint8_t* src = pixels + size_t(start[size_t(d)]) * height * stride;
+    th.emplace_back([&, d, n, region, src] {
+      if (n == 0) return;
+      rc[size_t(d)] = encode_host_batch(ctx->shards[size_t(d)].get(), src, width, height, stride, n, mode_id, max_side,
+                                        region, size_t(n) * slot, off[size_t(d)].data(), status + start[size_t(d)], kind);
+    });
+  }
+  for (auto& t : th) t.join();
+  for (int d = 0; d < nd; ++d)
+    if (rc[size_t(d)] != CDVZ_GPU_OK) {
+      const std::string msg = "device " + std::to_string(ctx->shards[size_t(d)]->device) + ": " + ctx->shards[size_t(d)]->err;
+      if (rc[size_t(d)] == CDVZ_GPU_USAGE) throw UsageError(msg);
+      if (rc[size_t(d)] == CDVZ_GPU_DATA) throw DataError(msg);
+      throw std::runtime_error(msg);
+    }
+  // Gather in frame order. In place, shard d's bytes move left (to the end of
+  // shard d-1's), so a forward memmove per shard is safe.
+  size_t written = 0;
+  offsets[0] = 0;
+  for (int d = 0; d < nd; ++d) {
+    const int n = start[size_t(d) + 1] - start[size_t(d)];
+    const size_t bytes = off[size_t(d)][size_t(n)];
+    const uint8_t* src = in_place ? out + size_t(start[size_t(d)]) * slot : scratch[size_t(d)].data();
+    if (!in_place && written + bytes > out_cap) {
+      // Frame-level overflow accounting, as the single-device path does it.
+      for (int i = 0; i < n; ++i) {
+        const size_t len = off[size_t(d)][size_t(i) + 1] - off[size_t(d)][size_t(i)];
+        const int fi = start[size_t(d)] + i;
+        if (status[fi] == CDVZ_GPU_OK) {
+          if (written + len > out_cap) {
+            status[fi] = CDVZ_GPU_USAGE;
+          } else {
+            std::memcpy(out + written, src + off[size_t(d)][size_t(i)], len);
+            written += len;
+          }
+        }
+        offsets[fi + 1] = written;
+      }
+      continue;
+    }
+    if (bytes && out + written != src) std::memmove(out + written, src, bytes);
+    for (int i = 0; i < n; ++i) offsets[start[size_t(d)] + i + 1] = written + off[size_t(d)][size_t(i) + 1];
+    written += bytes;
+  }
+  cdvz_gpu_ctx::Stats sum;
+  int launches = 0;
+  for (auto& sh : ctx->shards) {
+    for (int i = 0; i < 5; ++i) sum.stage_ms[i] += sh->stats.stage_ms[i];
+    sum.pyr_ms += sh->stats.pyr_ms;
+    sum.pyr_bytes += sh->stats.pyr_bytes;
+    launches += sh->launches;
+  }
+  ctx->stats = sum;
+  ctx->launches = launches;
+}
+
+// Host-frame batch encode of grey (kind 1) or RGB (kind 3) byte rasters, or
+// f64 grey rasters (kind 8; `stride` in bytes).
+int encode_host_batch(cdvz_gpu_ctx* ctx, const uint8_t* pixels, int width, int height, size_t stride, int count,
+                      int mode_id, int max_side, uint8_t* out, size_t out_cap, size_t* offsets, int* status, int kind) {
   return guarded(ctx, [&] {
+    const int channels = kind == 3 ? 3 : 1;
+    const size_t elem = kind == 8 ? sizeof(double) : 1;
     if (!ctx || (!pixels && count > 0) || !offsets || !status) throw UsageError("null argument");
     if (count < 0) throw UsageError("negative frame count");
-    if (stride < size_t(width) * channels) throw UsageError("row stride shorter than a row");
+    if (stride < size_t(width) * channels * elem) throw UsageError("row stride shorter than a row");
     offsets[0] = 0;
     if (count == 0) return;
     const size_t slot = mode_by_id(mode_id).budget + 28;
@@ -814,8 +1050,13 @@ int encode_host_batch(cdvz_gpu_ctx* ctx, const uint8_t* pixels, int width, int h
       }
       throw DataError("image smaller than 8 px per side");
     }
+    if (!ctx->shards.empty()) {
+      encode_multi(ctx, pixels, width, height, stride, count, mode_id, max_side, out, out_cap, offsets, status, kind);
+      return;
+    }
     CDVZ_CUDA_CHECK(cudaSetDevice(ctx->device));
-    const size_t frame_bytes = size_t(width) * height * channels;
+    const size_t row_bytes = size_t(width) * channels * elem;
+    const size_t frame_bytes = row_bytes * height;
     // Frames per call to run(): bounded so the device staging stays < 4 GB.
     const int group = int(std::max<size_t>(1, std::min<size_t>(size_t(count), (size_t(4) << 30) / frame_bytes)));
     ctx->stage_in.ensure(frame_bytes * group);
@@ -823,19 +1064,36 @@ int encode_host_batch(cdvz_gpu_ctx* ctx, const uint8_t* pixels, int width, int h
     ctx->stage_len.ensure(sizeof(uint32_t) * group);
     ctx->ensure_pinned_out(slot * group, group);
     size_t written = 0;
-    double acc_ms[5] = {0, 0, 0, 0, 0};
-    double acc_pyr_ms = 0, acc_pyr_bytes = 0;
+    cdvz_gpu_ctx::Stats acc;
     int acc_launches = 0;
+    auto fold = [&] {
+      ctx->collect_all();
+      for (int i = 0; i < 5; ++i) acc.stage_ms[i] += ctx->stats.stage_ms[i];
+      acc.pyr_ms += ctx->stats.pyr_ms;
+      acc.pyr_bytes += ctx->stats.pyr_bytes;
+      acc_launches += ctx->launches;
+    };
     for (int base = 0; base < count; base += group) {
       const int nf = std::min(group, count - base);
+      std::vector<int> retry;             // frames of this group that overflowed a capacity
+      std::vector<size_t> start(size_t(nf), 0);  // byte offset of each written container in `out`
       // Containers of frames [c0, c0 + cn) of this group are in pinned memory:
       // copied out in frame order while later chunks still run.
       auto copy_out = [&](int c0, int cn) {
         for (int i = c0; i < c0 + cn; ++i) {
           const size_t len = ctx->pin_len[size_t(i)];
+          const int dev_status = ctx->pin_status[size_t(i)];
           const int fi = base + i;
+          start[size_t(i)] = written;
           if (len == 0) {
-            status[fi] = CDVZ_GPU_INTERNAL;
+            if (dev_status & 2) {
+              status[fi] = CDVZ_GPU_DATA;  // validate(): non-finite or outside [0, 1]
+            } else if (dev_status == 4) {
+              status[fi] = CDVZ_GPU_OK;    // capacity only: re-encoded below with the maximal capacities
+              retry.push_back(i);
+            } else {
+              status[fi] = CDVZ_GPU_INTERNAL;
+            }
           } else if (written + len > out_cap) {
             status[fi] = CDVZ_GPU_USAGE;
           } else {
@@ -846,18 +1104,70 @@ int encode_host_batch(cdvz_gpu_ctx* ctx, const uint8_t* pixels, int width, int h
           offsets[fi + 1] = written;
         }
       };
-      ctx->run(ctx->stage_in.as<uint8_t>(), width, height, (long long)width * channels, nf, mode_id, max_side,
+      ctx->run(ctx->stage_in.as<uint8_t>(), width, height, (long long)row_bytes, nf, mode_id, max_side,
                ctx->stage_out.as<uint8_t>(), ctx->stage_len.as<uint32_t>(), pixels + size_t(base) * height * stride, stride,
-               ctx->pin_out, ctx->pin_len, channels, copy_out);
+               ctx->pin_out, ctx->pin_len, kind, copy_out, ctx->pin_status);
       CDVZ_CUDA_CHECK(cudaStreamSynchronize(ctx->st));
-      for (int i = 0; i < 5; ++i) acc_ms[i] += ctx->stage_ms[i];
-      acc_pyr_ms += ctx->pyr_ms;
-      acc_pyr_bytes += ctx->pyr_bytes;
-      acc_launches += ctx->launches;
+      fold();
+      if (retry.empty()) continue;
+      // Capacity retry: a frame whose survivor or orientation lists outgrew the
+      // batch capacities (adversarial content) is encoded again on its own with
+      // the largest counts the reference can produce, so it never fails where
+      // the reference succeeds. Its container is then spliced in frame order.
+      std::vector<std::vector<uint8_t>> redo(retry.size());
+      ctx->cap_boost = true;
+      try {
+        for (size_t r = 0; r < retry.size(); ++r) {
+          const int i = retry[r];
+          ctx->run(ctx->stage_in.as<uint8_t>() + size_t(i) * frame_bytes, width, height, (long long)row_bytes, 1, mode_id,
+                   max_side, ctx->stage_out.as<uint8_t>(), ctx->stage_len.as<uint32_t>(), nullptr, 0, nullptr, nullptr,
+                   kind);
+          CDVZ_CUDA_CHECK(cudaStreamSynchronize(ctx->st));
+          fold();
+          uint32_t len = 0;
+          int dev_status = 0;
+          CDVZ_CUDA_CHECK(cudaMemcpy(&len, ctx->stage_len.as<uint32_t>(), sizeof(len), cudaMemcpyDeviceToHost));
+          const Lane& L = ctx->lanes[ctx->last_lane];
+          CDVZ_CUDA_CHECK(cudaMemcpy(&dev_status, L.bt.status, sizeof(int), cudaMemcpyDeviceToHost));
+          if (len == 0) {
+            status[base + i] = (dev_status & 2) ? CDVZ_GPU_DATA : CDVZ_GPU_INTERNAL;
+            continue;
+          }
+          redo[r].resize(len);
+          CDVZ_CUDA_CHECK(cudaMemcpy(redo[r].data(), ctx->stage_out.as<uint8_t>(), len, cudaMemcpyDeviceToHost));
+        }
+      } catch (...) {
+        ctx->cap_boost = false;
+        throw;
+      }
+      ctx->cap_boost = false;
+      size_t grow = 0;
+      for (const auto& v : redo) grow += v.size();
+      if (written + grow > out_cap) {  // no room: the re-encoded frames are reported like any overflow
+        for (size_t q = 0; q < retry.size(); ++q)
+          if (!redo[q].empty()) status[base + retry[q]] = CDVZ_GPU_USAGE;
+        continue;
+      }
+      // Rebuild this group's section back to front: containers only move right.
+      size_t end = written + grow;
+      size_t r = retry.size();
+      for (int i = nf - 1; i >= 0; --i) {
+        const int fi = base + i;
+        const size_t old_len = size_t(offsets[fi + 1]) - start[size_t(i)];
+        const std::vector<uint8_t>* ins = (r > 0 && retry[r - 1] == i) ? &redo[--r] : nullptr;
+        const size_t len = ins ? ins->size() : old_len;
+        const size_t pos = end - len;
+        if (ins) {
+          if (len) std::memcpy(out + pos, ins->data(), len);
+        } else if (len && pos != start[size_t(i)]) {
+          std::memmove(out + pos, out + start[size_t(i)], len);
+        }
+        offsets[fi + 1] = end;
+        end = pos;
+      }
+      written += grow;
     }
-    for (int i = 0; i < 5; ++i) ctx->stage_ms[i] = acc_ms[i];
-    ctx->pyr_ms = acc_pyr_ms;
-    ctx->pyr_bytes = acc_pyr_bytes;
+    ctx->stats = acc;
     ctx->launches = acc_launches;
   });
 }
@@ -931,23 +1241,42 @@ int cdvz_gpu_encode_batch_rgb(cdvz_gpu_ctx* ctx, const uint8_t* rgb, int width, 
   return encode_host_batch(ctx, rgb, width, height, stride, count, mode_id, max_side, out, out_cap, offsets, status, 3);
 }
 
+int cdvz_gpu_encode_batch_f64(cdvz_gpu_ctx* ctx, const double* pixels, int width, int height, size_t stride, int count,
+                              int mode_id, int max_side, uint8_t* out, size_t out_cap, size_t* offsets, int* status) {
+  if (stride > (size_t(-1) >> 4)) return CDVZ_GPU_USAGE;
+  return encode_host_batch(ctx, reinterpret_cast<const uint8_t*>(pixels), width, height, stride * sizeof(double), count,
+                           mode_id, max_side, out, out_cap, offsets, status, 8);
+}
+
 int cdvz_gpu_stage_times(cdvz_gpu_ctx* ctx, double ms[5]) {
   if (!ctx || !ms) return CDVZ_GPU_USAGE;
-  for (int i = 0; i < 5; ++i) ms[i] = ctx->stage_ms[i];
-  return CDVZ_GPU_OK;
+  return guarded(ctx, [&] {
+    if (ctx->shards.empty()) {
+      CDVZ_CUDA_CHECK(cudaSetDevice(ctx->device));
+      ctx->collect_all();
+    }
+    for (int i = 0; i < 5; ++i) ms[i] = ctx->stats.stage_ms[i];
+  });
 }
 
 int cdvz_gpu_kernel_stats(cdvz_gpu_ctx* ctx, int* launches, double* pyramid_ms, double* pyramid_bytes) {
   if (!ctx) return CDVZ_GPU_USAGE;
   if (launches) *launches = ctx->launches;
-  if (pyramid_ms) *pyramid_ms = ctx->pyr_ms;
-  if (pyramid_bytes) *pyramid_bytes = ctx->pyr_bytes;
-  return CDVZ_GPU_OK;
+  if (!pyramid_ms && !pyramid_bytes) return CDVZ_GPU_OK;  // the launch count needs no synchronisation
+  return guarded(ctx, [&] {
+    if (ctx->shards.empty()) {
+      CDVZ_CUDA_CHECK(cudaSetDevice(ctx->device));
+      ctx->collect_all();
+    }
+    if (pyramid_ms) *pyramid_ms = ctx->stats.pyr_ms;
+    if (pyramid_bytes) *pyramid_bytes = ctx->stats.pyr_bytes;
+  });
 }
 
 int cdvz_gpu_debug_get(cdvz_gpu_ctx* ctx, const char* name, int frame, double* dst, size_t cap, size_t* n) {
   return guarded(ctx, [&] {
     if (!ctx || !name || !n) throw UsageError("null argument");
+    if (!ctx->shards.empty()) throw UsageError("debug arrays live on one device: use a single-device context");
     if (frame < 0 || frame >= ctx->last_frames) throw UsageError("frame index outside the last batch");
     CDVZ_CUDA_CHECK(cudaSetDevice(ctx->device));
     CDVZ_CUDA_CHECK(cudaStreamSynchronize(ctx->st));
@@ -1010,6 +1339,14 @@ int cdvz_gpu_debug_get(cdvz_gpu_ctx* ctx, const char* name, int frame, double* d
       const int o = std::stoi(s.substr(6, c2 - 6)), k = std::stoi(s.substr(c2 + 1));
       if (o < b.n_oct && k >= 0 && k < 4)
         v = get_d(b.pyr + (long long)frame * b.frame_doubles + b.plane_off[o][k], (long long)b.ow[o] * b.oh[o]);
+    } else if (s == "norms") {
+      // SCFVDescriptor::norms: scfv_delta of each selected component, ascending
+      // component order (scfv.cpp:240-251).
+      const auto all = get_d(b.norms + (long long)frame * b.nc, b.nc);
+      std::vector<uint8_t> mask(size_t((b.nc + 7) / 8));
+      CDVZ_CUDA_CHECK(cudaMemcpy(mask.data(), b.mask + (long long)frame * mask.size(), mask.size(), cudaMemcpyDeviceToHost));
+      for (int i = 0; i < b.nc; ++i)
+        if ((mask[size_t(i / 8)] >> (i % 8)) & 1) v.push_back(all[size_t(i)]);
     } else if (s == "status") {
       v = {double(get_int(b.status + frame))};
     } else {
@@ -1022,7 +1359,8 @@ int cdvz_gpu_debug_get(cdvz_gpu_ctx* ctx, const char* name, int frame, double* d
 
 int cdvz_gpu_synth_frames(cdvz_gpu_ctx* ctx, uint64_t base_seed, int count, int width, int height, uint8_t* d_out) {
   return guarded(ctx, [&] {
-    if (!ctx || !d_out) throw UsageError("null argument");
+    require_single(ctx);
+    if (!d_out) throw UsageError("null argument");
     if (width < 1 || height < 1 || count < 0) throw UsageError("bad synthetic frame geometry");
     CDVZ_CUDA_CHECK(cudaSetDevice(ctx->device));
     const int chunk = 64;
@@ -1077,7 +1415,8 @@ int cdvz_gpu_synth_frames(cdvz_gpu_ctx* ctx, uint64_t base_seed, int count, int 
 int cdvz_gpu_pyramid_bench(cdvz_gpu_ctx* ctx, const uint8_t* d_pixels, int width, int height, int count, int iters,
                            double* ms_per_iter, double* bytes_per_iter) {
   return guarded(ctx, [&] {
-    if (!ctx || !d_pixels || !ms_per_iter || !bytes_per_iter) throw UsageError("null argument");
+    require_single(ctx);
+    if (!d_pixels || !ms_per_iter || !bytes_per_iter) throw UsageError("null argument");
     if (width < 16 || height < 16 || count < 1 || iters < 1) throw UsageError("bad microbenchmark geometry");
     CDVZ_CUDA_CHECK(cudaSetDevice(ctx->device));
     Lane& L = ctx->lanes[0];
@@ -1116,13 +1455,18 @@ int cdvz_gpu_pyramid_bench(cdvz_gpu_ctx* ctx, const uint8_t* d_pixels, int width
 
 int cdvz_gpu_device_alloc(cdvz_gpu_ctx* ctx, size_t bytes, void** ptr) {
   return guarded(ctx, [&] {
+    require_single(ctx);
     CDVZ_CUDA_CHECK(cudaSetDevice(ctx->device));
     CDVZ_CUDA_CHECK(cudaMalloc(ptr, std::max<size_t>(bytes, 1)));
   });
 }
 
 int cdvz_gpu_device_free(cdvz_gpu_ctx* ctx, void* ptr) {
-  return guarded(ctx, [&] { CDVZ_CUDA_CHECK(cudaFree(ptr)); });
+  return guarded(ctx, [&] {
+    require_single(ctx);
+    CDVZ_CUDA_CHECK(cudaSetDevice(ctx->device));
+    CDVZ_CUDA_CHECK(cudaFree(ptr));
+  });
 }
 
 int cdvz_gpu_host_alloc(cdvz_gpu_ctx* ctx, size_t bytes, void** ptr) {
@@ -1135,6 +1479,8 @@ int cdvz_gpu_host_free(cdvz_gpu_ctx* ctx, void* ptr) {
 
 int cdvz_gpu_copy(cdvz_gpu_ctx* ctx, void* dst, const void* src, size_t bytes, int kind) {
   return guarded(ctx, [&] {
+    require_single(ctx);
+    CDVZ_CUDA_CHECK(cudaSetDevice(ctx->device));
     const cudaMemcpyKind k = kind == 1 ? cudaMemcpyHostToDevice : kind == 2 ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
     CDVZ_CUDA_CHECK(cudaMemcpyAsync(dst, src, bytes, k, ctx->st));
     CDVZ_CUDA_CHECK(cudaStreamSynchronize(ctx->st));

@@ -3,6 +3,8 @@
 // (resize_max_side / rescale_bilinear, proj/src/image.cpp:107-145), and the
 // deterministic synthetic frame generator used by the benchmarks
 // (synth_image / synth_corpus, proj/src/synthetic.cpp:11-61).
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace cdvz_gpu {
@@ -55,6 +57,40 @@ cudaError_t launch_resize_f64(const double* grey, int w_in, int h_in, double* ou
   const double sx = static_cast<double>(w_in) / w_out, sy = static_cast<double>(h_in) / h_out;
   dim3 grid((w_out + 127) / 128, h_out, frames);
   k_resize<double><<<grid, 128, 0, st>>>(grey, w_in, (long long)w_in * h_in, w_in, h_in, out, w_out, h_out, sx, sy);
+  return cudaGetLastError();
+}
+
+// validate (image.cpp:46-51) for f64 grey frames handed in by the caller:
+// a frame with a non-finite value or one outside [0, 1] gets status 2 (the
+// reference's DataError) and its raster is zeroed in the staging buffer, so
+// the rest of the pipeline runs on a harmless plane and k_pack emits nothing
+// for it. Grid (row blocks, frames); a second launch scrubs flagged frames.
+__global__ void k_validate_f64(const double* pix, long long frame_elems, long long n, int* status) {
+  const int f = blockIdx.y;
+  const double* p = pix + f * frame_elems;
+  int bad = 0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const double v = p[i];
+    bad |= !(v >= 0.0 && v <= 1.0);  // NaN fails both comparisons; +-inf fails one
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&status[f], 2);
+}
+
+__global__ void k_scrub_f64(double* pix, long long frame_elems, long long n, const int* status) {
+  const int f = blockIdx.y;
+  if (status[f] == 0) return;
+  double* p = pix + f * frame_elems;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    p[i] = 0.0;
+}
+
+cudaError_t launch_validate_f64(double* pix, int w, int h, int frames, int* status, cudaStream_t st) {
+  const long long n = (long long)w * h;
+  const dim3 grid(unsigned(std::min<long long>(64, (n + 255) / 256)), frames);
+  k_validate_f64<<<grid, 256, 0, st>>>(pix, n, n, status);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  k_scrub_f64<<<grid, 256, 0, st>>>(pix, n, n, status);
   return cudaGetLastError();
 }
 

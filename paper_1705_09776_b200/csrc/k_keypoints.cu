@@ -293,7 +293,9 @@ struct SelKey { unsigned long long k[5]; };
 
 __device__ __forceinline__ SelKey sel_key(double score, const KP& p, int idx) {
   SelKey s;
-  s.k[0] = ~static_cast<unsigned long long>(__double_as_longlong(score));      // score >= 0
+  // score >= 0; + 0.0 maps a -0.0 (a relevance value of -0.0 passes the
+  // bundle's [0, 1] check) to +0.0, which the reference's comparisons treat alike.
+  s.k[0] = ~static_cast<unsigned long long>(__double_as_longlong(score + 0.0));
   s.k[1] = ~static_cast<unsigned long long>(__double_as_longlong(fabs(p.p)));  // |p| >= 0
   // y, x >= 0 after refinement (margin >= 2), so their bit patterns order like the values.
   s.k[2] = static_cast<unsigned long long>(__double_as_longlong(p.y));

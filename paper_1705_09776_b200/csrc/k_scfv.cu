@@ -475,6 +475,7 @@ __global__ void __launch_bounds__(256) k_scfv_encode(Batch bt, Model md, EncodeC
 #pragma unroll
     for (int j = 0; j < 32; ++j) d[j] = (g[j] - mean) * (g[j] - mean);
     sdelta[i] = sqrt(packet_sum_seq(d, 32) / 32.0);
+    bt.norms[(long long)f * nc + i] = sdelta[i];
   }
   __syncthreads();
   uint8_t* chosen = reinterpret_cast<uint8_t*>(sdelta + nc);

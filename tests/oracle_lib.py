@@ -38,6 +38,8 @@ def lib() -> ctypes.CDLL:
         L.orc_encode_batch_u8.argtypes = [ctypes.c_char_p, S, P, I, I, I, I, I, I, P, S, P]
         L.orc_encode_rgb.argtypes = [ctypes.c_char_p, S, P, I, I, S, I, I, P, S, ctypes.POINTER(S)]
         L.orc_grey_rgb.argtypes = [P, I, I, S, P]
+        L.orc_synth_f64.argtypes = [U64, I, I, P]
+        L.orc_encode_f64.argtypes = [ctypes.c_char_p, S, P, I, I, I, I, P, S, ctypes.POINTER(S), P, S, ctypes.POINTER(S)]
         L.orc_trace_u8.argtypes = [ctypes.c_char_p, S, P, I, I, I, I, ctypes.POINTER(P)]
         L.orc_trace_free.argtypes = [P]
         L.orc_trace_get.argtypes = [P, ctypes.c_char_p, P, S, ctypes.POINTER(S)]
@@ -88,6 +90,23 @@ def encode(text: str, frame: np.ndarray, mode_id: int, max_side: int = 640) -> b
     return out[: n.value].tobytes()
 
 
+def stage_ms(text: str, frames: np.ndarray, mode_id: int, max_side: int = 640) -> dict:
+    """Single-threaded encode of each frame with the reference's StageTimings
+    labels (pipeline.cpp:19-94); mean ms per frame and label."""
+    acc = np.zeros(5, dtype=np.float64)
+    raw = text.encode()
+    cap = 16384 + 64
+    out = np.empty(cap, dtype=np.uint8)
+    n = ctypes.c_size_t()
+    for f in frames:
+        f = np.ascontiguousarray(f, dtype=np.uint8)
+        h, w = f.shape
+        _check(lib().orc_encode_u8(raw, len(raw), f.ctypes.data, w, h, w, mode_id, max_side, out.ctypes.data, cap,
+                                   ctypes.byref(n), acc.ctypes.data))
+    labels = ("detection", "selection", "description", "compression", "aggregation")
+    return {k: float(v) / max(1, len(frames)) for k, v in zip(labels, acc)}
+
+
 def encode_rgb(text: str, frame: np.ndarray, mode_id: int, max_side: int = 640) -> bytes:
     """encode_image(load_image(P6 raster)) for one [H, W, 3] uint8 frame."""
     frame = np.ascontiguousarray(frame, dtype=np.uint8)
@@ -99,6 +118,27 @@ def encode_rgb(text: str, frame: np.ndarray, mode_id: int, max_side: int = 640) 
     _check(lib().orc_encode_rgb(raw, len(raw), frame.ctypes.data, w, h, 3 * w, mode_id, max_side, out.ctypes.data, cap,
                                 ctypes.byref(n)))
     return out[: n.value].tobytes()
+
+
+def synth_f64(seed: int, w: int, h: int) -> np.ndarray:
+    """synth_image(seed, w, h) as the reference's f64 GrayImage (no quantisation)."""
+    out = np.empty((h, w), dtype=np.float64)
+    _check(lib().orc_synth_f64(seed, w, h, out.ctypes.data))
+    return out
+
+
+def encode_f64(text: str, img: np.ndarray, mode_id: int, max_side: int = 640):
+    """encode_image on an f64 GrayImage -> (container bytes, SCFVDescriptor.norms)."""
+    img = np.ascontiguousarray(img, dtype=np.float64)
+    h, w = img.shape
+    cap = 16384 + 64
+    out = np.empty(cap, dtype=np.uint8)
+    norms = np.empty(4096, dtype=np.float64)
+    n, nn = ctypes.c_size_t(), ctypes.c_size_t()
+    raw = text.encode()
+    _check(lib().orc_encode_f64(raw, len(raw), img.ctypes.data, w, h, mode_id, max_side, out.ctypes.data, cap,
+                                ctypes.byref(n), norms.ctypes.data, norms.size, ctypes.byref(nn)))
+    return out[: n.value].tobytes(), norms[: nn.value].copy()
 
 
 def grey_rgb(frame: np.ndarray) -> np.ndarray:
