@@ -89,6 +89,15 @@ int orc_train_bundle(uint64_t corpus_base, int count, int w, int h, uint64_t see
   });
 }
 
+// The oracle's detector beta of a bundle, row-major 4x4.
+int orc_bundle_beta(const char* text, size_t len, double* out16) {
+  return guarded([&] {
+    const ModelBundle b = parse_model(std::string(text, len));
+    for (int i = 0; i < 4; ++i)
+      for (int j = 0; j < 4; ++j) out16[i * 4 + j] = b.detector.beta[std::size_t(i)][std::size_t(j)];
+  });
+}
+
 // Canonical re-serialisation and CRC of a bundle text (model_io.cpp:84).
 int orc_bundle_crc(const char* text, size_t len, uint32_t* crc, int* components) {
   return guarded([&] {

@@ -53,43 +53,80 @@ void load_l(const Octave& oct, int y, int x, double l[4]) {
 
 }  // namespace
 
-// scale_space.cpp:56-73. The reference inverts the Vandermonde matrix with
-// Eigen::FullPivLU; the oracle (and the product host code) use Gauss-Jordan
-// with partial pivoting. The reference's own test pins beta only to 1e-12
-// (test_scale_space.cpp:42-51), which oracle/selftest.cpp re-checks.
+// scale_space.cpp:56-73: beta = V^-1 with Eigen::FullPivLU, restated step for
+// step (complete pivoting, then FullPivLU::_solve_impl on the identity).
+// Pinned bit for bit against the reference's own compute_beta built in
+// oracle/_ref (tests/test_ref_pin.py); the product's bundle.cpp runs the same
+// sequence.
 Mat4 compute_beta(const std::vector<double>& sigmas) {
   if (sigmas.size() != 4) throw DataError("exactly 4 scales are required");
   for (std::size_t i = 0; i < 4; ++i)
     for (std::size_t j = i + 1; j < 4; ++j)
       if (sigmas[i] == sigmas[j]) throw DataError("duplicate scale makes the fit singular");
-  double m[4][8];
+  double V[4][4];
   for (int k = 0; k < 4; ++k) {
     double pw = 1.0;
     for (int i = 0; i < 4; ++i) {
-      m[k][i] = pw;
+      V[k][i] = pw;
       pw *= sigmas[std::size_t(k)];
-    }
-    for (int i = 0; i < 4; ++i) m[k][4 + i] = (i == k) ? 1.0 : 0.0;
-  }
-  for (int c = 0; c < 4; ++c) {
-    int piv = c;
-    for (int r = c + 1; r < 4; ++r)
-      if (std::abs(m[r][c]) > std::abs(m[piv][c])) piv = r;
-    if (m[piv][c] == 0.0) throw DataError("scale node matrix is singular");
-    if (piv != c)
-      for (int j = 0; j < 8; ++j) std::swap(m[c][j], m[piv][j]);
-    const double d = m[c][c];
-    for (int j = 0; j < 8; ++j) m[c][j] /= d;
-    for (int r = 0; r < 4; ++r) {
-      if (r == c) continue;
-      const double f = m[r][c];
-      if (f == 0.0) continue;
-      for (int j = 0; j < 8; ++j) m[r][j] -= f * m[c][j];
     }
   }
   Mat4 beta{};
+  auto& OUT = beta;
+  // Complete-pivoting LU of V, P V Q = L U (Eigen FullPivLU::computeInPlace):
+  // pivot = largest |v| of the remaining corner, first in column-major order.
+  double lu[4][4];
+  int rowp[4] = {0, 1, 2, 3}, colq[4] = {0, 1, 2, 3};
+  double max_pivot = 0.0;
+  int nonzero = 4;
+  for (int k = 0; k < 4; ++k) {
+    int pr = k, pc = k;
+    double best = -1.0;
+    for (int j = k; j < 4; ++j)
+      for (int i = k; i < 4; ++i)
+        if (std::abs(V[i][j]) > best) {
+          best = std::abs(V[i][j]);
+          pr = i;
+          pc = j;
+        }
+    if (best == 0.0) {
+      nonzero = k;
+      break;
+    }
+    max_pivot = std::max(max_pivot, best);
+    if (pr != k) {
+      for (int j = 0; j < 4; ++j) std::swap(V[k][j], V[pr][j]);
+      std::swap(rowp[k], rowp[pr]);
+    }
+    if (pc != k) {
+      for (int i = 0; i < 4; ++i) std::swap(V[i][k], V[i][pc]);
+      std::swap(colq[k], colq[pc]);
+    }
+    for (int i = k + 1; i < 4; ++i) V[i][k] = V[i][k] / V[k][k];
+    for (int j = k + 1; j < 4; ++j)
+      for (int i = k + 1; i < 4; ++i) V[i][j] = V[i][j] - V[i][k] * V[k][j];
+  }
+  // isInvertible(): rank 4 with Eigen's threshold |u_ii| > 4 eps max|pivot|.
+  int rank = 0;
+  for (int i = 0; i < nonzero; ++i) rank += std::abs(V[i][i]) > 4.0 * 2.220446049250313e-16 * max_pivot ? 1 : 0;
+  if (rank != 4) throw DataError("scale node matrix is singular");
   for (int i = 0; i < 4; ++i)
-    for (int j = 0; j < 4; ++j) beta[i][j] = m[i][4 + j];
+    for (int j = 0; j < 4; ++j) lu[i][j] = V[i][j];
+  // inverse() = solve(I) (FullPivLU::_solve_impl): c = P e_col; unit-lower
+  // forward solve; upper solve in triangular_solve_matrix's column order
+  // (x_i = c_i * (1 / u_ii) for i descending, then removed from the rows
+  // above); x = Q c.
+  for (int col = 0; col < 4; ++col) {
+    double c[4];
+    for (int i = 0; i < 4; ++i) c[i] = rowp[i] == col ? 1.0 : 0.0;
+    for (int i = 0; i < 4; ++i)
+      for (int r = i + 1; r < 4; ++r) c[r] = c[r] - c[i] * lu[r][i];
+    for (int i = 3; i >= 0; --i) {
+      c[i] = c[i] * (1.0 / lu[i][i]);
+      for (int r = 0; r < i; ++r) c[r] = c[r] - c[i] * lu[r][i];
+    }
+    for (int i = 0; i < 4; ++i) OUT[colq[i]][col] = c[i];
+  }
   return beta;
 }
 

@@ -22,6 +22,7 @@
 // ratio-test matches; one warp per query re-ranks the head by (local matches,
 // similarity, id) and writes the reference's scores.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <numeric>
@@ -201,13 +202,14 @@ __device__ __forceinline__ double key_value(unsigned long long k) {
 }
 
 // Thread per (query, position p of the id order): key = similarity, value = item.
-__global__ void __launch_bounds__(256) k_global_keys(Decoded Q, Decoded X, const int* perm, int n, int nc,
+// Queries q0 + blockIdx.y of the batch; keys / vals hold this chunk's rows.
+__global__ void __launch_bounds__(256) k_global_keys(Decoded Q, Decoded X, const int* perm, int n, int nc, int q0,
                                                       unsigned long long* keys, int* vals) {
   const int q = blockIdx.y;
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n) return;
   const int it = perm[p];
-  keys[(long long)q * n + p] = order_key(global_sim(Q, q, X, it, nc));
+  keys[(long long)q * n + p] = order_key(global_sim(Q, q0 + q, X, it, nc));
   vals[(long long)q * n + p] = it;
 }
 
@@ -268,10 +270,10 @@ __device__ int count_local(const uint4* A, int na, const uint4* B, int nb, doubl
 
 // One CTA per (query, head rank r): the item is vals[q][r].
 __global__ void __launch_bounds__(kLMThreads) k_local_head(Decoded Q, Decoded X, const int* vals, int n, int head,
-                                                           double ratio, int max_codes, int* local) {
+                                                           double ratio, int max_codes, int q0, int* local) {
   extern __shared__ __align__(16) uint8_t lm_smem[];
-  const int q = blockIdx.y, r = blockIdx.x;
-  const int it = vals[(long long)q * n + r];
+  const int lq = blockIdx.y, r = blockIdx.x, q = q0 + lq;
+  const int it = vals[(long long)lq * n + r];
   const int na = Q.code_off[q + 1] - Q.code_off[q], nb = X.code_off[it + 1] - X.code_off[it];
   uint4* sA = reinterpret_cast<uint4*>(lm_smem);
   uint4* sB = sA + 2 * max_codes;
@@ -280,7 +282,7 @@ __global__ void __launch_bounds__(kLMThreads) k_local_head(Decoded Q, Decoded X,
   const int c = count_local(Q.codes + 2LL * Q.code_off[q], na, X.codes + 2LL * X.code_off[it], nb, ratio, sA, sB, ib,
                             ib + max_codes, ib + 2 * max_codes, ib + 3 * max_codes, ib + 4 * max_codes, ib + 5 * max_codes,
                             red);
-  if (threadIdx.x == 0) local[q * head + r] = c;
+  if (threadIdx.x == 0) local[(long long)lq * head + r] = c;
 }
 
 // One CTA per explicit (query, item) pair: global similarity + local matches.
@@ -306,14 +308,14 @@ __global__ void __launch_bounds__(kLMThreads) k_match_pairs(Decoded Q, Decoded X
 // One warp per query: re-rank the head by (local desc, similarity desc, id
 // asc) and write every item's final rank and score (eval.cpp:97-123).
 __global__ void __launch_bounds__(32) k_finish(const unsigned long long* keys, const int* vals, const int* local,
-                                               const int* id_rank, int n, int head, int max_results, int* out_items,
-                                               double* out_scores) {
+                                               const int* id_rank, int n, int head, int max_results, int q0,
+                                               int* out_items, double* out_scores) {
   const int q = blockIdx.x, lane = threadIdx.x;
   const unsigned long long* kq = keys + (long long)q * n;
   const int* vq = vals + (long long)q * n;
   const int* lq = local + (long long)q * head;
-  int* oi = out_items + (long long)q * max_results;
-  double* os = out_scores + (long long)q * max_results;
+  int* oi = out_items + (long long)(q0 + q) * max_results;
+  double* os = out_scores + (long long)(q0 + q) * max_results;
   for (int r = lane; r < head; r += 32) {
     const int lr = lq[r];
     const double sr = key_value(kq[r]);
@@ -568,44 +570,58 @@ int cdvz_gpu_retrieve(cdvz_gpu_index* idx, const uint8_t* qblob, const size_t* q
     DecodedSet qs;
     qs.decode(qblob, qoff, nq, idx->st, "query batch");
     check_queries(idx, qs);
-    const size_t tot = size_t(nq) * size_t(n);
+    // Queries run in chunks: qc * n stays below 2^31 (CUB's segment offsets
+    // are int) and qc within the grid's y limit; ~24 B of sort buffers per
+    // (query, item) pair bound a chunk to ~6 GB.
+    const long long cap_pairs = std::min<long long>(0x7fffffffLL, 1LL << 28);
+    long long qmax = 65535;
+    if (const char* e = std::getenv("CDVZ_GPU_RETRIEVE_QCHUNK")) qmax = std::max(1LL, std::min(qmax, std::atoll(e)));  // tests
+    const int qc = int(std::max<long long>(1, std::min<long long>({(long long)nq, qmax, cap_pairs / std::max(1, n)})));
+    const size_t tot = size_t(qc) * size_t(n);
     idx->keys.ensure(sizeof(unsigned long long) * tot);
     idx->vals.ensure(sizeof(int) * tot);
     idx->keys2.ensure(sizeof(unsigned long long) * tot);
     idx->vals2.ensure(sizeof(int) * tot);
-    idx->seg.ensure(sizeof(int) * (size_t(nq) + 1));
-    idx->local.ensure(sizeof(int) * std::max<size_t>(1, size_t(nq) * size_t(head)));
+    idx->seg.ensure(sizeof(int) * (size_t(qc) + 1));
+    idx->local.ensure(sizeof(int) * std::max<size_t>(1, size_t(qc) * size_t(head)));
     idx->out_i.ensure(sizeof(int) * size_t(nq) * size_t(mr));
     idx->out_s.ensure(sizeof(double) * size_t(nq) * size_t(mr));
-    std::vector<int> seg(size_t(nq) + 1);
-    for (int q = 0; q <= nq; ++q) seg[size_t(q)] = q * n;
+    std::vector<int> seg(size_t(qc) + 1);
+    for (int q = 0; q <= qc; ++q) seg[size_t(q)] = q * n;
     CDVZ_CUDA_CHECK(cudaMemcpyAsync(idx->seg.p, seg.data(), sizeof(int) * seg.size(), cudaMemcpyHostToDevice, idx->st));
-    k_global_keys<<<dim3((n + 255) / 256, nq), 256, 0, idx->st>>>(qs.view, idx->items.view, idx->perm.as<int>(), n,
-                                                                   idx->items.nc, idx->keys.as<unsigned long long>(),
-                                                                   idx->vals.as<int>());
-    CDVZ_CUDA_CHECK(cudaGetLastError());
-    // Stable descending sort by similarity within each query: items enter in
-    // ascending id order, so ties keep ascending ids (eval.cpp:91-94).
-    size_t temp_bytes = 0;
-    CDVZ_CUDA_CHECK(cub::DeviceSegmentedRadixSort::SortPairsDescending(
-        nullptr, temp_bytes, idx->keys.as<unsigned long long>(), idx->keys2.as<unsigned long long>(), idx->vals.as<int>(),
-        idx->vals2.as<int>(), int(tot), nq, idx->seg.as<int>(), idx->seg.as<int>() + 1, 0, 64, idx->st));
-    idx->temp.ensure(temp_bytes);
-    CDVZ_CUDA_CHECK(cub::DeviceSegmentedRadixSort::SortPairsDescending(
-        idx->temp.p, temp_bytes, idx->keys.as<unsigned long long>(), idx->keys2.as<unsigned long long>(),
-        idx->vals.as<int>(), idx->vals2.as<int>(), int(tot), nq, idx->seg.as<int>(), idx->seg.as<int>() + 1, 0, 64,
-        idx->st));
     const int mc = std::max(1, std::max(qs.max_codes, idx->items.max_codes));
-    if (head > 0) {
-      const size_t sm = lm_smem_bytes(mc);
-      CDVZ_CUDA_CHECK(cudaFuncSetAttribute(k_local_head, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
-      k_local_head<<<dim3(head, nq), kLMThreads, sm, idx->st>>>(qs.view, idx->items.view, idx->vals2.as<int>(), n, head,
-                                                                 ratio_test, mc, idx->local.as<int>());
+    for (int q0 = 0; q0 < nq; q0 += qc) {
+      const int nqc = std::min(qc, nq - q0);
+      const int ntot = nqc * n;
+      k_global_keys<<<dim3((n + 255) / 256, nqc), 256, 0, idx->st>>>(qs.view, idx->items.view, idx->perm.as<int>(), n,
+                                                                      idx->items.nc, q0,
+                                                                      idx->keys.as<unsigned long long>(),
+                                                                      idx->vals.as<int>());
+      CDVZ_CUDA_CHECK(cudaGetLastError());
+      // Stable descending sort by similarity within each query: items enter in
+      // ascending id order, so ties keep ascending ids (eval.cpp:91-94).
+      size_t temp_bytes = 0;
+      CDVZ_CUDA_CHECK(cub::DeviceSegmentedRadixSort::SortPairsDescending(
+          nullptr, temp_bytes, idx->keys.as<unsigned long long>(), idx->keys2.as<unsigned long long>(),
+          idx->vals.as<int>(), idx->vals2.as<int>(), ntot, nqc, idx->seg.as<int>(), idx->seg.as<int>() + 1, 0, 64,
+          idx->st));
+      idx->temp.ensure(temp_bytes);
+      CDVZ_CUDA_CHECK(cub::DeviceSegmentedRadixSort::SortPairsDescending(
+          idx->temp.p, temp_bytes, idx->keys.as<unsigned long long>(), idx->keys2.as<unsigned long long>(),
+          idx->vals.as<int>(), idx->vals2.as<int>(), ntot, nqc, idx->seg.as<int>(), idx->seg.as<int>() + 1, 0, 64,
+          idx->st));
+      if (head > 0) {
+        const size_t sm = lm_smem_bytes(mc);
+        CDVZ_CUDA_CHECK(cudaFuncSetAttribute(k_local_head, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
+        k_local_head<<<dim3(head, nqc), kLMThreads, sm, idx->st>>>(qs.view, idx->items.view, idx->vals2.as<int>(), n,
+                                                                    head, ratio_test, mc, q0, idx->local.as<int>());
+        CDVZ_CUDA_CHECK(cudaGetLastError());
+      }
+      k_finish<<<nqc, 32, 0, idx->st>>>(idx->keys2.as<unsigned long long>(), idx->vals2.as<int>(), idx->local.as<int>(),
+                                        idx->id_rank.as<int>(), n, head, mr, q0, idx->out_i.as<int>(),
+                                        idx->out_s.as<double>());
       CDVZ_CUDA_CHECK(cudaGetLastError());
     }
-    k_finish<<<nq, 32, 0, idx->st>>>(idx->keys2.as<unsigned long long>(), idx->vals2.as<int>(), idx->local.as<int>(),
-                                     idx->id_rank.as<int>(), n, head, mr, idx->out_i.as<int>(), idx->out_s.as<double>());
-    CDVZ_CUDA_CHECK(cudaGetLastError());
     CDVZ_CUDA_CHECK(cudaMemcpyAsync(out_items, idx->out_i.p, sizeof(int) * size_t(nq) * size_t(mr), cudaMemcpyDeviceToHost,
                                     idx->st));
     CDVZ_CUDA_CHECK(cudaMemcpyAsync(out_scores, idx->out_s.p, sizeof(double) * size_t(nq) * size_t(mr),

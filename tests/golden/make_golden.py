@@ -1,9 +1,10 @@
-"""Regenerates tests/golden/oracle_containers.json from the oracle.
+"""Regenerates tests/golden/oracle_containers.json.
 
-The reference ships no golden files (all its fixtures are seeded synthesis)
-and cannot be built here, so these hashes pin the oracle restatement itself:
-frames are synth_image(seed, w, h) quantised to bytes, encoded with the
-committed bundles. Run: python tests/golden/make_golden.py
+The reference ships no golden files (all its fixtures are seeded synthesis).
+Each container here is produced by the REFERENCE ITSELF (oracle/_ref, its
+sources built against the Eigen-subset, tests/ref_lib.py) and must equal the
+oracle's, so the hashes pin both: frames are synth_image(seed, w, h) quantised
+to bytes, encoded with the committed bundles. Run: python tests/golden/make_golden.py
 """
 import hashlib
 import json
@@ -13,6 +14,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, os.path.dirname(HERE))
 import oracle_lib  # noqa: E402
+import ref_lib  # noqa: E402
 
 CASES = [
     dict(seed=1000, w=640, h=480, mode=0, bundle="b8"),   # config 1: one VGA frame, 512B
@@ -27,10 +29,13 @@ CASES = [
 
 
 def main():
-    out = {"generator": "tests/golden/make_golden.py", "cases": []}
+    out = {"generator": "tests/golden/make_golden.py (containers of the reference's own encode_image, oracle/_ref; "
+                        "the oracle's are asserted equal)", "cases": []}
     for c in CASES:
-        frame = oracle_lib.synth_u8(c["seed"], c["w"], c["h"])
-        blob = oracle_lib.encode(oracle_lib.bundle_text(c["bundle"]), frame, c["mode"])
+        frame = ref_lib.synth_u8(c["seed"], c["w"], c["h"])
+        assert (frame == oracle_lib.synth_u8(c["seed"], c["w"], c["h"])).all()
+        blob = ref_lib.encode(oracle_lib.bundle_text(c["bundle"]), frame, c["mode"])
+        assert blob == oracle_lib.encode(oracle_lib.bundle_text(c["bundle"]), frame, c["mode"]), c
         out["cases"].append(dict(c, frame_sha256=hashlib.sha256(frame.tobytes()).hexdigest(),
                                  container_sha256=hashlib.sha256(blob).hexdigest(), container_bytes=len(blob)))
         print(c, len(blob))

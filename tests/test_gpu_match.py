@@ -44,6 +44,18 @@ def test_retrieve_matches_oracle(corpus_4k, depth, ratio):
     assert np.array_equal(got_s, want_s)
 
 
+def test_retrieve_query_chunks_match_one_pass(corpus_4k, monkeypatch):
+    """Query batches run in chunks (so queries x items never overflows the
+    sort's int offsets); chunks of 5 queries give the single-pass result."""
+    index, queries = corpus_4k[:32], corpus_4k[20:40]
+    idx = cg.Index(index)
+    want_i, want_s = idx.retrieve_batch(queries, 0.85, 10)
+    monkeypatch.setenv("CDVZ_GPU_RETRIEVE_QCHUNK", "5")
+    got_i, got_s = idx.retrieve_batch(queries, 0.85, 10)
+    idx.close()
+    assert np.array_equal(got_i, want_i) and np.array_equal(got_s, want_s)
+
+
 def test_indexed_image_retrieves_itself_first(corpus_4k):
     """test_pipeline.cpp:164-170 on the GPU."""
     idx = cg.Index(corpus_4k[:16], ids=[f"img{i}" for i in range(16)])
