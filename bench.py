@@ -17,9 +17,10 @@ frames in and containers out (H2D + D2H inside the timed region); without
 torchrun at N > 1 through one multi-device context (cdvz_gpu_create_multi).
 roofline: the octave kernel pair (k_blur pyramid + k_detect extrema), timed
 standalone in one extra unoverlapped step, against measured HBM.
-cpu_baseline / --impl reference: the CPU oracle (an Eigen-free restatement of
-the reference) on the host cores, with the GPU's containers of the same frames
-compared byte for byte.
+cpu_baseline / --impl reference: the reference's own CPU implementation
+(oracle/_ref: /root/reference/proj/src built against an Eigen-subset header;
+the oracle restatement when missing) on the host cores, with the GPU's
+containers of the same frames compared byte for byte.
 """
 from __future__ import annotations
 
@@ -165,69 +166,112 @@ def cpu_model() -> str:
     return "unknown"
 
 
-def cpu_baseline(frames: np.ndarray, bundle: str, mode_id: int, gpu_containers=None):
-    """The oracle on all host cores, frame-parallel (BASELINE.md CPU mode B),
-    over a bounded sample of the timed frames (one untimed pass first), plus
-    the reference's StageTimings split from a single-threaded pass over 4
-    frames. gpu_containers: the timed step's GPU containers of the same frames,
-    compared byte for byte with the oracle's (parity beside the timing)."""
+def _cpu_impl():
+    """The CPU implementation timed as the baseline: the reference itself
+    (oracle/_ref, its sources built against the Eigen-subset) when built, else
+    the oracle restatement. Returns (kind, encode_batch(text, frames, mode,
+    threads, workers), stage_ms(text, frames, mode))."""
     sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import ref_lib
+
+    if os.path.exists(ref_lib.LIB):
+        def stage(text, frames, mode_id):
+            acc = np.zeros(5, dtype=np.float64)
+            for f in frames:
+                ref_lib.encode(text, f, mode_id, workers=1, stage_ms=acc)
+            labels = ("detection", "selection", "description", "compression", "aggregation")
+            return {k: float(v) / max(1, len(frames)) for k, v in zip(labels, acc)}
+
+        return "reference", ref_lib.encode_batch, stage
     import oracle_lib
 
     oracle_lib.build()
+    return ("port", lambda text, frames, mode_id, threads, workers: oracle_lib.encode_batch(text, frames, mode_id,
+                                                                                          threads=threads),
+            oracle_lib.stage_ms)
+
+
+def cpu_baseline(frames: np.ndarray, bundle: str, mode_id: int, gpu_containers=None):
+    """The reference's CPU implementation on the host cores over a bounded
+    sample of the timed frames: mode B (frame-parallel, one
+    Engine worker per frame: the `value`) and mode A (frames in sequence, the
+    reference's intra-frame Engine{workers = nproc}), the StageTimings split
+    from a single-threaded pass over 4 frames, the CPU model, and parity: the
+    timed step's GPU containers of the same frames against the reference's."""
+    kind, encode_batch, stage_ms = _cpu_impl()
     cores = os.cpu_count() or 1
-    oracle_lib.encode_batch(bundle, frames[:cores], mode_id, threads=cores)  # untimed warm pass
+    encode_batch(bundle, frames[:cores], mode_id, cores, 1)  # untimed warm pass
     times = []
     want = None
     for _ in range(2):
         t0 = time.perf_counter()
-        want = oracle_lib.encode_batch(bundle, frames, mode_id, threads=cores)
+        want = encode_batch(bundle, frames, mode_id, cores, 1)
         times.append(time.perf_counter() - t0)
     dt = min(times)
-    stages = oracle_lib.stage_ms(bundle, frames[:4], mode_id)
-    out = {"value": len(frames) / dt, "unit": "frames/s", "cores": cores, "kind": "port",
-           "cpu_model": cpu_model(),
-           "sample": f"{len(frames)} of the timed synthetic 640x480 frames, 4K mode, B8 bundle, frame-parallel on "
-                     f"{cores} host threads (BASELINE.md mode B; best of 2 timed passes after a warm pass)",
+    na = min(len(frames), 8)
+    t0 = time.perf_counter()
+    encode_batch(bundle, frames[:na], mode_id, 1, cores)
+    mode_a = na / (time.perf_counter() - t0)
+    stages = stage_ms(bundle, frames[:4], mode_id)
+    out = {"value": len(frames) / dt, "unit": "frames/s", "cores": cores, "kind": kind, "cpu_model": cpu_model(),
+           "sample": f"{len(frames)} of the timed synthetic 640x480 frames, 4K mode, B8 bundle; mode B: "
+                     f"frame-parallel on {cores} host threads, Engine{{workers=1}} each (best of 2 timed passes after "
+                     "a warm pass)" + ("; the reference's own code (oracle/_ref)" if kind == "reference" else
+                                       "; oracle restatement"),
+           "mode_a": {"value": mode_a, "unit": "frames/s",
+                      "sample": f"{na} frames in sequence, Engine{{workers={cores}, tile_size=32}} (the reference's "
+                                "intra-frame tile engine, parallel.cpp:40-78)"},
            "stage_ms_per_frame_single_thread": stages}
     if gpu_containers is not None:
         same = sum(1 for a, b in zip(gpu_containers, want) if a == b)
         out["parity"] = {"byte_identical": same, "of": len(want),
-                         "note": "the GPU's containers from the last timed step vs the oracle's, same frames"}
+                         "note": f"the GPU's containers from the last timed step vs the {kind}'s, same frames"}
     return out
 
 
 def run_reference(args, rank, world):
-    """--impl reference: the reference's CPU path (oracle restatement) timed on
-    the host cores, rank 0 only."""
+    """--impl reference: the reference's CPU implementation of the path (its
+    own sources in oracle/_ref; the oracle restatement if that is missing),
+    frame-parallel on all host cores, rank 0 only."""
     if rank != 0:
         return
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     import oracle_lib
 
-    oracle_lib.build()
+    kind, encode_batch, _ = _cpu_impl()
     bundle = oracle_lib.bundle_text("b8")
     cores = os.cpu_count() or 1
     sample = max(cores, 2 * cores)
     frames = oracle_lib.synth_frames(BASE_SEED, sample, FRAME_W, FRAME_H, threads=cores)
     for _ in range(args.warmup):
-        oracle_lib.encode_batch(bundle, frames[:cores], 3, threads=cores)
+        encode_batch(bundle, frames[:cores], 3, cores, 1)
     times = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        oracle_lib.encode_batch(bundle, frames, 3, threads=cores)
+        encode_batch(bundle, frames, 3, cores, 1)
         times.append(time.perf_counter() - t0)
     total = sum(times)
     value = sample * args.steps / total
+    port = None
+    if kind == "reference":
+        # The oracle restatement on the same frames, one timed pass, beside the
+        # reference's own code (which runs on the Eigen-subset header here).
+        oracle_lib.build()
+        t0 = time.perf_counter()
+        oracle_lib.encode_batch(bundle, frames, 3, threads=cores)
+        port = sample / (time.perf_counter() - t0)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * total / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"VGA 640x480 synthetic frames, 4K mode, B8 bundle; each step = {sample} frames "
                                f"(bounded sample of the {BATCH}-frame batch)", "frames_per_step": sample},
-        "cpu_baseline": {"value": value, "unit": "frames/s", "cores": cores, "kind": "port", "cpu_model": cpu_model(),
-                         "sample": f"{sample} frames per step on {cores} host threads; oracle restatement "
-                                   "(the reference needs Eigen3/doctest/CLI11, absent)"},
+        "cpu_baseline": {"value": value, "unit": "frames/s", "cores": cores, "kind": kind, "cpu_model": cpu_model(),
+                         "sample": f"{sample} frames per step, frame-parallel on {cores} host threads with "
+                                   "Engine{workers=1} each; "
+                                   + ("the reference's own proj/src built against an Eigen-subset header (oracle/_ref)"
+                                      if kind == "reference" else "oracle restatement (oracle/_ref not built)"),
+                         "port_value": port},
         "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))

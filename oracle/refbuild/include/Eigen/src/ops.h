@@ -285,23 +285,22 @@ template <class DA, class DB>
 auto product(const DA& a, const DB& b) {
   using S = scalar_t<DA>;
   if (a.cols() != b.rows()) throw std::logic_error("Eigen-subset: product size mismatch");
-  Dense<S, Dynamic, Dynamic, 0, false> r(a.rows(), b.cols());
+  using R = Dense<S, DA::RowsAtCompileTime, DB::ColsAtCompileTime, 0, false>;
+  auto r = make_result<R>(a.rows(), b.cols());
   const Index K = a.cols();
   const bool lazy = (DA::SizeAtCompileTime != Dynamic && DB::SizeAtCompileTime != Dynamic) ||
                     (b.rows() + a.rows() + b.cols() < 20 && b.rows() > 0);
-  const auto ae = a.eval();
-  const auto be = b.eval();
   for (Index i = 0; i < a.rows(); ++i)
     for (Index j = 0; j < b.cols(); ++j) {
       S acc;
       if (K == 0) {
         acc = S(0);
       } else if (lazy) {  // coefficient-based: first product, then k ascending
-        acc = ae.coeff(i, 0) * be.coeff(0, j);
-        for (Index k = 1; k < K; ++k) acc = acc + ae.coeff(i, k) * be.coeff(k, j);
+        acc = a.coeff(i, 0) * b.coeff(0, j);
+        for (Index k = 1; k < K; ++k) acc = acc + a.coeff(i, k) * b.coeff(k, j);
       } else {  // GEMM/GEMV: zero accumulator, k ascending, added to a zeroed destination
         acc = S(0);
-        for (Index k = 0; k < K; ++k) acc = acc + ae.coeff(i, k) * be.coeff(k, j);
+        for (Index k = 0; k < K; ++k) acc = acc + a.coeff(i, k) * b.coeff(k, j);
         acc = S(0) + acc;
       }
       r.coeffRef(i, j) = acc;

@@ -1,6 +1,8 @@
 """Large-scale parity evidence: the bench workload and other configurations
-encoded on the GPU and by the CPU oracle (frame-parallel on the host cores);
-counts byte-identical containers.  python tools/parity_sweep.py [out.json]"""
+encoded on the GPU, by the CPU oracle and by the REFERENCE ITSELF (oracle/_ref,
+its sources built against the Eigen-subset), both frame-parallel on the host
+cores; counts byte-identical containers against each.
+python tools/parity_sweep.py [out.json]"""
 import json
 import os
 import sys
@@ -12,6 +14,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "tests"))
 import oracle_lib  # noqa: E402
+import ref_lib  # noqa: E402
 import paper_1705_09776_b200 as cg  # noqa: E402
 
 
@@ -24,8 +27,14 @@ def sweep(name, bundle, frames, mode, max_side=640):
     want = oracle_lib.encode_batch(text, frames, cg.mode_by_name(mode).id if isinstance(mode, str) else mode,
                                    max_side=max_side, threads=os.cpu_count() or 8)
     same = sum(int(a == b) for a, b in zip(got, want))
+    oracle_s = round(time.time() - t, 1)
+    t = time.time()
+    mid = cg.mode_by_name(mode).id if isinstance(mode, str) else mode
+    ref = ref_lib.encode_batch(text, frames, mid, threads=os.cpu_count() or 8, workers=1, max_side=max_side)
+    same_ref = sum(int(a == b) for a, b in zip(got, ref))
     row = {"case": name, "bundle": bundle, "mode": mode, "frames": len(frames), "size": list(frames.shape[1:3][::-1]),
-           "gpu_ok": int((status == 0).sum()), "byte_identical": same, "oracle_s": round(time.time() - t, 1)}
+           "gpu_ok": int((status == 0).sum()), "byte_identical": same, "byte_identical_vs_reference": same_ref,
+           "oracle_s": oracle_s, "reference_s": round(time.time() - t, 1)}
     print(json.dumps(row), flush=True)
     return row
 
@@ -43,7 +52,8 @@ def main(out):
         json.dump(rows, f, indent=1)
     total = sum(r["frames"] for r in rows)
     same = sum(r["byte_identical"] for r in rows)
-    print(f"{same}/{total} containers byte-identical")
+    same_ref = sum(r["byte_identical_vs_reference"] for r in rows)
+    print(f"{same}/{total} containers byte-identical to the oracle, {same_ref}/{total} to the reference")
 
 
 if __name__ == "__main__":
