@@ -92,7 +92,8 @@ struct Batch {
   int* or_count;                       // [frame]
   DescGeo* geo;                        // [frame][cap_or]
   int smp_cap;                         // samples per oriented point (max samples^2)
-  double2* smp;                        // [frame][cap_or][smp_cap] {weight (+0: skipped), ob = phi/2pi*8 - 0.5}
+  double2* smp;                        // [frame][cap_or][smp_cap] {weight (+0: skipped), fo}, row stride samples
+  uint8_t* smpb;                       // [frame][cap_or][32][32] orientation bin ob0 mod 8 of each sample
   double* desc;                        // [frame][cap_or][128]
   uint8_t* codes;                      // [frame][cap_or][code_stride]
   int code_stride;

@@ -22,6 +22,7 @@
 
 #include <cuda.h>
 #include <cudaTypedefs.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include "../../include/cdvz_gpu.h"
 #include "bundle.hpp"
@@ -33,7 +34,8 @@ cudaError_t launch_detect(const Batch& bt, const DetConst& dc, int o, const CUte
 cudaError_t launch_merge(const Batch& bt, int o, cudaStream_t st);
 int merge_cell_px(int W, int H);
 cudaError_t launch_select(const Batch& bt, const Model& md, const EncodeConst& ec, cudaStream_t st);
-cudaError_t launch_describe(const Batch& bt, const DetConst& dc, const Model& md, const EncodeConst& ec, cudaStream_t st);
+cudaError_t launch_describe(const Batch& bt, const DetConst& dc, cudaStream_t st);
+cudaError_t launch_compress(const Batch& bt, const Model& md, const EncodeConst& ec, cudaStream_t st);
 cudaError_t launch_scfv_pack(const Batch& bt, const Model& md, const EncodeConst& ec, uint8_t* out, uint32_t* lengths,
                              cudaStream_t st, cudaEvent_t after_aggregation);
 cudaError_t launch_resize_f64(const double* grey, int w_in, int h_in, double* out, int w_out, int h_out, int frames,
@@ -57,6 +59,16 @@ using namespace cdvz_gpu;
 namespace {
 
 thread_local std::string g_create_error;
+
+// NVTX ranges (header-only nvtx3: no-ops unless a profiler injects itself) name
+// the host side of a call in an Nsight / ncu --nvtx timeline: the public
+// entry, each device shard's thread, and each chunk's enqueue.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 struct DeviceBuffer {
   void* p = nullptr;
@@ -423,6 +435,7 @@ struct cdvz_gpu_ctx {
       nb.smp_cap = smax * smax;
     }
     nb.smp = static_cast<double2*>(alloc(sizeof(double2) * F * nb.cap_or * nb.smp_cap));
+    nb.smpb = static_cast<uint8_t*>(alloc(size_t(F) * nb.cap_or * 32 * 32));
     nb.desc = static_cast<double*>(alloc(sizeof(double) * F * nb.cap_or * 128));
     nb.codes = static_cast<uint8_t*>(alloc(F * nb.cap_or * nb.code_stride));
     nb.x = static_cast<double*>(alloc(sizeof(double) * F * nb.cap_or * 32));
@@ -490,8 +503,10 @@ struct cdvz_gpu_ctx {
   // Folds a finished chunk's events into its call's statistics (blocks until
   // the chunk is done). Stage labels follow the reference's time_stage calls
   // (pipeline.cpp:19-94): detection, selection, description (orientation +
-  // description), compression (transform + ternary + location quantisers,
-  // fused into the description kernel's epilogue: its own event pair), aggregation.
+  // description), compression (k_compress: transform + ternary + location
+  // quantisers, pipeline.cpp:37-50), aggregation (PCA + posteriors + Fisher +
+  // SCFV coding). The container pack follows, outside the labels, as
+  // serialize_container is outside encode_image.
   void collect(Lane& L) {
     if (!L.pending) return;
     CDVZ_CUDA_CHECK(cudaEventSynchronize(L.done));
@@ -500,8 +515,8 @@ struct cdvz_gpu_ctx {
     cudaEventElapsedTime(&t[0], L.start, L.stage[1]);
     cudaEventElapsedTime(&t[1], L.stage[1], L.stage[2]);
     cudaEventElapsedTime(&t[2], L.stage[2], L.stage[3]);
-    cudaEventElapsedTime(&t[3], L.stage[4], L.stage[5]);
-    cudaEventElapsedTime(&t[4], L.stage[3], L.stage[4]);
+    cudaEventElapsedTime(&t[3], L.stage[3], L.stage[4]);
+    cudaEventElapsedTime(&t[4], L.stage[4], L.stage[5]);
     for (int i = 0; i < 5; ++i) st_.stage_ms[i] += t[i];
     for (int o = 0; o < L.pending_oct; ++o) {
       float a = 0.f, b = 0.f;
@@ -615,6 +630,7 @@ struct cdvz_gpu_ctx {
       }
     }
     for (int c = 0; c < chunks; ++c) {
+      NvtxRange nv("cdvz chunk enqueue");
       const int base = cb[size_t(c)];
       const int nf = cb[size_t(c) + 1] - base;
       Lane& L = lanes[serial ? 0 : (lane0 + c) % kLanes];
@@ -685,10 +701,13 @@ struct cdvz_gpu_ctx {
       CDVZ_CUDA_CHECK(cudaEventRecord(L.stage[1], sB));
       CDVZ_CUDA_CHECK(launch_select(b, md, ec, sB));
       CDVZ_CUDA_CHECK(cudaEventRecord(L.stage[2], sB));
-      CDVZ_CUDA_CHECK(launch_describe(b, dc, md, ec, sB));
+      CDVZ_CUDA_CHECK(launch_describe(b, dc, sB));
       CDVZ_CUDA_CHECK(cudaEventRecord(L.stage[3], sB));
-      CDVZ_CUDA_CHECK(launch_scfv_pack(b, md, ec, d_out + (long long)base * ec.slot_bytes, d_len + base, sB, L.stage[4]));
-      CDVZ_CUDA_CHECK(cudaEventRecord(L.stage[5], sB));
+      CDVZ_CUDA_CHECK(launch_compress(b, md, ec, sB));
+      CDVZ_CUDA_CHECK(cudaEventRecord(L.stage[4], sB));
+      // The container pack runs after the aggregation event: the reference
+      // serialises outside encode_image's timed stages.
+      CDVZ_CUDA_CHECK(launch_scfv_pack(b, md, ec, d_out + (long long)base * ec.slot_bytes, d_len + base, sB, L.stage[5]));
       if (h_out) {
         CDVZ_CUDA_CHECK(cudaMemcpyAsync(h_out + size_t(base) * ec.slot_bytes, d_out + size_t(base) * ec.slot_bytes,
                                         size_t(nf) * ec.slot_bytes, cudaMemcpyDeviceToHost, sB));
@@ -706,7 +725,7 @@ struct cdvz_gpu_ctx {
       // The next chunk on this lane's stream A must not overwrite the pyramid
       // before stream B is done with it.
       CDVZ_CUDA_CHECK(cudaStreamWaitEvent(L.sA, L.done, 0));
-      launches += 1 + 5 + 5;  // k_select; k_orient, k_expand, k_geometry, k_sample, k_describe; SCFV + pack
+      launches += 1 + 5 + 1 + 5;  // k_select; k_orient, k_expand, k_geometry, k_sample, k_describe; k_compress; SCFV + pack
       L.pending = true;
       L.pending_call = call;
       L.pending_oct = b.n_oct;
@@ -977,6 +996,7 @@ void encode_multi(cdvz_gpu_ctx* ctx, const uint8_t* pixels, int width, int heigh
     const uint8_t* src = pixels + size_t(start[size_t(d)]) * height * stride;
     th.emplace_back([&, d, n, region, src] {
       if (n == 0) return;
+      NvtxRange r("cdvz_gpu shard");
       rc[size_t(d)] = encode_host_batch(ctx->shards[size_t(d)].get(), src, width, height, stride, n, mode_id, max_side,
                                         region, size_t(n) * slot, off[size_t(d)].data(), status + start[size_t(d)], kind);
     });
@@ -1034,6 +1054,7 @@ void encode_multi(cdvz_gpu_ctx* ctx, const uint8_t* pixels, int width, int heigh
 // f64 grey rasters (kind 8; `stride` in bytes).
 int encode_host_batch(cdvz_gpu_ctx* ctx, const uint8_t* pixels, int width, int height, size_t stride, int count,
                       int mode_id, int max_side, uint8_t* out, size_t out_cap, size_t* offsets, int* status, int kind) {
+  NvtxRange nv("cdvz_gpu_encode_batch");
   return guarded(ctx, [&] {
     const int channels = kind == 3 ? 3 : 1;
     const size_t elem = kind == 8 ? sizeof(double) : 1;

@@ -174,30 +174,29 @@ __device__ __forceinline__ float rsqrt_approx(float x) {
   return r;
 }
 
-// Conservative FP32 screen (FP32 pipe + MUFU, beside the FP64 work): a pixel
-// is dropped only when the discriminant is negative (the reference's own
-// exact test, in FP64), or no float root lies within [s_lo - 0.05, s_hi + 0.05],
-// or no in-range root can reach |p| >= thr with a margin of 1e-5 of the
-// coefficient magnitudes — orders of magnitude above FP32 rounding of the
-// reference's own formulas. Near-double roots and degenerate cases go to the
-// exact path.
-__device__ __forceinline__ bool screen_pixel(const double a[4], const double up[4], const double dn[4],
+// Conservative FP32 screen (FP32 pipe + MUFU, beside the FP64 work) on the
+// float copies of alpha (each alpha converted once, when its row is formed):
+// a pixel is dropped only when the discriminant is clearly negative (the
+// reference's own test is disc < 0: no real root), or no float root lies
+// within [s_lo - 0.05, s_hi + 0.05], or no in-range root can reach |p| >= thr
+// with a margin of 1e-5 of the coefficient magnitudes, or the up or down
+// neighbour is clearly past p — every margin orders of magnitude above the
+// float error (the alpha copies are within 6e-8 relative of the exact values;
+// fused multiply-adds are fine: this only screens). Near-double roots and
+// degenerate cases go to the exact path.
+__device__ __forceinline__ bool screen_pixel(const float a[4], const float up[4], const float dn[4],
                                               const DetConst& dc) {
-  const double qa = 3.0 * a[3], qb = 2.0 * a[2], qc = a[1];
-  if (qa == 0.0) return true;
-  const double disc = qb * qb - 4.0 * qa * qc;
-  if (disc < 0.0) return false;  // exactly the reference's test: no real root
-  if (!(disc > 1e-6 * (qb * qb))) return true;  // near-double root: let the exact path decide
-  // FP32 from here on (fused multiply-adds are fine: this only screens, and
-  // its margins dwarf FP32 rounding).
-  const float fa = float(qa), fb = float(qb), fc = float(qc), fd = float(disc);
+  const float fa = 3.0f * a[3], fb = 2.0f * a[2], fc = a[1];
+  if (fa == 0.0f) return true;
+  const float bb = fb * fb, ac4 = 4.0f * fa * fc;
+  const float fd = bb - ac4;
+  const float de = 1e-5f * (bb + fabsf(ac4)) + 1e-30f;
+  if (fd < -de) return false;         // the reference's disc < 0, by a margin
+  if (!(fd > de)) return true;        // near-double root, or not finite: the exact path decides
   const float sq = fd * rsqrt_approx(fd);
   const float q = -0.5f * (fb + copysignf(sq, fb));
   if (!(fabsf(q) > 1e-30f)) return true;
   const float r0 = q * rcp_approx(fa), r1 = fc * rcp_approx(q);
-  const float a0 = float(a[0]), a1 = float(a[1]), a2 = float(a[2]), a3 = float(a[3]);
-  const float u0 = float(up[0]), u1 = float(up[1]), u2 = float(up[2]), u3 = float(up[3]);
-  const float d0 = float(dn[0]), d1 = float(dn[1]), d2 = float(dn[2]), d3 = float(dn[3]);
   auto horner = [](float r, float c0, float c1, float c2, float c3) {
     return __fmaf_rn(r, __fmaf_rn(r, __fmaf_rn(r, c3, c2), c1), c0);
   };
@@ -209,24 +208,36 @@ __device__ __forceinline__ bool screen_pixel(const double a[4], const double up[
       if (!isfinite(r)) any = true;
       continue;
     }
-    const float p = horner(r, a0, a1, a2, a3);
-    const float bound = horner(r, fabsf(a0), fabsf(a1), fabsf(a2), fabsf(a3));
+    const float p = horner(r, a[0], a[1], a[2], a[3]);
+    const float bound = horner(r, fabsf(a[0]), fabsf(a[1]), fabsf(a[2]), fabsf(a[3]));
     if (!(__fmaf_rn(1e-5f, bound, fabsf(p) + 1e-6f) >= dc.scr_thr)) continue;
     // The exact test needs p above (p > 0) or below (p < 0) all eight
     // neighbours' cubics at the same scale; drop the root only when the up or
     // down neighbour is clearly past p. The float root is within ~1e-6 s of
     // the exact one and p is stationary there, so a margin of 1e-4 of the
     // magnitudes (values plus slopes) is far beyond the float error.
-    const float pu = horner(r, u0, u1, u2, u3), pd = horner(r, d0, d1, d2, d3);
-    const float bu = horner(r, fabsf(u0), fabsf(u1), fabsf(u2), fabsf(u3));
-    const float bd = horner(r, fabsf(d0), fabsf(d1), fabsf(d2), fabsf(d3));
-    const float su = __fmaf_rn(r, __fmaf_rn(r, 3.0f * fabsf(u3), 2.0f * fabsf(u2)), fabsf(u1));
-    const float sd = __fmaf_rn(r, __fmaf_rn(r, 3.0f * fabsf(d3), 2.0f * fabsf(d2)), fabsf(d1));
+    const float pu = horner(r, up[0], up[1], up[2], up[3]), pd = horner(r, dn[0], dn[1], dn[2], dn[3]);
+    const float bu = horner(r, fabsf(up[0]), fabsf(up[1]), fabsf(up[2]), fabsf(up[3]));
+    const float bd = horner(r, fabsf(dn[0]), fabsf(dn[1]), fabsf(dn[2]), fabsf(dn[3]));
+    const float su = __fmaf_rn(r, __fmaf_rn(r, 3.0f * fabsf(up[3]), 2.0f * fabsf(up[2])), fabsf(up[1]));
+    const float sd = __fmaf_rn(r, __fmaf_rn(r, 3.0f * fabsf(dn[3]), 2.0f * fabsf(dn[2])), fabsf(dn[1]));
     const float m = 1e-4f * (bound + bu + bd + su + sd) + 1e-7f;
     const bool past = p > 0.0f ? (pu >= p + m || pd >= p + m) : (pu <= p - m || pd <= p - m);
     if (!past) any = true;
   }
   return any;
+}
+
+__device__ __forceinline__ bool screen_pixel(const double a[4], const double up[4], const double dn[4],
+                                              const DetConst& dc) {
+  float af[4], uf[4], df[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    af[i] = float(a[i]);
+    uf[i] = float(up[i]);
+    df[i] = float(dn[i]);
+  }
+  return screen_pixel(af, uf, df, dc);
 }
 
 // ---------------------------------------------------------------- K1a: blur
@@ -588,6 +599,7 @@ constexpr int kStripCols = 30, kSegTarget = 96, kRing = 6, kDetWarps = 3, kPrefe
 struct DetWarpSmem {
   double grow[kGRows][4][34];  // G rows in flight: [row % kGRows][level][1 + lane], edges at 0 and 33
   double ring[kRing][4][32];   // alpha rows: [row % kRing][coefficient][lane]
+  float4 fring[4][32];         // float copies of alpha rows ra - 2 .. ra + 1 (the screen's inputs): [row % 4][lane]
   uint16_t queue[128];         // ((row - y0 + 2) << 5) | lane
 };
 
@@ -595,7 +607,7 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
 }
 
-__global__ void __launch_bounds__(32 * kDetWarps) k_detect_walk(Batch bt, DetConst dc, int o, int seg_rows) {
+__global__ void __maxnreg__(96) k_detect_walk(Batch bt, DetConst dc, int o, int seg_rows) {
   extern __shared__ __align__(16) uint8_t det_smem[];
   const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
   DetWarpSmem& S = reinterpret_cast<DetWarpSmem*>(det_smem)[wi];
@@ -636,7 +648,7 @@ __global__ void __launch_bounds__(32 * kDetWarps) k_detect_walk(Batch bt, DetCon
 #pragma unroll
   for (int i = 0; i < kPrefetch + 2; ++i) issue();  // rows y0 - 2 .. y0 + kPrefetch - 1
   const double oct_scale = ldexp(1.0, o);
-  double ap[4];  // own alpha of the previous row (screened one row late)
+  float apf[4];  // own alpha (float copy) of the previous row (screened one row late)
   int qn = 0;
   auto drain = [&]() {
     for (int qi = lane; qi - lane < qn; qi += 32) {
@@ -672,7 +684,7 @@ __global__ void __launch_bounds__(32 * kDetWarps) k_detect_walk(Batch bt, DetCon
       an[i] = sum;
     }
   };
-  auto screen_row = [&](int rs, const double a[4], const double up[4], const double dn[4]) {  // 3x3 neighbourhood complete
+  auto screen_row = [&](int rs, const float a[4], const float up[4], const float dn[4]) {  // 3x3 neighbourhood complete
     if (rs >= y0 && rs < y1) {
       const bool push = out_col && (!dc.screen || screen_pixel(a, up, dn, dc));
       const unsigned bal = __ballot_sync(0xffffffffu, push);
@@ -695,23 +707,26 @@ __global__ void __launch_bounds__(32 * kDetWarps) k_detect_walk(Batch bt, DetCon
       alpha_row(ra, a0);
       alpha_row(ra + 1, a1);
       const bool second = t + 1 < T;
+      const float a0f[4] = {float(a0[0]), float(a0[1]), float(a0[2]), float(a0[3])};
+      const float a1f[4] = {float(a1[0]), float(a1[1]), float(a1[2]), float(a1[3])};
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         S.ring[unsigned(ra) % kRing][i][lane] = a0[i];
         if (second) S.ring[unsigned(ra + 1) % kRing][i][lane] = a1[i];
       }
+      S.fring[unsigned(ra) % 4][lane] = make_float4(a0f[0], a0f[1], a0f[2], a0f[3]);
+      if (second) S.fring[unsigned(ra + 1) % 4][lane] = make_float4(a1f[0], a1f[1], a1f[2], a1f[3]);
       __syncwarp();
       issue();  // rows ra + kPrefetch + 1, ra + kPrefetch + 2 into the slots of rows ra - 1, ra
       issue();
       {
-        double au[4];  // own alpha of row ra - 2 (the ring keeps it)
-#pragma unroll
-        for (int i = 0; i < 4; ++i) au[i] = S.ring[unsigned(ra - 2) % kRing][i][lane];
-        screen_row(ra - 1, ap, au, a0);
+        const float4 u4 = S.fring[unsigned(ra - 2) % 4][lane];  // own alpha of row ra - 2 (the ring keeps it)
+        const float auf[4] = {u4.x, u4.y, u4.z, u4.w};
+        screen_row(ra - 1, apf, auf, a0f);
       }
-      if (second) screen_row(ra, a0, ap, a1);
+      if (second) screen_row(ra, a0f, apf, a1f);
 #pragma unroll
-      for (int i = 0; i < 4; ++i) ap[i] = a1[i];
+      for (int i = 0; i < 4; ++i) apf[i] = a1f[i];
     }
     __syncwarp();
     // Every queued pixel (rows <= the last alpha row - 1) has its
