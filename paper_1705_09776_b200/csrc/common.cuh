@@ -48,6 +48,7 @@ struct DetConst {
   int screen;          // 1: FP32 pre-screen before the exact test; 0: exact test on every pixel
   float scr_lo, scr_hi, scr_thr;  // screen constants: s_lo - 0.05, s_hi + 0.05, thr (FP32)
   int walk;            // 1: warp column-walk extrema kernel; 0: TMA tile kernel
+  int blur_unrolled;   // 1: k_blur's y pass unrolled by one accumulator period; 0: rolled (shifted accumulators)
 };
 
 // Per-batch geometry and buffer map (device pointers). One instance lives in
@@ -147,6 +148,7 @@ struct EncodeConst {
   uint32_t model_crc;
   double half_diag, cx, cy;     // fill_center_distance constants
   double log2_range;            // log2(64 / 0.5)
+  int post_dmma;                // 1: posteriors on the FP64 tensor cores (measurement only)
 };
 
 __host__ __device__ inline int mirror_index(int i, int n) {

@@ -30,7 +30,8 @@
 
 namespace cdvz_gpu {
 cudaError_t launch_octave(const Batch& bt, const DetConst& dc, int o, int src, cudaStream_t st);
-cudaError_t launch_detect(const Batch& bt, const DetConst& dc, int o, const CUtensorMap* tmap, cudaStream_t st);
+cudaError_t launch_detect(const Batch& bt, const DetConst& dc, int o, const CUtensorMap* tmap, const CUtensorMap* wmap,
+                          cudaStream_t st);
 cudaError_t launch_merge(const Batch& bt, int o, cudaStream_t st);
 int merge_cell_px(int W, int H);
 cudaError_t launch_select(const Batch& bt, const Model& md, const EncodeConst& ec, cudaStream_t st);
@@ -125,7 +126,8 @@ struct Lane {
   cudaEvent_t start = nullptr, done = nullptr;
   cudaEvent_t stage[6] = {};
   cudaEvent_t blur[2 * kMaxOctaves] = {}, det[2 * kMaxOctaves] = {};
-  CUtensorMap tmap[kMaxOctaves];   // 4-D view (x, y, level, frame) of each octave's G planes
+  CUtensorMap tmap[kMaxOctaves];   // 4-D view (x, y, level, frame) of each octave's G planes (k_detect tiles)
+  CUtensorMap wmap[kMaxOctaves];   // the same view with k_detect_walk's box: 34 columns x 2 rows x 4 levels
   bool tmap_ok[kMaxOctaves] = {};
   bool pending = false;   // events of an enqueued chunk not yet folded into the stats
   long long pending_call = 0;  // the call that enqueued it
@@ -178,6 +180,7 @@ struct cdvz_gpu_ctx {
   bool debug = false;
   bool serial = false;
   bool tma_disabled = false;
+  bool post_dmma = false;  // debug bit 128: SCFV posteriors on the FP64 tensor cores (measurement)
   bool cap_boost = false;  // plan the maximal survivor / orientation capacities (capacity retry of single frames)
   bool tiny_caps = false;  // debug bit 5: tiny batch capacities, so ordinary frames exercise the capacity retry
   // A multi-device context (cdvz_gpu_create_multi) owns one single-device
@@ -283,6 +286,7 @@ struct cdvz_gpu_ctx {
     dc.margin = b.margin;
     dc.screen = 1;
     dc.walk = 1;
+    dc.blur_unrolled = 0;
 
     for (int c = 0; c < 5; ++c) {
       md.rel_edges[c] = upload(b.relevance[std::size_t(c)].edges.data(), b.relevance[std::size_t(c)].edges.size());
@@ -470,7 +474,11 @@ struct cdvz_gpu_ctx {
       const CUresult r = encode(&L.tmap[o], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, nb.pyr + nb.plane_off[o][0], dims, strides,
                                 box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                                 CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-      L.tmap_ok[o] = (r == CUDA_SUCCESS);
+      const cuuint32_t wbox[4] = {34, 2, 4, 1};
+      const CUresult rw = encode(&L.wmap[o], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, nb.pyr + nb.plane_off[o][0], dims, strides,
+                                 wbox, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      L.tmap_ok[o] = (r == CUDA_SUCCESS) && (rw == CUDA_SUCCESS);
     }
     L.bt = nb;
     L.geo_w = W;
@@ -497,6 +505,7 @@ struct cdvz_gpu_ctx {
     ec.global_bytes = int(bu.global_bytes);
     ec.slot_bytes = int(m.budget + 28);
     ec.model_crc = bundle.model_crc;
+    ec.post_dmma = post_dmma ? 1 : 0;
     return ec;
   }
 
@@ -678,7 +687,7 @@ struct cdvz_gpu_ctx {
         CDVZ_CUDA_CHECK(cudaEventRecord(L.blur[2 * o + 1], L.sA));
         CDVZ_CUDA_CHECK(cudaStreamWaitEvent(sB, L.blur[2 * o + 1], 0));
         CDVZ_CUDA_CHECK(cudaEventRecord(L.det[2 * o], sB));
-        CDVZ_CUDA_CHECK(launch_detect(b, dc, o, L.tmap_ok[o] ? &L.tmap[o] : nullptr, sB));
+        CDVZ_CUDA_CHECK(launch_detect(b, dc, o, L.tmap_ok[o] ? &L.tmap[o] : nullptr, L.tmap_ok[o] ? &L.wmap[o] : nullptr, sB));
         CDVZ_CUDA_CHECK(cudaEventRecord(L.det[2 * o + 1], sB));
         CDVZ_CUDA_CHECK(launch_merge(b, o, sB));
         launches += 3;
@@ -906,6 +915,8 @@ int cdvz_gpu_set_debug(cdvz_gpu_ctx* ctx, int on) {
   ctx->serial = (on & 4) != 0;
   ctx->dc.walk = (on & 16) ? 0 : 1;
   ctx->tiny_caps = (on & 32) != 0;
+  ctx->dc.blur_unrolled = (on & 64) ? 1 : 0;
+  ctx->post_dmma = (on & 128) != 0;
   if (ctx->tma_disabled != ((on & 8) != 0)) {
     ctx->tma_disabled = (on & 8) != 0;
     for (auto& l : ctx->lanes) l.geo_w = 0;  // rebuild the tensor maps
@@ -1458,7 +1469,7 @@ int cdvz_gpu_pyramid_bench(cdvz_gpu_ctx* ctx, const uint8_t* d_pixels, int width
       CDVZ_CUDA_CHECK(cudaMemsetAsync(b.raw_count, 0, sizeof(int) * count * std::max(1, b.n_oct), L.sA));
       for (int o = 0; o < b.n_oct; ++o) {
         CDVZ_CUDA_CHECK(launch_octave(b, ctx->dc, o, o == 0 ? 0 : 2, L.sA));
-        CDVZ_CUDA_CHECK(launch_detect(b, ctx->dc, o, L.tmap_ok[o] ? &L.tmap[o] : nullptr, L.sA));
+        CDVZ_CUDA_CHECK(launch_detect(b, ctx->dc, o, L.tmap_ok[o] ? &L.tmap[o] : nullptr, L.tmap_ok[o] ? &L.wmap[o] : nullptr, L.sA));
       }
     };
     pass();  // warm-up

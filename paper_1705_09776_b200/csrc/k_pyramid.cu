@@ -294,7 +294,7 @@ struct BlurSmem {
   };
 };
 
-template <int R, int LVL, int SRC, int NT>
+template <int R, int LVL, int SRC, int NT, bool UNROLL>
 __device__ __forceinline__ void blur_level(const Batch& bt, const DetConst& dc, int f, int o, BlurSmem& S) {
   constexpr int CH = 2 * R + 1, NS = 2 * NT + 2 * R;
   static_assert(NS >= 2 * NT && NS <= 3 * NT && NS <= kBlurNS, "staging layout");
@@ -375,6 +375,76 @@ __device__ __forceinline__ void blur_level(const Batch& bt, const DetConst& dc, 
   double* gcol = G + cx;
   const bool vec = col1 && (w & 1) == 0 && (reinterpret_cast<uintptr_t>(gcol) & 15) == 0;
   const int nrows = h + 2 * R;  // virtual rows r = 0 .. nrows-1 (v = r - R)
+  if constexpr (!UNROLL) {
+    // Rolled row loop (a few hundred instructions, resident in the
+    // instruction cache): acc[s] holds output row v - R + s; row v adds
+    // k_|R-s| x[v] to each pending row, starts row v + R, completes row v - R,
+    // and the accumulators shift down by one (register moves, no FP64).
+#pragma unroll 1
+    for (int r = 0; r < nrows; ++r) {
+      const double* row;
+      if constexpr (SRC == 0 || SRC == 3) {
+        cp_wait<kBlurAhead - 2>();
+        __syncthreads();
+        issue(r + kBlurAhead, is);
+        convert(r + 1, next(rs));
+        row = S.u8.conv[r & 1];
+      } else {
+        cp_wait<kBlurAhead - 1>();
+        __syncthreads();
+        issue(r + kBlurAhead, is);
+        row = S.f64[rs];
+      }
+      double b[2 * R + 2];
+      const double2* sp = reinterpret_cast<const double2*>(row + 2 * t);
+#pragma unroll
+      for (int k = 0; k <= R; ++k) {
+        const double2 q = sp[k];
+        b[2 * k] = q.x;
+        b[2 * k + 1] = q.y;
+      }
+      double xa = tp[R] * b[0], xb = tp[R] * b[1];
+#pragma unroll
+      for (int j = 1; j <= 2 * R; ++j) {
+        const double k = tp[j < R ? R - j : j - R];
+        xa = xa + k * b[j];
+        xb = xb + k * b[j + 1];
+      }
+      double pa[R + 1], pb[R + 1];
+#pragma unroll
+      for (int j = 0; j <= R; ++j) {
+        pa[j] = tp[j] * xa;
+        pb[j] = tp[j] * xb;
+      }
+#pragma unroll
+      for (int s2 = 0; s2 < 2 * R; ++s2) {
+        const int j = s2 < R ? R - s2 : s2 - R;
+        acc0[s2] = acc0[s2] + pa[j];
+        acc1[s2] = acc1[s2] + pb[j];
+      }
+      acc0[2 * R] = pa[R];  // first term of output row v + R
+      acc1[2 * R] = pb[R];
+      rs = next(rs);
+      is = next(is);
+      const int y = r - 2 * R;  // complete: its last term (row y + R) was just added
+      if (y >= 0 && y < h) {
+        double* gp = gcol + (long long)y * w;
+        if (vec) {
+          *reinterpret_cast<double2*>(gp) = make_double2(acc0[0], acc1[0]);
+        } else {
+          if (col0) gp[0] = acc0[0];
+          if (col1) gp[1] = acc1[0];
+        }
+      }
+#pragma unroll
+      for (int s2 = 0; s2 < 2 * R; ++s2) {
+        acc0[s2] = acc0[s2 + 1];
+        acc1[s2] = acc1[s2 + 1];
+      }
+    }
+    cp_wait<0>();
+    return;
+  }
   for (int rc = 0; rc < nrows; rc += CH) {
 #pragma unroll
     for (int i = 0; i < CH; ++i) {
@@ -440,17 +510,17 @@ __device__ __forceinline__ void blur_level(const Batch& bt, const DetConst& dc, 
   cp_wait<0>();
 }
 
-template <int R0, int R1, int R2, int R3, int SRC, int NT>
+template <int R0, int R1, int R2, int R3, int SRC, int NT, bool UNROLL>
 __global__ void __launch_bounds__(NT) k_blur(Batch bt, DetConst dc, int o) {
   __shared__ __align__(16) BlurSmem S;
   // Level-major grid (blockIdx.z = level): the CTAs resident on an SM at any
-  // moment mostly share one level's unrolled loop in the instruction cache.
+  // moment mostly share one level's loop in the instruction cache.
   const int f = blockIdx.y;
   switch (blockIdx.z) {
-    case 0: blur_level<R0, 0, SRC, NT>(bt, dc, f, o, S); break;
-    case 1: blur_level<R1, 1, SRC, NT>(bt, dc, f, o, S); break;
-    case 2: blur_level<R2, 2, SRC, NT>(bt, dc, f, o, S); break;
-    default: blur_level<R3, 3, SRC, NT>(bt, dc, f, o, S); break;
+    case 0: blur_level<R0, 0, SRC, NT, UNROLL>(bt, dc, f, o, S); break;
+    case 1: blur_level<R1, 1, SRC, NT, UNROLL>(bt, dc, f, o, S); break;
+    case 2: blur_level<R2, 2, SRC, NT, UNROLL>(bt, dc, f, o, S); break;
+    default: blur_level<R3, 3, SRC, NT, UNROLL>(bt, dc, f, o, S); break;
   }
 }
 
@@ -596,19 +666,41 @@ __global__ void __launch_bounds__(kDetThreads, 2)
 // FP64 test (exact_detect, reading the 3x3 alpha neighbourhood from the ring)
 // before the ring can overwrite any row a queued pixel needs.
 constexpr int kStripCols = 30, kSegTarget = 96, kRing = 6, kDetWarps = 3, kPrefetch = 2, kGRows = kPrefetch + 2;  // kDetWarps: max warps per CTA
-struct DetWarpSmem {
-  double grow[kGRows][4][34];  // G rows in flight: [row % kGRows][level][1 + lane], edges at 0 and 33
+struct alignas(128) DetWarpSmem {
+  union {
+    double grow[kGRows][4][34];   // cp.async path: G rows in flight [row % kGRows][level][1 + lane], edges at 0 and 33
+    double gpair[2][4][2][34];    // TMA path: row pairs [pair % 2][level][row of pair][1 + lane] (one 4-D box each)
+  };
   double ring[kRing][4][32];   // alpha rows: [row % kRing][coefficient][lane]
   float4 fring[4][32];         // float copies of alpha rows ra - 2 .. ra + 1 (the screen's inputs): [row % 4][lane]
+  uint64_t bar[2];             // TMA path: one mbarrier per pair slot
   uint16_t queue[128];         // ((row - y0 + 2) << 5) | lane
 };
+static_assert(sizeof(double) * 4 * 2 * 34 % 128 == 0, "TMA pair slots stay 128-byte aligned");
 
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
 }
 
-__global__ void __maxnreg__(96) k_detect_walk(Batch bt, DetConst dc, int o, int seg_rows) {
-  extern __shared__ __align__(16) uint8_t det_smem[];
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done) : "r"(bar), "r"(parity) : "memory");
+  }
+}
+
+// TMA = true: G rows arrive as row pairs, one 4-D TMA box (34 columns x 2 rows
+// x 4 levels) per pair issued by lane 0 into a 2-slot ring with an mbarrier
+// per slot — one instruction per pair instead of 8-16 cp.async per lane and
+// row (needs even widths: 16-byte row strides; the walk map is built in
+// plan()). Columns of the box past the image arrive as zeros; they only feed
+// alpha outside the detection window, which is never screened or used.
+template <bool TMA>
+__global__ void __maxnreg__(96) k_detect_walk(Batch bt, DetConst dc, int o, int seg_rows,
+                                              const __grid_constant__ CUtensorMap wmap) {
+  extern __shared__ __align__(128) uint8_t det_smem[];
   const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
   DetWarpSmem& S = reinterpret_cast<DetWarpSmem*>(det_smem)[wi];
   const int f = blockIdx.z;
@@ -632,6 +724,22 @@ __global__ void __maxnreg__(96) k_detect_walk(Batch bt, DetConst dc, int o, int 
     for (int k = 0; k < 4; ++k) gp[k] = base + bt.plane_off[o][k] + xc;
   }
   int next_row = y0 - 2;
+  // TMA path: pair p holds rows y0 - 2 + 2p, y0 - 1 + 2p in slot p & 1 (phase p >> 1).
+  const int npairs = (y1 - y0 + 5) >> 1;  // rows y0 - 2 .. y1 + 1
+  auto issue_pair = [&](int p) {
+    if (lane == 0 && p < npairs) {
+      const uint32_t bar = smem_u32(&S.bar[p & 1]);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(uint32_t(sizeof(S.gpair[0])))
+                   : "memory");
+      asm volatile(
+          "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];"
+          ::"r"(smem_u32(&S.gpair[p & 1][0][0][0])), "l"(&wmap), "r"(xs0 - 2), "r"(y0 - 2 + 2 * p), "r"(0), "r"(f),
+          "r"(bar)
+          : "memory");
+    }
+  };
+  auto wait_pair = [&](int p) { mbar_wait(smem_u32(&S.bar[p & 1]), uint32_t((p >> 1) & 1)); };
   auto issue = [&]() {  // next G row into its slot (or an empty group past the segment)
     if (next_row <= y1 + 1) {
       double(*dst)[34] = S.grow[unsigned(next_row) % kGRows];
@@ -645,8 +753,19 @@ __global__ void __maxnreg__(96) k_detect_walk(Batch bt, DetConst dc, int o, int 
     ++next_row;
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
+  if constexpr (TMA) {
+    if (lane == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&S.bar[0])) : "memory");
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&S.bar[1])) : "memory");
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    issue_pair(0);
+    issue_pair(1);
+  } else {
 #pragma unroll
-  for (int i = 0; i < kPrefetch + 2; ++i) issue();  // rows y0 - 2 .. y0 + kPrefetch - 1
+    for (int i = 0; i < kPrefetch + 2; ++i) issue();  // rows y0 - 2 .. y0 + kPrefetch - 1
+  }
   const double oct_scale = ldexp(1.0, o);
   float apf[4];  // own alpha (float copy) of the previous row (screened one row late)
   int qn = 0;
@@ -665,14 +784,24 @@ __global__ void __maxnreg__(96) k_detect_walk(Batch bt, DetConst dc, int o, int 
   const int T = y1 - y0 + 2;  // alpha rows y0 - 1 .. y1
   // sigma^2-normalised Laplacian of row ra (image.cpp:220-238,
   // scale_space.cpp:148-151), then alpha = beta * L in column order.
+  // Row r of level k, slot column c (0..33): the cp.async ring, or the TMA
+  // pair ring (rows y0 - 2 + 2p and y0 - 1 + 2p in slot p & 1).
+  auto grow_at = [&](int r, int k) -> const double* {
+    if constexpr (TMA) {
+      const int d = r - (y0 - 2);
+      return &S.gpair[(d >> 1) & 1][k][d & 1][0];
+    } else {
+      return &S.grow[unsigned(r) % kGRows][k][0];
+    }
+  };
   auto alpha_row = [&](int ra, double an[4]) {
-    const double(*rU)[34] = S.grow[unsigned(ra - 1) % kGRows];
-    const double(*rC)[34] = S.grow[unsigned(ra) % kGRows];
-    const double(*rD)[34] = S.grow[unsigned(ra + 1) % kGRows];
     double L[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      const double lap = rU[k][lane + 1] + rD[k][lane + 1] + rC[k][lane] + rC[k][lane + 2] - 4.0 * rC[k][lane + 1];
+      const double* rU = grow_at(ra - 1, k);
+      const double* rC = grow_at(ra, k);
+      const double* rD = grow_at(ra + 1, k);
+      const double lap = rU[lane + 1] + rD[lane + 1] + rC[lane] + rC[lane + 2] - 4.0 * rC[lane + 1];
       L[k] = dc.s2[k] * lap;
     }
 #pragma unroll
@@ -701,8 +830,13 @@ __global__ void __maxnreg__(96) k_detect_walk(Batch bt, DetConst dc, int o, int 
       const int ra = y0 - 1 + t;
       // Rows ra - 1 .. ra + 2 must have landed: rows up to ra + kPrefetch
       // may still be in flight.
-      asm volatile("cp.async.wait_group %0;" ::"n"(kPrefetch - 2) : "memory");
-      __syncwarp();
+      if constexpr (TMA) {
+        wait_pair(t >> 1);
+        wait_pair((t >> 1) + 1);
+      } else {
+        asm volatile("cp.async.wait_group %0;" ::"n"(kPrefetch - 2) : "memory");
+        __syncwarp();
+      }
       double a0[4], a1[4];
       alpha_row(ra, a0);
       alpha_row(ra + 1, a1);
@@ -717,8 +851,12 @@ __global__ void __maxnreg__(96) k_detect_walk(Batch bt, DetConst dc, int o, int 
       S.fring[unsigned(ra) % 4][lane] = make_float4(a0f[0], a0f[1], a0f[2], a0f[3]);
       if (second) S.fring[unsigned(ra + 1) % 4][lane] = make_float4(a1f[0], a1f[1], a1f[2], a1f[3]);
       __syncwarp();
-      issue();  // rows ra + kPrefetch + 1, ra + kPrefetch + 2 into the slots of rows ra - 1, ra
-      issue();
+      if constexpr (TMA) {
+        issue_pair((t >> 1) + 2);  // into the slot of pair t/2 (rows ra - 1, ra), read by every lane above
+      } else {
+        issue();  // rows ra + kPrefetch + 1, ra + kPrefetch + 2 into the slots of rows ra - 1, ra
+        issue();
+      }
       {
         const float4 u4 = S.fring[unsigned(ra - 2) % 4][lane];  // own alpha of row ra - 2 (the ring keeps it)
         const float auf[4] = {u4.x, u4.y, u4.z, u4.w};
@@ -733,7 +871,7 @@ __global__ void __maxnreg__(96) k_detect_walk(Batch bt, DetConst dc, int o, int 
     // neighbourhood in the ring; the ring keeps the 6 rows they need.
     if (qn > 0) drain();
   }
-  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  if constexpr (!TMA) asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
 
 constexpr size_t kDetSmem = sizeof(double) * (4 * kGH * kGW + kAH * 4 * kAW);
@@ -747,7 +885,11 @@ cudaError_t launch_octave_variant(const Batch& bt, const DetConst& dc, int o, in
   dim3 grid((bt.ow[o] + 2 * nt - 1) / (2 * nt), bt.nframes, 4);
   const bool aligned8 = ((reinterpret_cast<uintptr_t>(bt.pix8) | uintptr_t(bt.stride8) | uintptr_t(bt.frame_bytes8)) & 3) == 0;
   const int s = src == 0 ? (aligned8 ? 0 : 3) : src;
-#define CDVZ_BLUR(S, N) k_blur<R0, R1, R2, R3, S, N><<<grid, N, 0, st>>>(bt, dc, o)
+#define CDVZ_BLUR(S, N)                                                  \
+  do {                                                                   \
+    if (dc.blur_unrolled) k_blur<R0, R1, R2, R3, S, N, true><<<grid, N, 0, st>>>(bt, dc, o);   \
+    else k_blur<R0, R1, R2, R3, S, N, false><<<grid, N, 0, st>>>(bt, dc, o);                   \
+  } while (0)
   if (s == 0) CDVZ_BLUR(0, 64);       // octave 0: u8 frames
   else if (s == 3) CDVZ_BLUR(3, 64);  // octave 0: u8 frames, unaligned rows
   else if (s == 1) CDVZ_BLUR(1, 64);  // octave 0: resized f64 frames
@@ -756,7 +898,8 @@ cudaError_t launch_octave_variant(const Batch& bt, const DetConst& dc, int o, in
   return cudaGetLastError();
 }
 
-cudaError_t launch_detect(const Batch& bt, const DetConst& dc, int o, const CUtensorMap* tmap, cudaStream_t st) {
+cudaError_t launch_detect(const Batch& bt, const DetConst& dc, int o, const CUtensorMap* tmap, const CUtensorMap* wmap,
+                          cudaStream_t st) {
   const int ww = bt.ow[o] - 2 * dc.margin, hh = bt.oh[o] - 2 * dc.margin;
   if (ww <= 0 || hh <= 0) return cudaSuccess;  // detect_extrema: empty window (scale_space.cpp:159)
   static size_t configured[kMaxDevices] = {};
@@ -777,11 +920,20 @@ cudaError_t launch_detect(const Batch& bt, const DetConst& dc, int o, const CUte
     constexpr int smem = int(sizeof(DetWarpSmem)) * kDetWarps;
     static size_t walk_configured[kMaxDevices] = {};
     cudaError_t e = once_per_device(walk_configured, 1, [&] {
-      cudaError_t r = cudaFuncSetAttribute(k_detect_walk, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      return r != cudaSuccess ? r : cudaFuncSetAttribute(k_detect_walk, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+      for (auto fn : {k_detect_walk<true>, k_detect_walk<false>}) {
+        cudaError_t r = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (r == cudaSuccess) r = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        if (r != cudaSuccess) return r;
+      }
+      return cudaSuccess;
     });
     if (e != cudaSuccess) return e;
-    k_detect_walk<<<grid, 32 * nw, int(sizeof(DetWarpSmem)) * nw, st>>>(bt, dc, o, seg_rows);
+    if (wmap) {
+      k_detect_walk<true><<<grid, 32 * nw, int(sizeof(DetWarpSmem)) * nw, st>>>(bt, dc, o, seg_rows, *wmap);
+    } else {
+      CUtensorMap none{};
+      k_detect_walk<false><<<grid, 32 * nw, int(sizeof(DetWarpSmem)) * nw, st>>>(bt, dc, o, seg_rows, none);
+    }
     return cudaGetLastError();
   }
   dim3 grid((ww + kDetW - 1) / kDetW, (hh + kDetH - 1) / kDetH, bt.nframes);

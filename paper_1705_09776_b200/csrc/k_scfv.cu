@@ -116,6 +116,18 @@ struct PostSmem {
 static_assert(sizeof(double) * (4 * 32 * kPM) >= sizeof(double) * 8 * kSoftmaxRowMax && kPM == kPN,
               "the operand tiles xs2..mv hold the 8 warps' softmax rows");
 
+// One k = 4 step of the FP64 tensor-core MMA (DMMA): D(8x8) = A(8x4) B(4x8) + C.
+// Fragments: lane (g = lane / 4, q = lane % 4) holds A[g][q], B[q][g] and
+// C/D[g][2q], C/D[g][2q + 1]. The products are fused into the accumulation
+// (not separately rounded), so results differ from the reference in the last
+// bits: this path exists to measure the tensor pipe against the SIMT kernel
+// and is off by default.
+__device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
+}
+
+template <bool DMMA>
 __global__ void __launch_bounds__(256, 2) k_posterior(Batch bt, Model md) {
   extern __shared__ __align__(16) uint8_t post_smem[];
   PostSmem& S = *reinterpret_cast<PostSmem*>(post_smem);
@@ -163,6 +175,42 @@ __global__ void __launch_bounds__(256, 2) k_posterior(Batch bt, Model md) {
     const double(*TIV)[kPN] = buf ? S.iv2 : S.iv;
     const double(*TMV)[kPN] = buf ? S.mv2 : S.mv;
     buf ^= 1;
+    if constexpr (DMMA) {
+      // Warp w: rows 8w .. 8w + 7 x the tile's 64 components (8 MMA tiles),
+      // both products over k = 0..31 in 8 steps.
+      const int wi = tid >> 5, lane = tid & 31, g = lane >> 2, qq = lane & 3;
+      double da[8][2], db[8][2];
+#pragma unroll
+      for (int ct = 0; ct < 8; ++ct) da[ct][0] = da[ct][1] = db[ct][0] = db[ct][1] = 0.0;
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        const int j = 4 * kk + qq;
+        const double ax2 = S.xs2[j][8 * wi + g], ax = S.xs[j][8 * wi + g];
+#pragma unroll
+        for (int ct = 0; ct < 8; ++ct) {
+          dmma_8x8x4(da[ct][0], da[ct][1], ax2, TIV[j][8 * ct + g]);
+          dmma_8x8x4(db[ct][0], db[ct][1], ax, TMV[j][8 * ct + g]);
+        }
+      }
+      const int t = 8 * wi + g;
+      double m = -INFINITY;
+#pragma unroll
+      for (int ct = 0; ct < 8; ++ct)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int cc = 8 * ct + 2 * qq + h, i = c0 + cc;
+          if (t < rows && i < nc) {
+            const double p = da[ct][h] - 2.0 * db[ct][h] + S.cst[cc];
+            const double lp = -0.5 * p + S.lnorm[cc];
+            gam[t * nc + i] = lp;
+            m = fmax(m, lp);
+          }
+        }
+      m = fmax(m, __shfl_xor_sync(0xffffffffu, m, 1));
+      m = fmax(m, __shfl_xor_sync(0xffffffffu, m, 2));
+      rm[0] = fmax(rm[0], m);  // this lane's row t (lanes of a quad agree)
+      continue;
+    }
     double a[4][4], b[4][4];
     {
       const double2 xa = *reinterpret_cast<const double2*>(&S.xs2[0][ty * 4]);
@@ -218,13 +266,17 @@ __global__ void __launch_bounds__(256, 2) k_posterior(Batch bt, Model md) {
       }
     }
   }
+  if constexpr (DMMA) {
+    if ((tid & 3) == 0) S.rmax[0][8 * (tid >> 5) + ((tid & 31) >> 2)] = rm[0];
+  } else {
 #pragma unroll
-  for (int r = 0; r < 4; ++r) S.rmax[tx][ty * 4 + r] = rm[r];
-  __syncthreads();
-  if (tid < kPM) {
-    double pk = S.rmax[0][tid];
-    for (int k = 1; k < 16; ++k) pk = fmax(pk, S.rmax[k][tid]);
-    S.rmax[0][tid] = pk;
+    for (int r = 0; r < 4; ++r) S.rmax[tx][ty * 4 + r] = rm[r];
+    __syncthreads();
+    if (tid < kPM) {
+      double pk = S.rmax[0][tid];
+      for (int k = 1; k < 16; ++k) pk = fmax(pk, S.rmax[k][tid]);
+      S.rmax[0][tid] = pk;
+    }
   }
   __syncthreads();
   const int wi = tid >> 5, lane = tid & 31;
@@ -656,13 +708,17 @@ cudaError_t launch_scfv_pack(const Batch& bt, const Model& md, const EncodeConst
   if (e != cudaSuccess) return e;
   static size_t post_configured[kMaxDevices] = {};
   e = once_per_device(post_configured, 1, [&] {
-    return cudaFuncSetAttribute(k_posterior, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(PostSmem)));
+    cudaError_t r = cudaFuncSetAttribute(k_posterior<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(PostSmem)));
+    return r != cudaSuccess ? r : cudaFuncSetAttribute(k_posterior<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(PostSmem)));
   });
   if (e != cudaSuccess) return e;
-  if (md.nc <= 32)
+  const dim3 pgrid((bt.cap_or + kPM - 1) / kPM, bt.nframes);
+  if (ec.post_dmma)  // measurement variant: not the reference's rounding
+    k_posterior<true><<<pgrid, 256, sizeof(PostSmem), st>>>(bt, md);
+  else if (md.nc <= 32)
     k_posterior_small<<<dim3((bt.cap_or + kSmallRows - 1) / kSmallRows, bt.nframes), kSmallRows * md.nc, 0, st>>>(bt, md);
   else
-    k_posterior<<<dim3((bt.cap_or + kPM - 1) / kPM, bt.nframes), 256, sizeof(PostSmem), st>>>(bt, md);
+    k_posterior<false><<<pgrid, 256, sizeof(PostSmem), st>>>(bt, md);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   k_fisher<<<dim3((md.nc + kFI - 1) / kFI, bt.nframes), 256, 0, st>>>(bt, md, ec.variance);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
