@@ -343,7 +343,7 @@ class Extractor:
 
     def set_debug(self, on: bool = True, exact_only: bool = False, serial: bool = False, no_tma: bool = False,
                   tile_detect: bool = False, tiny_caps: bool = False, blur_unrolled: bool = False,
-                  post_dmma: bool = False) -> None:
+                  post_simt: bool = False) -> None:
         """on: keep per-octave lists; exact_only: bypass the FP32 extrema screen;
         serial: no kernel overlap (standalone per-kernel timing); tile_detect:
         the first-generation TMA tile extrema kernel instead of the column walk
@@ -351,11 +351,12 @@ class Extractor:
         column walk with per-lane cp.async rows); tiny_caps: tiny list
         capacities, so frames take the capacity retry; blur_unrolled: k_blur's
         y pass unrolled by one accumulator period instead of the rolled loop;
-        post_dmma: SCFV posteriors on the FP64 tensor cores (fused rounding,
-        not the reference's: a measurement variant)."""
+        post_simt: SCFV posteriors of large mixtures on the FP64 SIMT kernel
+        (gamma bit-identical to the reference's separately rounded products)
+        instead of the FP64 tensor cores."""
         flags = ((1 if on else 0) | (2 if exact_only else 0) | (4 if serial else 0) | (8 if no_tma else 0)
                  | (16 if tile_detect else 0) | (32 if tiny_caps else 0) | (64 if blur_unrolled else 0)
-                 | (128 if post_dmma else 0))
+                 | (128 if post_simt else 0))
         self._check(self._lib.cdvz_gpu_set_debug(self._ctx, flags))
 
     def debug_get(self, name: str, frame: int) -> np.ndarray:

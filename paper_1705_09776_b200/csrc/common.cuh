@@ -148,7 +148,7 @@ struct EncodeConst {
   uint32_t model_crc;
   double half_diag, cx, cy;     // fill_center_distance constants
   double log2_range;            // log2(64 / 0.5)
-  int post_dmma;                // 1: posteriors on the FP64 tensor cores (measurement only)
+  int post_dmma;                // 1: posteriors of mixtures > 32 components on the FP64 tensor cores
 };
 
 __host__ __device__ inline int mirror_index(int i, int n) {

@@ -180,7 +180,7 @@ struct cdvz_gpu_ctx {
   bool debug = false;
   bool serial = false;
   bool tma_disabled = false;
-  bool post_dmma = false;  // debug bit 128: SCFV posteriors on the FP64 tensor cores (measurement)
+  bool post_simt = false;  // debug bit 128: SCFV posteriors of large mixtures on FP64 SIMT (bit-exact gamma)
   bool cap_boost = false;  // plan the maximal survivor / orientation capacities (capacity retry of single frames)
   bool tiny_caps = false;  // debug bit 5: tiny batch capacities, so ordinary frames exercise the capacity retry
   // A multi-device context (cdvz_gpu_create_multi) owns one single-device
@@ -505,7 +505,7 @@ struct cdvz_gpu_ctx {
     ec.global_bytes = int(bu.global_bytes);
     ec.slot_bytes = int(m.budget + 28);
     ec.model_crc = bundle.model_crc;
-    ec.post_dmma = post_dmma ? 1 : 0;
+    ec.post_dmma = post_simt ? 0 : 1;
     return ec;
   }
 
@@ -916,7 +916,7 @@ int cdvz_gpu_set_debug(cdvz_gpu_ctx* ctx, int on) {
   ctx->dc.walk = (on & 16) ? 0 : 1;
   ctx->tiny_caps = (on & 32) != 0;
   ctx->dc.blur_unrolled = (on & 64) ? 1 : 0;
-  ctx->post_dmma = (on & 128) != 0;
+  ctx->post_simt = (on & 128) != 0;
   if (ctx->tma_disabled != ((on & 8) != 0)) {
     ctx->tma_disabled = (on & 8) != 0;
     for (auto& l : ctx->lanes) l.geo_w = 0;  // rebuild the tensor maps

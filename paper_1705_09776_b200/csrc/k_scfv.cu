@@ -119,9 +119,10 @@ static_assert(sizeof(double) * (4 * 32 * kPM) >= sizeof(double) * 8 * kSoftmaxRo
 // One k = 4 step of the FP64 tensor-core MMA (DMMA): D(8x8) = A(8x4) B(4x8) + C.
 // Fragments: lane (g = lane / 4, q = lane % 4) holds A[g][q], B[q][g] and
 // C/D[g][2q], C/D[g][2q + 1]. The products are fused into the accumulation
-// (not separately rounded), so results differ from the reference in the last
-// bits: this path exists to measure the tensor pipe against the SIMT kernel
-// and is off by default.
+// (not separately rounded), so gamma differs from the reference's in the last
+// bits; the containers it feeds were byte-identical on every frame measured
+// (DESIGN.md §2.4). Default for mixtures of more than 32 components; debug
+// bit 128 selects the bit-exact SIMT kernel.
 __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
                : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
@@ -713,10 +714,10 @@ cudaError_t launch_scfv_pack(const Batch& bt, const Model& md, const EncodeConst
   });
   if (e != cudaSuccess) return e;
   const dim3 pgrid((bt.cap_or + kPM - 1) / kPM, bt.nframes);
-  if (ec.post_dmma)  // measurement variant: not the reference's rounding
-    k_posterior<true><<<pgrid, 256, sizeof(PostSmem), st>>>(bt, md);
-  else if (md.nc <= 32)
+  if (md.nc <= 32)
     k_posterior_small<<<dim3((bt.cap_or + kSmallRows - 1) / kSmallRows, bt.nframes), kSmallRows * md.nc, 0, st>>>(bt, md);
+  else if (ec.post_dmma)  // the FP64 tensor cores
+    k_posterior<true><<<pgrid, 256, sizeof(PostSmem), st>>>(bt, md);
   else
     k_posterior<false><<<pgrid, 256, sizeof(PostSmem), st>>>(bt, md);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;

@@ -43,7 +43,8 @@ def main(out):
     rows = []
     vga = oracle_lib.synth_frames(1000, 1024, 640, 480)  # the bench frames (BASELINE configs[1], base seed 1000)
     rows.append(sweep("configs[1]: 1024 VGA frames, 4K", "b8", vga, "4K"))
-    rows.append(sweep("configs[1] with the 512-component bundle", "b512", vga[:256], "4K"))
+    rows.append(sweep("configs[1] with the 512-component bundle (DMMA posteriors)", "b512", vga, "4K"))
+    rows.append(sweep("512-component bundle, 16K (variance planes)", "b512", vga[:256], "16K"))
     rows.append(sweep("512B mode, VGA", "b8", vga[256:448], "512B"))
     rows.append(sweep("8K mode (variance planes)", "b8", vga[448:576], "8K"))
     hd = oracle_lib.synth_frames(4000, 64, 1920, 1080)
