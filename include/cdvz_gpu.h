@@ -104,6 +104,22 @@ int cdvz_gpu_encode_batch(cdvz_gpu_ctx* ctx, const uint8_t* pixels, int width, i
                           int count, int mode_id, int max_side, uint8_t* out, size_t out_cap,
                           size_t* offsets, int* status);
 
+/* cdvz_gpu_encode_batch split in two for streams of batches (a video feed, a
+ * crawler): submit enqueues the copies, every kernel and the container copies
+ * back and returns a ticket at once; wait(ticket) hands the containers,
+ * offsets and status to the caller's buffers (exactly what encode_batch
+ * would have written) and returns the call's result code. Up to two
+ * submitted batches are in flight per context, so one batch's copies and
+ * kernels overlap the previous one's tail; a third submit first completes the
+ * oldest (its wait then returns the held result). All buffers of a submitted
+ * call must stay valid until its wait returns. Ticket 0 means the call
+ * completed inside submit (multi-device contexts and batches above 4 GB run
+ * synchronously). Errors found while enqueuing are returned by submit. */
+int cdvz_gpu_encode_batch_submit(cdvz_gpu_ctx* ctx, const uint8_t* pixels, int width, int height, size_t stride,
+                                 int count, int mode_id, int max_side, uint8_t* out, size_t out_cap,
+                                 size_t* offsets, int* status, uint64_t* ticket);
+int cdvz_gpu_encode_batch_wait(cdvz_gpu_ctx* ctx, uint64_t ticket);
+
 /* GrayImage form of cdvz_gpu_encode_batch — the reference's own input type
  * (proj/include/cdvz/image.hpp:11-18: row-major doubles, rows = height): the
  * raster an in-process producer hands to encode_image (synth_image,

@@ -101,6 +101,8 @@ def _lib() -> ctypes.CDLL:
         "cdvz_gpu_bundle_info": (I, [P, ctypes.POINTER(U32), ctypes.POINTER(I), ctypes.POINTER(I)]),
         "cdvz_gpu_encode_batch": (I, [P, P, I, I, S, I, I, I, P, S, P, P]),
         "cdvz_gpu_encode_batch_rgb": (I, [P, P, I, I, S, I, I, I, P, S, P, P]),
+        "cdvz_gpu_encode_batch_submit": (I, [P, P, I, I, S, I, I, I, P, S, P, P, ctypes.POINTER(U64)]),
+        "cdvz_gpu_encode_batch_wait": (I, [P, U64]),
         "cdvz_gpu_pnm_parse": (I, [P, S, ctypes.POINTER(I), ctypes.POINTER(I), ctypes.POINTER(I), ctypes.POINTER(S)]),
         "cdvz_gpu_encode_device": (I, [P, P, I, I, S, I, I, I, P, P]),
         "cdvz_gpu_container_slot": (S, [I]),
@@ -221,6 +223,25 @@ def parse_pnm(data: bytes):
     return w.value, h.value, ch.value, off.value
 
 
+class PendingBatch:
+    """A submitted batch (Extractor.encode_batch_submit); holds its buffers."""
+
+    def __init__(self, ex: "Extractor", frames: np.ndarray, n: int, slot: int):
+        self.ex, self.frames, self.n = ex, frames, n
+        self.out = np.empty(max(1, n * slot), dtype=np.uint8)
+        self.offsets = np.zeros(n + 1, dtype=np.uint64)
+        self.status = np.zeros(max(1, n), dtype=np.int32)
+        self.ticket = 0
+        self._done = None
+
+    def wait(self):
+        if self._done is None:
+            self.ex._check(self.ex._lib.cdvz_gpu_encode_batch_wait(self.ex._ctx, self.ticket))
+            res = [self.out[int(self.offsets[i]):int(self.offsets[i + 1])].tobytes() for i in range(self.n)]
+            self._done = (res, self.status[:self.n].copy())
+        return self._done
+
+
 class Extractor:
     """One GPU context holding a model bundle: the reference's
     ``encode_image(img, bundle, mode)`` for batches of frames (8-bit grey or
@@ -297,6 +318,27 @@ class Extractor:
         res = [out[int(offsets[i]):int(offsets[i + 1])].tobytes() for i in range(n)]
         return res, status[:n].copy()
 
+    def encode_batch_submit(self, frames: np.ndarray, mode, max_side: int = 640) -> "PendingBatch":
+        """cdvz_gpu_encode_batch_submit for uint8 [N, H, W] grey frames: returns
+        at once; ``.wait()`` gives (containers, status) like encode_batch.
+        Up to two batches are in flight per extractor (the frames array is
+        kept alive by the handle)."""
+        m = mode if isinstance(mode, ModeSpec) else (mode_by_name(mode) if isinstance(mode, str) else mode_by_id(mode))
+        frames = np.ascontiguousarray(frames, dtype=np.uint8)
+        if frames.ndim == 2:
+            frames = frames[None]
+        if frames.ndim != 3:
+            raise UsageError("frames must be [N, H, W] uint8")
+        n, h, w = frames.shape
+        slot = m.budget_bytes + 28
+        pb = PendingBatch(self, frames, n, slot)
+        t = ctypes.c_uint64()
+        self._check(self._lib.cdvz_gpu_encode_batch_submit(self._ctx, frames.ctypes.data, w, h, w, n, m.id, max_side,
+                                                           pb.out.ctypes.data, pb.out.nbytes, pb.offsets.ctypes.data,
+                                                           pb.status.ctypes.data, ctypes.byref(t)))
+        pb.ticket = t.value
+        return pb
+
     def encode_pnm(self, data: bytes, mode, max_side: int = 640) -> bytes:
         """load_image + encode_image + serialize_container for one in-memory
         PGM/PPM file (proj/src/image.cpp:53-92)."""
@@ -343,7 +385,7 @@ class Extractor:
 
     def set_debug(self, on: bool = True, exact_only: bool = False, serial: bool = False, no_tma: bool = False,
                   tile_detect: bool = False, tiny_caps: bool = False, blur_unrolled: bool = False,
-                  post_simt: bool = False) -> None:
+                  post_simt: bool = False, desc_registers: bool = False) -> None:
         """on: keep per-octave lists; exact_only: bypass the FP32 extrema screen;
         serial: no kernel overlap (standalone per-kernel timing); tile_detect:
         the first-generation TMA tile extrema kernel instead of the column walk
@@ -353,10 +395,12 @@ class Extractor:
         y pass unrolled by one accumulator period instead of the rolled loop;
         post_simt: SCFV posteriors of large mixtures on the FP64 SIMT kernel
         (gamma bit-identical to the reference's separately rounded products)
-        instead of the FP64 tensor cores."""
+        instead of the FP64 tensor cores; desc_registers: the
+        descriptor histograms with register bins (k_describe) instead of the
+        shared-memory cell accumulators (k_describe_cells)."""
         flags = ((1 if on else 0) | (2 if exact_only else 0) | (4 if serial else 0) | (8 if no_tma else 0)
                  | (16 if tile_detect else 0) | (32 if tiny_caps else 0) | (64 if blur_unrolled else 0)
-                 | (128 if post_simt else 0))
+                 | (128 if post_simt else 0) | (256 if desc_registers else 0))
         self._check(self._lib.cdvz_gpu_set_debug(self._ctx, flags))
 
     def debug_get(self, name: str, frame: int) -> np.ndarray:

@@ -49,6 +49,7 @@ struct DetConst {
   float scr_lo, scr_hi, scr_thr;  // screen constants: s_lo - 0.05, s_hi + 0.05, thr (FP32)
   int walk;            // 1: warp column-walk extrema kernel; 0: TMA tile kernel
   int blur_unrolled;   // 1: k_blur's y pass unrolled by one accumulator period; 0: rolled (shifted accumulators)
+  int desc_registers;  // 1: k_describe with register bins; 0: k_describe_cells (shared-memory cell accumulators)
 };
 
 // Per-batch geometry and buffer map (device pointers). One instance lives in

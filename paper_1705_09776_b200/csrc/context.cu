@@ -9,6 +9,8 @@
 // status 3 for that frame only.
 #include <algorithm>
 #include <cctype>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <functional>
@@ -171,7 +173,6 @@ struct cdvz_gpu_ctx {
   cudaStream_t st = nullptr;
   cudaStream_t copy_st = nullptr;          // host->device frame copies (encode_batch)
   std::vector<cudaEvent_t> copy_ev;        // one per chunk of a call
-  std::vector<cudaEvent_t> out_ev;         // one per chunk: its containers are in host memory
   std::string err;
   Bundle bundle;
   DetConst dc{};
@@ -190,29 +191,69 @@ struct cdvz_gpu_ctx {
   static constexpr int kLanes = 2;  // chunks in flight (each lane: its own streams and batch buffers; 4 measured no faster)
   Lane lanes[kLanes];
   int last_lane = 0;
-  DeviceBuffer stage_in, stage_out, stage_len;
-  uint8_t* pin_out = nullptr;    // pinned container slots (D2H target)
-  uint32_t* pin_len = nullptr;
-  int* pin_status = nullptr;     // per-frame device status (2 data error, 4 capacity, 8 unsupported scale)
-  size_t pin_out_bytes = 0, pin_len_count = 0;
+  // Staging of one host-frame call (encode_batch*): device input / output
+  // slots, pinned container slots and the per-chunk "containers are in host
+  // memory" events. Two of them, so a submitted call can be in flight while
+  // the next one is enqueued (cdvz_gpu_encode_batch_submit / _wait).
+  struct HostSlot {
+    DeviceBuffer stage_in, stage_out, stage_len;
+    uint8_t* pin_out = nullptr;    // pinned container slots (D2H target)
+    uint32_t* pin_len = nullptr;
+    int* pin_status = nullptr;     // per-frame device status (2 data error, 4 capacity, 8 unsupported scale)
+    size_t pin_out_bytes = 0, pin_len_count = 0;
+    std::vector<cudaEvent_t> out_ev;
+    std::vector<int> cb;           // chunk boundaries of the call in flight
+    bool ramp = true;              // geometric chunk ramp (one call at a time); full chunks when streaming
+    // the call in flight (submit -> wait)
+    bool busy = false;
+    unsigned long long ticket = 0;
+    const uint8_t* pixels = nullptr;
+    int width = 0, height = 0, count = 0, mode_id = 0, max_side = 0, kind = 1;
+    size_t stride = 0, out_cap = 0;
+    uint8_t* out = nullptr;
+    size_t* offsets = nullptr;
+    int* status = nullptr;
 
-  void ensure_pinned_out(size_t bytes, size_t count) {
-    if (bytes > pin_out_bytes) {
-      if (pin_out) cudaFreeHost(pin_out);
-      pin_out = nullptr;
-      CDVZ_CUDA_CHECK(cudaMallocHost(&pin_out, bytes));
-      pin_out_bytes = bytes;
+    void ensure_pinned_out(size_t bytes, size_t count_) {
+      if (bytes > pin_out_bytes) {
+        if (pin_out) cudaFreeHost(pin_out);
+        pin_out = nullptr;
+        CDVZ_CUDA_CHECK(cudaMallocHost(&pin_out, bytes));
+        pin_out_bytes = bytes;
+      }
+      if (count_ > pin_len_count) {
+        if (pin_len) cudaFreeHost(pin_len);
+        if (pin_status) cudaFreeHost(pin_status);
+        pin_len = nullptr;
+        pin_status = nullptr;
+        CDVZ_CUDA_CHECK(cudaMallocHost(&pin_len, count_ * sizeof(uint32_t)));
+        CDVZ_CUDA_CHECK(cudaMallocHost(&pin_status, count_ * sizeof(int)));
+        pin_len_count = count_;
+      }
     }
-    if (count > pin_len_count) {
+    void release() {
+      stage_in.release();
+      stage_out.release();
+      stage_len.release();
+      if (pin_out) cudaFreeHost(pin_out);
       if (pin_len) cudaFreeHost(pin_len);
       if (pin_status) cudaFreeHost(pin_status);
+      pin_out = nullptr;
       pin_len = nullptr;
       pin_status = nullptr;
-      CDVZ_CUDA_CHECK(cudaMallocHost(&pin_len, count * sizeof(uint32_t)));
-      CDVZ_CUDA_CHECK(cudaMallocHost(&pin_status, count * sizeof(int)));
-      pin_len_count = count;
+      pin_out_bytes = pin_len_count = 0;
+      for (auto& e : out_ev) cudaEventDestroy(e);
+      out_ev.clear();
     }
-  }
+  };
+  HostSlot hslot[2];
+  unsigned long long next_ticket = 1;
+  struct Finished {
+    unsigned long long ticket;
+    int rc;
+    std::string err;
+  };
+  std::vector<Finished> finished;  // submitted calls finished before their wait (result held for it)
   int last_frames = 0, last_mode = -1;
 
   cudaEvent_t ev[6] = {};
@@ -235,12 +276,7 @@ struct cdvz_gpu_ctx {
   ~cdvz_gpu_ctx() {
     for (auto& b : model_bufs) b.release();
     for (auto& l : lanes) l.destroy();
-    stage_in.release();
-    stage_out.release();
-    stage_len.release();
-    if (pin_out) cudaFreeHost(pin_out);
-    if (pin_len) cudaFreeHost(pin_len);
-    if (pin_status) cudaFreeHost(pin_status);
+    for (auto& h : hslot) h.release();
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
     for (auto& e : evp)
@@ -248,7 +284,6 @@ struct cdvz_gpu_ctx {
     for (auto& e : user_ev)
       if (e) cudaEventDestroy(e);
     for (auto& e : copy_ev) cudaEventDestroy(e);
-    for (auto& e : out_ev) cudaEventDestroy(e);
     if (copy_st) cudaStreamDestroy(copy_st);
     if (st) cudaStreamDestroy(st);
   }
@@ -287,6 +322,7 @@ struct cdvz_gpu_ctx {
     dc.screen = 1;
     dc.walk = 1;
     dc.blur_unrolled = 0;
+    dc.desc_registers = 0;
 
     for (int c = 0; c < 5; ++c) {
       md.rel_edges[c] = upload(b.relevance[std::size_t(c)].edges.data(), b.relevance[std::size_t(c)].edges.size());
@@ -516,9 +552,21 @@ struct cdvz_gpu_ctx {
   // quantisers, pipeline.cpp:37-50), aggregation (PCA + posteriors + Fisher +
   // SCFV coding). The container pack follows, outside the labels, as
   // serialize_container is outside encode_image.
+  // CDVZ_TRACE=1: each collected chunk prints its lane, call and device
+  // start / end times (ms after the context's first call) to stderr.
+  cudaEvent_t trace_base = nullptr;
+  bool trace = std::getenv("CDVZ_TRACE") != nullptr;
   void collect(Lane& L) {
     if (!L.pending) return;
     CDVZ_CUDA_CHECK(cudaEventSynchronize(L.done));
+    if (trace && trace_base) {
+      float a = 0.f, b = 0.f, c = 0.f;
+      cudaEventElapsedTime(&a, trace_base, L.start);
+      cudaEventElapsedTime(&b, trace_base, L.stage[1]);
+      cudaEventElapsedTime(&c, trace_base, L.stage[5]);
+      fprintf(stderr, "trace lane %d call %lld start %.3f detect_end %.3f agg_end %.3f\n", int(&L - lanes), L.pending_call,
+              a, b, c);
+    }
     Stats& st_ = open[L.pending_call];
     float t[5];
     cudaEventElapsedTime(&t[0], L.start, L.stage[1]);
@@ -561,7 +609,7 @@ struct cdvz_gpu_ctx {
   void run(const uint8_t* d_pix, int w, int h, long long stride, int frames, int mode_id, int max_side, uint8_t* d_out,
            uint32_t* d_len, const uint8_t* h_pix = nullptr, size_t h_stride = 0, uint8_t* h_out = nullptr,
            uint32_t* h_len = nullptr, int kind = 1, const std::function<void(int, int)>& on_chunk = nullptr,
-           int* h_status = nullptr) {
+           int* h_status = nullptr, HostSlot* hs = nullptr) {
     if (w < 8 || h < 8) throw DataError("image smaller than 8 px per side");
     int W, H;
     prepared_dims(w, h, max_side, W, H);
@@ -599,12 +647,38 @@ struct cdvz_gpu_ctx {
     // make the copy the long pole: at least four chunks per call, so each
     // chunk's copy overlaps the previous chunk's kernels.
     if (h_pix && double(w) * h * channels > 2.0 * double(W) * H) per = std::min(per, std::max(32, (frames + 3) / 4));
-    // Chunk boundaries. With host frames the first chunk is 1/16 of a chunk,
-    // so the only copy not hidden behind kernels is short (1/4 and 1/8
-    // measured 2-3% slower end to end).
+    // Chunk boundaries. With host frames the chunks ramp up geometrically
+    // from 1/16 of a full chunk (1/16, 1/8, 1/4, 1/2, 1, 1, ...): the copies
+    // are queued back to back, so the kernels start after the first short
+    // copy and each later copy lands while the earlier chunks compute; the
+    // last chunk is the remainder, so the call's unoverlapped tail is short.
+    // (Round 1 used one 1/16 lead chunk then full chunks: the second chunk's
+    // copy — 3 ms for 512 VGA frames — was exposed.)
     std::vector<int> cb{0};
-    if (h_pix && frames >= 32) cb.push_back(std::max(1, per / 16));
-    while (cb.back() < frames) cb.push_back(std::min(frames, cb.back() + per));
+    static const std::vector<int> chunk_env = [] {  // CDVZ_CHUNKS="32,64,...": schedule experiments
+      std::vector<int> v;
+      if (const char* e = std::getenv("CDVZ_CHUNKS"))
+        for (const char* q = e; *q;) {
+          char* end = nullptr;
+          const long x = std::strtol(q, &end, 10);
+          if (end == q) break;
+          if (x > 0) v.push_back(int(x));
+          q = *end ? end + 1 : end;
+        }
+      return v;
+    }();
+    if (h_pix && !chunk_env.empty()) {
+      for (size_t k = 0; cb.back() < frames; ++k)
+        cb.push_back(std::min(frames, cb.back() + std::min(per, chunk_env[std::min(k, chunk_env.size() - 1)])));
+    } else if (h_pix && frames >= 32 && (!hs || hs->ramp)) {
+      int c = std::max(1, per / 16);
+      while (cb.back() < frames) {
+        cb.push_back(std::min(frames, cb.back() + c));
+        c = std::min(per, 2 * c);
+      }
+    } else {
+      while (cb.back() < frames) cb.push_back(std::min(frames, cb.back() + per));
+    }
     const int chunks = int(cb.size()) - 1;
     const int n_lanes = serial ? 1 : kLanes;
     const long long call = ++call_seq;
@@ -618,6 +692,10 @@ struct cdvz_gpu_ctx {
       plan(L, W, H, per, resize || rgb, rgb && resize ? (long long)w * h : 0);
     }
     launches = 0;
+    if (trace && !trace_base) {
+      CDVZ_CUDA_CHECK(cudaEventCreate(&trace_base));
+      CDVZ_CUDA_CHECK(cudaEventRecord(trace_base, st));
+    }
     CDVZ_CUDA_CHECK(cudaEventRecord(ev[0], st));  // everything before this call
     // Host frames: every chunk's copy is queued up front on the copy stream
     // (back to back at full link bandwidth); a chunk's kernels wait only for
@@ -629,12 +707,21 @@ struct cdvz_gpu_ctx {
         CDVZ_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         copy_ev.push_back(e);
       }
-      CDVZ_CUDA_CHECK(cudaStreamWaitEvent(copy_st, ev[0], 0));
+      // Host frames go into the call's own staging slot, free once its
+      // previous call was waited for: the copies need not wait for earlier
+      // work on the context stream, so they overlap the previous call's
+      // kernels (a submitted stream of batches keeps the device busy).
+      const size_t row_bytes = size_t(w) * channels * elem;
+      const bool contiguous = size_t(stride) == row_bytes && h_stride == row_bytes;
       for (int c = 0; c < chunks; ++c) {
         const int base = cb[size_t(c)], nf = cb[size_t(c) + 1] - base;
-        CDVZ_CUDA_CHECK(cudaMemcpy2DAsync(const_cast<uint8_t*>(d_pix) + (long long)base * h * stride, size_t(stride),
-                                          h_pix + size_t(base) * h * h_stride, h_stride, size_t(w) * channels * elem,
-                                          size_t(h) * nf, cudaMemcpyHostToDevice, copy_st));
+        uint8_t* dst = const_cast<uint8_t*>(d_pix) + (long long)base * h * stride;
+        const uint8_t* src = h_pix + size_t(base) * h * h_stride;
+        if (contiguous)  // one linear transfer (a 2-D copy of 640-byte rows runs well below the link rate)
+          CDVZ_CUDA_CHECK(cudaMemcpyAsync(dst, src, row_bytes * h * nf, cudaMemcpyHostToDevice, copy_st));
+        else
+          CDVZ_CUDA_CHECK(cudaMemcpy2DAsync(dst, size_t(stride), src, h_stride, row_bytes, size_t(h) * nf,
+                                            cudaMemcpyHostToDevice, copy_st));
         CDVZ_CUDA_CHECK(cudaEventRecord(copy_ev[size_t(c)], copy_st));
       }
     }
@@ -652,8 +739,10 @@ struct cdvz_gpu_ctx {
       b.pix8 = d_pix + (long long)base * h * stride;
       b.stride8 = stride;
       b.frame_bytes8 = (long long)h * stride;
-      CDVZ_CUDA_CHECK(cudaStreamWaitEvent(L.sA, ev[0], 0));
-      CDVZ_CUDA_CHECK(cudaStreamWaitEvent(sB, ev[0], 0));
+      if (!h_pix) {  // device frames: ordered after everything already enqueued on the context stream
+        CDVZ_CUDA_CHECK(cudaStreamWaitEvent(L.sA, ev[0], 0));
+        CDVZ_CUDA_CHECK(cudaStreamWaitEvent(sB, ev[0], 0));
+      }
       if (h_pix) CDVZ_CUDA_CHECK(cudaStreamWaitEvent(L.sA, copy_ev[size_t(c)], 0));
       CDVZ_CUDA_CHECK(cudaEventRecord(L.start, L.sA));
       CDVZ_CUDA_CHECK(cudaMemsetAsync(b.status, 0, sizeof(int) * nf, L.sA));
@@ -723,12 +812,13 @@ struct cdvz_gpu_ctx {
         CDVZ_CUDA_CHECK(cudaMemcpyAsync(h_len + base, d_len + base, sizeof(uint32_t) * nf, cudaMemcpyDeviceToHost, sB));
         if (h_status)
           CDVZ_CUDA_CHECK(cudaMemcpyAsync(h_status + base, b.status, sizeof(int) * nf, cudaMemcpyDeviceToHost, sB));
-        while (int(out_ev.size()) <= c) {
+        std::vector<cudaEvent_t>& oev = hs->out_ev;
+        while (int(oev.size()) <= c) {
           cudaEvent_t e;
           CDVZ_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-          out_ev.push_back(e);
+          oev.push_back(e);
         }
-        CDVZ_CUDA_CHECK(cudaEventRecord(out_ev[size_t(c)], sB));
+        CDVZ_CUDA_CHECK(cudaEventRecord(oev[size_t(c)], sB));
       }
       CDVZ_CUDA_CHECK(cudaEventRecord(L.done, sB));
       // The next chunk on this lane's stream A must not overwrite the pyramid
@@ -744,9 +834,10 @@ struct cdvz_gpu_ctx {
     if (!serial) next_lane = (lane0 + chunks) % kLanes;
     // Host outputs: hand each chunk's containers to the caller in frame order
     // as soon as they land, while later chunks are still on the device.
+    if (h_out) hs->cb = cb;
     if (h_out && on_chunk)
       for (int c = 0; c < chunks; ++c) {
-        CDVZ_CUDA_CHECK(cudaEventSynchronize(out_ev[size_t(c)]));
+        CDVZ_CUDA_CHECK(cudaEventSynchronize(hs->out_ev[size_t(c)]));
         on_chunk(cb[size_t(c)], cb[size_t(c) + 1] - cb[size_t(c)]);
       }
     for (int l = 0; l < kLanes; ++l)
@@ -917,6 +1008,7 @@ int cdvz_gpu_set_debug(cdvz_gpu_ctx* ctx, int on) {
   ctx->tiny_caps = (on & 32) != 0;
   ctx->dc.blur_unrolled = (on & 64) ? 1 : 0;
   ctx->post_simt = (on & 128) != 0;
+  ctx->dc.desc_registers = (on & 256) ? 1 : 0;
   if (ctx->tma_disabled != ((on & 8) != 0)) {
     ctx->tma_disabled = (on & 8) != 0;
     for (auto& l : ctx->lanes) l.geo_w = 0;  // rebuild the tensor maps
@@ -952,9 +1044,12 @@ int cdvz_gpu_trim(cdvz_gpu_ctx* ctx) {
       if (l.sB) CDVZ_CUDA_CHECK(cudaStreamSynchronize(l.sB));
       l.release();
     }
-    ctx->stage_in.release();
-    ctx->stage_out.release();
-    ctx->stage_len.release();
+    for (auto& h : ctx->hslot) {
+      if (h.busy) throw UsageError("a submitted batch is in flight: wait for it before trimming");
+      h.stage_in.release();
+      h.stage_out.release();
+      h.stage_len.release();
+    }
   });
 }
 
@@ -1063,141 +1158,211 @@ void encode_multi(cdvz_gpu_ctx* ctx, const uint8_t* pixels, int width, int heigh
 
 // Host-frame batch encode of grey (kind 1) or RGB (kind 3) byte rasters, or
 // f64 grey rasters (kind 8; `stride` in bytes).
+// Frames per host-frame group: bounded so the device staging stays < 4 GB.
+int host_group_frames(size_t frame_bytes, int count) {
+  return int(std::max<size_t>(1, std::min<size_t>(size_t(count), (size_t(4) << 30) / frame_bytes)));
+}
+
+// Enqueues frames [base, base + nf) of the slot's call: the copies, every
+// kernel and the container copies back, with no host wait.
+void host_begin(cdvz_gpu_ctx* ctx, cdvz_gpu_ctx::HostSlot& hs, int base, int nf) {
+  const int channels = hs.kind == 3 ? 3 : 1;
+  const size_t elem = hs.kind == 8 ? sizeof(double) : 1;
+  const size_t row_bytes = size_t(hs.width) * channels * elem;
+  const size_t frame_bytes = row_bytes * hs.height;
+  const size_t slot = mode_by_id(hs.mode_id).budget + 28;
+  hs.stage_in.ensure(frame_bytes * nf);
+  hs.stage_out.ensure(slot * nf);
+  hs.stage_len.ensure(sizeof(uint32_t) * nf);
+  hs.ensure_pinned_out(slot * nf, nf);
+  ctx->run(hs.stage_in.as<uint8_t>(), hs.width, hs.height, (long long)row_bytes, nf, hs.mode_id, hs.max_side,
+           hs.stage_out.as<uint8_t>(), hs.stage_len.as<uint32_t>(), hs.pixels + size_t(base) * hs.height * hs.stride,
+           hs.stride, hs.pin_out, hs.pin_len, hs.kind, nullptr, hs.pin_status, &hs);
+}
+
+// Waits for the group enqueued by host_begin and hands its containers to the
+// caller in frame order (chunk by chunk, as they land), with per-frame status;
+// frames whose lists overflowed a batch capacity are re-encoded alone with the
+// maximal capacities and spliced in. `written` is the caller's output cursor.
+// With fold_now false (submitted calls), only this call's chunk events are
+// waited on: a later submitted call may already be queued behind it, and its
+// statistics are folded lazily (stage_times) instead of draining the device.
+void host_finish(cdvz_gpu_ctx* ctx, cdvz_gpu_ctx::HostSlot& hs, int base, int nf, size_t& written,
+                 cdvz_gpu_ctx::Stats& acc, int& acc_launches, bool fold_now = true) {
+  const size_t slot = mode_by_id(hs.mode_id).budget + 28;
+  const int channels = hs.kind == 3 ? 3 : 1;
+  const size_t elem = hs.kind == 8 ? sizeof(double) : 1;
+  const size_t row_bytes = size_t(hs.width) * channels * elem;
+  const size_t frame_bytes = row_bytes * hs.height;
+  uint8_t* out = hs.out;
+  size_t* offsets = hs.offsets;
+  int* status = hs.status;
+  auto fold = [&] {
+    ctx->collect_all();
+    for (int i = 0; i < 5; ++i) acc.stage_ms[i] += ctx->stats.stage_ms[i];
+    acc.pyr_ms += ctx->stats.pyr_ms;
+    acc.pyr_bytes += ctx->stats.pyr_bytes;
+    acc_launches += ctx->launches;
+  };
+  std::vector<int> retry;                    // frames of this group that overflowed a capacity
+  std::vector<size_t> start(size_t(nf), 0);  // byte offset of each written container in `out`
+  for (size_t c = 0; c + 1 < hs.cb.size(); ++c) {
+    CDVZ_CUDA_CHECK(cudaEventSynchronize(hs.out_ev[c]));
+    for (int i = hs.cb[c]; i < hs.cb[c + 1]; ++i) {
+      const size_t len = hs.pin_len[size_t(i)];
+      const int dev_status = hs.pin_status[size_t(i)];
+      const int fi = base + i;
+      start[size_t(i)] = written;
+      if (len == 0) {
+        if (dev_status & 2) {
+          status[fi] = CDVZ_GPU_DATA;  // validate(): non-finite or outside [0, 1]
+        } else if (dev_status == 4) {
+          status[fi] = CDVZ_GPU_OK;    // capacity only: re-encoded below with the maximal capacities
+          retry.push_back(i);
+        } else {
+          status[fi] = CDVZ_GPU_INTERNAL;
+        }
+      } else if (written + len > hs.out_cap) {
+        status[fi] = CDVZ_GPU_USAGE;
+      } else {
+        std::memcpy(out + written, hs.pin_out + size_t(i) * slot, len);
+        written += len;
+        status[fi] = CDVZ_GPU_OK;
+      }
+      offsets[fi + 1] = written;
+    }
+  }
+  if (fold_now) {
+    CDVZ_CUDA_CHECK(cudaStreamSynchronize(ctx->st));
+    fold();
+  }
+  if (retry.empty()) return;
+  // Capacity retry: a frame whose survivor or orientation lists outgrew the
+  // batch capacities (adversarial content) is encoded again on its own with
+  // the largest counts the reference can produce, so it never fails where
+  // the reference succeeds. Its container is then spliced in frame order.
+  std::vector<std::vector<uint8_t>> redo(retry.size());
+  ctx->cap_boost = true;
+  try {
+    for (size_t r = 0; r < retry.size(); ++r) {
+      const int i = retry[r];
+      ctx->run(hs.stage_in.as<uint8_t>() + size_t(i) * frame_bytes, hs.width, hs.height, (long long)row_bytes, 1,
+               hs.mode_id, hs.max_side, hs.stage_out.as<uint8_t>(), hs.stage_len.as<uint32_t>(), nullptr, 0, nullptr,
+               nullptr, hs.kind);
+      CDVZ_CUDA_CHECK(cudaStreamSynchronize(ctx->st));
+      fold();
+      uint32_t len = 0;
+      int dev_status = 0;
+      CDVZ_CUDA_CHECK(cudaMemcpy(&len, hs.stage_len.as<uint32_t>(), sizeof(len), cudaMemcpyDeviceToHost));
+      const Lane& L = ctx->lanes[ctx->last_lane];
+      CDVZ_CUDA_CHECK(cudaMemcpy(&dev_status, L.bt.status, sizeof(int), cudaMemcpyDeviceToHost));
+      if (len == 0) {
+        status[base + i] = (dev_status & 2) ? CDVZ_GPU_DATA : CDVZ_GPU_INTERNAL;
+        continue;
+      }
+      redo[r].resize(len);
+      CDVZ_CUDA_CHECK(cudaMemcpy(redo[r].data(), hs.stage_out.as<uint8_t>(), len, cudaMemcpyDeviceToHost));
+    }
+  } catch (...) {
+    ctx->cap_boost = false;
+    throw;
+  }
+  ctx->cap_boost = false;
+  size_t grow = 0;
+  for (const auto& v : redo) grow += v.size();
+  if (written + grow > hs.out_cap) {  // no room: the re-encoded frames are reported like any overflow
+    for (size_t q = 0; q < retry.size(); ++q)
+      if (!redo[q].empty()) status[base + retry[q]] = CDVZ_GPU_USAGE;
+    return;
+  }
+  // Rebuild this group's section back to front: containers only move right.
+  size_t end = written + grow;
+  size_t r = retry.size();
+  for (int i = nf - 1; i >= 0; --i) {
+    const int fi = base + i;
+    const size_t old_len = size_t(offsets[fi + 1]) - start[size_t(i)];
+    const std::vector<uint8_t>* ins = (r > 0 && retry[r - 1] == i) ? &redo[--r] : nullptr;
+    const size_t len = ins ? ins->size() : old_len;
+    const size_t pos = end - len;
+    if (ins) {
+      if (len) std::memcpy(out + pos, ins->data(), len);
+    } else if (len && pos != start[size_t(i)]) {
+      std::memmove(out + pos, out + start[size_t(i)], len);
+    }
+    offsets[fi + 1] = end;
+    end = pos;
+  }
+  written += grow;
+}
+
+// Argument checks shared by the synchronous and the submitted host batch.
+// Returns false when there is nothing to enqueue (count 0; frames below 8 px,
+// which also throws DataError after filling the per-frame outputs).
+bool host_args(cdvz_gpu_ctx* ctx, const uint8_t* pixels, int width, int height, size_t stride, int count,
+               size_t* offsets, int* status, int kind) {
+  const int channels = kind == 3 ? 3 : 1;
+  const size_t elem = kind == 8 ? sizeof(double) : 1;
+  if (!ctx || (!pixels && count > 0) || !offsets || !status) throw UsageError("null argument");
+  if (count < 0) throw UsageError("negative frame count");
+  if (stride < size_t(width) * channels * elem) throw UsageError("row stride shorter than a row");
+  offsets[0] = 0;
+  if (count == 0) return false;
+  if (width < 8 || height < 8) {
+    for (int i = 0; i < count; ++i) {
+      status[i] = CDVZ_GPU_DATA;
+      offsets[i + 1] = 0;
+    }
+    throw DataError("image smaller than 8 px per side");
+  }
+  return true;
+}
+
+void slot_args(cdvz_gpu_ctx::HostSlot& hs, const uint8_t* pixels, int width, int height, size_t stride, int count,
+               int mode_id, int max_side, uint8_t* out, size_t out_cap, size_t* offsets, int* status, int kind) {
+  hs.pixels = pixels;
+  hs.width = width;
+  hs.height = height;
+  hs.stride = stride;
+  hs.count = count;
+  hs.mode_id = mode_id;
+  hs.max_side = max_side;
+  hs.out = out;
+  hs.out_cap = out_cap;
+  hs.offsets = offsets;
+  hs.status = status;
+  hs.kind = kind;
+}
+
+// Host-frame batch encode of grey (kind 1) or RGB (kind 3) byte rasters, or
+// f64 grey rasters (kind 8; `stride` in bytes): groups of frames through
+// host_begin + host_finish, one after the other.
 int encode_host_batch(cdvz_gpu_ctx* ctx, const uint8_t* pixels, int width, int height, size_t stride, int count,
                       int mode_id, int max_side, uint8_t* out, size_t out_cap, size_t* offsets, int* status, int kind) {
   NvtxRange nv("cdvz_gpu_encode_batch");
   return guarded(ctx, [&] {
-    const int channels = kind == 3 ? 3 : 1;
-    const size_t elem = kind == 8 ? sizeof(double) : 1;
-    if (!ctx || (!pixels && count > 0) || !offsets || !status) throw UsageError("null argument");
-    if (count < 0) throw UsageError("negative frame count");
-    if (stride < size_t(width) * channels * elem) throw UsageError("row stride shorter than a row");
-    offsets[0] = 0;
-    if (count == 0) return;
-    const size_t slot = mode_by_id(mode_id).budget + 28;
-    if (width < 8 || height < 8) {
-      for (int i = 0; i < count; ++i) {
-        status[i] = CDVZ_GPU_DATA;
-        offsets[i + 1] = 0;
-      }
-      throw DataError("image smaller than 8 px per side");
-    }
+    if (!host_args(ctx, pixels, width, height, stride, count, offsets, status, kind)) return;
+    mode_by_id(mode_id);
     if (!ctx->shards.empty()) {
       encode_multi(ctx, pixels, width, height, stride, count, mode_id, max_side, out, out_cap, offsets, status, kind);
       return;
     }
     CDVZ_CUDA_CHECK(cudaSetDevice(ctx->device));
-    const size_t row_bytes = size_t(width) * channels * elem;
-    const size_t frame_bytes = row_bytes * height;
-    // Frames per call to run(): bounded so the device staging stays < 4 GB.
-    const int group = int(std::max<size_t>(1, std::min<size_t>(size_t(count), (size_t(4) << 30) / frame_bytes)));
-    ctx->stage_in.ensure(frame_bytes * group);
-    ctx->stage_out.ensure(slot * group);
-    ctx->stage_len.ensure(sizeof(uint32_t) * group);
-    ctx->ensure_pinned_out(slot * group, group);
+    for (auto& h : ctx->hslot)  // submitted calls finish first (their results stay with their tickets)
+      if (h.busy) throw UsageError("a submitted batch is in flight: wait for it before a synchronous call");
+    const int channels = kind == 3 ? 3 : 1;
+    const size_t elem = kind == 8 ? sizeof(double) : 1;
+    const size_t frame_bytes = size_t(width) * channels * elem * height;
+    const int group = host_group_frames(frame_bytes, count);
+    auto& hs = ctx->hslot[0];
+    slot_args(hs, pixels, width, height, stride, count, mode_id, max_side, out, out_cap, offsets, status, kind);
+    hs.ramp = true;
     size_t written = 0;
     cdvz_gpu_ctx::Stats acc;
     int acc_launches = 0;
-    auto fold = [&] {
-      ctx->collect_all();
-      for (int i = 0; i < 5; ++i) acc.stage_ms[i] += ctx->stats.stage_ms[i];
-      acc.pyr_ms += ctx->stats.pyr_ms;
-      acc.pyr_bytes += ctx->stats.pyr_bytes;
-      acc_launches += ctx->launches;
-    };
     for (int base = 0; base < count; base += group) {
       const int nf = std::min(group, count - base);
-      std::vector<int> retry;             // frames of this group that overflowed a capacity
-      std::vector<size_t> start(size_t(nf), 0);  // byte offset of each written container in `out`
-      // Containers of frames [c0, c0 + cn) of this group are in pinned memory:
-      // copied out in frame order while later chunks still run.
-      auto copy_out = [&](int c0, int cn) {
-        for (int i = c0; i < c0 + cn; ++i) {
-          const size_t len = ctx->pin_len[size_t(i)];
-          const int dev_status = ctx->pin_status[size_t(i)];
-          const int fi = base + i;
-          start[size_t(i)] = written;
-          if (len == 0) {
-            if (dev_status & 2) {
-              status[fi] = CDVZ_GPU_DATA;  // validate(): non-finite or outside [0, 1]
-            } else if (dev_status == 4) {
-              status[fi] = CDVZ_GPU_OK;    // capacity only: re-encoded below with the maximal capacities
-              retry.push_back(i);
-            } else {
-              status[fi] = CDVZ_GPU_INTERNAL;
-            }
-          } else if (written + len > out_cap) {
-            status[fi] = CDVZ_GPU_USAGE;
-          } else {
-            std::memcpy(out + written, ctx->pin_out + size_t(i) * slot, len);
-            written += len;
-            status[fi] = CDVZ_GPU_OK;
-          }
-          offsets[fi + 1] = written;
-        }
-      };
-      ctx->run(ctx->stage_in.as<uint8_t>(), width, height, (long long)row_bytes, nf, mode_id, max_side,
-               ctx->stage_out.as<uint8_t>(), ctx->stage_len.as<uint32_t>(), pixels + size_t(base) * height * stride, stride,
-               ctx->pin_out, ctx->pin_len, kind, copy_out, ctx->pin_status);
-      CDVZ_CUDA_CHECK(cudaStreamSynchronize(ctx->st));
-      fold();
-      if (retry.empty()) continue;
-      // Capacity retry: a frame whose survivor or orientation lists outgrew the
-      // batch capacities (adversarial content) is encoded again on its own with
-      // the largest counts the reference can produce, so it never fails where
-      // the reference succeeds. Its container is then spliced in frame order.
-      std::vector<std::vector<uint8_t>> redo(retry.size());
-      ctx->cap_boost = true;
-      try {
-        for (size_t r = 0; r < retry.size(); ++r) {
-          const int i = retry[r];
-          ctx->run(ctx->stage_in.as<uint8_t>() + size_t(i) * frame_bytes, width, height, (long long)row_bytes, 1, mode_id,
-                   max_side, ctx->stage_out.as<uint8_t>(), ctx->stage_len.as<uint32_t>(), nullptr, 0, nullptr, nullptr,
-                   kind);
-          CDVZ_CUDA_CHECK(cudaStreamSynchronize(ctx->st));
-          fold();
-          uint32_t len = 0;
-          int dev_status = 0;
-          CDVZ_CUDA_CHECK(cudaMemcpy(&len, ctx->stage_len.as<uint32_t>(), sizeof(len), cudaMemcpyDeviceToHost));
-          const Lane& L = ctx->lanes[ctx->last_lane];
-          CDVZ_CUDA_CHECK(cudaMemcpy(&dev_status, L.bt.status, sizeof(int), cudaMemcpyDeviceToHost));
-          if (len == 0) {
-            status[base + i] = (dev_status & 2) ? CDVZ_GPU_DATA : CDVZ_GPU_INTERNAL;
-            continue;
-          }
-          redo[r].resize(len);
-          CDVZ_CUDA_CHECK(cudaMemcpy(redo[r].data(), ctx->stage_out.as<uint8_t>(), len, cudaMemcpyDeviceToHost));
-        }
-      } catch (...) {
-        ctx->cap_boost = false;
-        throw;
-      }
-      ctx->cap_boost = false;
-      size_t grow = 0;
-      for (const auto& v : redo) grow += v.size();
-      if (written + grow > out_cap) {  // no room: the re-encoded frames are reported like any overflow
-        for (size_t q = 0; q < retry.size(); ++q)
-          if (!redo[q].empty()) status[base + retry[q]] = CDVZ_GPU_USAGE;
-        continue;
-      }
-      // Rebuild this group's section back to front: containers only move right.
-      size_t end = written + grow;
-      size_t r = retry.size();
-      for (int i = nf - 1; i >= 0; --i) {
-        const int fi = base + i;
-        const size_t old_len = size_t(offsets[fi + 1]) - start[size_t(i)];
-        const std::vector<uint8_t>* ins = (r > 0 && retry[r - 1] == i) ? &redo[--r] : nullptr;
-        const size_t len = ins ? ins->size() : old_len;
-        const size_t pos = end - len;
-        if (ins) {
-          if (len) std::memcpy(out + pos, ins->data(), len);
-        } else if (len && pos != start[size_t(i)]) {
-          std::memmove(out + pos, out + start[size_t(i)], len);
-        }
-        offsets[fi + 1] = end;
-        end = pos;
-      }
-      written += grow;
+      host_begin(ctx, hs, base, nf);
+      host_finish(ctx, hs, base, nf, written, acc, acc_launches);
     }
     ctx->stats = acc;
     ctx->launches = acc_launches;
@@ -1261,6 +1426,81 @@ int cdvz_gpu_pnm_parse(const uint8_t* file, size_t len, int* width, int* height,
     *channels = int(ch);
     *raster_offset = pos;
   });
+}
+
+// Submitted host batches (cdvz_gpu.h): at most two in flight per context, each
+// with its own staging slot. A submit that finds both slots taken first
+// finishes the older call into its caller's buffers (its wait then returns
+// the stored result).
+namespace {
+void finish_slot(cdvz_gpu_ctx* ctx, cdvz_gpu_ctx::HostSlot& hs) {
+  const int rc = guarded(ctx, [&] {
+    CDVZ_CUDA_CHECK(cudaSetDevice(ctx->device));
+    size_t written = 0;
+    cdvz_gpu_ctx::Stats acc;
+    int acc_launches = 0;
+    host_finish(ctx, hs, 0, hs.count, written, acc, acc_launches, false);
+  });
+  ctx->finished.push_back({hs.ticket, rc, rc == CDVZ_GPU_OK ? std::string() : ctx->err});
+  hs.busy = false;
+  hs.ticket = 0;
+}
+}  // namespace
+
+int cdvz_gpu_encode_batch_submit(cdvz_gpu_ctx* ctx, const uint8_t* pixels, int width, int height, size_t stride,
+                                 int count, int mode_id, int max_side, uint8_t* out, size_t out_cap, size_t* offsets,
+                                 int* status, uint64_t* ticket) {
+  NvtxRange nv("cdvz_gpu_encode_batch_submit");
+  return guarded(ctx, [&] {
+    if (!ticket) throw UsageError("null ticket");
+    *ticket = 0;  // 0: the call completed inside submit (nothing to wait for)
+    if (!host_args(ctx, pixels, width, height, stride, count, offsets, status, 1)) return;
+    mode_by_id(mode_id);
+    const bool one_group = size_t(count) <= size_t(host_group_frames(size_t(width) * height, count));
+    if (!ctx->shards.empty() || !one_group) {  // multi-device, or > 4 GB of frames: synchronous
+      for (auto& h : ctx->hslot)
+        if (h.busy) finish_slot(ctx, h);
+      if (encode_host_batch(ctx, pixels, width, height, stride, count, mode_id, max_side, out, out_cap, offsets, status,
+                            1) != CDVZ_GPU_OK)
+        throw std::runtime_error(ctx->err);
+      return;
+    }
+    CDVZ_CUDA_CHECK(cudaSetDevice(ctx->device));
+    cdvz_gpu_ctx::HostSlot* hs = nullptr;
+    for (auto& h : ctx->hslot)
+      if (!h.busy) hs = &h;
+    if (!hs) {  // both in flight: finish the older one now (its wait returns the held result)
+      hs = ctx->hslot[0].ticket < ctx->hslot[1].ticket ? &ctx->hslot[0] : &ctx->hslot[1];
+      finish_slot(ctx, *hs);
+    }
+    slot_args(*hs, pixels, width, height, stride, count, mode_id, max_side, out, out_cap, offsets, status, 1);
+    hs->ramp = false;  // streamed calls overlap each other: full chunks, like encode_device
+    hs->ticket = ctx->next_ticket++;
+    hs->busy = true;
+    try {
+      host_begin(ctx, *hs, 0, count);
+    } catch (...) {
+      hs->busy = false;
+      hs->ticket = 0;
+      throw;
+    }
+    *ticket = hs->ticket;
+  });
+}
+
+int cdvz_gpu_encode_batch_wait(cdvz_gpu_ctx* ctx, uint64_t ticket) {
+  if (!ctx) return guarded(ctx, [] { throw UsageError("null context"); });
+  if (ticket == 0) return CDVZ_GPU_OK;
+  for (auto& h : ctx->hslot)
+    if (h.busy && h.ticket == ticket) finish_slot(ctx, h);
+  for (size_t i = 0; i < ctx->finished.size(); ++i) {
+    if (ctx->finished[i].ticket != ticket) continue;
+    const int rc = ctx->finished[i].rc;
+    if (rc != CDVZ_GPU_OK) ctx->err = ctx->finished[i].err;
+    ctx->finished.erase(ctx->finished.begin() + long(i));
+    return rc;
+  }
+  return guarded(ctx, [] { throw UsageError("unknown or already waited ticket"); });
 }
 
 int cdvz_gpu_encode_batch(cdvz_gpu_ctx* ctx, const uint8_t* pixels, int width, int height, size_t stride, int count,

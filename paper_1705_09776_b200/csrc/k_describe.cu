@@ -400,7 +400,7 @@ __device__ __forceinline__ double div_two_pi(double a) {
   return fma(r, kInvTwoPi, q0);
 }
 
-__global__ void __launch_bounds__(kSampleThreads) k_sample(Batch bt) {
+__global__ void __launch_bounds__(kSampleThreads, 12) k_sample(Batch bt) {
   __shared__ double gexp[kMaxSamples * (kMaxSamples + 1) / 2];  // [j * (j + 1) / 2 + i], i <= j
   // Per-axis terms (u_i = v_i, the same expression): the reference's
   // px = (cx + u cos) - v sin and py = (cy + u sin) + v cos, evaluated in its
@@ -687,6 +687,227 @@ __global__ void __launch_bounds__(32 * kPBWarps, 8) k_describe(Batch bt) {
   }
 }
 
+// Phase B, shared-memory cell accumulators (the default): FOUR oriented points
+// per warp, row-synchronous.
+// Lane (q, cx, dv) of point q walks every sample row j in order; in row j it
+// visits, in increasing i, the samples whose cell column is cx (c0[i] in
+// {cx - 1, cx}), decodes each sample once and adds its two orientation
+// contributions (bins ob0 and ob0 + 1 mod 8) to cell (cx, c0[j] + dv).
+// Accumulators live in shared memory indexed by (set, bin, cell): at any
+// moment each (cell, bin) has exactly one owning lane, and a cell's chains
+// pass from lane dv = 1 to lane dv = 0 when the rows cross a cell boundary
+// with no exchange, so every bin is one sequential chain in the reference's
+// sample order (descriptor.cpp:98-116). Sets: the left (i < 16) and right
+// (i >= 16) sub-patch partials of the current 16-row band; the folded total
+// ((P0 + P1) + P2) + P3 of merge_and_normalize lives in registers (lane hl
+// folds cells hl and hl + 8). Rows of (weight, fo) records and their bins
+// stream into a 2-row shared ring with cp.async, one row ahead of the walk.
+// (k_describe below keeps the bins in registers instead: debug bit 256.)
+// Bank-conflict-free accumulator layout: the 16 lanes of a half-warp (points
+// q, q^1) touch cells (cx, cy) with distinct (q & 1, cy & 1, cx), which is the
+// double's bank slot (index mod 16); set, bin, cy >> 1 and q >> 1 select
+// 16-double rows.
+__device__ __forceinline__ int acc_index(int q, int set, int bin, int cy, int cx) {
+  return (q >> 1) * 512 + set * 256 + bin * 32 + (cy >> 1) * 16 + (q & 1) * 8 + (cy & 1) * 4 + cx;
+}
+struct CellSmem {
+  double2 ring[2][kPBPts][kMaxSamples];  // [slot][q][i]: (weight, fo)
+  uint8_t bin[2][kPBPts][kMaxSamples];   // [slot][q][i]: ob0 mod 8
+  double acc[kPBPts * 256];              // acc_index(); after phase B: per-point scratch [q][256]
+  double wf[kPBPts][kMaxSamples];        // [q][i]: f of the cell coordinate (1 - f formed on use)
+  int8_t c0[kPBPts][kMaxSamples];        // [q][i]: floor(u * inv_cell + 1.5) in -1 .. 4
+};
+
+
+__global__ void __launch_bounds__(32 * kPBWarps, 8) k_describe_cells(Batch bt) {
+  extern __shared__ __align__(16) uint8_t pb_smem[];
+  const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  CellSmem& S = reinterpret_cast<CellSmem*>(pb_smem)[wi];
+  const int f = blockIdx.y;
+  const int n_or = bt.or_count[f];
+  const int q = lane >> 3, hl = lane & 7;
+  const int cx = hl & 3, dv = hl >> 2;
+  const unsigned gmask = 0xffu << (kPBLanes * q);
+  for (int grp = blockIdx.x * kPBWarps + wi; kPBPts * grp < n_or; grp += gridDim.x * kPBWarps) {
+    const int idx = kPBPts * grp + q;
+    const bool live = idx < n_or;
+    const long long gslot = (long long)f * bt.cap_or + (live ? idx : 0);
+    const DescGeo g = bt.geo[gslot];
+    const int samples = live ? g.samples : 0;  // 0: no point, or flagged by k_geometry
+    const double2* smp = bt.smp + gslot * bt.smp_cap;
+    const uint8_t* smb = bt.smpb + gslot * kMaxSamples * kMaxSamples;
+    auto fetch_row = [&](int j) {
+      if (j < samples) {
+        double2* dst = S.ring[j & 1][q];
+        const double2* src = smp + (long long)j * samples;
+        for (int i = hl; i < samples; i += kPBLanes) cp_async16(dst + i, src + i);
+        if (hl < 2) cp_async16(S.bin[j & 1][q] + 16 * hl, smb + j * kMaxSamples + 16 * hl);
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    fetch_row(0);
+    // Per-axis cell coordinates (descriptor.cpp:89-96): identical for u (i) and v (j).
+    for (int i = hl; i < samples; i += kPBLanes) {
+      const double u = (i + 0.5) * g.step - g.half;
+      const double cu = u * g.inv_cell + 1.5;
+      const int c0 = static_cast<int>(floor(cu));
+      const double fu = cu - c0;
+      S.c0[q][i] = c0;
+      S.wf[q][i] = fu;
+    }
+    double* acc = S.acc;
+    for (int e = lane; e < kPBPts * 256; e += 32) acc[e] = 0.0;
+    __syncwarp();
+    // Column range of cx: c0 in {cx - 1, cx}; weight f (d = 1) below im.
+    int ia = 0, im = 0, ib = 0;
+    for (int i = 0; i < samples; ++i) {
+      const int c = S.c0[q][i];
+      ia += c < cx - 1;
+      im += c < cx;
+      ib += c < cx + 1;
+    }
+    const int rows = __reduce_max_sync(0xffffffffu, samples);
+    double tot[2][8];  // lane hl's fold of cells hl and hl + 8
+#pragma unroll
+    for (int c = 0; c < 2; ++c)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) tot[c][k] = 0.0;
+    for (int j = 0; j < rows; ++j) {
+      fetch_row(j + 1);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+      __syncwarp();
+      if (j == kSub && samples > kSub) {
+        // Band boundary: the first two sub-patch partials are complete.
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const int e = acc_index(q, 0, k, c * 2 + (hl >> 2), hl & 3);  // cell hl + 8c
+            tot[c][k] = acc[e] + acc[256 + e];
+            acc[e] = 0.0;
+            acc[256 + e] = 0.0;
+          }
+      }
+      __syncwarp();
+      if (j < samples) {
+        const int cy = S.c0[q][j] + dv;
+        if (cy >= 0 && cy < 4) {
+          const double fv = S.wf[q][j];
+          const double wv = dv ? fv : 1.0 - fv;
+          const double2* rowp = S.ring[j & 1][q];
+          const uint8_t* rowb = S.bin[j & 1][q];
+          const double* wfq = S.wf[q];
+          const int cell = acc_index(q, 0, 0, cy, cx);
+          // Visit i: weight * wv * wu * wo for wo = 1 - fo (bin ob0) and fo
+          // (bin ob0 + 1), descriptor.cpp:89-116. Two-stage software
+          // pipeline: visit i + 1 is decoded while visit i's two chains are
+          // updated.
+          auto decode = [&](int i, int& o0, int& o1, double& x0, double& x1) {
+            const double2 rec = rowp[i];
+            const double fu = wfq[i];
+            const double wu = i < im ? fu : 1.0 - fu;
+            const double fo = rec.y;
+            const int b0 = rowb[i];
+            const double base = rec.x * wv * wu;
+            const int so = cell + (i < kSub ? 0 : 256);
+            o0 = so + 32 * b0;
+            o1 = so + 32 * ((b0 + 1) & 7);
+            x0 = base * (1.0 - fo);
+            x1 = base * fo;
+          };
+          // The next visit's two loads are issued before this visit's
+          // stores; a load that hits a bin just updated takes the updated
+          // value from registers instead (o0 != o1 always), so each chain's
+          // critical path is one add.
+          if (ia < ib) {
+            int o0, o1;
+            double x0, x1;
+            decode(ia, o0, o1, x0, x1);
+            double a0 = acc[o0], a1 = acc[o1];
+            for (int i = ia; i < ib; ++i) {
+              const double s0 = a0 + x0, s1 = a1 + x1;
+              int n0 = o0, n1 = o1;
+              double y0 = 0.0, y1 = 0.0, b0 = 0.0, b1 = 0.0;
+              if (i + 1 < ib) {
+                decode(i + 1, n0, n1, y0, y1);
+                b0 = acc[n0];
+                b1 = acc[n1];
+              }
+              acc[o0] = s0;
+              acc[o1] = s1;
+              a0 = n0 == o0 ? s0 : (n0 == o1 ? s1 : b0);
+              a1 = n1 == o0 ? s0 : (n1 == o1 ? s1 : b1);
+              o0 = n0;
+              o1 = n1;
+              x0 = y0;
+              x1 = y1;
+            }
+          }
+        }
+      }
+      __syncwarp();
+    }
+#pragma unroll
+    for (int c = 0; c < 2; ++c)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int e = acc_index(q, 0, k, c * 2 + (hl >> 2), hl & 3);
+        tot[c][k] = samples > kSub ? (tot[c][k] + acc[e]) + acc[256 + e] : acc[e];
+      }
+    __syncwarp();
+    // normalize_descriptor (descriptor.cpp:124-145): up to 5 rounds of L2
+    // normalise + clamp at 0.2; the norm in the Eigen SSE2 reduction order
+    // (four stride-4 running sums, then (s0 + s2) + (s1 + s3)).
+    // Element index of (cell, bin) is cell * 8 + bin.
+    double* sq = acc + 256 * q;
+    bool done = samples == 0;
+    for (int round = 0; round < 5; ++round) {
+#pragma unroll
+      for (int c = 0; c < 2; ++c)
+#pragma unroll
+        for (int k = 0; k < 8; ++k) sq[8 * (hl + 8 * c) + k] = tot[c][k] * tot[c][k];
+      __syncwarp();
+      double red = 0.0;
+      if (hl < 4) {
+        red = sq[hl];
+#pragma unroll 8
+        for (int k = 1; k < 32; ++k) red = red + sq[hl + 4 * k];
+      }
+      const int gb = kPBLanes * q;
+      const double r0 = __shfl_sync(0xffffffffu, red, gb), r1 = __shfl_sync(0xffffffffu, red, gb + 1);
+      const double r2 = __shfl_sync(0xffffffffu, red, gb + 2), r3 = __shfl_sync(0xffffffffu, red, gb + 3);
+      __syncwarp();
+      const double norm = sqrt((r0 + r2) + (r1 + r3));
+      bool clipped = false;
+      if (!done) {
+        if (norm == 0.0) {
+          done = true;
+        } else {
+#pragma unroll
+          for (int c = 0; c < 2; ++c)
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              tot[c][k] = tot[c][k] / norm;
+              if (tot[c][k] > 0.2) { tot[c][k] = 0.2; clipped = true; }
+            }
+        }
+      }
+      if (!(__ballot_sync(0xffffffffu, clipped) & gmask)) done = true;
+      if (__all_sync(0xffffffffu, done)) break;
+    }
+    if (samples > 0) {
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const int cl = hl + 8 * c;
+        double2* dout = reinterpret_cast<double2*>(bt.desc + ((long long)f * bt.cap_or + idx) * 128 + 8 * cl);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) dout[k] = make_double2(tot[c][2 * k], tot[c][2 * k + 1]);
+      }
+    }
+    __syncwarp();
+  }
+}
+
 // Compression (pipeline.cpp:37-50, the reference's "compression" stage):
 // transform_descriptor (transform_coding.cpp:81-91), quantize_ternary
 // (:202-217) and the location quantisers quantize_coord / quantize_sigma_log /
@@ -779,10 +1000,17 @@ cudaError_t launch_describe(const Batch& bt, const DetConst& dc, cudaStream_t st
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   static size_t configured[kMaxDevices] = {};
-  constexpr int smem = int(sizeof(PhaseBSmem)) * kPBWarps;
-  e = once_per_device(configured, 1, [&] { return cudaFuncSetAttribute(k_describe, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); });
+  constexpr int smem = int(sizeof(PhaseBSmem)) * kPBWarps, csmem = int(sizeof(CellSmem)) * kPBWarps;
+  e = once_per_device(configured, 1, [&] {
+    cudaError_t r = cudaFuncSetAttribute(k_describe, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    return r != cudaSuccess ? r : cudaFuncSetAttribute(k_describe_cells, cudaFuncAttributeMaxDynamicSharedMemorySize, csmem);
+  });
   if (e != cudaSuccess) return e;
-  k_describe<<<dim3((bt.cap_or + kPBPts * kPBWarps - 1) / (kPBPts * kPBWarps), bt.nframes), 32 * kPBWarps, smem, st>>>(bt);
+  const dim3 grid((bt.cap_or + kPBPts * kPBWarps - 1) / (kPBPts * kPBWarps), bt.nframes);
+  if (dc.desc_registers)
+    k_describe<<<grid, 32 * kPBWarps, smem, st>>>(bt);
+  else
+    k_describe_cells<<<grid, 32 * kPBWarps, csmem, st>>>(bt);
   return cudaGetLastError();
 }
 

@@ -184,8 +184,22 @@ __device__ __forceinline__ float rsqrt_approx(float x) {
 // float error (the alpha copies are within 6e-8 relative of the exact values;
 // fused multiply-adds are fine: this only screens). Near-double roots and
 // degenerate cases go to the exact path.
-__device__ __forceinline__ bool screen_pixel(const float a[4], const float up[4], const float dn[4],
-                                              const DetConst& dc) {
+//
+// The magnitude bounds are taken at the largest screened scale r_max =
+// s_hi + 0.05 (r <= r_max, so they bound the per-root values from above and
+// only widen the margins): B(x) = sum |x_i| r_max^i for the pixel's own cubic,
+// M(x) = B(x) + sum i |x_i| r_max^(i-1) (value plus slope) for a neighbour's;
+// both are formed once per pixel, when its alpha row is made.
+__device__ __forceinline__ float mag_bound(const float a[4], float rm) {
+  return __fmaf_rn(rm, __fmaf_rn(rm, __fmaf_rn(rm, fabsf(a[3]), fabsf(a[2])), fabsf(a[1])), fabsf(a[0]));
+}
+__device__ __forceinline__ float nbr_bound(const float a[4], float rm) {
+  const float slope = __fmaf_rn(rm, __fmaf_rn(rm, 3.0f * fabsf(a[3]), 2.0f * fabsf(a[2])), fabsf(a[1]));
+  return mag_bound(a, rm) + slope;
+}
+
+__device__ __forceinline__ bool screen_pixel(const float a[4], float ba, const float up[4], float mu, const float dn[4],
+                                              float md, const DetConst& dc) {
   const float fa = 3.0f * a[3], fb = 2.0f * a[2], fc = a[1];
   if (fa == 0.0f) return true;
   const float bb = fb * fb, ac4 = 4.0f * fa * fc;
@@ -197,9 +211,16 @@ __device__ __forceinline__ bool screen_pixel(const float a[4], const float up[4]
   const float q = -0.5f * (fb + copysignf(sq, fb));
   if (!(fabsf(q) > 1e-30f)) return true;
   const float r0 = q * rcp_approx(fa), r1 = fc * rcp_approx(q);
-  auto horner = [](float r, float c0, float c1, float c2, float c3) {
-    return __fmaf_rn(r, __fmaf_rn(r, __fmaf_rn(r, c3, c2), c1), c0);
+  auto horner = [](float r, const float c[4]) {
+    return __fmaf_rn(r, __fmaf_rn(r, __fmaf_rn(r, c[3], c[2]), c[1]), c[0]);
   };
+  // The exact test needs p above (p > 0) or below (p < 0) all eight
+  // neighbours' cubics at the same scale; drop the root only when the up or
+  // down neighbour is clearly past p. The float root is within ~1e-6 s of the
+  // exact one and p is stationary there, so a margin of 1e-4 of the
+  // magnitudes (values plus slopes) is far beyond the float error.
+  const float m = 1e-4f * (ba + mu + md) + 1e-7f;
+  const float tmargin = __fmaf_rn(1e-5f, ba, 1e-6f);
   bool any = false;
 #pragma unroll
   for (int k = 0; k < 2; ++k) {
@@ -208,20 +229,9 @@ __device__ __forceinline__ bool screen_pixel(const float a[4], const float up[4]
       if (!isfinite(r)) any = true;
       continue;
     }
-    const float p = horner(r, a[0], a[1], a[2], a[3]);
-    const float bound = horner(r, fabsf(a[0]), fabsf(a[1]), fabsf(a[2]), fabsf(a[3]));
-    if (!(__fmaf_rn(1e-5f, bound, fabsf(p) + 1e-6f) >= dc.scr_thr)) continue;
-    // The exact test needs p above (p > 0) or below (p < 0) all eight
-    // neighbours' cubics at the same scale; drop the root only when the up or
-    // down neighbour is clearly past p. The float root is within ~1e-6 s of
-    // the exact one and p is stationary there, so a margin of 1e-4 of the
-    // magnitudes (values plus slopes) is far beyond the float error.
-    const float pu = horner(r, up[0], up[1], up[2], up[3]), pd = horner(r, dn[0], dn[1], dn[2], dn[3]);
-    const float bu = horner(r, fabsf(up[0]), fabsf(up[1]), fabsf(up[2]), fabsf(up[3]));
-    const float bd = horner(r, fabsf(dn[0]), fabsf(dn[1]), fabsf(dn[2]), fabsf(dn[3]));
-    const float su = __fmaf_rn(r, __fmaf_rn(r, 3.0f * fabsf(up[3]), 2.0f * fabsf(up[2])), fabsf(up[1]));
-    const float sd = __fmaf_rn(r, __fmaf_rn(r, 3.0f * fabsf(dn[3]), 2.0f * fabsf(dn[2])), fabsf(dn[1]));
-    const float m = 1e-4f * (bound + bu + bd + su + sd) + 1e-7f;
+    const float p = horner(r, a);
+    if (!(fabsf(p) + tmargin >= dc.scr_thr)) continue;
+    const float pu = horner(r, up), pd = horner(r, dn);
     const bool past = p > 0.0f ? (pu >= p + m || pd >= p + m) : (pu <= p - m || pd <= p - m);
     if (!past) any = true;
   }
@@ -237,7 +247,7 @@ __device__ __forceinline__ bool screen_pixel(const double a[4], const double up[
     uf[i] = float(up[i]);
     df[i] = float(dn[i]);
   }
-  return screen_pixel(af, uf, df, dc);
+  return screen_pixel(af, mag_bound(af, dc.scr_hi), uf, nbr_bound(uf, dc.scr_hi), df, nbr_bound(df, dc.scr_hi), dc);
 }
 
 // ---------------------------------------------------------------- K1a: blur
@@ -673,6 +683,7 @@ struct alignas(128) DetWarpSmem {
   };
   double ring[kRing][4][32];   // alpha rows: [row % kRing][coefficient][lane]
   float4 fring[4][32];         // float copies of alpha rows ra - 2 .. ra + 1 (the screen's inputs): [row % 4][lane]
+  float mring[4][32];          // their neighbour bounds M (screen_pixel)
   uint64_t bar[2];             // TMA path: one mbarrier per pair slot
   uint16_t queue[128];         // ((row - y0 + 2) << 5) | lane
 };
@@ -767,7 +778,8 @@ __global__ void __maxnreg__(96) k_detect_walk(Batch bt, DetConst dc, int o, int 
     for (int i = 0; i < kPrefetch + 2; ++i) issue();  // rows y0 - 2 .. y0 + kPrefetch - 1
   }
   const double oct_scale = ldexp(1.0, o);
-  float apf[4];  // own alpha (float copy) of the previous row (screened one row late)
+  float apf[4];       // own alpha (float copy) of the previous row (screened one row late)
+  float bp = 0.f, mp = 0.f;  // its magnitude and neighbour bounds
   int qn = 0;
   auto drain = [&]() {
     for (int qi = lane; qi - lane < qn; qi += 32) {
@@ -813,9 +825,10 @@ __global__ void __maxnreg__(96) k_detect_walk(Batch bt, DetConst dc, int o, int 
       an[i] = sum;
     }
   };
-  auto screen_row = [&](int rs, const float a[4], const float up[4], const float dn[4]) {  // 3x3 neighbourhood complete
+  auto screen_row = [&](int rs, const float a[4], float ba, const float up[4], float mu, const float dn[4],
+                        float md) {  // 3x3 neighbourhood complete
     if (rs >= y0 && rs < y1) {
-      const bool push = out_col && (!dc.screen || screen_pixel(a, up, dn, dc));
+      const bool push = out_col && (!dc.screen || screen_pixel(a, ba, up, mu, dn, md, dc));
       const unsigned bal = __ballot_sync(0xffffffffu, push);
       if (push) S.queue[qn + __popc(bal & ((1u << lane) - 1u))] = uint16_t(((rs - y0 + 2) << 5) | lane);
       qn += __popc(bal);
@@ -848,8 +861,14 @@ __global__ void __maxnreg__(96) k_detect_walk(Batch bt, DetConst dc, int o, int 
         S.ring[unsigned(ra) % kRing][i][lane] = a0[i];
         if (second) S.ring[unsigned(ra + 1) % kRing][i][lane] = a1[i];
       }
+      const float b0 = mag_bound(a0f, dc.scr_hi), m0 = nbr_bound(a0f, dc.scr_hi);
+      const float b1 = mag_bound(a1f, dc.scr_hi), m1 = nbr_bound(a1f, dc.scr_hi);
       S.fring[unsigned(ra) % 4][lane] = make_float4(a0f[0], a0f[1], a0f[2], a0f[3]);
-      if (second) S.fring[unsigned(ra + 1) % 4][lane] = make_float4(a1f[0], a1f[1], a1f[2], a1f[3]);
+      S.mring[unsigned(ra) % 4][lane] = m0;
+      if (second) {
+        S.fring[unsigned(ra + 1) % 4][lane] = make_float4(a1f[0], a1f[1], a1f[2], a1f[3]);
+        S.mring[unsigned(ra + 1) % 4][lane] = m1;
+      }
       __syncwarp();
       if constexpr (TMA) {
         issue_pair((t >> 1) + 2);  // into the slot of pair t/2 (rows ra - 1, ra), read by every lane above
@@ -860,11 +879,13 @@ __global__ void __maxnreg__(96) k_detect_walk(Batch bt, DetConst dc, int o, int 
       {
         const float4 u4 = S.fring[unsigned(ra - 2) % 4][lane];  // own alpha of row ra - 2 (the ring keeps it)
         const float auf[4] = {u4.x, u4.y, u4.z, u4.w};
-        screen_row(ra - 1, apf, auf, a0f);
+        screen_row(ra - 1, apf, bp, auf, S.mring[unsigned(ra - 2) % 4][lane], a0f, m0);
       }
-      if (second) screen_row(ra, a0f, apf, a1f);
+      if (second) screen_row(ra, a0f, b0, apf, mp, a1f, m1);
 #pragma unroll
       for (int i = 0; i < 4; ++i) apf[i] = a1f[i];
+      bp = b1;
+      mp = m1;
     }
     __syncwarp();
     // Every queued pixel (rows <= the last alpha row - 1) has its

@@ -161,3 +161,21 @@ def test_cpp_reference_signature_struct_out(tmp_path, bundle_b8):
     assert len(codes) == int(fields["codes"][0]) > 0
     assert all(len(c) == 5 + 103 and c[4] == 4 for c in codes)
     assert "stage detection" in txt.read_text()
+
+
+def test_submit_wait_streams_batches(bundle_b8):
+    """cdvz_gpu_encode_batch_submit / _wait: three batches submitted before
+    any wait (the third submit completes the first), waited out of order —
+    every batch's containers equal encode_batch's and the oracle's."""
+    ex = cg.Extractor(bundle_b8, max_batch=16)
+    batches = [oracle_lib.synth_frames(5000 + 100 * k, 6, 320, 240) for k in range(3)]
+    pend = [ex.encode_batch_submit(b, "4K") for b in batches]
+    got = [pend[2].wait(), pend[0].wait(), pend[1].wait()]
+    got = [got[1], got[2], got[0]]
+    for k, b in enumerate(batches):
+        want, st = ex.encode_batch(b, "4K")
+        assert got[k][0] == want and got[k][1].tolist() == [0] * 6
+        assert want[0] == oracle_lib.encode(bundle_b8, b[0], 3)
+    with pytest.raises(cg.UsageError):
+        pend[0].ex._check(pend[0].ex._lib.cdvz_gpu_encode_batch_wait(ex._ctx, pend[0].ticket))
+    ex.close()
