@@ -18,7 +18,7 @@ def gbytes(s):
 def main(rep, frames=256, w=640, h=480, m=10):
     rows = ncu_summary.summarise(rep)
     blur = next(r for r in rows if r["kernel"].startswith("void k_blur<5, 5, 6, 8, 0"))
-    det = next(r for r in rows if r["kernel"].startswith("k_detect_walk"))
+    det = next(r for r in rows if "k_detect_walk" in r["kernel"])
     traffic = sum(gbytes(r[k]) for r in (blur, det) for k in ("dram_read", "dram_write")) * 1e9
     algo = frames * (w * h * (1 + 32) + 32 * (w - 2 * m) * (h - 2 * m))
     out = {"dram_bytes_per_launch_pair": traffic, "algorithmic_bytes_per_launch_pair": algo,
