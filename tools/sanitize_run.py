@@ -6,9 +6,10 @@ kernel of the product path on a handful of frames, no torch.
 * encode: 2 frames of 320x240 (SAN_W / SAN_H / SAN_N override) in 4K mode (u8 path: k_blur<.., 0>, k_detect_walk,
   merge, select, orient, expand, geometry, sample, describe, PCA,
   posterior-small, Fisher, SCFV, pack), the same frames with the 512-component
-  bundle (k_posterior), one f64 frame at three times the size (resized) (k_validate, f64 k_resize,
+  bundle (k_posterior on the FP64 tensor cores), one f64 frame at three times the size (resized) (k_validate, f64 k_resize,
   k_blur<.., 1>), one odd-width RGB frame (k_grey_rgb, unaligned u8 rows),
-  on-device synthesis, and the debug paths (exact-only extrema, the TMA tile kernel and its plain-load
+  on-device synthesis, streamed submit / wait batches, the register-bin
+  describe variant, and the debug paths (exact-only extrema, the TMA tile kernel and its plain-load
   variant, tiny capacities -> the capacity retry);
 * match: an 8-container index, retrieve + match_pairs (k_match.cu).
 Exit 0 when every container equals the oracle's (sanity: the sanitizer run
@@ -51,11 +52,22 @@ def encode_part():
         got, st = ex.encode_batch(frames[:1], "4K")
         assert got[0] == want0, flags
     ex.set_debug(False)
+    # streamed submit / wait (two batches in flight) and the describe variant with register bins
+    p0 = ex.encode_batch_submit(frames, "4K")
+    p1 = ex.encode_batch_submit(frames[:1], "8K")
+    assert p0.wait()[0][0] == want0 and p1.wait()[1].tolist() == [0]
+    ex.set_debug(False, desc_registers=True)
+    got, st = ex.encode_batch(frames[:1], "4K")
+    assert got[0] == want0
+    ex.set_debug(False)
     ex.close()
     ex = cg.Extractor(b512, max_batch=4)
     got, st = ex.encode_batch(frames[:2], "4K")
     for i in range(2):
         assert got[i] == oracle_lib.encode(b512, frames[i], 3), f"b512 frame {i}"
+    ex.set_debug(False, post_simt=True)  # the SIMT posterior kernel too
+    got2, st = ex.encode_batch(frames[:2], "4K")
+    assert got2 == got
     ex.close()
 
 
