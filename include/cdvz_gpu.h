@@ -132,6 +132,24 @@ int cdvz_gpu_encode_batch_f64(cdvz_gpu_ctx* ctx, const double* pixels, int width
                               int count, int mode_id, int max_side, uint8_t* out, size_t out_cap, size_t* offsets,
                               int* status);
 
+/* train_model (proj/src/pipeline.cpp:99-166, TrainOptions pipeline.hpp:22-28)
+ * with the heavy work on device `device`: pass 1 over the corpus (detection,
+ * selection, description) and the detection of each image's synthetic partner
+ * (apply_transform, synthetic.cpp:78-90) run through the extractor; the PCA
+ * covariance and projection, the EM iterations of the GMM and the descriptor
+ * transform run as GPU kernels; relevance tables, k-means++ seeding, the
+ * eigensolver and the quantiles on the host. `corpus` holds `count` >= 20
+ * GrayImages of one size (row-major doubles in [0, 1], row stride `stride`
+ * doubles). Writes the bundle text (serialize_model) to `out` (needs *out_len
+ * bytes; pass out = NULL to query). Defaults of the reference: seed 7, 8
+ * components, 25 EM iterations, select_n 300, max_side 640, 16 bins. The
+ * libm (exp / log) and eigensolver differ from glibc / Eigen in the last
+ * bits, so the PCA, GMM and quantizer sections are numerically, not bitwise,
+ * the reference's. */
+int cdvz_gpu_train_model(int device, const double* corpus, int count, int width, int height, size_t stride,
+                         uint64_t seed, int gmm_components, int em_iterations, int select_n, int max_side,
+                         int relevance_bins, char* out, size_t out_cap, size_t* out_len);
+
 /* PPM form of cdvz_gpu_encode_batch: `count` interleaved 8-bit RGB frames
  * (row stride `stride` >= 3*width bytes). Each pixel becomes the grey value
  * (0.299 r + 0.587 g + 0.114 b) * (1/255) on the device, exactly as

@@ -102,6 +102,7 @@ def _lib() -> ctypes.CDLL:
         "cdvz_gpu_encode_batch": (I, [P, P, I, I, S, I, I, I, P, S, P, P]),
         "cdvz_gpu_encode_batch_rgb": (I, [P, P, I, I, S, I, I, I, P, S, P, P]),
         "cdvz_gpu_encode_batch_submit": (I, [P, P, I, I, S, I, I, I, P, S, P, P, ctypes.POINTER(U64)]),
+        "cdvz_gpu_train_model": (I, [I, P, I, I, I, S, U64, I, I, I, I, I, P, S, ctypes.POINTER(S)]),
         "cdvz_gpu_encode_batch_wait": (I, [P, U64]),
         "cdvz_gpu_pnm_parse": (I, [P, S, ctypes.POINTER(I), ctypes.POINTER(I), ctypes.POINTER(I), ctypes.POINTER(S)]),
         "cdvz_gpu_encode_device": (I, [P, P, I, I, S, I, I, I, P, P]),
@@ -221,6 +222,26 @@ def parse_pnm(data: bytes):
                                   ctypes.byref(off))
     _raise(code, lib.cdvz_gpu_last_error(None).decode())
     return w.value, h.value, ch.value, off.value
+
+
+def train_model(corpus: np.ndarray, seed: int = 7, gmm_components: int = 8, em_iterations: int = 25,
+                select_n: int = 300, max_side: int = 640, relevance_bins: int = 16, device: int = 0) -> str:
+    """train_model (proj/src/pipeline.cpp:99-166) on the GPU (cdvz_gpu_train_model):
+    ``corpus`` is float64 [N, H, W] (N >= 20 GrayImages in [0, 1]); returns the
+    bundle text. Defaults are the reference's TrainOptions."""
+    lib = _lib()
+    c = np.ascontiguousarray(corpus, dtype=np.float64)
+    if c.ndim != 3:
+        raise UsageError("corpus must be float64 [N, H, W]")
+    n, h, w = c.shape
+    ln = ctypes.c_size_t()
+    cap = (1 << 20) + 2048 * max(1, gmm_components)  # ~1.4 KB of text per component, plus the rest
+    buf = ctypes.create_string_buffer(cap)
+    rc = lib.cdvz_gpu_train_model(device, c.ctypes.data, n, w, h, w, seed, gmm_components, em_iterations, select_n,
+                                  max_side, relevance_bins, buf, cap, ctypes.byref(ln))
+    if rc:
+        _raise(rc, lib.cdvz_gpu_last_error(None).decode())
+    return buf.raw[:ln.value].decode()
 
 
 class PendingBatch:

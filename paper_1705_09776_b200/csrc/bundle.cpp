@@ -446,4 +446,8 @@ Budget budget_for(const Mode& m, int nc) {
   return b;
 }
 
+// Public forms of two helpers the trainer shares (train_host.cpp, context.cu).
+std::vector<double> gaussian_kernel_taps(double sigma) { return gaussian_taps(sigma); }
+double eigen_packet_sum(const double* v, std::size_t n) { return packet_sum(v, n); }
+
 }  // namespace cdvz_gpu

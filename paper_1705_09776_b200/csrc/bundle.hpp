@@ -47,6 +47,11 @@ struct Bundle {
 Bundle parse_bundle(const std::string& text);       // model_io.cpp:141-273 + validate
 std::string serialize_bundle(const Bundle& b);      // model_io.cpp:86-139 (canonical text)
 
+// gaussian_kernel (image.cpp:163-175) and Eigen's SSE2 packet-order sum of a
+// contiguous vector.
+std::vector<double> gaussian_kernel_taps(double sigma);
+double eigen_packet_sum(const double* v, std::size_t n);
+
 struct Mode { int id; const char* name; std::size_t budget; int elements; double fraction; bool variance; };
 const Mode& mode_by_id(int id);                     // transform_coding.cpp:21-37
 

@@ -29,6 +29,7 @@
 #include "../../include/cdvz_gpu.h"
 #include "bundle.hpp"
 #include "common.cuh"
+#include "train_host.hpp"
 
 namespace cdvz_gpu {
 cudaError_t launch_octave(const Batch& bt, const DetConst& dc, int o, int src, cudaStream_t st);
@@ -1760,3 +1761,351 @@ int cdvz_gpu_copy(cdvz_gpu_ctx* ctx, void* dst, const void* src, size_t bytes, i
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------- training
+// train_model (proj/src/pipeline.cpp:99-166) with the heavy work on the GPU:
+// pass 1 (detection, selection, description of every corpus image) is the
+// extractor's own pipeline; the partner images (apply_transform) are built
+// and detected on the device; the PCA covariance and projection, the EM
+// iterations and the descriptor transform run as the kernels of train.cu;
+// the ordered, tiny steps (relevance histograms, k-means++, the 128 x 128
+// eigensolver, quantiles) run on the host (train_host.cpp).
+namespace cdvz_gpu {
+cudaError_t launch_rotate90(const double* in, int w, int h, int k, double* out, cudaStream_t st);
+cudaError_t launch_blur_clamp(const double* in, int w, int h, const double* d_taps, int r, double* tmp, double* out,
+                              cudaStream_t st);
+cudaError_t launch_covariance(const double* centred, long long n, double* cov, cudaStream_t st);
+cudaError_t launch_pca_rows(const double* raw, long long n, const double* mean, const double* basis, double* x,
+                            cudaStream_t st);
+cudaError_t launch_em_step(const double* x, long long n, int nc, const double* means, const double* stds,
+                           const double* log_w, const double* log_norm, double* gamma, double* nk, double* mu,
+                           double* ex2, cudaStream_t st);
+cudaError_t launch_transform_rows(const double* raw, long long n, const double* ta, const double* tb, double scale,
+                                  double* out, cudaStream_t st);
+}  // namespace cdvz_gpu
+
+namespace {
+
+// Defaults of a fresh bundle (ScaleSpaceConfig::defaults, scale_space.cpp:85-91;
+// RelevanceModel::uniform, relevance.cpp:45-52; TransformPair::defaults,
+// transform_coding.cpp:59-79) with neutral quantizer / PCA / GMM sections.
+Bundle default_training_bundle(int select_n) {
+  Bundle b;
+  b.num_octaves = 4;
+  b.sigmas.resize(4);
+  for (int k = 0; k < 4; ++k) b.sigmas[std::size_t(k)] = 1.4 * std::pow(2.0, k / 4.0);
+  b.response_threshold = 0.02;
+  b.edge_r = 10.0;
+  b.select_n = select_n;
+  for (auto& t : b.relevance) {
+    t.edges = {0.0, 1.0};
+    t.values = {1.0};
+  }
+  double h[8][8] = {};
+  h[0][0] = 1.0;
+  for (int n = 1; n < 8; n *= 2)
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j < n; ++j) {
+        const double v = h[i][j];
+        h[i][j + n] = v;
+        h[i + n][j] = v;
+        h[i + n][j + n] = -v;
+      }
+  for (int i = 0; i < 8; ++i)
+    for (int j = 0; j < 8; ++j) {
+      b.tr_a[i][j] = h[i][j];
+      b.tr_b[i][j] = h[(i + 1) % 8][j];
+    }
+  b.tr_scale = 1.0 / 8.0;
+  for (int e = 0; e < 128; ++e) {
+    b.t0[e] = -1.0;
+    b.t1[e] = 1.0;
+    b.priority[e] = e;
+    b.degenerate[e] = 0;
+    b.pca_mean[e] = 0.0;
+  }
+  b.pca_basis.assign(32 * 128, 0.0);
+  for (int r = 0; r < 32; ++r) b.pca_basis[std::size_t(r) * 128 + r] = 1.0;
+  b.nc = 1;
+  b.weights = {1.0};
+  b.means.assign(32, 0.0);
+  b.stds.assign(32, 1.0);
+  return b;
+}
+
+struct OwnedBuffer : DeviceBuffer {
+  OwnedBuffer() = default;
+  OwnedBuffer(const OwnedBuffer&) = delete;
+  OwnedBuffer& operator=(const OwnedBuffer&) = delete;
+  ~OwnedBuffer() { release(); }
+};
+
+struct FrameLists {
+  std::vector<TrainPoint> selected, keypoints;
+  std::vector<double> desc;  // oriented descriptors, 128 each
+  int status = 0;
+};
+
+// One pipeline run over `count` device f64 frames (one call's worth) and the
+// per-frame lists of its single chunk, read back from the lane.
+std::vector<FrameLists> run_lists(cdvz_gpu_ctx* ctx, const double* d_frames, int w, int h, int count, int max_side,
+                                  OwnedBuffer& out, OwnedBuffer& len, bool want_desc) {
+  if (count > ctx->max_batch) throw UsageError("training run larger than the context's batch");
+  const size_t slot = mode_by_id(3).budget + 28;
+  out.ensure(slot * count);
+  len.ensure(sizeof(uint32_t) * count);
+  ctx->run(reinterpret_cast<const uint8_t*>(d_frames), w, h, (long long)w * 8, count, 3, max_side, out.as<uint8_t>(),
+           len.as<uint32_t>(), nullptr, 0, nullptr, nullptr, 8);
+  CDVZ_CUDA_CHECK(cudaStreamSynchronize(ctx->st));
+  ctx->collect_all();
+  const Lane& L = ctx->lanes[ctx->last_lane];
+  const Batch& b = L.bt;
+  auto get_i = [&](const int* p, long long n) {
+    std::vector<int> v(std::size_t(std::max(0LL, n)));
+    if (n > 0) CDVZ_CUDA_CHECK(cudaMemcpy(v.data(), p, sizeof(int) * n, cudaMemcpyDeviceToHost));
+    return v;
+  };
+  auto to_points = [&](const KP* p, int n) {
+    std::vector<KP> k(std::size_t(std::max(0, n)));
+    if (n > 0) CDVZ_CUDA_CHECK(cudaMemcpy(k.data(), p, sizeof(KP) * n, cudaMemcpyDeviceToHost));
+    std::vector<TrainPoint> out_;
+    out_.reserve(k.size());
+    for (const KP& q : k) out_.push_back({q.x, q.y, q.sigma, q.p, q.d, q.rho, q.pss});
+    return out_;
+  };
+  const auto status = get_i(b.status, count);
+  const auto sel_count = get_i(b.sel_count, count);
+  const auto or_count = get_i(b.or_count, count);
+  const int last = (b.n_oct - 1) & 1;
+  const auto acc_count = get_i(b.acc_count, 2LL * count);
+  std::vector<FrameLists> res(static_cast<size_t>(count));
+  for (int f = 0; f < count; ++f) {
+    FrameLists& r = res[size_t(f)];
+    r.status = status[size_t(f)];
+    r.selected = to_points(b.sel + (long long)f * b.select_n, sel_count[size_t(f)]);
+    r.keypoints = b.n_oct > 0 ? to_points(b.acc[last] + (long long)f * b.cap_acc, acc_count[size_t(f) * 2 + last])
+                              : std::vector<TrainPoint>{};
+    if (want_desc && or_count[size_t(f)] > 0) {
+      r.desc.resize(size_t(or_count[size_t(f)]) * 128);
+      CDVZ_CUDA_CHECK(cudaMemcpy(r.desc.data(), b.desc + (long long)f * b.cap_or * 128,
+                                 sizeof(double) * r.desc.size(), cudaMemcpyDeviceToHost));
+    }
+  }
+  return res;
+}
+
+}  // namespace
+
+extern "C" int cdvz_gpu_train_model(int device, const double* corpus, int count, int width, int height, size_t stride,
+                                    uint64_t seed, int gmm_components, int em_iterations, int select_n, int max_side,
+                                    int relevance_bins, char* out, size_t out_cap, size_t* out_len) {
+  NvtxRange nv("cdvz_gpu_train_model");
+  return guarded(nullptr, [&] {
+    if (!corpus || !out_len) throw UsageError("null argument");
+    if (count < 20) throw DataError("training corpus needs at least 20 images");  // pipeline.cpp:101
+    if (width < 8 || height < 8) throw DataError("image smaller than 8 px per side");
+    if (stride < size_t(width)) throw UsageError("row stride shorter than a row");
+    // Pass-1 context: defaults, the uniform selector, neutral coding sections.
+    const std::string text0 = serialize_bundle(default_training_bundle(select_n));
+    cdvz_gpu_ctx* raw_ctx = nullptr;
+    if (cdvz_gpu_create(text0.data(), text0.size(), device, std::max(count, 1), &raw_ctx) != CDVZ_GPU_OK)
+      throw std::runtime_error(cdvz_gpu_last_error(nullptr));
+    std::unique_ptr<cdvz_gpu_ctx> ctx(raw_ctx);
+    cudaStream_t st = ctx->st;
+    OwnedBuffer d_corpus, d_prep, d_out, d_len, d_a, d_b, d_c, d_taps;
+    d_corpus.ensure(sizeof(double) * size_t(count) * width * height);
+    CDVZ_CUDA_CHECK(cudaMemcpy2D(d_corpus.p, sizeof(double) * width, corpus, sizeof(double) * stride,
+                                 sizeof(double) * width, size_t(height) * count, cudaMemcpyHostToDevice));
+    int W = width, H = height;
+    prepared_dims(width, height, max_side, W, H);
+    // Pass 1 (pipeline.cpp:115-121): every corpus image's selected points and
+    // oriented descriptors; the prepared (resized) rasters are kept for the
+    // partner images.
+    auto lists = run_lists(ctx.get(), d_corpus.as<double>(), width, height, count, max_side, d_out, d_len, true);
+    d_prep.ensure(sizeof(double) * size_t(count) * W * H);
+    {
+      const Lane& L = ctx->lanes[ctx->last_lane];
+      const double* src = (W != width || H != height) ? L.bt.pixf : d_corpus.as<double>();
+      CDVZ_CUDA_CHECK(cudaMemcpy(d_prep.p, src, sizeof(double) * size_t(count) * W * H, cudaMemcpyDeviceToDevice));
+    }
+    std::vector<double> raw;
+    std::vector<std::pair<TrainPoint, bool>> labeled;
+    for (int i = 0; i < count; ++i) {
+      const FrameLists& fl = lists[size_t(i)];
+      if (fl.status != 0) throw std::runtime_error("training frame " + std::to_string(i) + " failed on the device");
+      raw.insert(raw.end(), fl.desc.begin(), fl.desc.end());
+      // Partner (pipeline.cpp:124-140): apply_transform, detect_keypoints, map_point, labels.
+      const SynthTransform t = partner_transform(size_t(i));
+      const int k = ((t.quarter_turns % 4) + 4) % 4;
+      const int rw = (k % 2) ? H : W, rh = (k % 2) ? W : H;
+      int pw = 0, ph = 0;
+      transform_size(t, W, H, pw, ph);
+      const size_t big = size_t(std::max(rw * rh, pw * ph));
+      d_a.ensure(sizeof(double) * big);
+      d_b.ensure(sizeof(double) * big);
+      d_c.ensure(sizeof(double) * big);
+      CDVZ_CUDA_CHECK(launch_rotate90(d_prep.as<double>() + size_t(i) * W * H, W, H, k, d_a.as<double>(), st));
+      const double* cur = d_a.as<double>();
+      if (t.scale != 1.0) {
+        CDVZ_CUDA_CHECK(launch_resize_f64(cur, rw, rh, d_b.as<double>(), pw, ph, 1, st));
+        cur = d_b.as<double>();
+      }
+      double* partner = (cur == d_a.as<double>()) ? d_b.as<double>() : d_a.as<double>();
+      if (t.blur_sigma > 0.0) {
+        const std::vector<double> taps = gaussian_kernel_taps(t.blur_sigma);
+        d_taps.ensure(sizeof(double) * taps.size());
+        CDVZ_CUDA_CHECK(cudaMemcpyAsync(d_taps.p, taps.data(), sizeof(double) * taps.size(), cudaMemcpyHostToDevice, st));
+        CDVZ_CUDA_CHECK(launch_blur_clamp(cur, pw, ph, d_taps.as<double>(), int(taps.size() / 2), d_c.as<double>(),
+                                          partner, st));
+      } else {
+        partner = const_cast<double*>(cur);
+      }
+      CDVZ_CUDA_CHECK(cudaStreamSynchronize(st));
+      // detect_keypoints on the partner as it is (no resize_max_side).
+      const auto pl = run_lists(ctx.get(), partner, pw, ph, 1, std::max(pw, ph), d_out, d_len, false);
+      std::vector<std::array<double, 3>> mapped(fl.selected.size());
+      for (size_t s = 0; s < fl.selected.size(); ++s) {
+        double mx = fl.selected[s].x, my = fl.selected[s].y, ms = fl.selected[s].sigma;
+        map_point(t, W, H, mx, my, ms);
+        mapped[s] = {mx, my, ms};
+      }
+      label_matches(fl.selected, pl[0].keypoints, mapped, 2.0, 1.3, labeled);
+    }
+    Bundle b = default_training_bundle(select_n);
+    b.relevance = train_relevance(labeled, relevance_bins, 10);  // pipeline.cpp:151
+    const long long n = (long long)(raw.size() / 128);
+    // train_pca (scfv.cpp:328-352).
+    if (n < 10 * 128) throw DataError("PCA training needs at least 1280 samples");
+    for (double v : raw)
+      if (!std::isfinite(v)) throw DataError("PCA training data contains non-finite values");
+    {
+      std::vector<double> col(static_cast<size_t>(n));
+      for (int j = 0; j < 128; ++j) {
+        for (long long t = 0; t < n; ++t) col[size_t(t)] = raw[size_t(t) * 128 + j];
+        b.pca_mean[j] = eigen_packet_sum(col.data(), col.size()) / static_cast<double>(n);
+      }
+      std::vector<double> centred(raw.size());
+      for (long long t = 0; t < n; ++t)
+        for (int j = 0; j < 128; ++j) centred[size_t(t) * 128 + j] = raw[size_t(t) * 128 + j] - b.pca_mean[j];
+      d_a.ensure(sizeof(double) * centred.size());
+      d_b.ensure(sizeof(double) * 128 * 128);
+      CDVZ_CUDA_CHECK(cudaMemcpy(d_a.p, centred.data(), sizeof(double) * centred.size(), cudaMemcpyHostToDevice));
+      CDVZ_CUDA_CHECK(launch_covariance(d_a.as<double>(), n, d_b.as<double>(), st));
+      std::vector<double> cov(128 * 128), vals, vecs;
+      CDVZ_CUDA_CHECK(cudaMemcpyAsync(cov.data(), d_b.p, sizeof(double) * cov.size(), cudaMemcpyDeviceToHost, st));
+      CDVZ_CUDA_CHECK(cudaStreamSynchronize(st));
+      sym_eigen128(cov, vals, vecs);
+      for (int r = 0; r < 32; ++r) {  // strongest 32, sign: largest-magnitude coefficient positive
+        double v[128];
+        for (int j = 0; j < 128; ++j) v[j] = vecs[size_t(j) * 128 + (127 - r)];
+        int arg = 0;
+        for (int j = 1; j < 128; ++j)
+          if (std::abs(v[j]) > std::abs(v[arg])) arg = j;
+        const double sgn = v[arg] < 0.0 ? -1.0 : 1.0;
+        for (int j = 0; j < 128; ++j) b.pca_basis[size_t(r) * 128 + j] = sgn < 0.0 ? -v[j] : v[j];
+      }
+    }
+    // pca_reduce of the corpus, then train_gmm (scfv.cpp:354-430).
+    OwnedBuffer d_raw, d_x, d_mean, d_basis;
+    d_raw.ensure(sizeof(double) * raw.size());
+    d_x.ensure(sizeof(double) * size_t(n) * 32);
+    d_mean.ensure(sizeof(double) * 128);
+    d_basis.ensure(sizeof(double) * 32 * 128);
+    CDVZ_CUDA_CHECK(cudaMemcpy(d_raw.p, raw.data(), sizeof(double) * raw.size(), cudaMemcpyHostToDevice));
+    CDVZ_CUDA_CHECK(cudaMemcpy(d_mean.p, b.pca_mean, sizeof(double) * 128, cudaMemcpyHostToDevice));
+    CDVZ_CUDA_CHECK(cudaMemcpy(d_basis.p, b.pca_basis.data(), sizeof(double) * 32 * 128, cudaMemcpyHostToDevice));
+    CDVZ_CUDA_CHECK(launch_pca_rows(d_raw.as<double>(), n, d_mean.as<double>(), d_basis.as<double>(), d_x.as<double>(), st));
+    std::vector<double> x(size_t(n) * 32);
+    CDVZ_CUDA_CHECK(cudaMemcpyAsync(x.data(), d_x.p, sizeof(double) * x.size(), cudaMemcpyDeviceToHost, st));
+    CDVZ_CUDA_CHECK(cudaStreamSynchronize(st));
+    const int nc = gmm_components;
+    if (nc < 1) throw DataError("GMM needs at least one component");
+    if (n < std::max<long long>(10 * 32, 2LL * nc)) throw DataError("GMM training corpus is too small");
+    {
+      constexpr double kFloor = 1e-3;  // kGmmSigmaFloor (scfv.hpp:26)
+      std::mt19937_64 rng(seed);
+      const auto centers = kmeanspp(x, n, nc, rng);
+      b.nc = nc;
+      b.weights.assign(size_t(nc), 1.0 / nc);
+      b.means.assign(size_t(nc) * 32, 0.0);
+      b.stds.assign(size_t(nc) * 32, 0.0);
+      for (int i = 0; i < nc; ++i)
+        for (int j = 0; j < 32; ++j) b.means[size_t(i) * 32 + j] = x[size_t(centers[size_t(i)]) * 32 + j];
+      std::vector<double> col(static_cast<size_t>(n));
+      double gstd[32];
+      for (int j = 0; j < 32; ++j) {
+        for (long long t = 0; t < n; ++t) col[size_t(t)] = x[size_t(t) * 32 + j];
+        const double gm = eigen_packet_sum(col.data(), col.size()) / static_cast<double>(n);
+        for (long long t = 0; t < n; ++t) {
+          const double d = col[size_t(t)] - gm;
+          col[size_t(t)] = d * d;
+        }
+        gstd[j] = std::max(std::sqrt(eigen_packet_sum(col.data(), col.size()) / static_cast<double>(n)), kFloor);
+      }
+      for (int i = 0; i < nc; ++i)
+        for (int j = 0; j < 32; ++j) b.stds[size_t(i) * 32 + j] = gstd[j];
+      OwnedBuffer d_means, d_stds, d_logw, d_lnorm, d_gamma, d_nk, d_mu, d_ex2;
+      d_means.ensure(sizeof(double) * nc * 32);
+      d_stds.ensure(sizeof(double) * nc * 32);
+      d_logw.ensure(sizeof(double) * nc);
+      d_lnorm.ensure(sizeof(double) * nc);
+      d_gamma.ensure(sizeof(double) * size_t(n) * nc);
+      d_nk.ensure(sizeof(double) * nc);
+      d_mu.ensure(sizeof(double) * nc * 32);
+      d_ex2.ensure(sizeof(double) * nc * 32);
+      const size_t unc = static_cast<size_t>(nc);
+      std::vector<double> logw(unc), lnorm(unc), nk(unc), mu(unc * 32), ex2(unc * 32);
+      for (int iter = 0; iter < em_iterations; ++iter) {
+        for (int i = 0; i < nc; ++i) {  // log_weighted_densities' per-component constants (scfv.cpp:25-27)
+          double s = 0.0;
+          for (int j = 0; j < 32; ++j) s += std::log(b.stds[size_t(i) * 32 + j]);
+          lnorm[size_t(i)] = s;
+          logw[size_t(i)] = std::log(b.weights[size_t(i)]);
+        }
+        CDVZ_CUDA_CHECK(cudaMemcpyAsync(d_means.p, b.means.data(), sizeof(double) * nc * 32, cudaMemcpyHostToDevice, st));
+        CDVZ_CUDA_CHECK(cudaMemcpyAsync(d_stds.p, b.stds.data(), sizeof(double) * nc * 32, cudaMemcpyHostToDevice, st));
+        CDVZ_CUDA_CHECK(cudaMemcpyAsync(d_logw.p, logw.data(), sizeof(double) * nc, cudaMemcpyHostToDevice, st));
+        CDVZ_CUDA_CHECK(cudaMemcpyAsync(d_lnorm.p, lnorm.data(), sizeof(double) * nc, cudaMemcpyHostToDevice, st));
+        CDVZ_CUDA_CHECK(launch_em_step(d_x.as<double>(), n, nc, d_means.as<double>(), d_stds.as<double>(),
+                                       d_logw.as<double>(), d_lnorm.as<double>(), d_gamma.as<double>(),
+                                       d_nk.as<double>(), d_mu.as<double>(), d_ex2.as<double>(), st));
+        CDVZ_CUDA_CHECK(cudaMemcpyAsync(nk.data(), d_nk.p, sizeof(double) * nc, cudaMemcpyDeviceToHost, st));
+        CDVZ_CUDA_CHECK(cudaMemcpyAsync(mu.data(), d_mu.p, sizeof(double) * nc * 32, cudaMemcpyDeviceToHost, st));
+        CDVZ_CUDA_CHECK(cudaMemcpyAsync(ex2.data(), d_ex2.p, sizeof(double) * nc * 32, cudaMemcpyDeviceToHost, st));
+        CDVZ_CUDA_CHECK(cudaStreamSynchronize(st));
+        for (int i = 0; i < nc; ++i) {  // M step (scfv.cpp:412-423)
+          if (nk[size_t(i)] < 1e-10) continue;  // starved component keeps its parameters
+          for (int j = 0; j < 32; ++j) {
+            const double m = mu[size_t(i) * 32 + j];
+            b.means[size_t(i) * 32 + j] = m;
+            b.stds[size_t(i) * 32 + j] = std::sqrt(std::max(ex2[size_t(i) * 32 + j] - m * m, kFloor * kFloor));
+          }
+        }
+        std::vector<double> w(unc);
+        for (int i = 0; i < nc; ++i) w[size_t(i)] = std::max(nk[size_t(i)] / static_cast<double>(n), 1e-12);
+        const double ws = eigen_packet_sum(w.data(), w.size());
+        for (int i = 0; i < nc; ++i) b.weights[size_t(i)] = w[size_t(i)] / ws;
+      }
+    }
+    // train_thresholds on the transformed corpus (pipeline.cpp:158-162).
+    {
+      OwnedBuffer d_ta, d_tb, d_tr;
+      d_ta.ensure(sizeof(double) * 64);
+      d_tb.ensure(sizeof(double) * 64);
+      d_tr.ensure(sizeof(double) * raw.size());
+      CDVZ_CUDA_CHECK(cudaMemcpy(d_ta.p, &b.tr_a[0][0], sizeof(double) * 64, cudaMemcpyHostToDevice));
+      CDVZ_CUDA_CHECK(cudaMemcpy(d_tb.p, &b.tr_b[0][0], sizeof(double) * 64, cudaMemcpyHostToDevice));
+      CDVZ_CUDA_CHECK(launch_transform_rows(d_raw.as<double>(), n, d_ta.as<double>(), d_tb.as<double>(), b.tr_scale,
+                                            d_tr.as<double>(), st));
+      std::vector<double> tr(raw.size());
+      CDVZ_CUDA_CHECK(cudaMemcpyAsync(tr.data(), d_tr.p, sizeof(double) * tr.size(), cudaMemcpyDeviceToHost, st));
+      CDVZ_CUDA_CHECK(cudaStreamSynchronize(st));
+      train_thresholds(tr, n, 1.0 / 3.0, b);
+    }
+    const std::string text = serialize_bundle(b);
+    parse_bundle(text);  // bundle.validate() (pipeline.cpp:164)
+    *out_len = text.size();
+    if (out && out_cap >= text.size()) std::memcpy(out, text.data(), text.size());
+    else if (out) throw UsageError("output buffer too small for the bundle text");
+  });
+}
