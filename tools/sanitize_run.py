@@ -11,7 +11,8 @@ kernel of the product path on a handful of frames, no torch.
   on-device synthesis, streamed submit / wait batches, the register-bin
   describe variant, and the debug paths (exact-only extrema, the TMA tile kernel and its plain-load
   variant, tiny capacities -> the capacity retry);
-* match: an 8-container index, retrieve + match_pairs (k_match.cu).
+* match: an 8-container index, retrieve + match_pairs (k_match.cu);
+* train: cdvz_gpu_train_model on a 20-image corpus (train.cu).
 Exit 0 when every container equals the oracle's (sanity: the sanitizer run
 must not change results).
 """
@@ -84,10 +85,20 @@ def match_part():
     idx.close()
 
 
+def train_part():
+    """cdvz_gpu_train_model on a 20-image corpus (the training kernels)."""
+    golden = 0x9E3779B97F4A7C15
+    corpus = np.stack([oracle_lib.synth_f64((401 + i * golden) % (1 << 64), 256, 256) for i in range(20)])
+    text = cg.train_model(corpus, seed=11, gmm_components=8, em_iterations=3)
+    cg.bundle_check(text)
+
+
 if __name__ == "__main__":
     what = sys.argv[1] if len(sys.argv) > 1 else "all"
     if what in ("all", "encode"):
         encode_part()
     if what in ("all", "match"):
         match_part()
+    if what in ("all", "train"):
+        train_part()
     print("sanitize_run ok")
