@@ -48,6 +48,14 @@ inline void raise_for(int code, const char* msg) {
   if (code == CDVZ_GPU_DATA) throw DataError(msg);
   throw std::runtime_error(msg);
 }
+// raise_for with the context's last error, read after `code` is computed (the
+// message must not be an argument evaluated alongside the call).
+inline void check(int code, const cdvz_gpu_ctx* ctx = nullptr) {
+  if (code != CDVZ_GPU_OK) raise_for(code, cdvz_gpu_last_error(ctx));
+}
+inline void check_index(int code, const cdvz_gpu_index* idx) {
+  if (code != CDVZ_GPU_OK) raise_for(code, cdvz_gpu_index_last_error(idx));
+}
 
 struct ModeSpec {  // transform_coding.hpp:13-20
   int id;
@@ -305,7 +313,7 @@ class ModelBundle {
  public:
   explicit ModelBundle(std::string text) : text_(std::move(text)) {
     int code = cdvz_gpu_bundle_check(text_.data(), text_.size(), &crc_, &components_);
-    raise_for(code, cdvz_gpu_last_error(nullptr));
+    check(code);
   }
   static ModelBundle load(const std::string& path) {  // load_model (model_io.cpp:282-288)
     std::ifstream in(path, std::ios::binary);
@@ -314,6 +322,11 @@ class ModelBundle {
     buf << in.rdbuf();
     return ModelBundle(buf.str());
   }
+  void save(const std::string& path) const {  // save_model (model_io.cpp:274-280)
+    std::ofstream out(path, std::ios::binary);
+    if (!out) throw DataError("cannot write model bundle: " + path);
+    out.write(text_.data(), std::streamsize(text_.size()));
+  }
   uint32_t crc() const { return crc_; }
   int components() const { return components_; }
   const std::string& text() const { return text_; }
@@ -321,7 +334,7 @@ class ModelBundle {
     auto it = ctx_.find(device);
     if (it != ctx_.end()) return it->second.get();
     cdvz_gpu_ctx* c = nullptr;
-    raise_for(cdvz_gpu_create(text_.data(), text_.size(), device, max_batch, &c), cdvz_gpu_last_error(nullptr));
+    check(cdvz_gpu_create(text_.data(), text_.size(), device, max_batch, &c));
     ctx_[device] = std::shared_ptr<cdvz_gpu_ctx>(c, cdvz_gpu_destroy);
     return c;
   }
@@ -331,8 +344,7 @@ class ModelBundle {
     auto it = multi_.find(devices);
     if (it != multi_.end()) return it->second.get();
     cdvz_gpu_ctx* c = nullptr;
-    raise_for(cdvz_gpu_create_multi(text_.data(), text_.size(), devices.data(), int(devices.size()), max_batch, &c),
-              cdvz_gpu_last_error(nullptr));
+    check(cdvz_gpu_create_multi(text_.data(), text_.size(), devices.data(), int(devices.size()), max_batch, &c));
     multi_[devices] = std::shared_ptr<cdvz_gpu_ctx>(c, cdvz_gpu_destroy);
     return c;
   }
@@ -344,10 +356,42 @@ class ModelBundle {
   mutable std::map<std::vector<int>, std::shared_ptr<cdvz_gpu_ctx>> multi_;
 };
 
+struct TrainOptions {  // pipeline.hpp:22-28
+  std::uint64_t seed = 7;
+  int gmm_components = 8;
+  int em_iterations = 25;
+  int select_n = 300;
+  int max_side = 640;
+  int relevance_bins = 16;
+};
+
+// train_model (pipeline.hpp:34-35, pipeline.cpp:99-166) on the GPU
+// (cdvz_gpu_train_model). The corpus images must share one
+// size (synth_corpus's do). `eng` is accepted for signature parity.
+inline ModelBundle train_model(const std::vector<GrayImage>& corpus, const TrainOptions& opts = {},
+                               const Engine& eng = {}, int device = 0) {
+  (void)eng;
+  if (corpus.size() < 20) throw DataError("training corpus needs at least 20 images");
+  const int w = corpus[0].w, h = corpus[0].h;
+  std::vector<double> pix;
+  pix.reserve(corpus.size() * std::size_t(w) * h);
+  for (const auto& g : corpus) {
+    if (g.w != w || g.h != h) throw UsageError("the GPU trainer takes a corpus of one image size");
+    pix.insert(pix.end(), g.pix.begin(), g.pix.end());
+  }
+  std::size_t len = 0;
+  std::string text(std::size_t(1 << 20) + 2048 * std::size_t(std::max(1, opts.gmm_components)), '\0');
+  check(cdvz_gpu_train_model(device, pix.data(), int(corpus.size()), w, h, std::size_t(w), opts.seed,
+                                 opts.gmm_components, opts.em_iterations, opts.select_n, opts.max_side,
+                                 opts.relevance_bins, text.data(), text.size(), &len));
+  text.resize(len);
+  return ModelBundle(std::move(text));
+}
+
 inline void add_timings(cdvz_gpu_ctx* ctx, StageTimings* timings) {
   if (!timings) return;
   double ms[5];
-  raise_for(cdvz_gpu_stage_times(ctx, ms), cdvz_gpu_last_error(ctx));
+  check(cdvz_gpu_stage_times(ctx, ms), ctx);
   const char* labels[5] = {"detection", "selection", "description", "compression", "aggregation"};
   for (int i = 0; i < 5; ++i) timings->add(labels[i], ms[i]);
 }
@@ -365,17 +409,16 @@ inline EncodedImage encode_image(const GrayImage& img, const ModelBundle& bundle
   std::vector<uint8_t> buf(cdvz_gpu_container_slot(mode.id));
   std::size_t offsets[2] = {0, 0};
   int status = 0;
-  raise_for(cdvz_gpu_encode_batch_f64(ctx, img.pix.data(), img.w, img.h, std::size_t(img.w), 1, mode.id, opts.max_side,
-                                      buf.data(), buf.size(), offsets, &status),
-            cdvz_gpu_last_error(ctx));
+  check(cdvz_gpu_encode_batch_f64(ctx, img.pix.data(), img.w, img.h, std::size_t(img.w), 1, mode.id, opts.max_side,
+                                      buf.data(), buf.size(), offsets, &status), ctx);
   if (status == CDVZ_GPU_DATA) throw DataError("image values must be finite and in [0, 1]");
   raise_for(status, "frame failed on the device");
   buf.resize(offsets[1]);
   EncodedImage enc = parse_container(buf);
   std::size_t n = 0;
-  raise_for(cdvz_gpu_debug_get(ctx, "norms", 0, nullptr, 0, &n), cdvz_gpu_last_error(ctx));
+  check(cdvz_gpu_debug_get(ctx, "norms", 0, nullptr, 0, &n), ctx);
   enc.global_desc.norms.resize(n);
-  raise_for(cdvz_gpu_debug_get(ctx, "norms", 0, enc.global_desc.norms.data(), n, &n), cdvz_gpu_last_error(ctx));
+  check(cdvz_gpu_debug_get(ctx, "norms", 0, enc.global_desc.norms.data(), n, &n), ctx);
   add_timings(ctx, timings);
   return enc;
 }
@@ -399,9 +442,8 @@ inline std::vector<std::vector<uint8_t>> encode_batch(const std::vector<const Gr
   std::vector<uint8_t> buf(slot * frames.size());
   std::vector<std::size_t> offsets(frames.size() + 1);
   std::vector<int> status(frames.size());
-  raise_for(cdvz_gpu_encode_batch(ctx, pix.data(), w, h, std::size_t(w), int(frames.size()), mode.id, opts.max_side,
-                                  buf.data(), buf.size(), offsets.data(), status.data()),
-            cdvz_gpu_last_error(ctx));
+  check(cdvz_gpu_encode_batch(ctx, pix.data(), w, h, std::size_t(w), int(frames.size()), mode.id, opts.max_side,
+                                  buf.data(), buf.size(), offsets.data(), status.data()), ctx);
   for (std::size_t i = 0; i < frames.size(); ++i) {
     raise_for(status[i], "frame failed on the device");
     out[i].assign(buf.begin() + long(offsets[i]), buf.begin() + long(offsets[i + 1]));
@@ -437,11 +479,22 @@ inline PnmImage load_pnm(const std::string& path) {  // load_image's file handli
   const std::string bytes((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
   PnmImage img;
   std::size_t off = 0;
-  raise_for(cdvz_gpu_pnm_parse(reinterpret_cast<const uint8_t*>(bytes.data()), bytes.size(), &img.width, &img.height,
-                               &img.channels, &off),
-            cdvz_gpu_last_error(nullptr));
+  check(cdvz_gpu_pnm_parse(reinterpret_cast<const uint8_t*>(bytes.data()), bytes.size(), &img.width, &img.height,
+                               &img.channels, &off));
   img.raster.assign(bytes.begin() + long(off), bytes.begin() + long(off) + long(img.width) * img.height * img.channels);
   return img;
+}
+
+// load_image's raster conversion (image.cpp:78-90): grey = v / 255, colour =
+// (0.299 r + 0.587 g + 0.114 b) / 255, in the reference's operation order.
+inline GrayImage to_gray(const PnmImage& img) {
+  GrayImage g = make_image(img.width, img.height);
+  const double inv = 1.0 / 255.0;
+  for (std::size_t i = 0; i < g.pix.size(); ++i) {
+    const uint8_t* px = img.raster.data() + i * std::size_t(img.channels);
+    g.pix[i] = img.channels == 3 ? (0.299 * px[0] + 0.587 * px[1] + 0.114 * px[2]) * inv : px[0] * inv;
+  }
+  return g;
 }
 
 // encode_image(load_image(path), ...) for an in-memory PGM/PPM raster.
@@ -453,9 +506,8 @@ inline std::vector<uint8_t> encode_image(const PnmImage& img, const ModelBundle&
   int status = 0;
   const std::size_t stride = std::size_t(img.width) * img.channels;
   auto fn = img.channels == 3 ? cdvz_gpu_encode_batch_rgb : cdvz_gpu_encode_batch;
-  raise_for(fn(ctx, img.raster.data(), img.width, img.height, stride, 1, mode.id, opts.max_side, buf.data(), buf.size(),
-               offsets, &status),
-            cdvz_gpu_last_error(ctx));
+  check(fn(ctx, img.raster.data(), img.width, img.height, stride, 1, mode.id, opts.max_side, buf.data(), buf.size(),
+               offsets, &status), ctx);
   raise_for(status, "frame failed on the device");
   buf.resize(offsets[1]);
   return buf;
@@ -496,9 +548,8 @@ class Index {
     std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return ids_[a] < ids_[b]; });
     for (std::size_t r = 0; r < order.size(); ++r) rank[std::size_t(order[r])] = int32_t(r);
     cdvz_gpu_index* idx = nullptr;
-    raise_for(cdvz_gpu_index_create(device, blob.empty() ? nullptr : blob.data(), off.data(), int(items.size()),
-                                    rank.data(), &idx),
-              cdvz_gpu_index_last_error(nullptr));
+    check_index(cdvz_gpu_index_create(device, blob.empty() ? nullptr : blob.data(), off.data(), int(items.size()),
+                                    rank.data(), &idx), nullptr);
     idx_.reset(idx, cdvz_gpu_index_destroy);
   }
   cdvz_gpu_index* handle() const { return idx_.get(); }
@@ -523,9 +574,8 @@ inline std::vector<RankedList> retrieve(const std::vector<std::pair<std::string,
   std::vector<double> scores(queries.size() * n);
   std::vector<RankedList> out(queries.size());
   if (queries.empty()) return out;
-  raise_for(cdvz_gpu_retrieve(index.handle(), blob.data(), off.data(), int(queries.size()), opts.ratio_test,
-                              opts.rerank_depth, 0, items.data(), scores.data()),
-            cdvz_gpu_index_last_error(index.handle()));
+  check_index(cdvz_gpu_retrieve(index.handle(), blob.data(), off.data(), int(queries.size()), opts.ratio_test,
+                              opts.rerank_depth, 0, items.data(), scores.data()), index.handle());
   for (std::size_t q = 0; q < queries.size(); ++q) {
     out[q].query = queries[q].first;
     for (std::size_t r = 0; r < n; ++r)
@@ -541,9 +591,8 @@ inline MatchResult match_pair(const std::vector<uint8_t>& a, const Index& index,
   const int32_t pair[2] = {0, item};
   MatchResult r;
   int32_t local = 0;
-  raise_for(cdvz_gpu_match_pairs(index.handle(), a.data(), off, 1, pair, 1, opts.ratio_test, &r.global_similarity,
-                                 &local),
-            cdvz_gpu_index_last_error(index.handle()));
+  check_index(cdvz_gpu_match_pairs(index.handle(), a.data(), off, 1, pair, 1, opts.ratio_test, &r.global_similarity,
+                                 &local), index.handle());
   r.local_match_count = local;
   return r;
 }

@@ -95,3 +95,25 @@ def test_cpp_retrieval_shim_compiles_and_links(tmp_path):
                     "-lcdvz_gpu", f"-Wl,-rpath,{lib_dir}", "-o", str(exe)], check=True)
     p = subprocess.run([str(exe)], capture_output=True, text=True)
     assert p.returncode == 1 and "usage" in p.stderr
+
+
+def test_cpp_train_shim_compiles_and_checks_the_corpus(tmp_path):
+    """examples/train.cpp (the reference CLI's run_train over the shim) builds;
+    list_images' and train_model's corpus errors surface before any device
+    work: not a directory (usage), no images / fewer than 20 (data)."""
+    import subprocess
+
+    exe = tmp_path / "train"
+    lib_dir = os.path.dirname(cg.library_path())
+    subprocess.run(["g++", "-std=c++17", "-O1", os.path.join(ROOT, "examples", "train.cpp"), f"-L{lib_dir}",
+                    "-lcdvz_gpu", f"-Wl,-rpath,{lib_dir}", "-o", str(exe)], check=True)
+    p = subprocess.run([str(exe), str(tmp_path / "missing"), "b.txt"], capture_output=True, text=True)
+    assert p.returncode == 1 and "not a directory" in p.stderr
+    corpus = tmp_path / "corpus"
+    corpus.mkdir()
+    p = subprocess.run([str(exe), str(corpus), "b.txt"], capture_output=True, text=True)
+    assert p.returncode == 2 and "no .pgm/.ppm" in p.stderr
+    for i in range(3):
+        (corpus / f"{i}.pgm").write_bytes(b"P5\n16 16\n255\n" + bytes(256))
+    p = subprocess.run([str(exe), str(corpus), "b.txt"], capture_output=True, text=True)
+    assert p.returncode == 2 and "at least 20" in p.stderr

@@ -82,3 +82,30 @@ def test_train_model_argument_errors():
     small = np.zeros((5, 64, 64))
     with pytest.raises(cg.DataError):
         cg.train_model(small)
+
+
+def test_cpp_train_cli_matches_the_python_binding(tmp_path):
+    """examples/train.cpp (run_train over the shim: PGM files, load_image's
+    v / 255, train_model, save_model) writes the bundle the ctypes binding
+    trains from the same rasters."""
+    import os
+    import subprocess
+
+    rasters = [np.round(oracle_lib.synth_f64((401 + i * GOLDEN) % (1 << 64), 128, 128) * 255.0).astype(np.uint8)
+               for i in range(20)]
+    corpus = tmp_path / "corpus"
+    corpus.mkdir()
+    for i, r in enumerate(rasters):
+        (corpus / f"img{i:02d}.pgm").write_bytes(b"P5\n128 128\n255\n" + r.tobytes())
+    exe = tmp_path / "train"
+    lib_dir = os.path.dirname(cg.library_path())
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    subprocess.run(["g++", "-std=c++17", "-O1", os.path.join(root, "examples", "train.cpp"), f"-L{lib_dir}",
+                    "-lcdvz_gpu", f"-Wl,-rpath,{lib_dir}", "-o", str(exe)], check=True)
+    out = tmp_path / "bundle.txt"
+    p = subprocess.run([str(exe), str(corpus), str(out), "5", "4", "6", "120"], capture_output=True, text=True)
+    assert p.returncode == 0, p.stderr
+    want = cg.train_model(np.stack([r.astype(np.float64) * (1.0 / 255.0) for r in rasters]), seed=5,
+                          gmm_components=4, em_iterations=6, select_n=120)
+    assert out.read_text() == want
+    assert f"crc {cg.bundle_check(want)[0]:08x}" in p.stdout
