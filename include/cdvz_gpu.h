@@ -252,6 +252,12 @@ int cdvz_gpu_trim(cdvz_gpu_ctx* ctx);
 int cdvz_gpu_pyramid_bench(cdvz_gpu_ctx* ctx, const uint8_t* d_pixels, int width, int height, int count, int iters,
                            double* ms_per_iter, double* bytes_per_iter);
 
+/* Verification hook for the kernels' FP64 math (csrc/dmath.cuh): evaluates
+ * the CUDA library's atan2(a, b) (fn 0) or exp(a) (fn 1; b unused) and the
+ * constant-memory restatement the kernels call on `n` host inputs on
+ * `device`, writing both results (host arrays). No reference counterpart. */
+int cdvz_gpu_math_check(int device, int fn, const double* a, const double* b, size_t n, double* lib, double* ours);
+
 /* ------------------------------------------------------------------------
  * Compressed-domain matching and retrieval: an index of
  * CDVZ1 containers decoded on the device, queried in batches.

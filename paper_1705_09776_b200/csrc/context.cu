@@ -2109,3 +2109,30 @@ extern "C" int cdvz_gpu_train_model(int device, const double* corpus, int count,
     else if (out) throw UsageError("output buffer too small for the bundle text");
   });
 }
+
+namespace cdvz_gpu {
+cudaError_t launch_math_check(int fn, const double* a, const double* b, long long n, double* lib, double* ours,
+                              cudaStream_t st);
+}
+
+extern "C" int cdvz_gpu_math_check(int device, int fn, const double* a, const double* b, size_t n, double* lib,
+                                   double* ours) {
+  return guarded(nullptr, [&] {
+    if (!a || !lib || !ours || (fn == 0 && !b)) throw UsageError("null argument");
+    if (fn != 0 && fn != 1) throw UsageError("fn must be 0 (atan2) or 1 (exp)");
+    CDVZ_CUDA_CHECK(cudaSetDevice(device));
+    if (n == 0) return;
+    const size_t bytes = sizeof(double) * n;
+    OwnedBuffer da, db, dl, dov;
+    da.ensure(bytes);
+    db.ensure(bytes);
+    dl.ensure(bytes);
+    dov.ensure(bytes);
+    CDVZ_CUDA_CHECK(cudaMemcpy(da.p, a, bytes, cudaMemcpyHostToDevice));
+    if (fn == 0) CDVZ_CUDA_CHECK(cudaMemcpy(db.p, b, bytes, cudaMemcpyHostToDevice));
+    CDVZ_CUDA_CHECK(launch_math_check(fn, da.as<double>(), db.as<double>(), (long long)n, dl.as<double>(),
+                                      dov.as<double>(), nullptr));
+    CDVZ_CUDA_CHECK(cudaMemcpy(lib, dl.p, bytes, cudaMemcpyDeviceToHost));
+    CDVZ_CUDA_CHECK(cudaMemcpy(ours, dov.p, bytes, cudaMemcpyDeviceToHost));
+  });
+}

@@ -17,6 +17,7 @@
 // For descriptors the ownership is (cell, orientation parity), so each sample
 // adds at most one term per lane.
 #include "common.cuh"
+#include "dmath.cuh"
 
 namespace cdvz_gpu {
 
@@ -105,7 +106,7 @@ struct Frame { const double* lvl; int w, h; double x, y, sigma; };
 // bin is always the one the double computation gives.
 __device__ __forceinline__ int orient_bin(double gx, double gy) {
   if (fmax(fabs(gx), fabs(gy)) < 1e-30) {  // outside FP32's comfortable range: FP64 only
-    const double ang = wrap_angle(atan2(gy, gx));
+    const double ang = wrap_angle(dm::atan2(gy, gx));
     return static_cast<int>(floor(ang / kTwoPi * 36 + 0.5)) % 36;
   }
   float a = atan2f(float(gy), float(gx));
@@ -113,7 +114,7 @@ __device__ __forceinline__ int orient_bin(double gx, double gy) {
   const float t = a * 5.72957795f + 0.5f;  // 36 / 2pi
   const float fl = floorf(t), fr = t - fl;
   if (fr > 1e-3f && fr < 1.0f - 1e-3f) return int(fl) % 36;
-  const double ang = wrap_angle(atan2(gy, gx));
+  const double ang = wrap_angle(dm::atan2(gy, gx));
   return static_cast<int>(floor(ang / kTwoPi * 36 + 0.5)) % 36;
 }
 
@@ -195,7 +196,7 @@ __global__ void __launch_bounds__(32 * kOrientWarps) k_orient(Batch bt, DetConst
       const double mag = hypot(gx, gy);
       if (mag != 0.0) {
         bin = orient_bin(gx, gy);
-        val = mag * exp(-d2 / denom);
+        val = mag * dm::exp(-d2 / denom);
         atomicAdd(&S.cnt[bin], 1);
       }
     }
@@ -435,7 +436,7 @@ __global__ void __launch_bounds__(kSampleThreads, 12) k_sample(Batch bt) {
       const int i = q - j * (j + 1) / 2;
       const double v = (j + 0.5) * g.step - g.half;
       const double u = (i + 0.5) * g.step - g.half;
-      gexp[q] = exp(-(u * u + v * v) / g.gauss_denom);
+      gexp[q] = dm::exp(-(u * u + v * v) / g.gauss_denom);
     }
     __syncthreads();
     const float inv_samples = 1.0f / float(samples);
@@ -458,7 +459,7 @@ __global__ void __launch_bounds__(kSampleThreads, 12) k_sample(Batch bt) {
         if (mag != 0.0) {
           const int lo = min(i, j), hi = max(i, j);
           wgt = mag * gexp[hi * (hi + 1) / 2 + lo];
-          const double phi = wrap_angle(atan2(gy, gx) - theta);
+          const double phi = wrap_angle(dm::atan2(gy, gx) - theta);
           // ob = phi / 2pi * 8 - 0.5, ob0 = floor(ob), fo = ob - ob0 (descriptor.cpp:86-98)
           const double ob = div_two_pi(phi) * 8 - 0.5;
           const double obf = floor(ob);

@@ -6,6 +6,7 @@
 #include <algorithm>
 
 #include "common.cuh"
+#include "dmath.cuh"
 
 namespace cdvz_gpu {
 
@@ -134,7 +135,7 @@ __global__ void k_synth_canvas(const SynthParams* params, int w, int h, double* 
     double c = 0.0;
     for (int b = 0; b < p.n_blobs; ++b) {
       const double dx = x - p.blob[b][0], dy = y - p.blob[b][1];
-      c += p.blob[b][2] * exp(-(dx * dx + dy * dy) / p.blob[b][3]);
+      c += p.blob[b][2] * dm::exp(-(dx * dx + dy * dy) / p.blob[b][3]);
     }
     for (int k = 0; k < 5; ++k)
       c += p.wave[k][3] * sin(2.0 * 3.14159265358979323846 * (p.wave[k][0] * x + p.wave[k][1] * y) + p.wave[k][2]);

@@ -14,6 +14,7 @@
 // oracle restates them, so the SCFV floats agree with the
 // oracle up to libm (exp/log) ulps and the emitted bits agree exactly.
 #include "common.cuh"
+#include "dmath.cuh"
 
 namespace cdvz_gpu {
 
@@ -291,7 +292,7 @@ __global__ void __launch_bounds__(256, 2) k_posterior(Batch bt, Model md) {
     for (int t = wi; t < rows; t += 8) {
       const double pk = S.rmax[0][t];
       double* g = gam + t * nc;
-      for (int i = lane; i < nc; i += 32) buf[i] = exp(g[i] - pk);
+      for (int i = lane; i < nc; i += 32) buf[i] = dm::exp(g[i] - pk);
       __syncwarp();
       double total = 0.0;
       if (nc < 4) {
@@ -324,7 +325,7 @@ __global__ void __launch_bounds__(256, 2) k_posterior(Batch bt, Model md) {
   // softmax_rows: e = exp(logp - peak) ...
   for (int t = wi; t < rows; t += 8) {
     const double pk = S.rmax[0][t];
-    for (int i = lane; i < nc; i += 32) gam[t * nc + i] = exp(gam[t * nc + i] - pk);
+    for (int i = lane; i < nc; i += 32) gam[t * nc + i] = dm::exp(gam[t * nc + i] - pk);
   }
   __syncthreads();
   // ... e.sum() in Eigen's packet order (packet_sum_seq) ...
@@ -424,7 +425,7 @@ __global__ void __launch_bounds__(1024) k_posterior_small(Batch bt, Model md) {
     double* e = lp[tid];
     double pk = e[0];
     for (int i = 1; i < nc; ++i) pk = fmax(pk, e[i]);
-    for (int i = 0; i < nc; ++i) e[i] = exp(e[i] - pk);
+    for (int i = 0; i < nc; ++i) e[i] = dm::exp(e[i] - pk);
     const double tot = packet_sum_seq(e, nc);
     double* gam = bt.gamma + ((long long)f * bt.cap_or + row0 + tid) * nc;
     for (int i = 0; i < nc; ++i) gam[i] = e[i] / tot;

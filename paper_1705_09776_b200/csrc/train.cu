@@ -13,6 +13,7 @@
 // operations (--fmad=false): sums over samples ascend, vector reductions use
 // the Eigen packet order (packet_sum_seq).
 #include "common.cuh"
+#include "dmath.cuh"
 
 namespace cdvz_gpu {
 
@@ -126,7 +127,7 @@ __global__ void k_em_softmax(double* logp, long long n, int nc) {
   double* row = logp + t * nc;
   double peak = row[0];
   for (int i = 1; i < nc; ++i) peak = fmax(peak, row[i]);
-  for (int i = 0; i < nc; ++i) row[i] = exp(row[i] - peak);
+  for (int i = 0; i < nc; ++i) row[i] = dm::exp(row[i] - peak);
   const double sum = packet_sum_strided(row, nc, 1);
   for (int i = 0; i < nc; ++i) row[i] = row[i] / sum;
 }
