@@ -42,19 +42,6 @@ __device__ __forceinline__ double wrap_angle(double a) {
   return r < 0.0 ? r + kTwoPi : r;
 }
 
-// descriptor.cpp:25-35 — a term is skipped when its fraction is exactly 0.
-__device__ __forceinline__ double sample_bilinear(const double* img, int w, double qx, double qy) {
-  const int x0 = static_cast<int>(floor(qx));
-  const int y0 = static_cast<int>(floor(qy));
-  const double fx = qx - x0, fy = qy - y0;
-  const double* p = img + (long long)y0 * w + x0;  // read-only here: the non-coherent (texture) path
-  double v = (1.0 - fy) * (1.0 - fx) * __ldg(p);
-  if (fx > 0.0) v += (1.0 - fy) * fx * __ldg(p + 1);
-  if (fy > 0.0) v += fy * (1.0 - fx) * __ldg(p + w);
-  if (fx > 0.0 && fy > 0.0) v += fy * fx * __ldg(p + w + 1);
-  return v;
-}
-
 // sample_bilinear split in two so that a caller can issue the loads of
 // several taps before any arithmetic: the tap geometry (x0 = floor(qx),
 // fx = qx - x0, ...) and the four texels — a neighbour whose fraction is 0 is
@@ -89,11 +76,18 @@ __device__ __forceinline__ BTexels btexels(const double* img, const BTap& t) {
   const double* p = img + t.off;
   return {ldg_early(p), ldg_early(p + t.dx), ldg_early(p + t.dy), ldg_early(p + t.dx + t.dy)};
 }
+// The reference skips a term whose fraction is 0 (descriptor.cpp:25-35).
+// Adding it instead is exact: its product is +0 (every factor is finite and
+// non-negative — fractions in [0, 1), pyramid values are Gaussian-blur sums
+// starting from +0.0, never -0.0 — and the fallback texel is a real one), and
+// r, itself a product of non-negative factors, is never -0.0, so r + (+0) == r.
+// Unconditional terms spare the compare and the two selects per term that
+// the skip costs after if-conversion.
 __device__ __forceinline__ double bmix(const BTap& t, const BTexels& v) {
   double r = (1.0 - t.fy) * (1.0 - t.fx) * v.v00;
-  if (t.fx > 0.0) r += (1.0 - t.fy) * t.fx * v.v01;
-  if (t.fy > 0.0) r += t.fy * (1.0 - t.fx) * v.v10;
-  if (t.fx > 0.0 && t.fy > 0.0) r += t.fy * t.fx * v.v11;
+  r += (1.0 - t.fy) * t.fx * v.v01;
+  r += t.fy * (1.0 - t.fx) * v.v10;
+  r += t.fy * t.fx * v.v11;
   return r;
 }
 
