@@ -50,16 +50,16 @@ __device__ __forceinline__ double wrap_angle(double a) {
 // sum in its order.
 struct BTap {
   double fx, fy;
-  int off, dx, dy;
+  unsigned off, dx, dy;  // texel index within the level (32-bit: one IMAD.WIDE per address)
 };
 __device__ __forceinline__ BTap btap(int w, double qx, double qy) {
   const double xf = floor(qx), yf = floor(qy);
   BTap t;
   t.fx = qx - xf;  // == qx - x0: x0 = (int)floor(qx) is exact in double
   t.fy = qy - yf;
-  t.off = int(yf) * w + int(xf);
-  t.dx = t.fx > 0.0 ? 1 : 0;
-  t.dy = t.fy > 0.0 ? w : 0;
+  t.off = unsigned(int(yf)) * unsigned(w) + unsigned(int(xf));
+  t.dx = t.fx > 0.0 ? 1u : 0u;
+  t.dy = t.fy > 0.0 ? unsigned(w) : 0u;
   return t;
 }
 struct BTexels {
@@ -73,8 +73,8 @@ __device__ __forceinline__ double ldg_early(const double* p) {
   return v;
 }
 __device__ __forceinline__ BTexels btexels(const double* img, const BTap& t) {
-  const double* p = img + t.off;
-  return {ldg_early(p), ldg_early(p + t.dx), ldg_early(p + t.dy), ldg_early(p + t.dx + t.dy)};
+  return {ldg_early(img + t.off), ldg_early(img + (t.off + t.dx)), ldg_early(img + (t.off + t.dy)),
+          ldg_early(img + (t.off + t.dx + t.dy))};
 }
 // The reference skips a term whose fraction is 0 (descriptor.cpp:25-35).
 // Adding it instead is exact: its product is +0 (every factor is finite and
@@ -408,6 +408,7 @@ __global__ void __launch_bounds__(kSampleThreads, 12) k_sample(Batch bt) {
     const DescGeo g = bt.geo[slot];
     const double theta = bt.oriented[slot].theta;
     const double* lvl = bt.pyr + g.lvl_off;
+    asm("" : "+l"(lvl));  // one 64-bit base: each texel address is then a single IMAD.WIDE.U32
     const int samples = g.samples, ns = samples * samples;
     double2* out = bt.smp + slot * bt.smp_cap;
     uint8_t* outb = bt.smpb + slot * kMaxSamples * kMaxSamples;
