@@ -238,6 +238,39 @@ __device__ __forceinline__ bool screen_pixel(const float a[4], float ba, const f
   return any;
 }
 
+// screen_pixel with no early exits: every predicate of the test above is
+// evaluated for both roots and combined with bitwise logic, so the walk's
+// screen is straight-line predicated code (no divergent branches and
+// reconvergence points per pixel). The result is the same function of the
+// inputs: where the branchy form returns early, the garbage values computed
+// past that point (rsqrt of a negative, rcp of 0) are masked by the same
+// predicate.
+__device__ __forceinline__ bool screen_pixel_flat(const float a[4], float ba, const float up[4], float mu,
+                                                   const float dn[4], float md, const DetConst& dc) {
+  const float fa = 3.0f * a[3], fb = 2.0f * a[2], fc = a[1];
+  const float bb = fb * fb, ac4 = 4.0f * fa * fc;
+  const float fd = bb - ac4;
+  const float de = 1e-5f * (bb + fabsf(ac4)) + 1e-30f;
+  const float sq = fd * rsqrt_approx(fd);
+  const float q = -0.5f * (fb + copysignf(sq, fb));
+  const float r0 = q * rcp_approx(fa), r1 = fc * rcp_approx(q);
+  const float m = 1e-4f * (ba + mu + md) + 1e-7f;
+  const float tmargin = __fmaf_rn(1e-5f, ba, 1e-6f);
+  auto horner = [](float r, const float c[4]) {
+    return __fmaf_rn(r, __fmaf_rn(r, __fmaf_rn(r, c[3], c[2]), c[1]), c[0]);
+  };
+  auto root_ok = [&](float r) {
+    const bool in = r >= dc.scr_lo && r <= dc.scr_hi;
+    const float p = horner(r, a), pu = horner(r, up), pd = horner(r, dn);
+    const bool strong = fabsf(p) + tmargin >= dc.scr_thr;
+    const bool past = p > 0.0f ? ((pu >= p + m) | (pd >= p + m)) : ((pu <= p - m) | (pd <= p - m));
+    return (in & strong & !past) | (!in & !isfinite(r));
+  };
+  const bool any = root_ok(r0) | root_ok(r1);
+  const bool undecided = !(fd > de) | !(fabsf(q) > 1e-30f);  // near-double root, not finite, q ~ 0
+  return (fa == 0.0f) | (!(fd < -de) & (undecided | any));
+}
+
 __device__ __forceinline__ bool screen_pixel(const double a[4], const double up[4], const double dn[4],
                                               const DetConst& dc) {
   float af[4], uf[4], df[4];
@@ -828,7 +861,7 @@ __global__ void __maxnreg__(96) k_detect_walk(Batch bt, DetConst dc, int o, int 
   auto screen_row = [&](int rs, const float a[4], float ba, const float up[4], float mu, const float dn[4],
                         float md) {  // 3x3 neighbourhood complete
     if (rs >= y0 && rs < y1) {
-      const bool push = out_col && (!dc.screen || screen_pixel(a, ba, up, mu, dn, md, dc));
+      const bool push = out_col & (!dc.screen | screen_pixel_flat(a, ba, up, mu, dn, md, dc));
       const unsigned bal = __ballot_sync(0xffffffffu, push);
       if (push) S.queue[qn + __popc(bal & ((1u << lane) - 1u))] = uint16_t(((rs - y0 + 2) << 5) | lane);
       qn += __popc(bal);
