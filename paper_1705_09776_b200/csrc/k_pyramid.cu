@@ -715,8 +715,6 @@ struct alignas(128) DetWarpSmem {
     double gpair[2][4][2][34];    // TMA path: row pairs [pair % 2][level][row of pair][1 + lane] (one 4-D box each)
   };
   double ring[kRing][4][32];   // alpha rows: [row % kRing][coefficient][lane]
-  float4 fring[4][32];         // float copies of alpha rows ra - 2 .. ra + 1 (the screen's inputs): [row % 4][lane]
-  float mring[4][32];          // their neighbour bounds M (screen_pixel)
   uint64_t bar[2];             // TMA path: one mbarrier per pair slot
   uint16_t queue[128];         // ((row - y0 + 2) << 5) | lane
 };
@@ -811,8 +809,12 @@ __global__ void __maxnreg__(96) k_detect_walk(Batch bt, DetConst dc, int o, int 
     for (int i = 0; i < kPrefetch + 2; ++i) issue();  // rows y0 - 2 .. y0 + kPrefetch - 1
   }
   const double oct_scale = ldexp(1.0, o);
-  float apf[4];       // own alpha (float copy) of the previous row (screened one row late)
-  float bp = 0.f, mp = 0.f;  // its magnitude and neighbour bounds
+  // Float copies of the lane's own alpha (the screen's inputs, each alpha
+  // converted once): the previous row (screened one row late) with its
+  // magnitude and neighbour bounds, and the row before it with its neighbour
+  // bound. Registers, not shared memory: every lane reads only its own column.
+  float apf[4] = {0.f, 0.f, 0.f, 0.f}, a2f[4] = {0.f, 0.f, 0.f, 0.f};
+  float bp = 0.f, mp = 0.f, m2 = 0.f;
   int qn = 0;
   auto drain = [&]() {
     for (int qi = lane; qi - lane < qn; qi += 32) {
@@ -896,12 +898,6 @@ __global__ void __maxnreg__(96) k_detect_walk(Batch bt, DetConst dc, int o, int 
       }
       const float b0 = mag_bound(a0f, dc.scr_hi), m0 = nbr_bound(a0f, dc.scr_hi);
       const float b1 = mag_bound(a1f, dc.scr_hi), m1 = nbr_bound(a1f, dc.scr_hi);
-      S.fring[unsigned(ra) % 4][lane] = make_float4(a0f[0], a0f[1], a0f[2], a0f[3]);
-      S.mring[unsigned(ra) % 4][lane] = m0;
-      if (second) {
-        S.fring[unsigned(ra + 1) % 4][lane] = make_float4(a1f[0], a1f[1], a1f[2], a1f[3]);
-        S.mring[unsigned(ra + 1) % 4][lane] = m1;
-      }
       __syncwarp();
       if constexpr (TMA) {
         issue_pair((t >> 1) + 2);  // into the slot of pair t/2 (rows ra - 1, ra), read by every lane above
@@ -909,14 +905,14 @@ __global__ void __maxnreg__(96) k_detect_walk(Batch bt, DetConst dc, int o, int 
         issue();  // rows ra + kPrefetch + 1, ra + kPrefetch + 2 into the slots of rows ra - 1, ra
         issue();
       }
-      {
-        const float4 u4 = S.fring[unsigned(ra - 2) % 4][lane];  // own alpha of row ra - 2 (the ring keeps it)
-        const float auf[4] = {u4.x, u4.y, u4.z, u4.w};
-        screen_row(ra - 1, apf, bp, auf, S.mring[unsigned(ra - 2) % 4][lane], a0f, m0);
-      }
+      screen_row(ra - 1, apf, bp, a2f, m2, a0f, m0);
       if (second) screen_row(ra, a0f, b0, apf, mp, a1f, m1);
 #pragma unroll
-      for (int i = 0; i < 4; ++i) apf[i] = a1f[i];
+      for (int i = 0; i < 4; ++i) {
+        a2f[i] = a0f[i];
+        apf[i] = a1f[i];
+      }
+      m2 = m0;
       bp = b1;
       mp = m1;
     }
