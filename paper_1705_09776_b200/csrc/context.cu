@@ -403,7 +403,7 @@ struct cdvz_gpu_ctx {
       for (int k = 0; k < 4; ++k) nb.plane_off[n_oct][k] = pd + (long long)k * w * h;
       pd += 4LL * w * h;
       nb.bm_off[n_oct] = bw;
-      bw += (2LL * w * h + 31) / 32;
+      bw += ((2LL * w * h + 31) / 32 + 3) & ~3LL;  // 16-byte aligned octave bitmaps (k_merge_octave's uint4 passes)
       ++n_oct;
       w /= 2;
       h /= 2;
@@ -415,7 +415,7 @@ struct cdvz_gpu_ctx {
                        " octaves on a raster this large; the GPU kernels support at most " + std::to_string(kMaxOctaves));
     nb.n_oct = n_oct;
     nb.frame_doubles = std::max<long long>(pd, 1);
-    nb.bitmap_words = std::max<long long>(bw, 1);
+    nb.bitmap_words = std::max<long long>(bw, 4);
     // Survivor capacities per frame: a synthetic 1080p octave keeps ~1% of its
     // pixels (21k); 1/16 of the prepared raster leaves 6x headroom.
     nb.cap_oct = std::max(32768, int(std::min<long long>(1LL << 26, (long long)W * H / 16)));

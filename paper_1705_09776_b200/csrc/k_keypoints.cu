@@ -88,34 +88,35 @@ __global__ void __launch_bounds__(kMergeThreads) k_merge_octave(Batch bt, int o)
   if (n > bt.cap_oct) n = bt.cap_oct;
   const KP* raw = bt.raw + ((long long)f * bt.n_oct + o) * bt.cap_oct;
 
-  // Exclusive popcount prefix of the bitmap, per word, in shared memory.
-  // Warp w owns a contiguous segment of words and reads it coalesced: pass 1
-  // counts the segment, a block scan places the segments, pass 2 re-reads
-  // each 32-word chunk and scans it across the lanes.
+  // Exclusive popcount prefix of the bitmap, per word: thread t owns a
+  // contiguous run of 16-byte groups (plan() pads every octave's bitmap to
+  // whole groups), counts it, a block scan places the runs, and a second read
+  // of the run (L1) writes its prefixes — two vector loads and four popcounts
+  // per group, no per-word shuffles.
   // In shared memory when it fits (merge_smem_bytes), else in global scratch.
-  int* prefix = (size_t(nwords) * sizeof(int) <= kMergeSmemBudget) ? sm : bt.bm_prefix + f * bt.bitmap_words + bt.bm_off[o];
+  const int n4 = (nwords + 3) >> 2;
+  int* prefix = (size_t(4 * n4) * sizeof(int) <= kMergeSmemBudget) ? sm : bt.bm_prefix + f * bt.bitmap_words + bt.bm_off[o];
+  uint4* bm4 = reinterpret_cast<uint4*>(bm);
   {
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    const int seg = (nwords + nw - 1) / nw;
-    const int lo = min(nwords, wid * seg), hi = min(nwords, lo + seg);
+    const int per = (n4 + int(blockDim.x) - 1) / int(blockDim.x);
+    const int g0 = min(n4, int(threadIdx.x) * per), g1 = min(n4, g0 + per);
     int cnt = 0;
-    for (int i = lo + lane; i < hi; i += 32) cnt += __popc(bm[i]);
-    cnt = __reduce_add_sync(0xffffffffu, cnt);
+    for (int g = g0; g < g1; ++g) {
+      const uint4 v = bm4[g];
+      cnt += __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
+    }
     int total = 0;
-    // One value per warp through the block scan (lanes other than 0 add 0).
-    int base = block_exclusive_scan(lane == 0 ? cnt : 0, warp_tot, total);
-    base = __shfl_sync(0xffffffffu, base, 0);
-    for (int c = lo; c < hi; c += 32) {
-      const int i = c + lane;
-      const int v = i < hi ? __popc(bm[i]) : 0;
-      int incl = v;
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const int t = __shfl_up_sync(0xffffffffu, incl, d);
-        if (lane >= d) incl += t;
-      }
-      if (i < hi) prefix[i] = base + incl - v;
-      base += __shfl_sync(0xffffffffu, incl, 31);
+    int run = block_exclusive_scan(cnt, warp_tot, total);
+    int4* p4 = reinterpret_cast<int4*>(prefix);
+    for (int g = g0; g < g1; ++g) {
+      const uint4 v = bm4[g];
+      int4 q;
+      q.x = run;
+      q.y = q.x + __popc(v.x);
+      q.z = q.y + __popc(v.y);
+      q.w = q.z + __popc(v.z);
+      run = q.w + __popc(v.w);
+      p4[g] = q;
     }
   }
   __syncthreads();
@@ -129,7 +130,9 @@ __global__ void __launch_bounds__(kMergeThreads) k_merge_octave(Batch bt, int o)
     out_sorted[rank] = k;
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < nwords; i += blockDim.x) bm[i] = 0u;  // ready for the next batch
+  // Ready for the next batch: only the words holding a survivor's bit are
+  // non-zero, so clearing those (one store per survivor) clears the bitmap.
+  for (int i = threadIdx.x; i < n; i += blockDim.x) bm[raw[i].key >> 5] = 0u;
   if (threadIdx.x == 0) {
     bt.raw_count[f * bt.n_oct + o] = 0;
     bt.oct_count[f * bt.n_oct + o] = n;
@@ -253,7 +256,7 @@ int merge_cell_px(int W, int H) {
 // Dynamic shared memory of octave o's merge: its bitmap prefix (when it fits)
 // and, above octave 0, the dedup grid that reuses the same space.
 size_t merge_smem_bytes(const Batch& bt, int o) {
-  const size_t words = (size_t(2) * bt.ow[o] * bt.oh[o] + 31) / 32;
+  const size_t words = ((size_t(2) * bt.ow[o] * bt.oh[o] + 31) / 32 + 3) & ~size_t(3);  // padded to 16-byte groups
   const size_t need = words * sizeof(int) <= kMergeSmemBudget ? words : 0;  // else global prefix
   const size_t cells = size_t(bt.W / bt.merge_cell + 3) * (bt.H / bt.merge_cell + 3);
   const size_t grid = o > 0 ? 2 * cells + 1 : 0;
