@@ -499,27 +499,33 @@ def main():
             ctx._check(lib.cdvz_gpu_encode_batch_wait(ctx._ctx, t))
 
         wait(submit(0))
-        if dist:
-            dist.barrier()
-        t0 = time.perf_counter()
-        pend, k = None, 0
-        for _ in range(args.steps):
-            for _ in range(calls):
-                t = submit(k)
-                if pend is not None:
-                    wait(pend)
-                pend, k = t, k ^ 1
-        wait(pend)
-        e2e_s = max_over_ranks(time.perf_counter() - t0)
-        assert int((status[k ^ 1] != 0).sum()) == 0 and offsets[k ^ 1][-1] > 0
+        wait(submit(1))  # both output sets touched before timing
         e2e_frames = sum_over_ranks(pool_n * calls)
-        e2e = {"value": e2e_frames * args.steps / e2e_s, "unit": "frames/s",
+        # Three timed repeats of the K streamed steps; the median is reported
+        # (host-side jitter on a shared box can stall one repeat).
+        rates = []
+        for _ in range(3):
+            if dist:
+                dist.barrier()
+            t0 = time.perf_counter()
+            pend, k = None, 0
+            for _ in range(args.steps):
+                for _ in range(calls):
+                    t = submit(k)
+                    if pend is not None:
+                        wait(pend)
+                    pend, k = t, k ^ 1
+            wait(pend)
+            e2e_s = max_over_ranks(time.perf_counter() - t0)
+            assert int((status[k ^ 1] != 0).sum()) == 0 and offsets[k ^ 1][-1] > 0
+            rates.append(e2e_frames * args.steps / e2e_s)
+        e2e = {"value": sorted(rates)[1], "unit": "frames/s", "repeats": rates,
                "h2d_bytes_per_step": int(e2e_frames * FRAME_W * FRAME_H),
                "d2h_bytes_per_step": int(e2e_frames * (slot + 4)),
                "note": "host wall clock around the public C ABI, every step's H2D of its frames from pinned host "
                        "memory and D2H of its containers inside the timed region; steps streamed through "
                        "cdvz_gpu_encode_batch_submit / _wait (two batches in flight: one step's copies and kernels "
-                       "overlap the previous step's tail); "
+                       "overlap the previous step's tail); median of three timed repeats of the K steps; "
                        + (f"{calls} call(s) per step over a pinned pool of {pool_n} distinct frames"
                           + (f" on a {world}-device context (cdvz_gpu_create_multi)" if ctx is not lead.ex else ""))}
         if ctx is not lead.ex:
