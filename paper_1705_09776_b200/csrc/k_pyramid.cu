@@ -647,7 +647,7 @@ __global__ void __launch_bounds__(kDetThreads, 2)
 #pragma unroll
         for (int lv = 0; lv < 4; ++lv) {
           const double* g = Gt + (lv * kGH + r + 1) * kGW + cc + 1;
-          const double lap = g[-kGW] + g[kGW] + g[-1] + g[1] - 4.0 * g[0];
+          const double lap = fma(-4.0, g[0], g[-kGW] + g[kGW] + g[-1] + g[1]);  // 4c is exact: == s - 4c
           L[lv] = dc.s2[lv] * lap;
         }
 #pragma unroll
@@ -848,7 +848,9 @@ __global__ void __maxnreg__(96) k_detect_walk(Batch bt, DetConst dc, int o, int 
       const double* rU = grow_at(ra - 1, k);
       const double* rC = grow_at(ra, k);
       const double* rD = grow_at(ra + 1, k);
-      const double lap = rU[lane + 1] + rD[lane + 1] + rC[lane] + rC[lane + 2] - 4.0 * rC[lane + 1];
+      // (((up + down) + left) + right) - 4c with one rounding for the last
+      // step: 4c is exact, so the fused multiply-add is RN(s - 4c) itself.
+      const double lap = fma(-4.0, rC[lane + 1], rU[lane + 1] + rD[lane + 1] + rC[lane] + rC[lane + 2]);
       L[k] = dc.s2[k] * lap;
     }
 #pragma unroll
