@@ -515,13 +515,23 @@ class Index:
         return {"count": n.value, "mode_id": m.value, "model_crc": crc.value, "components": nc.value,
                 "total_codes": tot.value}
 
-    def retrieve_batch(self, queries, ratio_test: float = 0.85, rerank_depth: int = 50, max_results: int = 0):
-        """retrieve() for every query -> (items int32 [nq, k], scores float64 [nq, k])."""
+    def retrieve_batch(self, queries, ratio_test: float = 0.85, rerank_depth: int = 50, max_results: int = 0,
+                       out=None):
+        """retrieve() for every query -> (items int32 [nq, k], scores float64 [nq, k]).
+        out: optional preallocated (items, scores) of those shapes and dtypes —
+        e.g. views of pinned buffers (Extractor.pinned_buffer), which the
+        device-to-host copy of the ranked lists fills at full link speed."""
         blob, offs = _pack(list(queries))
         nq = len(offs) - 1
         k = self.count if max_results <= 0 else min(self.count, max_results)
-        items = np.empty((nq, k), dtype=np.int32)
-        scores = np.empty((nq, k), dtype=np.float64)
+        if out is None:
+            items = np.empty((nq, k), dtype=np.int32)
+            scores = np.empty((nq, k), dtype=np.float64)
+        else:
+            items, scores = out
+            if (items.shape != (nq, k) or items.dtype != np.int32 or not items.flags.c_contiguous
+                    or scores.shape != (nq, k) or scores.dtype != np.float64 or not scores.flags.c_contiguous):
+                raise UsageError(f"out must be C-contiguous int32 and float64 arrays of shape {(nq, k)}")
         self._check(self._lib.cdvz_gpu_retrieve(self._idx, blob.ctypes.data, offs.ctypes.data, nq, ratio_test,
                                                 rerank_depth, max_results, items.ctypes.data, scores.ctypes.data))
         return items, scores

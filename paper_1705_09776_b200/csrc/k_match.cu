@@ -307,16 +307,20 @@ __global__ void __launch_bounds__(kLMThreads) k_match_pairs(Decoded Q, Decoded X
 
 // One warp per query: re-rank the head by (local desc, similarity desc, id
 // asc) and write every item's final rank and score (eval.cpp:97-123).
-__global__ void __launch_bounds__(32) k_finish(const unsigned long long* keys, const int* vals, const int* local,
-                                               const int* id_rank, int n, int head, int max_results, int q0,
-                                               int* out_items, double* out_scores) {
+// CTA per query: threads r < head rank the re-ranked head, every thread
+// copies the tail (the full ranked list is the output: n entries per query).
+constexpr int kFinishThreads = 256;
+__global__ void __launch_bounds__(kFinishThreads) k_finish(const unsigned long long* keys, const int* vals,
+                                                           const int* local, const int* id_rank, int n, int head,
+                                                           int max_results, int q0, int* out_items,
+                                                           double* out_scores) {
   const int q = blockIdx.x, lane = threadIdx.x;
   const unsigned long long* kq = keys + (long long)q * n;
   const int* vq = vals + (long long)q * n;
   const int* lq = local + (long long)q * head;
   int* oi = out_items + (long long)(q0 + q) * max_results;
   double* os = out_scores + (long long)(q0 + q) * max_results;
-  for (int r = lane; r < head; r += 32) {
+  for (int r = lane; r < head; r += kFinishThreads) {
     const int lr = lq[r];
     const double sr = key_value(kq[r]);
     const int ir = id_rank[vq[r]];
@@ -332,7 +336,7 @@ __global__ void __launch_bounds__(32) k_finish(const unsigned long long* keys, c
       os[pos] = lr + (sr + 1.0) / 2.0;
     }
   }
-  for (int r = head + lane; r < min(n, max_results); r += 32) {
+  for (int r = head + lane; r < min(n, max_results); r += kFinishThreads) {
     oi[r] = vq[r];
     os[r] = (key_value(kq[r]) + 1.0) / 2.0 - 1.0;
   }
@@ -617,7 +621,7 @@ int cdvz_gpu_retrieve(cdvz_gpu_index* idx, const uint8_t* qblob, const size_t* q
                                                                     head, ratio_test, mc, q0, idx->local.as<int>());
         CDVZ_CUDA_CHECK(cudaGetLastError());
       }
-      k_finish<<<nqc, 32, 0, idx->st>>>(idx->keys2.as<unsigned long long>(), idx->vals2.as<int>(), idx->local.as<int>(),
+      k_finish<<<nqc, kFinishThreads, 0, idx->st>>>(idx->keys2.as<unsigned long long>(), idx->vals2.as<int>(), idx->local.as<int>(),
                                         idx->id_rank.as<int>(), n, head, mr, q0, idx->out_i.as<int>(),
                                         idx->out_s.as<double>());
       CDVZ_CUDA_CHECK(cudaGetLastError());
