@@ -56,6 +56,26 @@ def test_retrieve_query_chunks_match_one_pass(corpus_4k, monkeypatch):
     assert np.array_equal(got_i, want_i) and np.array_equal(got_s, want_s)
 
 
+def test_retrieve_into_pinned_buffers(corpus_4k, ex_b8):
+    """retrieve_batch(out=...) fills caller-provided (pinned) arrays with the
+    same ranked lists (here the whole index is re-ranked); bad
+    shapes / dtypes are a UsageError."""
+    index, queries = corpus_4k[:40], corpus_4k[30:40]
+    idx = cg.Index(index)
+    want_i, want_s = idx.retrieve_batch(queries, 0.85, 300)  # head = all 40 items
+    nq, n = len(queries), len(index)
+    pin_i, pin_s = ex_b8.pinned_buffer(4 * nq * n), ex_b8.pinned_buffer(8 * nq * n)
+    out = (pin_i.array.view(np.int32).reshape(nq, n), pin_s.array.view(np.float64).reshape(nq, n))
+    got_i, got_s = idx.retrieve_batch(queries, 0.85, 300, out=out)
+    assert got_i is out[0] and got_s is out[1]
+    assert np.array_equal(got_i, want_i) and np.array_equal(got_s, want_s)
+    oracle_i, oracle_s = oracle_lib.retrieve(index, queries, 0.85, 300)
+    assert np.array_equal(got_i, oracle_i) and np.array_equal(got_s, oracle_s)
+    with pytest.raises(cg.UsageError):
+        idx.retrieve_batch(queries, 0.85, 300, out=(out[0][:, :5], out[1]))
+    idx.close()
+
+
 def test_indexed_image_retrieves_itself_first(corpus_4k):
     """test_pipeline.cpp:164-170 on the GPU."""
     idx = cg.Index(corpus_4k[:16], ids=[f"img{i}" for i in range(16)])
