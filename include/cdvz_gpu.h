@@ -112,9 +112,13 @@ int cdvz_gpu_encode_batch(cdvz_gpu_ctx* ctx, const uint8_t* pixels, int width, i
  * submitted batches are in flight per context, so one batch's copies and
  * kernels overlap the previous one's tail; a third submit first completes the
  * oldest (its wait then returns the held result). All buffers of a submitted
- * call must stay valid until its wait returns. Ticket 0 means the call
- * completed inside submit (multi-device contexts and batches above 4 GB run
- * synchronously). Errors found while enqueuing are returned by submit. */
+ * call must stay valid until its wait returns. On a multi-device context
+ * submit hands every device its share through that device's own submit and
+ * wait gathers the containers in frame order (two calls in flight there too),
+ * provided out_cap leaves a full slot (cdvz_gpu_container_slot) per frame.
+ * Ticket 0 means the call completed inside submit (a multi-device call
+ * without that room, or a batch above 4 GB, runs synchronously). Errors
+ * found while enqueuing are returned by submit. */
 int cdvz_gpu_encode_batch_submit(cdvz_gpu_ctx* ctx, const uint8_t* pixels, int width, int height, size_t stride,
                                  int count, int mode_id, int max_side, uint8_t* out, size_t out_cap,
                                  size_t* offsets, int* status, uint64_t* ticket);

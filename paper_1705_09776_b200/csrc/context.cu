@@ -262,6 +262,21 @@ struct cdvz_gpu_ctx {
     std::string err;
   };
   std::vector<Finished> finished;  // submitted calls finished before their wait (result held for it)
+  // A multi-device context's submitted calls: each shard's share runs through
+  // that shard's own submit / wait (two in flight per shard), and the wait
+  // gathers the shards' containers in frame order.
+  struct MultiCall {
+    unsigned long long ticket = 0;
+    std::vector<uint64_t> shard_ticket;
+    std::vector<int> start;
+    std::vector<std::vector<size_t>> off;
+    uint8_t* out = nullptr;
+    size_t out_cap = 0;
+    size_t* offsets = nullptr;
+    int* status = nullptr;
+    size_t slot = 0;
+  };
+  std::vector<MultiCall> multi_calls;
   int last_frames = 0, last_mode = -1;
 
   cudaEvent_t ev[6] = {};
@@ -1084,6 +1099,56 @@ int encode_host_batch(cdvz_gpu_ctx* ctx, const uint8_t* pixels, int width, int h
 // one host thread per device (the GPU analogue of the reference's
 // run_indexed fan-out, parallel.cpp:40-78), containers gathered in frame
 // order. The lowest-index failing device's error wins, as in run_indexed.
+// Gathers per-shard container regions (shard d wrote frames start[d] ..
+// start[d+1] with local offsets off[d]) into `out` in frame order.
+void gather_multi(const std::vector<int>& start, const std::vector<std::vector<size_t>>& off, bool in_place,
+                  const std::vector<std::vector<uint8_t>>& scratch, uint8_t* out, size_t out_cap, size_t* offsets,
+                  int* status, size_t slot) {
+  const int nd = int(start.size()) - 1;
+  // Gather in frame order. In place, shard d's bytes move left (to the end of
+  // shard d-1's), so a forward memmove per shard is safe.
+  size_t written = 0;
+  offsets[0] = 0;
+  for (int d = 0; d < nd; ++d) {
+    const int n = start[size_t(d) + 1] - start[size_t(d)];
+    const size_t bytes = off[size_t(d)][size_t(n)];
+    const uint8_t* src = in_place ? out + size_t(start[size_t(d)]) * slot : scratch[size_t(d)].data();
+    if (!in_place && written + bytes > out_cap) {
+      // Frame-level overflow accounting, as the single-device path does it.
+      for (int i = 0; i < n; ++i) {
+        const size_t len = off[size_t(d)][size_t(i) + 1] - off[size_t(d)][size_t(i)];
+        const int fi = start[size_t(d)] + i;
+        if (status[fi] == CDVZ_GPU_OK) {
+          if (written + len > out_cap) {
+            status[fi] = CDVZ_GPU_USAGE;
+          } else {
+            std::memcpy(out + written, src + off[size_t(d)][size_t(i)], len);
+            written += len;
+          }
+        }
+        offsets[fi + 1] = written;
+      }
+      continue;
+    }
+    if (bytes && out + written != src) std::memmove(out + written, src, bytes);
+    for (int i = 0; i < n; ++i) offsets[start[size_t(d)] + i + 1] = written + off[size_t(d)][size_t(i) + 1];
+    written += bytes;
+  }
+}
+
+void fold_multi_stats(cdvz_gpu_ctx* ctx) {
+  cdvz_gpu_ctx::Stats sum;
+  int launches = 0;
+  for (auto& sh : ctx->shards) {
+    for (int i = 0; i < 5; ++i) sum.stage_ms[i] += sh->stats.stage_ms[i];
+    sum.pyr_ms += sh->stats.pyr_ms;
+    sum.pyr_bytes += sh->stats.pyr_bytes;
+    launches += sh->launches;
+  }
+  ctx->stats = sum;
+  ctx->launches = launches;
+}
+
 void encode_multi(cdvz_gpu_ctx* ctx, const uint8_t* pixels, int width, int height, size_t stride, int count,
                   int mode_id, int max_side, uint8_t* out, size_t out_cap, size_t* offsets, int* status, int kind) {
   const int nd = int(ctx->shards.size());
@@ -1123,45 +1188,8 @@ void encode_multi(cdvz_gpu_ctx* ctx, const uint8_t* pixels, int width, int heigh
       if (rc[size_t(d)] == CDVZ_GPU_DATA) throw DataError(msg);
       throw std::runtime_error(msg);
     }
-  // Gather in frame order. In place, shard d's bytes move left (to the end of
-  // shard d-1's), so a forward memmove per shard is safe.
-  size_t written = 0;
-  offsets[0] = 0;
-  for (int d = 0; d < nd; ++d) {
-    const int n = start[size_t(d) + 1] - start[size_t(d)];
-    const size_t bytes = off[size_t(d)][size_t(n)];
-    const uint8_t* src = in_place ? out + size_t(start[size_t(d)]) * slot : scratch[size_t(d)].data();
-    if (!in_place && written + bytes > out_cap) {
-      // Frame-level overflow accounting, as the single-device path does it.
-      for (int i = 0; i < n; ++i) {
-        const size_t len = off[size_t(d)][size_t(i) + 1] - off[size_t(d)][size_t(i)];
-        const int fi = start[size_t(d)] + i;
-        if (status[fi] == CDVZ_GPU_OK) {
-          if (written + len > out_cap) {
-            status[fi] = CDVZ_GPU_USAGE;
-          } else {
-            std::memcpy(out + written, src + off[size_t(d)][size_t(i)], len);
-            written += len;
-          }
-        }
-        offsets[fi + 1] = written;
-      }
-      continue;
-    }
-    if (bytes && out + written != src) std::memmove(out + written, src, bytes);
-    for (int i = 0; i < n; ++i) offsets[start[size_t(d)] + i + 1] = written + off[size_t(d)][size_t(i) + 1];
-    written += bytes;
-  }
-  cdvz_gpu_ctx::Stats sum;
-  int launches = 0;
-  for (auto& sh : ctx->shards) {
-    for (int i = 0; i < 5; ++i) sum.stage_ms[i] += sh->stats.stage_ms[i];
-    sum.pyr_ms += sh->stats.pyr_ms;
-    sum.pyr_bytes += sh->stats.pyr_bytes;
-    launches += sh->launches;
-  }
-  ctx->stats = sum;
-  ctx->launches = launches;
+  gather_multi(start, off, in_place, scratch, out, out_cap, offsets, status, slot);
+  fold_multi_stats(ctx);
 }
 
 // Host-frame batch encode of grey (kind 1) or RGB (kind 3) byte rasters, or
@@ -1455,6 +1483,27 @@ void finish_slot(cdvz_gpu_ctx* ctx, cdvz_gpu_ctx::HostSlot& hs) {
 }
 }  // namespace
 
+// Waits for every shard of the multi-device call multi_calls[i], gathers its
+// containers in frame order and drops the record; the call's return code.
+static int finish_multi(cdvz_gpu_ctx* ctx, size_t i, std::string& err) {
+  cdvz_gpu_ctx::MultiCall mc = std::move(ctx->multi_calls[i]);
+  ctx->multi_calls.erase(ctx->multi_calls.begin() + long(i));
+  int rc = CDVZ_GPU_OK;
+  for (size_t d = 0; d < mc.shard_ticket.size(); ++d) {
+    cdvz_gpu_ctx* sh = ctx->shards[d].get();
+    const int r = cdvz_gpu_encode_batch_wait(sh, mc.shard_ticket[d]);
+    if (r != CDVZ_GPU_OK && rc == CDVZ_GPU_OK) {
+      rc = r;
+      err = "device " + std::to_string(sh->device) + ": " + sh->err;
+    }
+  }
+  if (rc != CDVZ_GPU_OK) return rc;
+  return guarded(ctx, [&] {
+    gather_multi(mc.start, mc.off, true, {}, mc.out, mc.out_cap, mc.offsets, mc.status, mc.slot);
+    fold_multi_stats(ctx);
+  });
+}
+
 int cdvz_gpu_encode_batch_submit(cdvz_gpu_ctx* ctx, const uint8_t* pixels, int width, int height, size_t stride,
                                  int count, int mode_id, int max_side, uint8_t* out, size_t out_cap, size_t* offsets,
                                  int* status, uint64_t* ticket) {
@@ -1465,7 +1514,51 @@ int cdvz_gpu_encode_batch_submit(cdvz_gpu_ctx* ctx, const uint8_t* pixels, int w
     if (!host_args(ctx, pixels, width, height, stride, count, offsets, status, 1)) return;
     mode_by_id(mode_id);
     const bool one_group = size_t(count) <= size_t(host_group_frames(size_t(width) * height, count));
-    if (!ctx->shards.empty() || !one_group) {  // multi-device, or > 4 GB of frames: synchronous
+    const size_t slot_bytes = mode_by_id(mode_id).budget + 28;
+    if (!ctx->shards.empty() && out_cap >= size_t(count) * slot_bytes) {
+      // Multi-device: each shard's share through the shard's own submit (its
+      // copies and kernels enqueued, nothing waited for); the wait gathers.
+      while (ctx->multi_calls.size() >= 2) {  // two calls in flight: finish the oldest now
+        const unsigned long long t = ctx->multi_calls.front().ticket;
+        std::string err;
+        const int rc = finish_multi(ctx, 0, err);
+        ctx->finished.push_back({t, rc, err});
+      }
+      const int nd = int(ctx->shards.size());
+      cdvz_gpu_ctx::MultiCall mc;
+      mc.start.resize(size_t(nd) + 1);
+      for (int d = 0; d <= nd; ++d) mc.start[size_t(d)] = int((long long)count * d / nd);
+      mc.off.resize(size_t(nd));
+      mc.shard_ticket.assign(size_t(nd), 0);
+      mc.out = out;
+      mc.out_cap = out_cap;
+      mc.offsets = offsets;
+      mc.status = status;
+      mc.slot = slot_bytes;
+      for (int d = 0; d < nd; ++d) {
+        const int n = mc.start[size_t(d) + 1] - mc.start[size_t(d)];
+        mc.off[size_t(d)].assign(size_t(n) + 1, 0);
+        if (n == 0) continue;
+        cdvz_gpu_ctx* sh = ctx->shards[size_t(d)].get();
+        const int rc = cdvz_gpu_encode_batch_submit(sh, pixels + size_t(mc.start[size_t(d)]) * height * stride, width,
+                                                    height, stride, n, mode_id, max_side,
+                                                    out + size_t(mc.start[size_t(d)]) * slot_bytes, size_t(n) * slot_bytes,
+                                                    mc.off[size_t(d)].data(), status + mc.start[size_t(d)],
+                                                    &mc.shard_ticket[size_t(d)]);
+        if (rc != CDVZ_GPU_OK) {
+          const std::string msg = "device " + std::to_string(sh->device) + ": " + sh->err;
+          for (int e = 0; e < d; ++e) cdvz_gpu_encode_batch_wait(ctx->shards[size_t(e)].get(), mc.shard_ticket[size_t(e)]);
+          if (rc == CDVZ_GPU_USAGE) throw UsageError(msg);
+          if (rc == CDVZ_GPU_DATA) throw DataError(msg);
+          throw std::runtime_error(msg);
+        }
+      }
+      mc.ticket = ctx->next_ticket++;
+      *ticket = mc.ticket;
+      ctx->multi_calls.push_back(std::move(mc));
+      return;
+    }
+    if (!ctx->shards.empty() || !one_group) {  // multi-device without room in place, or > 4 GB of frames: synchronous
       for (auto& h : ctx->hslot)
         if (h.busy) finish_slot(ctx, h);
       if (encode_host_batch(ctx, pixels, width, height, stride, count, mode_id, max_side, out, out_cap, offsets, status,
@@ -1499,6 +1592,13 @@ int cdvz_gpu_encode_batch_submit(cdvz_gpu_ctx* ctx, const uint8_t* pixels, int w
 int cdvz_gpu_encode_batch_wait(cdvz_gpu_ctx* ctx, uint64_t ticket) {
   if (!ctx) return guarded(ctx, [] { throw UsageError("null context"); });
   if (ticket == 0) return CDVZ_GPU_OK;
+  for (size_t i = 0; i < ctx->multi_calls.size(); ++i) {
+    if (ctx->multi_calls[i].ticket != ticket) continue;
+    std::string err;
+    const int rc = finish_multi(ctx, i, err);
+    if (rc != CDVZ_GPU_OK) ctx->err = err;
+    return rc;
+  }
   for (auto& h : ctx->hslot)
     if (h.busy && h.ticket == ticket) finish_slot(ctx, h);
   for (size_t i = 0; i < ctx->finished.size(); ++i) {

@@ -163,6 +163,27 @@ def test_cpp_reference_signature_struct_out(tmp_path, bundle_b8):
     assert "stage detection" in txt.read_text()
 
 
+def test_multi_device_submit_wait_streams_batches(bundle_b8):
+    """A multi-device context (two shards here, on one GPU) streams batches
+    too: submit enqueues every shard's share and returns, wait gathers in
+    frame order; a third submit completes the oldest; results equal a
+    single-device context's and the oracle's."""
+    single = cg.Extractor(bundle_b8, max_batch=16)
+    multi = cg.Extractor(bundle_b8, max_batch=16, devices=[0, 0])
+    batches = [oracle_lib.synth_frames(6000 + 100 * k, 7, 320, 240) for k in range(3)]
+    pend = [multi.encode_batch_submit(b, "4K") for b in batches]
+    assert all(p.ticket != 0 for p in pend)
+    got = {2: pend[2].wait(), 0: pend[0].wait(), 1: pend[1].wait()}
+    for k, b in enumerate(batches):
+        want, st = single.encode_batch(b, "4K")
+        assert got[k][0] == want and got[k][1].tolist() == [0] * 7
+    assert got[0][0][0] == oracle_lib.encode(bundle_b8, batches[0][0], 3)
+    with pytest.raises(cg.UsageError):
+        multi._check(multi._lib.cdvz_gpu_encode_batch_wait(multi._ctx, pend[1].ticket))
+    multi.close()
+    single.close()
+
+
 def test_submit_wait_streams_batches(bundle_b8):
     """cdvz_gpu_encode_batch_submit / _wait: three batches submitted before
     any wait (the third submit completes the first), waited out of order —
