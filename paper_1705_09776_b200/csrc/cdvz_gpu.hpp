@@ -460,6 +460,67 @@ inline std::vector<std::vector<uint8_t>> encode_batch(const std::vector<const Gr
 }
 
 // encode_image + serialize_container (pipeline.cpp:54-97, container.cpp:32-58).
+// A stream of batches (a video feed, a crawl) through
+// cdvz_gpu_encode_batch_submit / _wait: submit packs the frames, enqueues the
+// copies and kernels and returns; wait() hands back the containers. Two
+// batches in flight per context overlap one batch's copies and kernels with
+// the previous one's tail. No reference counterpart (the reference encodes
+// one image per call); the containers equal encode_batch's.
+class PendingBatch {
+ public:
+  std::vector<std::vector<uint8_t>> wait() {
+    if (!ctx_) throw UsageError("batch already waited for");
+    cdvz_gpu_ctx* ctx = ctx_;
+    ctx_ = nullptr;
+    check(cdvz_gpu_encode_batch_wait(ctx, ticket_), ctx);
+    std::vector<std::vector<uint8_t>> out(status_.size());
+    for (std::size_t i = 0; i < status_.size(); ++i) {
+      raise_for(status_[i], "frame failed on the device");
+      out[i].assign(buf_.begin() + long(offsets_[i]), buf_.begin() + long(offsets_[i + 1]));
+    }
+    return out;
+  }
+  ~PendingBatch() {
+    if (ctx_) cdvz_gpu_encode_batch_wait(ctx_, ticket_);  // buffers must outlive the device work
+  }
+  PendingBatch(const PendingBatch&) = delete;
+  PendingBatch& operator=(const PendingBatch&) = delete;
+
+ private:
+  friend std::unique_ptr<PendingBatch> submit_batch(const std::vector<const GrayImage8*>&, const ModelBundle&,
+                                                    const ModeSpec&, const EncodeOptions&, const std::vector<int>&);
+  PendingBatch() = default;
+  cdvz_gpu_ctx* ctx_ = nullptr;
+  std::uint64_t ticket_ = 0;
+  std::vector<uint8_t> pix_, buf_;
+  std::vector<std::size_t> offsets_;
+  std::vector<int> status_;
+};
+
+inline std::unique_ptr<PendingBatch> submit_batch(const std::vector<const GrayImage8*>& frames,
+                                                  const ModelBundle& bundle, const ModeSpec& mode,
+                                                  const EncodeOptions& opts = {},
+                                                  const std::vector<int>& devices = {0}) {
+  std::unique_ptr<PendingBatch> p(new PendingBatch());
+  if (frames.empty()) throw UsageError("empty batch");
+  const int w = frames[0]->width, h = frames[0]->height;
+  p->pix_.resize(std::size_t(w) * h * frames.size());
+  for (std::size_t i = 0; i < frames.size(); ++i) {
+    if (frames[i]->width != w || frames[i]->height != h) throw UsageError("frames of one batch must share a size");
+    std::copy(frames[i]->pix.begin(), frames[i]->pix.end(), p->pix_.begin() + long(i) * w * h);
+  }
+  cdvz_gpu_ctx* ctx = bundle.context(devices);
+  p->buf_.resize(cdvz_gpu_container_slot(mode.id) * frames.size());
+  p->offsets_.resize(frames.size() + 1);
+  p->status_.resize(frames.size());
+  check(cdvz_gpu_encode_batch_submit(ctx, p->pix_.data(), w, h, std::size_t(w), int(frames.size()), mode.id,
+                                     opts.max_side, p->buf_.data(), p->buf_.size(), p->offsets_.data(),
+                                     p->status_.data(), &p->ticket_),
+        ctx);
+  p->ctx_ = ctx;
+  return p;
+}
+
 inline std::vector<uint8_t> encode_image(const GrayImage8& img, const ModelBundle& bundle, const ModeSpec& mode,
                                          StageTimings* timings = nullptr, const EncodeOptions& opts = {}) {
   return encode_batch({&img}, bundle, mode, timings, opts)[0];

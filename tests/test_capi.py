@@ -117,3 +117,16 @@ def test_cpp_train_shim_compiles_and_checks_the_corpus(tmp_path):
         (corpus / f"{i}.pgm").write_bytes(b"P5\n16 16\n255\n" + bytes(256))
     p = subprocess.run([str(exe), str(corpus), "b.txt"], capture_output=True, text=True)
     assert p.returncode == 2 and "at least 20" in p.stderr
+
+
+def test_cpp_stream_shim_compiles(tmp_path):
+    """examples/stream.cpp (the shim's submit_batch / PendingBatch) builds;
+    without arguments it is a usage error."""
+    import subprocess
+
+    exe = tmp_path / "stream"
+    lib_dir = os.path.dirname(cg.library_path())
+    subprocess.run(["g++", "-std=c++17", "-O1", os.path.join(ROOT, "examples", "stream.cpp"), f"-L{lib_dir}",
+                    "-lcdvz_gpu", f"-Wl,-rpath,{lib_dir}", "-o", str(exe)], check=True)
+    p = subprocess.run([str(exe)], capture_output=True, text=True)
+    assert p.returncode == 1 and "usage" in p.stderr

@@ -200,3 +200,34 @@ def test_submit_wait_streams_batches(bundle_b8):
     with pytest.raises(cg.UsageError):
         pend[0].ex._check(pend[0].ex._lib.cdvz_gpu_encode_batch_wait(ex._ctx, pend[0].ticket))
     ex.close()
+
+
+def test_cpp_stream_example_matches_encode_batch(bundle_b8, tmp_path):
+    """examples/stream.cpp streams a raw frame file through the shim's
+    submit_batch / PendingBatch::wait (batch k + 1 submitted before batch k
+    is waited for); its containers equal encode_batch's."""
+    import os
+    import struct
+    import subprocess
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    frames = oracle_lib.synth_frames(4200, 10, 320, 240)
+    (tmp_path / "frames.u8").write_bytes(frames.tobytes())
+    (tmp_path / "bundle.txt").write_text(bundle_b8)
+    exe = tmp_path / "stream"
+    lib_dir = os.path.dirname(cg.library_path())
+    subprocess.run(["g++", "-std=c++17", "-O1", os.path.join(root, "examples", "stream.cpp"), f"-L{lib_dir}",
+                    "-lcdvz_gpu", f"-Wl,-rpath,{lib_dir}", "-o", str(exe)], check=True)
+    out = tmp_path / "out.bin"
+    p = subprocess.run([str(exe), str(tmp_path / "bundle.txt"), "4K", "320", "240", str(tmp_path / "frames.u8"), "4",
+                        str(out)], capture_output=True, text=True)
+    assert p.returncode == 0, p.stderr
+    blob, got = out.read_bytes(), []
+    while blob:
+        (n,) = struct.unpack("<I", blob[:4])
+        got.append(blob[4:4 + n])
+        blob = blob[4 + n:]
+    ex = cg.Extractor(bundle_b8, max_batch=16)
+    want, st = ex.encode_batch(frames, "4K")
+    ex.close()
+    assert got == want
