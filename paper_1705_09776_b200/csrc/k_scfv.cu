@@ -375,13 +375,14 @@ __global__ void __launch_bounds__(256, 2) k_posterior(Batch bt, Model md) {
 
 // posteriors_matrix + softmax_rows for small mixtures (nc <= 32, e.g. the
 // 8-component bundles): the 64-component tiles of k_posterior would be mostly
-// padding. Thread (t, i) of a CTA forms logp of row t and component i with
-// exactly k_posterior's arithmetic (sums over j ascending, separately
-// rounded); the CTA's first warp then runs the row softmax (peak, exp, the
-// packet-order sum of eigen_sum, division) one row per lane.
-constexpr int kSmallRows = 32;
-__global__ void __launch_bounds__(1024) k_posterior_small(Batch bt, Model md) {
-  __shared__ double xs[kSmallRows][33];
+// padding. Thread per row: the row's 32 coordinates stay in registers, the
+// mixture's 1/sigma^2 and mu/sigma^2 rows are shared-memory broadcasts, and
+// logp of every component is formed with exactly k_posterior's arithmetic
+// (sums over j ascending, separately rounded); the same thread then runs the
+// row softmax (peak, exp, the packet-order sum of eigen_sum, division).
+constexpr int kSmallRows = 64;
+__global__ void __launch_bounds__(kSmallRows) k_posterior_small(Batch bt, Model md) {
+  __shared__ double iv[32][32], mv[32][32];  // [component][j]
   __shared__ double lp[kSmallRows][33];
   __shared__ double cst[32], lnorm[32];
   const int f = blockIdx.y;
@@ -389,12 +390,10 @@ __global__ void __launch_bounds__(1024) k_posterior_small(Batch bt, Model md) {
   const int nc = md.nc;
   const int row0 = blockIdx.x * kSmallRows;
   if (row0 >= n) return;
-  const int rows = min(kSmallRows, n - row0);
   const int tid = threadIdx.x;
-  const double* X = bt.x + ((long long)f * bt.cap_or + row0) * 32;
-  for (int q = tid; q < kSmallRows * 32; q += blockDim.x) {
-    const int t = q >> 5, j = q & 31;
-    xs[t][j] = t < rows ? X[t * 32 + j] : 0.0;
+  for (int q = tid; q < nc * 32; q += kSmallRows) {
+    iv[q >> 5][q & 31] = md.inv_var[q];
+    mv[q >> 5][q & 31] = md.m_over_v[q];
   }
   if (tid < nc) {
     const double* m2 = md.m2_over_v + tid * 32;
@@ -404,32 +403,34 @@ __global__ void __launch_bounds__(1024) k_posterior_small(Batch bt, Model md) {
     lnorm[tid] = md.log_norm[tid];
   }
   __syncthreads();
-  {
-    const int t = tid / nc, i = tid - t * nc;
-    if (t < rows) {
-      const double* iv = md.inv_var + i * 32;
-      const double* mv = md.m_over_v + i * 32;
-      double a = (xs[t][0] * xs[t][0]) * iv[0];
-      double b = xs[t][0] * mv[0];
-      for (int j = 1; j < 32; ++j) {
-        const double x = xs[t][j];
-        a = a + (x * x) * iv[j];
-        b = b + x * mv[j];
-      }
-      const double p = a - 2.0 * b + cst[i];
-      lp[t][i] = -0.5 * p + lnorm[i];
+  const int t = row0 + tid;
+  if (t >= n) return;
+  double x[32];
+  const double2* X = reinterpret_cast<const double2*>(bt.x + ((long long)f * bt.cap_or + t) * 32);
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const double2 v = X[j];
+    x[2 * j] = v.x;
+    x[2 * j + 1] = v.y;
+  }
+  double* e = lp[tid];
+  for (int i = 0; i < nc; ++i) {
+    double a = (x[0] * x[0]) * iv[i][0];
+    double b = x[0] * mv[i][0];
+#pragma unroll
+    for (int j = 1; j < 32; ++j) {
+      a = a + (x[j] * x[j]) * iv[i][j];
+      b = b + x[j] * mv[i][j];
     }
+    const double p = a - 2.0 * b + cst[i];
+    e[i] = -0.5 * p + lnorm[i];
   }
-  __syncthreads();
-  if (tid < rows) {
-    double* e = lp[tid];
-    double pk = e[0];
-    for (int i = 1; i < nc; ++i) pk = fmax(pk, e[i]);
-    for (int i = 0; i < nc; ++i) e[i] = dm::exp(e[i] - pk);
-    const double tot = packet_sum_seq(e, nc);
-    double* gam = bt.gamma + ((long long)f * bt.cap_or + row0 + tid) * nc;
-    for (int i = 0; i < nc; ++i) gam[i] = e[i] / tot;
-  }
+  double pk = e[0];
+  for (int i = 1; i < nc; ++i) pk = fmax(pk, e[i]);
+  for (int i = 0; i < nc; ++i) e[i] = dm::exp(e[i] - pk);
+  const double tot = packet_sum_seq(e, nc);
+  double* gam = bt.gamma + ((long long)f * bt.cap_or + t) * nc;
+  for (int i = 0; i < nc; ++i) gam[i] = e[i] / tot;
 }
 
 // fv_mean_matrix / fv_var_matrix (scfv.cpp:166-203). gamma^T X (and
@@ -716,7 +717,7 @@ cudaError_t launch_scfv_pack(const Batch& bt, const Model& md, const EncodeConst
   if (e != cudaSuccess) return e;
   const dim3 pgrid((bt.cap_or + kPM - 1) / kPM, bt.nframes);
   if (md.nc <= 32)
-    k_posterior_small<<<dim3((bt.cap_or + kSmallRows - 1) / kSmallRows, bt.nframes), kSmallRows * md.nc, 0, st>>>(bt, md);
+    k_posterior_small<<<dim3((bt.cap_or + kSmallRows - 1) / kSmallRows, bt.nframes), kSmallRows, 0, st>>>(bt, md);
   else if (ec.post_dmma)  // the FP64 tensor cores
     k_posterior<true><<<pgrid, 256, sizeof(PostSmem), st>>>(bt, md);
   else
