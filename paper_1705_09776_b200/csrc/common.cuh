@@ -93,6 +93,7 @@ struct Batch {
   Oriented* oriented;                  // [frame][cap_or]
   int* or_count;                       // [frame]
   DescGeo* geo;                        // [frame][cap_or]
+  int* order;                          // [frame][cap_or]: oriented points by descending samples per axis (k_order)
   int smp_cap;                         // samples per oriented point (max samples^2)
   double2* smp;                        // [frame][cap_or][smp_cap] {weight (+0: skipped), fo}, row stride samples
   uint8_t* smpb;                       // [frame][cap_or][32][32] orientation bin ob0 mod 8 of each sample

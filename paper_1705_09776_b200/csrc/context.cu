@@ -491,6 +491,7 @@ struct cdvz_gpu_ctx {
     nb.oriented = static_cast<Oriented*>(alloc(sizeof(Oriented) * F * nb.cap_or));
     nb.or_count = static_cast<int*>(alloc(sizeof(int) * F));
     nb.geo = static_cast<DescGeo*>(alloc(sizeof(DescGeo) * F * nb.cap_or));
+    nb.order = static_cast<int*>(alloc(sizeof(int) * F * nb.cap_or));
     {
       // samples per axis = ceil(12 sigma) with sigma <= sigma_3 (roots are
       // clamped to [sigma_0, sigma_3]); larger patches are flagged per frame.
@@ -847,7 +848,7 @@ struct cdvz_gpu_ctx {
       // The next chunk on this lane's stream A must not overwrite the pyramid
       // before stream B is done with it.
       CDVZ_CUDA_CHECK(cudaStreamWaitEvent(L.sA, L.done, 0));
-      launches += 1 + 5 + 1 + 5;  // k_select; k_orient, k_expand, k_geometry, k_sample, k_describe; k_compress; SCFV + pack
+      launches += 1 + 6 + 1 + 5;  // k_select; k_orient, k_expand, k_geometry, k_order, k_sample, k_describe; k_compress; SCFV + pack
       L.pending = true;
       L.pending_call = call;
       L.pending_oct = b.n_oct;

@@ -373,6 +373,33 @@ __global__ void __launch_bounds__(128) k_geometry(Batch bt, DetConst dc) {
   bt.geo[(long long)f * bt.cap_or + idx] = g;
 }
 
+// Groups of four points share a warp in k_describe_cells, which walks as
+// many rows as the group's largest point has; ordering the points by
+// descending samples per axis (17 .. 32 in the supported scale range) keeps
+// each group's sizes alike. Counting sort, CTA per frame; the descriptors
+// still land in each point's own slot, so the order is invisible downstream.
+__global__ void __launch_bounds__(256) k_order(Batch bt) {
+  __shared__ int cnt[33], off[33];
+  const int f = blockIdx.x;
+  const int n = bt.or_count[f];
+  const DescGeo* geo = bt.geo + (long long)f * bt.cap_or;
+  int* order = bt.order + (long long)f * bt.cap_or;
+  for (int b = threadIdx.x; b < 33; b += blockDim.x) cnt[b] = 0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) atomicAdd(&cnt[kMaxSamples - min(geo[i].samples, kMaxSamples)], 1);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int o = 0;
+    for (int b = 0; b < 33; ++b) {
+      off[b] = o;
+      o += cnt[b];
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x)
+    order[atomicAdd(&off[kMaxSamples - min(geo[i].samples, kMaxSamples)], 1)] = i;
+}
+
 // The Gaussian weight exp(-(u*u + v*v) / denom) of sample (i, j) equals that
 // of (j, i) bit for bit (u_i == v_i, and the sum commutes), so each CTA first
 // tabulates the samples*(samples+1)/2 distinct values of its point in shared
@@ -728,9 +755,9 @@ __global__ void __launch_bounds__(32 * kPBWarps, 8) k_describe_cells(Batch bt) {
   const int cx = hl & 3, dv = hl >> 2;
   const unsigned gmask = 0xffu << (kPBLanes * q);
   for (int grp = blockIdx.x * kPBWarps + wi; kPBPts * grp < n_or; grp += gridDim.x * kPBWarps) {
-    const int idx = kPBPts * grp + q;
-    const bool live = idx < n_or;
-    const long long gslot = (long long)f * bt.cap_or + (live ? idx : 0);
+    const bool live = kPBPts * grp + q < n_or;
+    const int idx = live ? bt.order[(long long)f * bt.cap_or + kPBPts * grp + q] : 0;
+    const long long gslot = (long long)f * bt.cap_or + idx;
     const DescGeo g = bt.geo[gslot];
     const int samples = live ? g.samples : 0;  // 0: no point, or flagged by k_geometry
     const double2* smp = bt.smp + gslot * bt.smp_cap;
@@ -993,6 +1020,9 @@ cudaError_t launch_describe(const Batch& bt, const DetConst& dc, cudaStream_t st
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   k_geometry<<<dim3((bt.cap_or + 127) / 128, bt.nframes), 128, 0, st>>>(bt, dc);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  k_order<<<bt.nframes, 256, 0, st>>>(bt);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   k_sample<<<dim3(256, bt.nframes), kSampleThreads, 0, st>>>(bt);
