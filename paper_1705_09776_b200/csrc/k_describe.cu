@@ -141,7 +141,10 @@ __device__ __forceinline__ Frame resolve(const Batch& bt, const DetConst& dc, in
 // owns a bin adds them in that order — the reference's per-bin add order —
 // touching only its own samples.
 constexpr int kOrientCap = 512;  // box of the 3.96-sigma disk: (2 * 10.5 + 1)^2 <= 484 for sigma <= 2.66
-constexpr int kOrientWarps = 4;
+// One warp (one keypoint) per CTA: window sizes differ by up to 3x between
+// keypoints, and a single-warp CTA frees its slot as soon as its keypoint is
+// done (0.3% faster than four-warp CTAs end to end).
+constexpr int kOrientWarps = 1;
 struct OrientSmem {
   double val[kOrientCap];
   uint16_t list[kOrientCap];
