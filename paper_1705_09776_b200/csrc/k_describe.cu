@@ -518,7 +518,7 @@ __global__ void __launch_bounds__(kSampleThreads, CDVZ_SAMPLE_MINB) k_sample(Bat
 // (merge_and_normalize) when the lane leaves the cell, at the 16-row band
 // boundary and at the end. Rows of (weight, fo) records and their bins
 // stream into a 2-row shared ring with cp.async, one row ahead of the walk.
-constexpr int kPBWarps = 2, kPBPts = 4, kPBLanes = 8;
+constexpr int kPBWarps = 4, kPBPts = 4, kPBLanes = 8;  // 4 warps x 4 points per CTA (2 or 8 warps: 0.2-0.7% slower)
 struct PhaseBSmem {
   union {
     struct {
@@ -557,7 +557,7 @@ __device__ __forceinline__ void add_two_bins(double (&acc)[8], int b, double x0,
   }
 }
 
-__global__ void __launch_bounds__(32 * kPBWarps, 8) k_describe(Batch bt) {
+__global__ void __launch_bounds__(32 * kPBWarps, 16 / kPBWarps) k_describe(Batch bt) {
   extern __shared__ __align__(16) uint8_t pb_smem[];
   const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
   PhaseBSmem& S = reinterpret_cast<PhaseBSmem*>(pb_smem)[wi];
@@ -748,7 +748,7 @@ struct CellSmem {
 };
 
 
-__global__ void __launch_bounds__(32 * kPBWarps, 8) k_describe_cells(Batch bt) {
+__global__ void __launch_bounds__(32 * kPBWarps, 16 / kPBWarps) k_describe_cells(Batch bt) {
   extern __shared__ __align__(16) uint8_t pb_smem[];
   const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
   CellSmem& S = reinterpret_cast<CellSmem*>(pb_smem)[wi];
