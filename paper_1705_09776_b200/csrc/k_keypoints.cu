@@ -16,6 +16,7 @@
 // relevance.cpp:71-93) with an exact MSB-first radix select on the 5-field
 // key, then a bitonic sort of the winners.
 #include <algorithm>
+#include <cstddef>
 
 #include "common.cuh"
 
@@ -123,16 +124,39 @@ __global__ void __launch_bounds__(kMergeThreads) k_merge_octave(Batch bt, int o)
 
   const int src = (o + 1) & 1, dst = o & 1;  // acc ping-pong: octave o writes acc[o & 1]
   KP* out_sorted = (o == 0) ? bt.acc[dst] + (long long)f * bt.cap_acc : bt.cur + (long long)f * bt.cap_acc;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    const KP k = raw[i];
-    const uint32_t word = k.key >> 5, bit = k.key & 31u;
-    const int rank = prefix[word] + __popc(bm[word] & ((1u << bit) - 1u));
-    out_sorted[rank] = k;
+  if (n <= bt.cap_acc) {
+    // Ranks from the keys alone, then the 64-byte records move in 16-byte
+    // pieces by consecutive threads (coalesced stores; each record's four
+    // pieces are one contiguous read).
+    int* src_of = bt.scratch_idx + (long long)f * bt.cap_acc;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const uint32_t key = raw[i].key;
+      const uint32_t word = key >> 5, bit = key & 31u;
+      src_of[prefix[word] + __popc(bm[word] & ((1u << bit) - 1u))] = i;
+    }
+    __syncthreads();
+    // Every rank is known, so the bitmap can be cleared for the next batch on
+    // the way: only the words holding a survivor's bit are non-zero, and
+    // each record's last piece carries its key (one store per survivor).
+    static_assert(offsetof(KP, key) == 60, "KP key in the last 4 bytes");
+    const uint4* s4 = reinterpret_cast<const uint4*>(raw);
+    uint4* d4 = reinterpret_cast<uint4*>(out_sorted);
+    for (int c = threadIdx.x; c < 4 * n; c += blockDim.x) {
+      const uint4 v = s4[4 * src_of[c >> 2] + (c & 3)];
+      d4[c] = v;
+      if ((c & 3) == 3) bm[v.w >> 5] = 0u;
+    }
+  } else {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const KP k = raw[i];
+      const uint32_t word = k.key >> 5, bit = k.key & 31u;
+      const int rank = prefix[word] + __popc(bm[word] & ((1u << bit) - 1u));
+      out_sorted[rank] = k;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += blockDim.x) bm[raw[i].key >> 5] = 0u;  // ready for the next batch
   }
   __syncthreads();
-  // Ready for the next batch: only the words holding a survivor's bit are
-  // non-zero, so clearing those (one store per survivor) clears the bitmap.
-  for (int i = threadIdx.x; i < n; i += blockDim.x) bm[raw[i].key >> 5] = 0u;
   if (threadIdx.x == 0) {
     bt.raw_count[f * bt.n_oct + o] = 0;
     bt.oct_count[f * bt.n_oct + o] = n;
