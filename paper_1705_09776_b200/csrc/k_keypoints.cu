@@ -460,13 +460,19 @@ __global__ void __launch_bounds__(kMergeThreads) k_select(Batch bt, Model md, En
     atomicAdd(&rnk[i], r);
   }
   __syncthreads();
+  // Sorted source list, then the records move as coalesced 16-byte pieces.
+  int* src = rnk + bt.select_n;  // a second int array after the ranks
+  for (int i = threadIdx.x; i < got; i += blockDim.x) src[rnk[i]] = win[i];
+  __syncthreads();
   KP* sel = bt.sel + (long long)f * bt.select_n;
-  for (int i = threadIdx.x; i < got; i += blockDim.x) sel[rnk[i]] = acc[win[i]];
+  const uint4* s4 = reinterpret_cast<const uint4*>(acc);
+  uint4* d4 = reinterpret_cast<uint4*>(sel);
+  for (int c = threadIdx.x; c < 4 * got; c += blockDim.x) d4[c] = s4[4 * src[c >> 2] + (c & 3)];
   if (threadIdx.x == 0) bt.sel_count[f] = got;
 }
 
 size_t select_smem_bytes(const Batch& bt) {
-  return select_key_offset(bt.select_n) + size_t(bt.select_n) * (sizeof(SelKey) + sizeof(int));
+  return select_key_offset(bt.select_n) + size_t(bt.select_n) * (sizeof(SelKey) + 2 * sizeof(int));
 }
 
 
