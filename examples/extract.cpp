@@ -10,16 +10,22 @@
 #include "../paper_1705_09776_b200/csrc/cdvz_gpu.hpp"
 
 int main(int argc, char** argv) {
-  if (argc != 5) {
-    std::fprintf(stderr, "usage: extract <bundle> <mode> <in.pgm|in.ppm> <out.cdvz>\n");
+  if (argc != 5 && argc != 6) {
+    std::fprintf(stderr, "usage: extract <bundle> <mode> <in.pgm|in.ppm> <out.cdvz> [timings.csv]\n");
     return 1;
   }
   try {
     const auto bundle = cdvz::gpu::ModelBundle::load(argv[1]);
-    const auto& mode = cdvz::gpu::mode_by_name(argv[2]);
+    const cdvz::gpu::ModeSpec mode = cdvz::gpu::mode_by_name(argv[2]);
     const cdvz::gpu::PnmImage img = cdvz::gpu::load_pnm(argv[3]);
-    const auto bytes = cdvz::gpu::encode_image(img, bundle, mode);
+    cdvz::gpu::StageTimings timings;
+    const auto bytes = cdvz::gpu::encode_image(img, bundle, mode, argc == 6 ? &timings : nullptr);
     std::ofstream(argv[4], std::ios::binary).write(reinterpret_cast<const char*>(bytes.data()), std::streamsize(bytes.size()));
+    if (argc == 6) {  // the CLI's --timings (cdvz.cpp:52-56)
+      std::ofstream out(argv[5]);
+      if (!out) throw cdvz::gpu::DataError(std::string("cannot write timings: ") + argv[5]);
+      out << timings.to_csv();
+    }
     std::printf("%dx%d %s: %zu bytes\n", img.width, img.height, img.channels == 3 ? "PPM" : "PGM", bytes.size());
     return 0;
   } catch (const cdvz::gpu::UsageError& e) {

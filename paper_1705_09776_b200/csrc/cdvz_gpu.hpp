@@ -25,6 +25,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdio>
 #include <fstream>
 #include <iterator>
 #include <map>
@@ -304,6 +305,20 @@ class StageTimings {  // parallel.hpp:117-134: device ms per label
     for (const auto& e : entries_) s += e.total_ms;
     return s;
   }
+  // The reference's CSV (parallel.cpp:106-118): stage,calls,total_ms,percent.
+  std::string to_csv() const {
+    std::ostringstream out;
+    out << "stage,calls,total_ms,percent\n";
+    const double sum = total_ms();
+    for (const auto& e : entries_) {
+      char line[160];
+      std::snprintf(line, sizeof(line), "%s,%lld,%.3f,%.3f\n", e.stage.c_str(), e.calls, e.total_ms,
+                    sum > 0.0 ? 100.0 * e.total_ms / sum : 0.0);
+      out << line;
+    }
+    return out.str();
+  }
+  void clear() { entries_.clear(); }
  private:
   std::vector<Entry> entries_;
 };
@@ -560,7 +575,8 @@ inline GrayImage to_gray(const PnmImage& img) {
 
 // encode_image(load_image(path), ...) for an in-memory PGM/PPM raster.
 inline std::vector<uint8_t> encode_image(const PnmImage& img, const ModelBundle& bundle, const ModeSpec& mode,
-                                         const EncodeOptions& opts = {}, int device = 0) {
+                                         StageTimings* timings = nullptr, const EncodeOptions& opts = {},
+                                         int device = 0) {
   cdvz_gpu_ctx* ctx = bundle.context(device);
   std::vector<uint8_t> buf(cdvz_gpu_container_slot(mode.id));
   std::size_t offsets[2] = {0, 0};
@@ -571,6 +587,7 @@ inline std::vector<uint8_t> encode_image(const PnmImage& img, const ModelBundle&
                offsets, &status), ctx);
   raise_for(status, "frame failed on the device");
   buf.resize(offsets[1]);
+  add_timings(ctx, timings);
   return buf;
 }
 

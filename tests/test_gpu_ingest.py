@@ -77,3 +77,12 @@ def test_cpp_example_extracts_pgm_and_ppm_files(tmp_path, bundle_b8):
     bad.write_bytes(cases[1][0][:-10])
     r = subprocess.run([exe, str(bundle), "4K", str(bad), str(tmp_path / "x.cdvz")], capture_output=True)
     assert r.returncode == 2
+    # --timings: the reference's StageTimings CSV (stage,calls,total_ms,percent), five labels in order.
+    csv_path = tmp_path / "t.csv"
+    subprocess.run([exe, str(bundle), "4K", str(tmp_path / "in0.pnm"), str(tmp_path / "o.cdvz"), str(csv_path)],
+                   check=True, capture_output=True)
+    lines = csv_path.read_text().splitlines()
+    assert lines[0] == "stage,calls,total_ms,percent"
+    assert [ln.split(",")[0] for ln in lines[1:]] == ["detection", "selection", "description", "compression",
+                                                     "aggregation"]
+    assert abs(sum(float(ln.split(",")[3]) for ln in lines[1:]) - 100.0) < 0.03  # five values rounded to 0.001
