@@ -83,7 +83,6 @@ struct Batch {
   uint8_t* flags;                      // [frame][2*cap_acc]
   double* scratch_d;                   // [frame][cap_acc]
   int* status;                         // [frame] 0 ok, 3 internal (capacity)
-  int* negz;                           // [frame] f64 input holding -0.0 values (k_validate_f64; k_sample's exact-skip taps)
   // Selection / orientation / description.
   int select_n;
   KP* sel;                             // [frame][select_n]

@@ -38,7 +38,7 @@ cudaError_t launch_detect(const Batch& bt, const DetConst& dc, int o, const CUte
 cudaError_t launch_merge(const Batch& bt, int o, cudaStream_t st);
 int merge_cell_px(int W, int H);
 cudaError_t launch_select(const Batch& bt, const Model& md, const EncodeConst& ec, cudaStream_t st);
-cudaError_t launch_describe(const Batch& bt, const DetConst& dc, bool f64_input, cudaStream_t st);
+cudaError_t launch_describe(const Batch& bt, const DetConst& dc, cudaStream_t st);
 cudaError_t launch_compress(const Batch& bt, const Model& md, const EncodeConst& ec, cudaStream_t st);
 cudaError_t launch_scfv_pack(const Batch& bt, const Model& md, const EncodeConst& ec, uint8_t* out, uint32_t* lengths,
                              cudaStream_t st, cudaEvent_t after_aggregation);
@@ -46,7 +46,7 @@ cudaError_t launch_resize_f64(const double* grey, int w_in, int h_in, double* ou
                               cudaStream_t st);
 cudaError_t launch_grey_rgb(const uint8_t* rgb, long long stride, long long frame_bytes, int w, int h, double* out,
                             int frames, cudaStream_t st);
-cudaError_t launch_validate_f64(double* pix, int w, int h, int frames, int* status, int* negz, cudaStream_t st);
+cudaError_t launch_validate_f64(double* pix, int w, int h, int frames, int* status, cudaStream_t st);
 cudaError_t launch_resize(const uint8_t* pix, long long stride, long long frame_bytes, int w_in, int h_in, double* out,
                           int w_out, int h_out, int frames, cudaStream_t st);
 struct SynthParams {
@@ -484,7 +484,6 @@ struct cdvz_gpu_ctx {
     nb.flags = static_cast<uint8_t*>(alloc(F * 2 * nb.cap_acc));
     nb.scratch_d = static_cast<double*>(alloc(sizeof(double) * F * nb.cap_acc));
     nb.status = static_cast<int*>(alloc(sizeof(int) * F));
-    nb.negz = static_cast<int*>(alloc(sizeof(int) * F));
     nb.sel = static_cast<KP*>(alloc(sizeof(KP) * F * nb.select_n));
     nb.sel_count = static_cast<int*>(alloc(sizeof(int) * F));
     nb.thetas = static_cast<double*>(alloc(sizeof(double) * F * nb.select_n * 36));
@@ -771,10 +770,9 @@ struct cdvz_gpu_ctx {
       if (h_pix) CDVZ_CUDA_CHECK(cudaStreamWaitEvent(L.sA, copy_ev[size_t(c)], 0));
       CDVZ_CUDA_CHECK(cudaEventRecord(L.start, L.sA));
       CDVZ_CUDA_CHECK(cudaMemsetAsync(b.status, 0, sizeof(int) * nf, L.sA));
-      CDVZ_CUDA_CHECK(cudaMemsetAsync(b.negz, 0, sizeof(int) * nf, L.sA));
       if (f64) {  // validate (image.cpp:46-51), then resize_max_side on the caller's grey plane
         double* src = reinterpret_cast<double*>(const_cast<uint8_t*>(b.pix8));
-        CDVZ_CUDA_CHECK(launch_validate_f64(src, w, h, nf, b.status, b.negz, L.sA));
+        CDVZ_CUDA_CHECK(launch_validate_f64(src, w, h, nf, b.status, L.sA));
         launches += 2;
         if (resize) {
           CDVZ_CUDA_CHECK(launch_resize_f64(src, w, h, const_cast<double*>(b.pixf), W, H, nf, L.sA));
@@ -825,7 +823,7 @@ struct cdvz_gpu_ctx {
       CDVZ_CUDA_CHECK(cudaEventRecord(L.stage[1], sB));
       CDVZ_CUDA_CHECK(launch_select(b, md, ec, sB));
       CDVZ_CUDA_CHECK(cudaEventRecord(L.stage[2], sB));
-      CDVZ_CUDA_CHECK(launch_describe(b, dc, f64, sB));
+      CDVZ_CUDA_CHECK(launch_describe(b, dc, sB));
       CDVZ_CUDA_CHECK(cudaEventRecord(L.stage[3], sB));
       CDVZ_CUDA_CHECK(launch_compress(b, md, ec, sB));
       CDVZ_CUDA_CHECK(cudaEventRecord(L.stage[4], sB));
@@ -850,7 +848,7 @@ struct cdvz_gpu_ctx {
       // The next chunk on this lane's stream A must not overwrite the pyramid
       // before stream B is done with it.
       CDVZ_CUDA_CHECK(cudaStreamWaitEvent(L.sA, L.done, 0));
-      launches += 1 + 6 + (f64 ? 1 : 0) + 1 + 5;  // k_select; k_orient, k_expand, k_geometry, k_order, k_sample (x2 for f64 input), k_describe; k_compress; SCFV + pack
+      launches += 1 + 6 + 1 + 5;  // k_select; k_orient, k_expand, k_geometry, k_order, k_sample, k_describe; k_compress; SCFV + pack
       L.pending = true;
       L.pending_call = call;
       L.pending_oct = b.n_oct;

@@ -77,12 +77,10 @@ __device__ __forceinline__ BTexels btexels(const double* img, const BTap& t) {
           ldg_early(img + (t.off + t.dx + t.dy))};
 }
 // The reference skips a term whose fraction is 0 (descriptor.cpp:25-35).
-// Adding it instead is exact when no texel is -0.0: the term's product is
-// then +0 (every factor finite and non-negative, the fallback texel a real
-// one) and r, a product of non-negative factors, is never -0.0, so
-// r + (+0) == r. Pyramid values are blur sums of the input, so a -0.0 texel
-// needs -0.0 input pixels: only f64 input can hold them, and such frames
-// take bmix_skip below (Batch::negz, set by k_validate_f64).
+// Adding it instead is exact: its product is +0 (every factor is finite and
+// non-negative — fractions in [0, 1), pyramid values are Gaussian-blur sums
+// starting from +0.0, never -0.0 — and the fallback texel is a real one), and
+// r, itself a product of non-negative factors, is never -0.0, so r + (+0) == r.
 // Unconditional terms spare the compare and the two selects per term that
 // the skip costs after if-conversion.
 __device__ __forceinline__ double bmix(const BTap& t, const BTexels& v) {
@@ -90,15 +88,6 @@ __device__ __forceinline__ double bmix(const BTap& t, const BTexels& v) {
   r += (1.0 - t.fy) * t.fx * v.v01;
   r += t.fy * (1.0 - t.fx) * v.v10;
   r += t.fy * t.fx * v.v11;
-  return r;
-}
-// The reference's skips, for frames whose f64 input holds -0.0 (Batch::negz):
-// there a texel can be -0.0, r can be -0.0, and -0.0 + (+0) would be +0.
-__device__ __forceinline__ double bmix_skip(const BTap& t, const BTexels& v) {
-  double r = (1.0 - t.fy) * (1.0 - t.fx) * v.v00;
-  if (t.fx > 0.0) r += (1.0 - t.fy) * t.fx * v.v01;
-  if (t.fy > 0.0) r += t.fy * (1.0 - t.fx) * v.v10;
-  if (t.fx > 0.0 && t.fy > 0.0) r += t.fy * t.fx * v.v11;
   return r;
 }
 
@@ -439,7 +428,6 @@ __device__ __forceinline__ double div_two_pi(double a) {
 #ifndef CDVZ_SAMPLE_MINB
 #define CDVZ_SAMPLE_MINB 12
 #endif
-template <bool SKIP>
 __global__ void __launch_bounds__(kSampleThreads, CDVZ_SAMPLE_MINB) k_sample(Batch bt) {
   __shared__ double gexp[kMaxSamples * (kMaxSamples + 1) / 2];  // [j * (j + 1) / 2 + i], i <= j
   // Per-axis terms (u_i = v_i, the same expression): the reference's
@@ -447,9 +435,6 @@ __global__ void __launch_bounds__(kSampleThreads, CDVZ_SAMPLE_MINB) k_sample(Bat
   // order from per-column sums and per-row products.
   __shared__ double ax_px[kMaxSamples], ax_py[kMaxSamples], ax_vs[kMaxSamples], ax_vc[kMaxSamples];
   const int f = blockIdx.y;
-  // SKIP = true runs only the frames whose f64 input holds -0.0 (bmix_skip);
-  // SKIP = false all the others.
-  if ((bt.negz[f] != 0) != SKIP) return;
   const int n_or = bt.or_count[f];
   for (int idx = blockIdx.x; idx < n_or; idx += gridDim.x) {
     const long long slot = (long long)f * bt.cap_or + idx;
@@ -496,8 +481,8 @@ __global__ void __launch_bounds__(kSampleThreads, CDVZ_SAMPLE_MINB) k_sample(Bat
         const BTap tr = btap(g.w, px + 1.0, py), tl = btap(g.w, px - 1.0, py);
         const BTap tu = btap(g.w, px, py + 1.0), td = btap(g.w, px, py - 1.0);
         const BTexels vr = btexels(lvl, tr), vl = btexels(lvl, tl), vu = btexels(lvl, tu), vd = btexels(lvl, td);
-        const double gx = SKIP ? 0.5 * (bmix_skip(tr, vr) - bmix_skip(tl, vl)) : 0.5 * (bmix(tr, vr) - bmix(tl, vl));
-        const double gy = SKIP ? 0.5 * (bmix_skip(tu, vu) - bmix_skip(td, vd)) : 0.5 * (bmix(tu, vu) - bmix(td, vd));
+        const double gx = 0.5 * (bmix(tr, vr) - bmix(tl, vl));
+        const double gy = 0.5 * (bmix(tu, vu) - bmix(td, vd));
         const double mag = hypot(gx, gy);
         if (mag != 0.0) {
           const int lo = min(i, j), hi = max(i, j);
@@ -1030,7 +1015,7 @@ __global__ void __launch_bounds__(16 * kCompPts) k_compress(Batch bt, Model md, 
   }
 }
 
-cudaError_t launch_describe(const Batch& bt, const DetConst& dc, bool f64_input, cudaStream_t st) {
+cudaError_t launch_describe(const Batch& bt, const DetConst& dc, cudaStream_t st) {
   k_orient<<<dim3((bt.select_n + kOrientWarps - 1) / kOrientWarps, bt.nframes), 32 * kOrientWarps, 0, st>>>(bt, dc);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
@@ -1043,14 +1028,9 @@ cudaError_t launch_describe(const Batch& bt, const DetConst& dc, bool f64_input,
   k_order<<<bt.nframes, 256, 0, st>>>(bt);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  k_sample<false><<<dim3(256, bt.nframes), kSampleThreads, 0, st>>>(bt);
+  k_sample<<<dim3(256, bt.nframes), kSampleThreads, 0, st>>>(bt);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  if (f64_input) {  // frames whose f64 input may hold -0.0 (Batch::negz)
-    k_sample<true><<<dim3(256, bt.nframes), kSampleThreads, 0, st>>>(bt);
-    e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
-  }
   static size_t configured[kMaxDevices] = {};
   constexpr int smem = int(sizeof(PhaseBSmem)) * kPBWarps, csmem = int(sizeof(CellSmem)) * kPBWarps;
   e = once_per_device(configured, 1, [&] {

@@ -66,21 +66,15 @@ cudaError_t launch_resize_f64(const double* grey, int w_in, int h_in, double* ou
 // reference's DataError) and its raster is zeroed in the staging buffer, so
 // the rest of the pipeline runs on a harmless plane and k_pack emits nothing
 // for it. Grid (row blocks, frames); a second launch scrubs flagged frames.
-// validate() (image.cpp:46-51) per frame; also flags frames holding -0.0
-// (valid input: -0.0 >= 0.0), for which k_sample takes the reference's
-// skip-the-term bilinear path (a -0.0 texel is the one case where adding a
-// skipped +0 term would change a zero's sign).
-__global__ void k_validate_f64(const double* pix, long long frame_elems, long long n, int* status, int* negz) {
+__global__ void k_validate_f64(const double* pix, long long frame_elems, long long n, int* status) {
   const int f = blockIdx.y;
   const double* p = pix + f * frame_elems;
-  int bad = 0, nz = 0;
+  int bad = 0;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
     const double v = p[i];
     bad |= !(v >= 0.0 && v <= 1.0);  // NaN fails both comparisons; +-inf fails one
-    nz |= v == 0.0 && signbit(v);
   }
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&status[f], 2);
-  if (__syncthreads_or(nz) && threadIdx.x == 0) atomicOr(&negz[f], 1);
 }
 
 __global__ void k_scrub_f64(double* pix, long long frame_elems, long long n, const int* status) {
@@ -91,10 +85,10 @@ __global__ void k_scrub_f64(double* pix, long long frame_elems, long long n, con
     p[i] = 0.0;
 }
 
-cudaError_t launch_validate_f64(double* pix, int w, int h, int frames, int* status, int* negz, cudaStream_t st) {
+cudaError_t launch_validate_f64(double* pix, int w, int h, int frames, int* status, cudaStream_t st) {
   const long long n = (long long)w * h;
   const dim3 grid(unsigned(std::min<long long>(64, (n + 255) / 256)), frames);
-  k_validate_f64<<<grid, 256, 0, st>>>(pix, n, n, status, negz);
+  k_validate_f64<<<grid, 256, 0, st>>>(pix, n, n, status);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   k_scrub_f64<<<grid, 256, 0, st>>>(pix, n, n, status);
