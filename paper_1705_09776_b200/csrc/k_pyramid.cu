@@ -418,6 +418,16 @@ __device__ __forceinline__ void blur_level(const Batch& bt, const DetConst& dc, 
   double* gcol = G + cx;
   const bool vec = col1 && (w & 1) == 0 && (reinterpret_cast<uintptr_t>(gcol) & 15) == 0;
   const int nrows = h + 2 * R;  // virtual rows r = 0 .. nrows-1 (v = r - R)
+  // The reference's sums start from 0.0 (acc = 0.0; acc += ...), ours from
+  // the first product: the values are the same except that an all -0.0 sum
+  // stays -0.0 here and is +0.0 there. Only f64 base rows can hold -0.0 (a
+  // GrayImage of -0.0 pixels passes validate()); their G values take one
+  // + 0.0, which maps -0.0 to +0.0 and leaves every other value alone, so the
+  // pyramid never holds -0.0 — as the reference's never does.
+  auto canon = [](double v) {
+    if constexpr (SRC == 1) return __dadd_rn(v, 0.0);
+    else return v;
+  };
   if constexpr (!UNROLL) {
     // Rolled row loop (a few hundred instructions, resident in the
     // instruction cache): acc[s] holds output row v - R + s; row v adds
@@ -473,10 +483,10 @@ __device__ __forceinline__ void blur_level(const Batch& bt, const DetConst& dc, 
       if (y >= 0 && y < h) {
         double* gp = gcol + (long long)y * w;
         if (vec) {
-          *reinterpret_cast<double2*>(gp) = make_double2(acc0[0], acc1[0]);
+          *reinterpret_cast<double2*>(gp) = make_double2(canon(acc0[0]), canon(acc1[0]));
         } else {
-          if (col0) gp[0] = acc0[0];
-          if (col1) gp[1] = acc1[0];
+          if (col0) gp[0] = canon(acc0[0]);
+          if (col1) gp[1] = canon(acc1[0]);
         }
       }
 #pragma unroll
@@ -542,10 +552,10 @@ __device__ __forceinline__ void blur_level(const Batch& bt, const DetConst& dc, 
         const int so = ((i - R) % CH + CH) % CH;
         double* gp = gcol + (long long)y * w;
         if (vec) {
-          *reinterpret_cast<double2*>(gp) = make_double2(acc0[so], acc1[so]);
+          *reinterpret_cast<double2*>(gp) = make_double2(canon(acc0[so]), canon(acc1[so]));
         } else {
-          if (col0) gp[0] = acc0[so];
-          if (col1) gp[1] = acc1[so];
+          if (col0) gp[0] = canon(acc0[so]);
+          if (col1) gp[1] = canon(acc1[so]);
         }
       }
     }

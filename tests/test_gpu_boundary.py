@@ -51,6 +51,30 @@ def test_f64_grayimage_matches_oracle(ex, bundle_b8):
         assert got_n.shape == want_n.shape and np.allclose(got_n, want_n, rtol=1e-12, atol=0)
 
 
+def test_f64_negative_zero_pixels_match_oracle(ex, bundle_b8):
+    """-0.0 passes validate() (-0.0 >= 0.0). The reference's blur sums start
+    from 0.0, so its pyramid never holds -0.0; the GPU's f64-base blur maps an
+    all -0.0 sum to +0.0 the same way, so zero signs downstream (the bilinear
+    taps, atan2's +-pi) match. Bands and a +-0 checkerboard next to textured
+    regions, in a batch with an ordinary frame, against the oracle; and the
+    pyramid levels of a -0.0 frame hold no -0.0."""
+    frames = np.stack([oracle_lib.synth_f64(5200 + i, 320, 240) for i in range(3)])
+    frames[0, :, 100:160] = -0.0
+    frames[0, 60:120, :] = 0.0
+    frames[1, 40:200, 40:200] = np.where((np.indices((160, 160)).sum(0) % 2) == 0, -0.0, 0.0)
+    frames[1, 90:110, :] = -0.0
+    assert np.signbit(frames[0]).any() and np.signbit(frames[1]).any() and not np.signbit(frames[2]).any()
+    for mode in (3, 5):
+        got, status = ex.encode_batch(frames, mode)
+        assert status.tolist() == [0, 0, 0]
+        for i in range(3):
+            assert got[i] == oracle_lib.encode_f64(bundle_b8, frames[i], mode)[0], f"mode {mode} frame {i}"
+    ex.encode_batch(frames[0:1], 3)
+    for lvl in range(4):
+        g = ex.debug_get(f"gauss:0:{lvl}", 0)
+        assert g.size > 0 and (g == 0.0).any() and not (np.signbit(g) & (g == 0.0)).any(), lvl
+
+
 def test_f64_validate_per_frame(ex, bundle_b8):
     """validate(): a NaN, an inf or a value outside [0, 1] fails that frame
     alone with a DataError status; the neighbours are unaffected."""
