@@ -78,9 +78,10 @@ __device__ __forceinline__ BTexels btexels(const double* img, const BTap& t) {
 }
 // The reference skips a term whose fraction is 0 (descriptor.cpp:25-35).
 // Adding it instead is exact: its product is +0 (every factor is finite and
-// non-negative — fractions in [0, 1), pyramid values are Gaussian-blur sums
-// starting from +0.0, never -0.0 — and the fallback texel is a real one), and
-// r, itself a product of non-negative factors, is never -0.0, so r + (+0) == r.
+// non-negative — fractions in [0, 1), pyramid values never -0.0, as the
+// reference's 0.0-started blur sums never are (`canon` in blur_level) — and
+// the fallback texel is a real one), and r, itself a product of non-negative
+// factors, is never -0.0, so r + (+0) == r.
 // Unconditional terms spare the compare and the two selects per term that
 // the skip costs after if-conversion.
 __device__ __forceinline__ double bmix(const BTap& t, const BTexels& v) {
