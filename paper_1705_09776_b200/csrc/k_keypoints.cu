@@ -320,6 +320,7 @@ struct SelKey { unsigned long long k[5]; };
 
 // k_select's dynamic shared memory: winner indices, then (16-byte aligned)
 // their keys and ranks.
+constexpr int kRankSortMax = 2048;  // winners rank-sorted with their keys in shared memory (104 KB at the limit)
 __host__ __device__ inline size_t select_key_offset(int select_n) {
   return (size_t(select_n) * sizeof(int) + 15) & ~size_t(15);
 }
@@ -435,44 +436,76 @@ __global__ void __launch_bounds__(kMergeThreads) k_select(Batch bt, Model md, En
     for (int i = threadIdx.x; i < n; i += blockDim.x) state[i] = 1;
     __syncthreads();
   }
-  // Gather winners (any order), then order them by the full key: a rank
-  // sort (keys are unique — the index is the last word), each winner's rank
-  // counted over chunks of the others by several threads, three barriers in
-  // all instead of a bitonic network's log^2 stages.
+  // Gather winners (any order), then order them by the full key. Up to
+  // kRankSortMax winners: a rank sort (keys are unique — the index is the last
+  // word), each winner's rank counted over chunks of the others by several
+  // threads, three barriers in all; larger selection budgets: a bitonic
+  // network on the indices (shared memory for the keys would not fit).
   int* win = reinterpret_cast<int*>(ssm);
-  SelKey* wkey = reinterpret_cast<SelKey*>(ssm + select_key_offset(bt.select_n));
-  int* rnk = reinterpret_cast<int*>(wkey + bt.select_n);
   const int got = compact(
       n, [&](int i) { return state[i] == 1; }, [&](int i, int pos) { win[pos] = i; }, warp_tot);
   __syncthreads();
-  for (int i = threadIdx.x; i < got; i += blockDim.x) {
-    wkey[i] = sel_key(score[win[i]], acc[win[i]], win[i]);
-    rnk[i] = 0;
-  }
-  __syncthreads();
-  const int chunks = got > 0 ? max(1, int(blockDim.x) / got) : 1;
-  for (int t = threadIdx.x; t < got * chunks; t += blockDim.x) {
-    const int i = t % got, c = t / got;
-    const int j0 = c * got / chunks, j1 = (c + 1) * got / chunks;
-    const SelKey ki = wkey[i];
-    int r = 0;
-    for (int j = j0; j < j1; ++j) r += key_less(wkey[j], ki) ? 1 : 0;
-    atomicAdd(&rnk[i], r);
-  }
-  __syncthreads();
-  // Sorted source list, then the records move as coalesced 16-byte pieces.
-  int* src = rnk + bt.select_n;  // a second int array after the ranks
-  for (int i = threadIdx.x; i < got; i += blockDim.x) src[rnk[i]] = win[i];
-  __syncthreads();
   KP* sel = bt.sel + (long long)f * bt.select_n;
-  const uint4* s4 = reinterpret_cast<const uint4*>(acc);
-  uint4* d4 = reinterpret_cast<uint4*>(sel);
-  for (int c = threadIdx.x; c < 4 * got; c += blockDim.x) d4[c] = s4[4 * src[c >> 2] + (c & 3)];
+  if (bt.select_n <= kRankSortMax) {
+    SelKey* wkey = reinterpret_cast<SelKey*>(ssm + select_key_offset(bt.select_n));
+    int* rnk = reinterpret_cast<int*>(wkey + bt.select_n);
+    for (int i = threadIdx.x; i < got; i += blockDim.x) {
+      wkey[i] = sel_key(score[win[i]], acc[win[i]], win[i]);
+      rnk[i] = 0;
+    }
+    __syncthreads();
+    const int chunks = got > 0 ? max(1, int(blockDim.x) / got) : 1;
+    for (int t = threadIdx.x; t < got * chunks; t += blockDim.x) {
+      const int i = t % got, c = t / got;
+      const int j0 = c * got / chunks, j1 = (c + 1) * got / chunks;
+      const SelKey ki = wkey[i];
+      int r = 0;
+      for (int j = j0; j < j1; ++j) r += key_less(wkey[j], ki) ? 1 : 0;
+      atomicAdd(&rnk[i], r);
+    }
+    __syncthreads();
+    // Sorted source list, then the records move as coalesced 16-byte pieces.
+    int* src = rnk + bt.select_n;
+    for (int i = threadIdx.x; i < got; i += blockDim.x) src[rnk[i]] = win[i];
+    __syncthreads();
+    const uint4* s4 = reinterpret_cast<const uint4*>(acc);
+    uint4* d4 = reinterpret_cast<uint4*>(sel);
+    for (int c = threadIdx.x; c < 4 * got; c += blockDim.x) d4[c] = s4[4 * src[c >> 2] + (c & 3)];
+  } else {
+    int P = 1;
+    while (P < got) P <<= 1;
+    for (int i = got + threadIdx.x; i < P; i += blockDim.x) win[i] = -1;
+    __syncthreads();
+    for (int size = 2; size <= P; size <<= 1)
+      for (int stride = size >> 1; stride > 0; stride >>= 1) {
+        for (int i = threadIdx.x; i < P; i += blockDim.x) {
+          const int j = i ^ stride;
+          if (j > i) {
+            const int a = win[i], b = win[j];
+            bool a_after_b;
+            if (a < 0) a_after_b = b >= 0;
+            else if (b < 0) a_after_b = false;
+            else a_after_b = key_less(sel_key(score[b], acc[b], b), sel_key(score[a], acc[a], a));
+            const bool up = (i & size) == 0;
+            if (up == a_after_b) {
+              win[i] = b;
+              win[j] = a;
+            }
+          }
+        }
+        __syncthreads();
+      }
+    for (int r = threadIdx.x; r < got; r += blockDim.x) sel[r] = acc[win[r]];
+  }
   if (threadIdx.x == 0) bt.sel_count[f] = got;
 }
 
 size_t select_smem_bytes(const Batch& bt) {
-  return select_key_offset(bt.select_n) + size_t(bt.select_n) * (sizeof(SelKey) + 2 * sizeof(int));
+  if (bt.select_n <= kRankSortMax)
+    return select_key_offset(bt.select_n) + size_t(bt.select_n) * (sizeof(SelKey) + 2 * sizeof(int));
+  size_t p = 1;
+  while (p < size_t(bt.select_n)) p <<= 1;
+  return p * sizeof(int);
 }
 
 
