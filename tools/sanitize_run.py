@@ -8,8 +8,10 @@ kernel of the product path on a handful of frames, no torch.
   posterior-small, Fisher, SCFV, pack), the same frames with the 512-component
   bundle (k_posterior on the FP64 tensor cores), one f64 frame at three times the size (resized) (k_validate, f64 k_resize,
   k_blur<.., 1>), one odd-width RGB frame (k_grey_rgb, unaligned u8 rows),
-  on-device synthesis, streamed submit / wait batches, the register-bin
-  describe variant, and the debug paths (exact-only extrema, the TMA tile kernel and its plain-load
+  on-device synthesis, streamed submit / wait batches (one context and a
+  two-shard multi-device context), an f64 frame with -0.0 pixels, a
+  selection budget above the rank-sort limit, the register-bin describe
+  variant, and the debug paths (exact-only extrema, the TMA tile kernel and its plain-load
   variant, tiny capacities -> the capacity retry);
 * match: an 8-container index, retrieve + match_pairs (k_match.cu);
 * train: cdvz_gpu_train_model on a 20-image corpus (train.cu).
@@ -61,7 +63,32 @@ def encode_part():
     got, st = ex.encode_batch(frames[:1], "4K")
     assert got[0] == want0
     ex.set_debug(False)
+    # an f64 frame with a -0.0 band (the f64-base blur's zero canonicalisation)
+    negz = oracle_lib.synth_f64(78, w, h)
+    negz[:, w // 3:w // 2] = -0.0
+    got, st = ex.encode_batch(negz[None], "4K")
+    assert st.tolist() == [0] and got[0] == oracle_lib.encode_f64(b8, negz, 3)[0]
     ex.close()
+    # a multi-device context (two shards on one GPU), streamed
+    mx = cg.Extractor(b8, max_batch=4, devices=[0, 0])
+    q0 = mx.encode_batch_submit(frames, "4K")
+    q1 = mx.encode_batch_submit(frames, "4K")
+    assert q0.wait()[0][0] == want0 and q1.wait()[0][0] == want0
+    mx.close()
+    # a selection budget above the rank-sort limit (k_select's bitonic network)
+    import zlib
+    lines = b8.split("\n")
+    k = lines.index(next(ln for ln in lines if ln.startswith("section selector")))
+    _, name, nl, _ = lines[k].split()
+    body = lines[k + 1:k + 1 + int(nl)]
+    body[0] = "n = 3000"
+    lines[k] = f"section {name} {nl} %08x" % zlib.crc32(("\n".join(body) + "\n").encode())
+    lines[k + 1:k + 1 + int(nl)] = body
+    big = "\n".join(lines)
+    bx = cg.Extractor(big, max_batch=4)
+    got, st = bx.encode_batch(frames[:1], "4K")
+    assert st.tolist() == [0] and got[0] == oracle_lib.encode(big, frames[0], 3)
+    bx.close()
     ex = cg.Extractor(b512, max_batch=4)
     got, st = ex.encode_batch(frames[:2], "4K")
     for i in range(2):
