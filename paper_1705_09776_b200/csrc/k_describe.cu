@@ -426,10 +426,7 @@ __device__ __forceinline__ double div_two_pi(double a) {
   return fma(r, kInvTwoPi, q0);
 }
 
-#ifndef CDVZ_SAMPLE_MINB
-#define CDVZ_SAMPLE_MINB 12
-#endif
-__global__ void __launch_bounds__(kSampleThreads, CDVZ_SAMPLE_MINB) k_sample(Batch bt) {
+__global__ void __launch_bounds__(kSampleThreads, 12) k_sample(Batch bt) {
   __shared__ double gexp[kMaxSamples * (kMaxSamples + 1) / 2];  // [j * (j + 1) / 2 + i], i <= j
   // Per-axis terms (u_i = v_i, the same expression): the reference's
   // px = (cx + u cos) - v sin and py = (cy + u sin) + v cos, evaluated in its
