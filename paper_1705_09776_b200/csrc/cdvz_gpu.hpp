@@ -26,6 +26,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <fstream>
 #include <iterator>
 #include <map>
@@ -660,6 +661,17 @@ inline std::vector<RankedList> retrieve(const std::vector<std::pair<std::string,
       out[q].items.push_back({index.ids()[std::size_t(items[q * n + r])], scores[q * n + r]});
   }
   return out;
+}
+
+// format_double (common.cpp:37-49): the shortest %.*g that parses back exactly.
+inline std::string format_double(double v) {
+  char buf[40];
+  for (int prec = 1; prec <= 17; ++prec) {
+    std::snprintf(buf, sizeof(buf), "%.*g", prec, v);
+    if (std::strtod(buf, nullptr) == v) return buf;
+  }
+  std::snprintf(buf, sizeof(buf), "%.17g", v);
+  return buf;
 }
 
 // match_pair (eval.cpp:66-74) of query container a and index item i.

@@ -130,3 +130,18 @@ def test_cpp_stream_shim_compiles(tmp_path):
                     "-lcdvz_gpu", f"-Wl,-rpath,{lib_dir}", "-o", str(exe)], check=True)
     p = subprocess.run([str(exe)], capture_output=True, text=True)
     assert p.returncode == 1 and "usage" in p.stderr
+
+
+def test_cpp_match_shim_compiles(tmp_path):
+    """examples/match.cpp (the reference CLI's match over the shim) builds;
+    without arguments it is a usage error, a missing file a data error."""
+    import subprocess
+
+    exe = tmp_path / "match"
+    lib_dir = os.path.dirname(cg.library_path())
+    subprocess.run(["g++", "-std=c++17", "-O1", os.path.join(ROOT, "examples", "match.cpp"), f"-L{lib_dir}",
+                    "-lcdvz_gpu", f"-Wl,-rpath,{lib_dir}", "-o", str(exe)], check=True)
+    p = subprocess.run([str(exe)], capture_output=True, text=True)
+    assert p.returncode == 1 and "usage" in p.stderr
+    p = subprocess.run([str(exe), str(tmp_path / "a.cdvz"), str(tmp_path / "b.cdvz")], capture_output=True, text=True)
+    assert p.returncode == 2 and "cannot open" in p.stderr

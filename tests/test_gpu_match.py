@@ -188,3 +188,35 @@ def test_cpp_retrieval_example_matches_python(corpus_4k, tmp_path):
     want = cg.Index(corpus_4k[:6], ids=paths).retrieve(corpus_4k[2])
     assert [g[0] for g in got] == [w[0] for w in want]
     assert all(abs(g[1] - w[1]) <= 1e-9 * max(1.0, abs(w[1])) for g, w in zip(got, want))
+
+
+def test_cpp_match_example_matches_python(corpus_4k, tmp_path):
+    """examples/match.cpp prints the reference CLI's two lines
+    (cdvz.cpp:82-89): format_double of global_similarity and the local match
+    count, equal to Index.match_pairs for the same pair."""
+    import os
+    import subprocess
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = tmp_path / "match"
+    lib_dir = os.path.dirname(cg.library_path())
+    subprocess.run(["g++", "-std=c++17", "-O1", os.path.join(root, "examples", "match.cpp"), f"-L{lib_dir}",
+                    "-lcdvz_gpu", f"-Wl,-rpath,{lib_dir}", "-o", str(exe)], check=True)
+
+    def fmt(v):
+        for prec in range(1, 18):
+            s = "%.*g" % (prec, v)
+            if float(s) == v:
+                return s
+        return "%.17g" % v
+
+    for qa, qb in [(0, 1), (2, 2), (5, 30)]:
+        (tmp_path / "a.cdvz").write_bytes(corpus_4k[qa])
+        (tmp_path / "b.cdvz").write_bytes(corpus_4k[qb])
+        p = subprocess.run([str(exe), str(tmp_path / "a.cdvz"), str(tmp_path / "b.cdvz")], capture_output=True,
+                           text=True)
+        assert p.returncode == 0, p.stderr
+        idx = cg.Index([corpus_4k[qb]])
+        sim, loc = idx.match_pairs([corpus_4k[qa]], [(0, 0)])
+        idx.close()
+        assert p.stdout == f"global_similarity {fmt(float(sim[0]))}\nlocal_match_count {int(loc[0])}\n"
