@@ -57,5 +57,30 @@ def main(out):
     print(f"{same}/{total} containers byte-identical to the oracle, {same_ref}/{total} to the reference")
 
 
+def main_extended(out):
+    """Unseen content: 8192 more VGA frames (other seeds) in 4K and 16K with the
+    8-component bundle and 2048 with the 512-component one, 1024 at 1280x720
+    resized, against the oracle and the reference."""
+    rows = []
+    for k, (seed, mode) in enumerate([(200000, "4K"), (300000, "16K"), (400000, "1K"), (500000, "2K")]):
+        for part in range(2):
+            vga = oracle_lib.synth_frames(seed + 1024 * part, 1024, 640, 480)
+            rows.append(sweep(f"VGA seeds {seed + 1024 * part}+, {mode}", "b8", vga, mode))
+    for part in range(2):
+        vga = oracle_lib.synth_frames(600000 + 1024 * part, 1024, 640, 480)
+        rows.append(sweep(f"VGA seeds {600000 + 1024 * part}+, 4K, 512 components", "b512", vga, "4K"))
+    hd = oracle_lib.synth_frames(700000, 1024, 1280, 720)
+    rows.append(sweep("1280x720 -> 640x360, 8K", "b8", hd, "8K"))
+    with open(out, "w") as f:
+        json.dump(rows, f, indent=1)
+    total = sum(r["frames"] for r in rows)
+    same = sum(r["byte_identical"] for r in rows)
+    same_ref = sum(r["byte_identical_vs_reference"] for r in rows)
+    print(f"{same}/{total} containers byte-identical to the oracle, {same_ref}/{total} to the reference")
+
+
 if __name__ == "__main__":
+    if len(sys.argv) > 2 and sys.argv[2] == "extended":
+        main_extended(sys.argv[1])
+        sys.exit(0)
     main(sys.argv[1] if len(sys.argv) > 1 else "gpurun_out/parity_sweep.json")
